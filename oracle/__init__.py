@@ -1,0 +1,29 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+A plain, slow, obviously-correct CPU (numpy, fp64) implementation of what the
+hot path of arXiv 2304.12387 computes.  Only `tests/`, `__graft_entry__.smoke()`
+and `bench.py`'s `cpu_baseline` / `--impl reference` legs may import it.  The
+product path (`paper_2304_12387_b200/`) never imports it and shares no code
+with it; the only shared module is `synth/` (seeded inputs, no arithmetic of
+the method).
+
+Citations: ``P:n`` = /root/reference/PAPER.md line n (section / equation named
+beside it).  Every function names the passage it follows.
+
+What is computed by its plain definition (dense element matrices by direct
+Gauss-Legendre quadrature, global assembly, Algorithm 1 literally, the entry
+formula of S~ and the sparse triple product, MINRES step by step):
+  basis1d   - GLL nodes, GL rule, Lagrange l_i, histopolation h_j       (§2.1)
+  fem       - element geometry, RT/L2 reference bases, M^e, W^e, B^e    (eq. matrices)
+  space     - canonical numbering, Algorithm 1 index tables, D in CSR   (Alg. 1)
+  operators - assembled M, W, Z, block apply, diagonals, S~ two paths
+  solvers   - Chebyshev-Jacobi S^-1, block-diagonal preconditioner, MINRES
+  sample    - element-local evaluation of sampled output rows (full-size parity)
+
+Parity pins (tests/test_oracle_*.py, `-m "not gpu"`): closed-form 1D tables,
+SPD / exactness of M, B = W D, D's incidence structure,
+M-matrix S~, Prop. 2.1/2.2 spectra, dense-solve MINRES,
+manufactured-solution convergence rates, closed-form traces.
+Parity unpinned: trilinear-element values of M^e beyond the invariants above
+(no closed form exists).
+"""

@@ -1,0 +1,135 @@
+"""Preconditioner and MINRES (oracle; test infrastructure).
+
+P:411-421 Remark: B = diag(tau M~, S~); S^-1 = approximate inverse of S~.
+P:669 / P:889: S^-1 is one AMG V-cycle in the paper; this build's slice uses a fixed
+Chebyshev-Jacobi polynomial in S~ (reading A9/A10), identical on the GPU.
+P:169: MINRES; relative tolerance 1e-12 (preconditioned norm, reading A8).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def chebyshev_jacobi(S, r, degree: int, ratio: float, lam_max: float = 2.0):
+    """k-step Chebyshev semi-iteration for S y = r, Jacobi-scaled, y0 = 0, on the
+    interval [lam_max/ratio, lam_max] (reading A10; Saad, Iterative Methods, Alg. 12.1)."""
+    Dinv = 1.0 / S.diagonal()
+    a, b = lam_max / ratio, lam_max
+    theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    r = r.copy()
+    y = np.zeros_like(r)
+    d = Dinv * r / theta
+    for k in range(degree):
+        y = y + d
+        if k == degree - 1:
+            break
+        r = r - S @ d
+        rho_new = 1.0 / (2.0 * sigma - rho)
+        d = rho_new * rho * d + (2.0 * rho_new / delta) * (Dinv * r)
+        rho = rho_new
+    return y
+
+
+class BlockDiagPrecond:
+    """P^-1 = diag((tau M~)^-1, S^-1)."""
+
+    def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, exact_schur=False, exact_blocks=False):
+        self.asm, self.tau, self.degree, self.ratio = asm, tau, degree, ratio
+        self.n_rt = asm.n_rt
+        self.exact_schur = exact_schur
+        self.exact_blocks = exact_blocks
+        if exact_schur or exact_blocks:
+            import scipy.sparse.linalg as spla
+            if exact_blocks:   # Prop 2.1/2.2: A = M, S = C + D M^-1 D^T exactly
+                Minv = np.linalg.inv(asm.M.toarray())
+                Zd = np.zeros((asm.n_l2, asm.n_l2))
+                nl = asm.p ** asm.dim
+                for e, Ze in enumerate(asm.Z):
+                    Zd[e * nl:(e + 1) * nl, e * nl:(e + 1) * nl] = Ze
+                Dd = asm.D.toarray()
+                self.Sfull = Zd + Dd @ Minv @ Dd.T
+                self.Mfull = asm.M.toarray()
+            else:
+                self._lu = spla.splu(asm.S.tocsc())
+
+    def apply(self, v):
+        vu, vq = v[: self.n_rt], v[self.n_rt:]
+        if self.exact_blocks:
+            zu = np.linalg.solve(self.tau * self.Mfull, vu)
+            zq = np.linalg.solve(self.Sfull, vq)
+        else:
+            zu = vu / (self.tau * self.asm.Mdiag)
+            if self.exact_schur:
+                zq = self._lu.solve(vq)
+            else:
+                zq = chebyshev_jacobi(self.asm.S, vq, self.degree, self.ratio)
+        return np.concatenate([zu, zq])
+
+
+class Breakdown(RuntimeError):
+    pass
+
+
+def minres(apply_A, apply_Pinv, b, rtol=1e-12, maxit=1000):
+    """Preconditioned MINRES, Elman-Silvester-Wathen form, x0 = 0
+    (SURVEY.md §8(c) step 10). Returns x, iterations, converged, |eta|/gamma_1 history."""
+    n = len(b)
+    x = np.zeros(n)
+    v_old = np.zeros(n)
+    w_old = np.zeros(n)
+    w = np.zeros(n)
+    v = b.copy()
+    z = apply_Pinv(v)
+    g2 = float(np.dot(z, v))
+    if g2 < 0:
+        raise Breakdown("preconditioner not SPD")
+    gamma = math.sqrt(g2)
+    if gamma == 0.0:
+        return x, 0, True, [0.0]
+    gamma0 = gamma
+    gamma_old = 1.0
+    eta = gamma
+    s_old = s = 0.0
+    c_old = c = 1.0
+    hist = [1.0]
+    it = 0
+    conv = False
+    for j in range(1, maxit + 1):
+        z = z / gamma
+        Az = apply_A(z)
+        delta = float(np.dot(Az, z))
+        v_new = Az - (delta / gamma) * v - (gamma / gamma_old) * v_old
+        z_new = apply_Pinv(v_new)
+        g2 = float(np.dot(z_new, v_new))
+        if g2 < 0:
+            raise Breakdown("preconditioner not SPD")
+        gamma_new = math.sqrt(g2)
+        a0 = c * delta - c_old * s * gamma
+        a1 = math.hypot(a0, gamma_new)
+        a2 = s * delta + c_old * c * gamma
+        a3 = s_old * gamma
+        c_new = a0 / a1
+        s_new = gamma_new / a1
+        w_new = (z - a3 * w_old - a2 * w) / a1
+        x = x + c_new * eta * w_new
+        eta = -s_new * eta
+        hist.append(abs(eta) / gamma0)
+        it = j
+        # rotate
+        v_old, v = v, v_new
+        z = z_new
+        gamma_old, gamma = gamma, gamma_new
+        w_old, w = w, w_new
+        c_old, c = c, c_new
+        s_old, s = s, s_new
+        if abs(eta) <= rtol * gamma0:
+            conv = True
+            break
+        if gamma_new == 0.0:
+            conv = True
+            break
+    return x, it, conv, hist
