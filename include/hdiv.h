@@ -1,0 +1,156 @@
+/* hdiv.h — C-ABI of libhdiv: the B200 hot path of arXiv 2304.12387's matrix-free
+ * block-preconditioned saddle-point solver for RT_p / L2_{p-1} (interpolation-histopolation
+ * basis) grad-div and Darcy problems on structured quadrilateral / hexahedral meshes.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n.
+ *
+ * Conventions for every call
+ *  - Vectors are DEVICE pointers (fp64), caller-owned (e.g. torch tensors), in the canonical
+ *    numbering of DESIGN.md §Layout (the library's HBM layout IS the canonical numbering):
+ *      RT (3D): x-faces I+(n_x+1)(J+n_y K), then y-faces I+n_x(J+(n_y+1)K), then z-faces
+ *               I+n_x(J+n_y K);  n_a = N_a p subcells per axis;  (2D: x-faces, y-faces).
+ *      L2     : element-contiguous e p^d + (a + p(b + p c)), e = ex + N_x(ey + N_y ez).
+ *      block  : x = [u (n_rt) ; q~ (n_l2)].
+ *    With nranks > 1 the vectors are this rank's slab (its own canonical numbering; the
+ *    interface face plane is replicated on both ranks and kept bitwise identical).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). Applies are
+ *    asynchronous on that stream; nothing is synchronised unless stated.
+ *  - Inputs and outputs must not alias unless stated.
+ *  - Errors are returned as hdiv_status; nothing propagates across the ABI. Validation
+ *    (order, det J > 0 at every quadrature point, coefficient signs, shapes) happens in
+ *    hdiv_setup before any device work.  A CUDA launch error is HDIV_ERR_CUDA.
+ *  - The handle is read-only after setup except for the MINRES workspace: concurrent applies
+ *    on distinct outputs are safe; hdiv_minres_solve serialises on its own workspace.
+ */
+#ifndef HDIV_H
+#define HDIV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hdiv_ctx* hdiv_handle;          /* opaque, library-owned */
+
+typedef enum {
+  HDIV_OK = 0,
+  HDIV_ERR_INVALID_ORDER = 1,   /* p < 1 or p > HDIV_MAX_ORDER                        */
+  HDIV_ERR_INVALID_MESH = 2,    /* det J <= 0 at a quadrature point, bad counts/slab   */
+  HDIV_ERR_COEFFICIENT = 3,     /* alpha, beta, eps <= 0 or gamma < 0                  */
+  HDIV_ERR_SHAPE = 4,           /* inconsistent sizes / dim                            */
+  HDIV_ERR_CUDA = 5,            /* CUDA runtime error (allocation, launch)             */
+  HDIV_ERR_NCCL = 6,            /* NCCL error                                          */
+  HDIV_ERR_BREAKDOWN = 7,       /* MINRES gamma^2 < 0: preconditioner not SPD          */
+  HDIV_ERR_UNSUPPORTED = 8,     /* e.g. W^-1 on a non-affine element (NEXT-2)          */
+  HDIV_ERR_NULL = 9             /* NULL handle or required pointer                      */
+} hdiv_status;
+
+#define HDIV_MAX_ORDER 6
+
+typedef enum {
+  HDIV_GRAD_DIV = 0,  /* [M_beta, D^T; D, -W_alpha^-1]            */
+  HDIV_DARCY = 1      /* [M_{1/eps}, D^T; D, -W^-1 W_gamma W^-1];   */
+                      /* gamma piecewise constant, gamma = 0 allowed (zero (2,2) block)     */
+} hdiv_kind;
+
+typedef struct {
+  int dim;                    /* 2 or 3                                                      */
+  int64_t nx, ny, nz;         /* GLOBAL element counts (2D: nz = 1)                          */
+  int64_t ez_begin, ez_end;   /* this rank's slab of element layers [begin, end) along the   */
+                              /* last axis (z in 3D, y in 2D); single GPU: [0, nz) / [0, ny) */
+  const double* vertices;     /* HOST, vertex layers begin..end inclusive of the slab,       */
+                              /* [layers][..][nx+1][dim], x fastest; NULL => uniform unit box */
+} hdiv_mesh_desc;
+
+typedef struct {              /* HOST per-element arrays of the slab [E_local], or NULL       */
+  const double *alpha, *beta, *gamma, *eps;
+  double alpha0, beta0, gamma0, eps0;   /* constants used where an array is NULL              */
+} hdiv_coeffs;
+
+typedef struct {
+  double tau;          /* (1,1) preconditioner scale tau M~; <= 0 => 1 (A7)      */
+  int cheb_degree;     /* S^-1 = Chebyshev-Jacobi polynomial degree on S~; <= 0 => 4 (A10)   */
+  double cheb_ratio;   /* interval [2/ratio, 2]; <= 0 => 30                                  */
+  int kernel;          /* 0 auto, 1 force the general quadrature kernel, 2 force affine tile */
+} hdiv_options;
+
+typedef struct {
+  int iters;           /* first j with |eta_j| <= rtol * gamma_1 (reading A8)         */
+  int converged;       /* 0 on iteration limit (not an error)                                */
+  double rel_resid;    /* |eta| / gamma_1 at exit                                            */
+  double t_solve_ms;   /* device time of the solve (CUDA events on `stream`)                 */
+} hdiv_report;
+
+/* Setup (setup list of SURVEY §3): validates, uploads 1D tables, precomputes
+ * per-element geometry/coefficients, assembles diag(M), diag(W), the
+ * Schur approximation S~ (CSR) and allocates the MINRES workspace.
+ * nccl_unique_id: 128-byte ncclUniqueId (rank 0's, broadcast by the caller) or NULL for one
+ * GPU; the library creates and owns the communicator.  Blocks until setup is complete.
+ * Returns the handle in *out (NULL on error). */
+hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* coeffs,
+                       hdiv_kind kind, const hdiv_options* opts,
+                       const void* nccl_unique_id, int rank, int nranks,
+                       void* stream, hdiv_handle* out);
+
+void hdiv_destroy(hdiv_handle h);
+const char* hdiv_status_string(hdiv_status s);
+const char* hdiv_last_error(void);      /* thread-local detail of the last error              */
+int hdiv_version(void);
+
+/* Local (this rank) and global vector sizes. */
+hdiv_status hdiv_sizes(hdiv_handle h, int64_t* n_rt_local, int64_t* n_l2_local,
+                       int64_t* n_rt_global, int64_t* n_l2_global);
+
+/* y_u = M_beta u  (sum-factorised).  u, y_u: [n_rt]. */
+hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* y_u, void* stream);
+/* y_q = D u  (topological +-1).  u: [n_rt], y_q: [n_l2]. */
+hdiv_status hdiv_apply_div(hdiv_handle h, const double* u, double* y_q, void* stream);
+/* y_u = D^T q  .  q: [n_l2], y_u: [n_rt]. */
+hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* y_u, void* stream);
+/* y = A x with A = [M, D^T; D, -Z], Z = W_alpha^-1 (grad-div) or W^-1 W_gamma W^-1 (Darcy)
+ * (P:207-211).  x, y: [n_rt + n_l2].  Multi-GPU: includes the interface
+ * reverse-add over NCCL. */
+hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* stream);
+/* Same as hdiv_apply_block with HOST x, y (pinned or pageable): H2D copy, apply, D2H copy on
+ * `stream`; blocks until y is on the host (end-to-end path). */
+hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* x_host, double* y_host,
+                                  void* stream);
+/* Number of kernels one hdiv_apply_block launches (for launch accounting). */
+hdiv_status hdiv_apply_launches(hdiv_handle h, int* n);
+
+/* diag(M_beta) = M~, assembled (interface-summed).  diag: [n_rt]. */
+hdiv_status hdiv_assemble_mass_diag(hdiv_handle h, double* diag, void* stream);
+/* C~ = W~^-1 (grad-div) or diag(W)^-1 diag(W_gamma) diag(W)^-1 (Darcy). [n_l2] */
+hdiv_status hdiv_assemble_schur_diag_term(hdiv_handle h, double* ctil, void* stream);
+
+/* S~ = C~ + D M~^-1 D^T in CSR (eq. approx-schur-entries), rows = local L2 DOFs,
+ * columns sorted ascending (local numbering; multi-GPU ghost columns are not exported).
+ * Query nnz first; caller allocates row_ptr[n_l2+1], col[nnz], val[nnz] (device). */
+hdiv_status hdiv_schur_nnz(hdiv_handle h, int64_t* nnz);
+hdiv_status hdiv_assemble_schur_csr(hdiv_handle h, int64_t* row_ptr, int64_t* col,
+                                    double* val, void* stream);
+/* y = S~ x (the SpMV used inside S^-1).  x, y: [n_l2]. */
+hdiv_status hdiv_apply_schur(hdiv_handle h, const double* x, double* y, void* stream);
+/* D in CSR by Algorithm 1: row_ptr[n_l2+1] (= 2d i), col[2d n_l2], val. */
+hdiv_status hdiv_export_div_csr(hdiv_handle h, int64_t* row_ptr, int64_t* col, double* val,
+                                void* stream);
+/* z = P^-1 v with P = diag(tau M~, S^), S^-1 = Chebyshev-Jacobi on S~. */
+hdiv_status hdiv_apply_precond(hdiv_handle h, const double* v, double* z, void* stream);
+
+/* Block-diagonally preconditioned MINRES for A x = b, x0 = 0, stopping at
+ * |eta| <= rtol * gamma_1.  b, x: [n_rt + n_l2] device.  Blocks until done; fills
+ * *report.  Non-convergence is HDIV_OK with converged = 0. */
+hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double rtol,
+                              int maxit, hdiv_report* report, void* stream);
+
+/* Diagnostic, host only (no GPU needed): the library's 1D tables for order p with Q points
+ * (reading A3: Q = p+2).  Outputs (caller-owned host arrays): xq[Q], wq[Q] Gauss-Legendre on
+ * [0,1]; Bl[Q][p+1] = l_i(x_q); Bh[Q][p] = h_j(x_q); Ml[(p+1)^2], Mh[p^2], Mhinv[p^2]. */
+hdiv_status hdiv_debug_tables(int p, int Q, double* xq, double* wq, double* Bl, double* Bh,
+                              double* Ml, double* Mh, double* Mhinv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDIV_H */

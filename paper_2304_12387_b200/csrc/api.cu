@@ -1,0 +1,485 @@
+// api.cu — the C-ABI of libhdiv (include/hdiv.h).  Argument marshalling, validation and
+// dispatch only; every step of the hot path runs in the kernels of this directory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace hdiv {
+
+static thread_local std::string g_err;
+void set_error(const std::string& s) { g_err = s; }
+
+hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s);      // comm.cu
+void comm_free(hdiv_ctx* h);
+hdiv_status comm_reverse_add(hdiv_ctx* h, double* y_rt, cudaStream_t s);  // interface planes
+hdiv_status comm_setup_schur_ghosts(hdiv_ctx* h, cudaStream_t s);
+
+static hdiv_status fail(hdiv_status st, const std::string& msg) {
+  set_error(msg);
+  return st;
+}
+
+// Vertex corner X[v][d] of local element (ex,ey,ez), v = a + 2b + 4c
+static void corners(const std::vector<double>& V, int dim, int64_t NLx, int64_t NLy, int64_t ex,
+                    int64_t ey, int64_t ez, double X[8][3]) {
+  for (int v = 0; v < (1 << dim); ++v) {
+    int a = v & 1, b = (v >> 1) & 1, c = (v >> 2) & 1;
+    int64_t g = (dim == 3) ? ((ez + c) * (NLy + 1) + (ey + b)) * (NLx + 1) + (ex + a)
+                           : (ey + b) * (NLx + 1) + (ex + a);
+    for (int d = 0; d < dim; ++d) X[v][d] = V[g * dim + d];
+  }
+}
+
+cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
+                            cudaStream_t s) {
+  cudaError_t e = (h->kernel == 2) ? launch_affine_apply(h, x, y, MODE_BLOCK, skip, s)
+                                   : launch_general_apply(h, x, y, MODE_BLOCK, skip, s);
+  if (e != cudaSuccess) return e;
+  if (h->nranks > 1) {
+    if (comm_reverse_add(h, y, s) != HDIV_OK) return cudaErrorUnknown;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace hdiv
+
+using namespace hdiv;
+
+extern "C" {
+
+int hdiv_version(void) { return 1; }
+
+const char* hdiv_last_error(void) { return g_err.c_str(); }
+
+const char* hdiv_status_string(hdiv_status s) {
+  switch (s) {
+    case HDIV_OK: return "ok";
+    case HDIV_ERR_INVALID_ORDER: return "invalid order";
+    case HDIV_ERR_INVALID_MESH: return "invalid mesh";
+    case HDIV_ERR_COEFFICIENT: return "coefficient error";
+    case HDIV_ERR_SHAPE: return "shape error";
+    case HDIV_ERR_CUDA: return "CUDA error";
+    case HDIV_ERR_NCCL: return "NCCL error";
+    case HDIV_ERR_BREAKDOWN: return "MINRES breakdown (preconditioner not SPD)";
+    case HDIV_ERR_UNSUPPORTED: return "unsupported";
+    case HDIV_ERR_NULL: return "null argument";
+  }
+  return "unknown";
+}
+
+void hdiv_destroy(hdiv_handle h) {
+  if (!h) return;
+  minres_free(h);
+  comm_free(h);
+  cudaFree(h->d_vert);
+  cudaFree(h->d_coef);
+  cudaFree(h->d_mdiag);
+  cudaFree(h->d_ctil);
+  cudaFree(h->d_c2);
+  cudaFree(h->d_sdinv);
+  cudaFree(h->d_srow);
+  cudaFree(h->d_scol);
+  cudaFree(h->d_sval);
+  cudaFree(h->d_scratch);
+  cudaFree(h->d_xbuf);
+  cudaFree(h->d_ybuf);
+  delete h;
+}
+
+hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co, hdiv_kind kind,
+                       const hdiv_options* opts, const void* nccl_id, int rank, int nranks,
+                       void* stream, hdiv_handle* out) {
+  if (!out) return fail(HDIV_ERR_NULL, "out is NULL");
+  *out = nullptr;
+  if (!mesh || !co) return fail(HDIV_ERR_NULL, "mesh/coeffs NULL");
+  if (p < 1 || p > HDIV_MAX_ORDER) return fail(HDIV_ERR_INVALID_ORDER, "p out of [1,6]");
+  if (mesh->dim != 2 && mesh->dim != 3) return fail(HDIV_ERR_SHAPE, "dim must be 2 or 3");
+  if (kind != HDIV_GRAD_DIV && kind != HDIV_DARCY) return fail(HDIV_ERR_SHAPE, "bad kind");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HDIV_ERR_SHAPE, "bad rank");
+  if (nranks > 1 && !nccl_id) return fail(HDIV_ERR_NULL, "nccl id required for nranks > 1");
+  const int dim = mesh->dim;
+  const int64_t N[3] = {mesh->nx, mesh->ny, dim == 3 ? mesh->nz : 1};
+  for (int d = 0; d < dim; ++d)
+    if (N[d] < 1) return fail(HDIV_ERR_INVALID_MESH, "element counts must be >= 1");
+  const int last = dim - 1;
+  if (mesh->ez_begin < 0 || mesh->ez_end > N[last] || mesh->ez_end <= mesh->ez_begin)
+    return fail(HDIV_ERR_INVALID_MESH, "bad slab range");
+  if (nranks == 1 && (mesh->ez_begin != 0 || mesh->ez_end != N[last]))
+    return fail(HDIV_ERR_INVALID_MESH, "single rank must own the whole mesh");
+  cudaStream_t s = (cudaStream_t)stream;
+
+  auto* h = new hdiv_ctx();
+  h->dim = dim; h->p = p; h->Q = p + 2; h->kind = kind;
+  h->rank = rank; h->nranks = nranks;
+  h->opts.tau = (opts && opts->tau > 0) ? opts->tau : 1.0;
+  h->opts.cheb_degree = (opts && opts->cheb_degree > 0) ? opts->cheb_degree : 4;
+  h->opts.cheb_ratio = (opts && opts->cheb_ratio > 0) ? opts->cheb_ratio : 30.0;
+  h->opts.kernel = opts ? opts->kernel : 0;
+  for (int d = 0; d < 3; ++d) { h->N[d] = N[d]; h->NL[d] = N[d]; }
+  h->ez0 = mesh->ez_begin; h->ez1 = mesh->ez_end;
+  h->NL[last] = h->ez1 - h->ez0;
+  if (dim == 2) h->NL[2] = 1;
+  for (int d = 0; d < 3; ++d) h->n[d] = (d < dim) ? h->NL[d] * p : 1;
+  h->E = h->NL[0] * h->NL[1] * h->NL[2];
+  auto rt_count = [&](const int64_t* n) -> int64_t {
+    if (dim == 2) return (n[0] + 1) * n[1] + n[0] * (n[1] + 1);
+    return (n[0] + 1) * n[1] * n[2] + n[0] * (n[1] + 1) * n[2] + n[0] * n[1] * (n[2] + 1);
+  };
+  h->nrt = rt_count(h->n);
+  const int64_t pd = (dim == 2) ? (int64_t)p * p : (int64_t)p * p * p;
+  h->nl2 = h->E * pd;
+  {
+    int64_t ng[3] = {N[0] * p, N[1] * p, dim == 3 ? N[2] * p : 1};
+    h->nrt_g = rt_count(ng);
+    h->nl2_g = N[0] * N[1] * N[2] * pd;
+  }
+  if (dim == 2) {
+    h->off[0] = 0; h->off[1] = (h->n[0] + 1) * h->n[1]; h->off[2] = h->nrt;
+  } else {
+    h->off[0] = 0;
+    h->off[1] = (h->n[0] + 1) * h->n[1] * h->n[2];
+    h->off[2] = h->off[1] + h->n[0] * (h->n[1] + 1) * h->n[2];
+  }
+
+  // ---- vertices (host) ----
+  const int64_t nvx = h->NL[0] + 1, nvy = h->NL[1] + 1, nvz = (dim == 3) ? h->NL[2] + 1 : 1;
+  const int64_t nv = nvx * nvy * nvz;
+  std::vector<double> V(nv * dim);
+  if (mesh->vertices) {
+    std::memcpy(V.data(), mesh->vertices, sizeof(double) * V.size());
+  } else {   // uniform unit box
+    for (int64_t k = 0; k < nvz; ++k)
+      for (int64_t j = 0; j < nvy; ++j)
+        for (int64_t i = 0; i < nvx; ++i) {
+          int64_t g = (k * nvy + j) * nvx + i;
+          V[g * dim + 0] = (double)i / N[0];
+          if (dim == 2) V[g * dim + 1] = (double)(j + h->ez0) / N[1];
+          else {
+            V[g * dim + 1] = (double)j / N[1];
+            V[g * dim + 2] = (double)(k + h->ez0) / N[2];
+          }
+        }
+  }
+
+  // ---- coefficients (host validation) ----
+  const int64_t E = h->E;
+  std::vector<double> mw(E), c2(E);
+  bool any_gamma = false;
+  for (int64_t e = 0; e < E; ++e) {
+    if (kind == HDIV_GRAD_DIV) {
+      double al = co->alpha ? co->alpha[e] : co->alpha0;
+      double be = co->beta ? co->beta[e] : co->beta0;
+      if (!(al > 0) || !(be > 0)) {
+        delete h;
+        return fail(HDIV_ERR_COEFFICIENT, "alpha, beta must be > 0");
+      }
+      mw[e] = be; c2[e] = al;
+    } else {
+      double ep = co->eps ? co->eps[e] : co->eps0;
+      double ga = co->gamma ? co->gamma[e] : co->gamma0;
+      if (!(ep > 0) || !(ga >= 0)) {
+        delete h;
+        return fail(HDIV_ERR_COEFFICIENT, "eps > 0 and gamma >= 0 required");
+      }
+      mw[e] = 1.0 / ep; c2[e] = ga;
+      if (ga > 0) any_gamma = true;
+    }
+  }
+  h->has_z = (kind == HDIV_GRAD_DIV) || any_gamma;
+
+  // ---- geometry classification per element (host) ----
+  bool all_box = true, all_affine = true;
+  std::vector<double> coef(4 * E);
+  for (int64_t e = 0; e < E && (all_box || all_affine); ++e) {
+    int64_t ex = e % h->NL[0], ey = (e / h->NL[0]) % h->NL[1], ez = (dim == 3) ? e / (h->NL[0] * h->NL[1]) : 0;
+    double X[8][3];
+    corners(V, dim, h->NL[0], h->NL[1], ex, ey, ez, X);
+    double scale = 0.0;
+    for (int v = 1; v < (1 << dim); ++v)
+      for (int d = 0; d < dim; ++d) scale = std::fmax(scale, std::fabs(X[v][d] - X[0][d]));
+    const double tol = 1e-13 * scale;
+    // parallelogram / parallelepiped: X_v = X_0 + sum of the axis edge vectors
+    for (int v = 3; v < (1 << dim); ++v) {
+      if (v == 4) continue;
+      int a = v & 1, b = (v >> 1) & 1, c = (v >> 2) & 1;
+      for (int d = 0; d < dim; ++d) {
+        double pred = X[0][d] + a * (X[1][d] - X[0][d]) + b * (X[2][d] - X[0][d]) +
+                      (dim == 3 ? c * (X[4][d] - X[0][d]) : 0.0);
+        if (std::fabs(pred - X[v][d]) > tol) all_affine = false;
+      }
+    }
+    // axis-aligned box: edge vectors along the axes
+    double hsz[3] = {X[1][0] - X[0][0], X[2][1] - X[0][1], dim == 3 ? X[4][2] - X[0][2] : 1.0};
+    for (int d = 0; d < dim; ++d) {
+      if (d != 0 && std::fabs(X[1][d] - X[0][d]) > tol) all_box = false;
+      if (d != 1 && std::fabs(X[2][d] - X[0][d]) > tol) all_box = false;
+      if (dim == 3 && d != 2 && std::fabs(X[4][d] - X[0][d]) > tol) all_box = false;
+    }
+    if (!all_affine) all_box = false;
+    for (int d = 0; d < dim; ++d)
+      if (all_box && !(hsz[d] > 0)) {
+        delete h;
+        return fail(HDIV_ERR_INVALID_MESH, "det J <= 0 (inverted box element)");
+      }
+  }
+  h->geom = all_box ? GEOM_BOX : (all_affine ? GEOM_AFFINE : GEOM_TRILINEAR);
+  if (h->has_z && h->geom == GEOM_TRILINEAR) {
+    delete h;
+    return fail(HDIV_ERR_UNSUPPORTED,
+                "W^-1 on non-affine elements (trilinear grad-div / Darcy gamma>0) is NEXT-2");
+  }
+  int want = h->opts.kernel;
+  if (want == 2 && !(dim == 3 && all_box)) {
+    delete h;
+    return fail(HDIV_ERR_UNSUPPORTED, "affine tile kernel needs 3D axis-aligned boxes");
+  }
+  h->kernel = (want == 1) ? 1 : ((dim == 3 && all_box) ? 2 : 1);
+  for (int64_t e = 0; e < E; ++e) {
+    int64_t ex = e % h->NL[0], ey = (e / h->NL[0]) % h->NL[1], ez = (dim == 3) ? e / (h->NL[0] * h->NL[1]) : 0;
+    double X[8][3];
+    corners(V, dim, h->NL[0], h->NL[1], ex, ey, ez, X);
+    double zc = 0.0;
+    if (h->geom != GEOM_TRILINEAR) {
+      double det;
+      double J[3][3] = {{0}};
+      for (int d = 0; d < dim; ++d) {
+        J[d][0] = X[1][d] - X[0][d];
+        J[d][1] = X[2][d] - X[0][d];
+        if (dim == 3) J[d][2] = X[4][d] - X[0][d];
+      }
+      if (dim == 2) det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      else
+        det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+              J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+              J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      if (!(det > 0)) {
+        delete h;
+        return fail(HDIV_ERR_INVALID_MESH, "det J <= 0");
+      }
+      // Z_e = z_e (M_h^-1)^{(x)d}: grad-div det/alpha ; Darcy gamma det
+      zc = (kind == HDIV_GRAD_DIV) ? det / c2[e] : c2[e] * det;
+      if (h->kernel == 2) {
+        double hx = J[0][0], hy = J[1][1], hz = J[2][2];
+        coef[4 * e + 0] = mw[e] * hx / (hy * hz);
+        coef[4 * e + 1] = mw[e] * hy / (hx * hz);
+        coef[4 * e + 2] = mw[e] * hz / (hx * hy);
+        coef[4 * e + 3] = zc;
+        continue;
+      }
+    }
+    coef[4 * e + 0] = mw[e];
+    coef[4 * e + 1] = zc;
+    coef[4 * e + 2] = 0.0;
+    coef[4 * e + 3] = 0.0;
+  }
+  // general-kernel coefficients are needed for the diagonal even on the box path
+  std::vector<double> gcoef(4 * E);
+  for (int64_t e = 0; e < E; ++e) {
+    gcoef[4 * e] = mw[e];
+    gcoef[4 * e + 1] = 0.0;
+    gcoef[4 * e + 2] = gcoef[4 * e + 3] = 0.0;
+  }
+
+  std::string err;
+  if (!build_tables(p, h->Q, &h->tab, &err)) {
+    delete h;
+    return fail(HDIV_ERR_INVALID_ORDER, err);
+  }
+  std::memcpy(h->taff.Ml, h->tab.Ml, sizeof(h->taff.Ml));
+  std::memcpy(h->taff.Mh, h->tab.Mh, sizeof(h->taff.Mh));
+  std::memcpy(h->taff.Mhinv, h->tab.Mhinv, sizeof(h->taff.Mhinv));
+
+#define SETUP_TRY(expr)                                                                  \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                     \
+      hdiv_destroy(h);                                                                   \
+      return HDIV_ERR_CUDA;                                                              \
+    }                                                                                    \
+  } while (0)
+
+  SETUP_TRY(cudaMalloc(&h->d_vert, sizeof(double) * V.size()));
+  SETUP_TRY(cudaMalloc(&h->d_coef, sizeof(double) * 4 * E));
+  SETUP_TRY(cudaMalloc(&h->d_c2, sizeof(double) * E));
+  SETUP_TRY(cudaMalloc(&h->d_mdiag, sizeof(double) * h->nrt));
+  SETUP_TRY(cudaMalloc(&h->d_ctil, sizeof(double) * h->nl2));
+  SETUP_TRY(cudaMemcpyAsync(h->d_vert, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, s));
+  SETUP_TRY(cudaMemcpyAsync(h->d_c2, c2.data(), sizeof(double) * E, cudaMemcpyHostToDevice, s));
+  // the diagonal kernel reads {mass weight} from d_coef: upload general layout first
+  SETUP_TRY(cudaMemcpyAsync(h->d_coef, gcoef.data(), sizeof(double) * 4 * E, cudaMemcpyHostToDevice, s));
+  if (h->geom == GEOM_TRILINEAR) {
+    int* bad = nullptr;
+    SETUP_TRY(cudaMalloc(&bad, sizeof(int)));
+    SETUP_TRY(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    SETUP_TRY(launch_geometry_check(h, bad, s));
+    int hb = 0;
+    SETUP_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SETUP_TRY(cudaStreamSynchronize(s));
+    cudaFree(bad);
+    if (hb) {
+      hdiv_destroy(h);
+      return fail(HDIV_ERR_INVALID_MESH, "det J <= 0 at a quadrature point");
+    }
+  }
+  SETUP_TRY(launch_mass_diag(h, h->d_mdiag, s));
+  SETUP_TRY(launch_ctil(h, h->d_c2, h->d_ctil, s));
+  SETUP_TRY(cudaMemcpyAsync(h->d_coef, coef.data(), sizeof(double) * 4 * E, cudaMemcpyHostToDevice, s));
+  if (nranks > 1) {
+    hdiv_status cs = comm_init(h, nccl_id, s);
+    if (cs != HDIV_OK) { hdiv_destroy(h); return cs; }
+    cs = comm_reverse_add(h, h->d_mdiag, s);   // interface faces: sum of both sides
+    if (cs != HDIV_OK) { hdiv_destroy(h); return cs; }
+  }
+  {
+    hdiv_status ss = build_schur(h, s);
+    if (ss != HDIV_OK) { hdiv_destroy(h); return ss; }
+    if (nranks > 1) {
+      ss = comm_setup_schur_ghosts(h, s);
+      if (ss != HDIV_OK) { hdiv_destroy(h); return ss; }
+    }
+  }
+  SETUP_TRY(cudaStreamSynchronize(s));
+  SETUP_TRY(cudaGetLastError());
+#undef SETUP_TRY
+  *out = h;
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_sizes(hdiv_handle h, int64_t* nrt, int64_t* nl2, int64_t* nrt_g, int64_t* nl2_g) {
+  if (!h) return fail(HDIV_ERR_NULL, "NULL handle");
+  if (nrt) *nrt = h->nrt;
+  if (nl2) *nl2 = h->nl2;
+  if (nrt_g) *nrt_g = h->nrt_g;
+  if (nl2_g) *nl2_g = h->nl2_g;
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* yu, void* stream) {
+  if (!h || !u || !yu) return fail(HDIV_ERR_NULL, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  HDIV_CUDA_TRY(h->kernel == 2 ? launch_affine_apply(h, u, yu, MODE_MASS, nullptr, s)
+                               : launch_general_apply(h, u, yu, MODE_MASS, nullptr, s));
+  if (h->nranks > 1) return comm_reverse_add(h, yu, s);
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_div(hdiv_handle h, const double* u, double* yq, void* stream) {
+  if (!h || !u || !yq) return fail(HDIV_ERR_NULL, "NULL argument");
+  HDIV_CUDA_TRY(launch_div(h, u, yq, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* yu, void* stream) {
+  if (!h || !q || !yu) return fail(HDIV_ERR_NULL, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  HDIV_CUDA_TRY(launch_divT(h, q, yu, s));
+  if (h->nranks > 1) return comm_reverse_add(h, yu, s);
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* stream) {
+  if (!h || !x || !y) return fail(HDIV_ERR_NULL, "NULL argument");
+  HDIV_CUDA_TRY(apply_block_dev(h, x, y, nullptr, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_launches(hdiv_handle h, int* n) {
+  if (!h || !n) return fail(HDIV_ERR_NULL, "NULL argument");
+  *n = (h->kernel == 2) ? 1 : 1;   // general path: one kernel (+ a memset node)
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* xh, double* yh, void* stream) {
+  if (!h || !xh || !yh) return fail(HDIV_ERR_NULL, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * (h->nrt + h->nl2);
+  if (!h->d_xbuf) HDIV_CUDA_TRY(cudaMalloc(&h->d_xbuf, bytes));
+  if (!h->d_ybuf) HDIV_CUDA_TRY(cudaMalloc(&h->d_ybuf, bytes));
+  HDIV_CUDA_TRY(cudaMemcpyAsync(h->d_xbuf, xh, bytes, cudaMemcpyHostToDevice, s));
+  HDIV_CUDA_TRY(apply_block_dev(h, h->d_xbuf, h->d_ybuf, nullptr, s));
+  HDIV_CUDA_TRY(cudaMemcpyAsync(yh, h->d_ybuf, bytes, cudaMemcpyDeviceToHost, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_assemble_mass_diag(hdiv_handle h, double* diag, void* stream) {
+  if (!h || !diag) return fail(HDIV_ERR_NULL, "NULL argument");
+  HDIV_CUDA_TRY(cudaMemcpyAsync(diag, h->d_mdiag, sizeof(double) * h->nrt,
+                                cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_assemble_schur_diag_term(hdiv_handle h, double* ctil, void* stream) {
+  if (!h || !ctil) return fail(HDIV_ERR_NULL, "NULL argument");
+  HDIV_CUDA_TRY(cudaMemcpyAsync(ctil, h->d_ctil, sizeof(double) * h->nl2,
+                                cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_schur_nnz(hdiv_handle h, int64_t* nnz) {
+  if (!h || !nnz) return fail(HDIV_ERR_NULL, "NULL argument");
+  *nnz = h->snnz;
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_assemble_schur_csr(hdiv_handle h, int64_t* rp, int64_t* col, double* val,
+                                    void* stream) {
+  if (!h || !rp || !col || !val) return fail(HDIV_ERR_NULL, "NULL argument");
+  HDIV_CUDA_TRY(launch_schur_export(h, rp, col, val, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_schur(hdiv_handle h, const double* x, double* y, void* stream) {
+  if (!h || !x || !y) return fail(HDIV_ERR_NULL, "NULL argument");
+  if (h->nranks > 1) return fail(HDIV_ERR_UNSUPPORTED, "apply_schur with ghosts: use minres");
+  HDIV_CUDA_TRY(launch_spmv(h, x, y, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_export_div_csr(hdiv_handle h, int64_t* rp, int64_t* col, double* val,
+                                void* stream) {
+  if (!h || !rp || !col || !val) return fail(HDIV_ERR_NULL, "NULL argument");
+  HDIV_CUDA_TRY(launch_div_csr(h, rp, col, val, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_precond(hdiv_handle h, const double* v, double* z, void* stream) {
+  if (!h || !v || !z) return fail(HDIV_ERR_NULL, "NULL argument");
+  return apply_precond(h, v, z, (cudaStream_t)stream);
+}
+
+hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double rtol, int maxit,
+                              hdiv_report* rep, void* stream) {
+  if (!h || !b || !x) return fail(HDIV_ERR_NULL, "NULL argument");
+  if (maxit < 1) return fail(HDIV_ERR_SHAPE, "maxit < 1");
+  return minres(h, b, x, rtol, maxit, rep, (cudaStream_t)stream);
+}
+
+hdiv_status hdiv_debug_tables(int p, int Q, double* xq, double* wq, double* Bl, double* Bh,
+                              double* Ml, double* Mh, double* Mhinv) {
+  Tab1D t;
+  std::string err;
+  if (!build_tables(p, Q, &t, &err)) return fail(HDIV_ERR_INVALID_ORDER, err);
+  for (int q = 0; q < Q; ++q) {
+    if (xq) xq[q] = t.xq[q];
+    if (wq) wq[q] = t.wq[q];
+    for (int i = 0; i <= p; ++i) if (Bl) Bl[q * (p + 1) + i] = t.Bl[q][i];
+    for (int j = 0; j < p; ++j) if (Bh) Bh[q * p + j] = t.Bh[q][j];
+  }
+  for (int i = 0; i <= p; ++i)
+    for (int j = 0; j <= p; ++j) if (Ml) Ml[i * (p + 1) + j] = t.Ml[i][j];
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      if (Mh) Mh[i * p + j] = t.Mh[i][j];
+      if (Mhinv) Mhinv[i * p + j] = t.Mhinv[i][j];
+    }
+  return HDIV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// internal.h — libhdiv internals (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hdiv.h"
+
+namespace hdiv {
+
+constexpr int MAXP = HDIV_MAX_ORDER;
+constexpr int MAXQ = MAXP + 2;
+
+// 1D tables on [0,1].  Passed to kernels by value (__grid_constant__).
+struct Tab1D {
+  int p, Q;
+  double xq[MAXQ], wq[MAXQ];            // Gauss-Legendre rule, Q = p+2 (reading A3)
+  double Bl[MAXQ][MAXP + 1];            // l_i(x_q)   Lagrange on GLL nodes
+  double Bh[MAXQ][MAXP];                // h_j(x_q)   histopolation, h_j = -sum_{i<=j} l_i'
+  double Ml[MAXP + 1][MAXP + 1];        // 1D masses B^T W B
+  double Mh[MAXP][MAXP];
+  double Mhinv[MAXP][MAXP];
+};
+
+// Small table set for the affine (axis-aligned box) kernels.
+struct TabAffine {
+  double Ml[MAXP + 1][MAXP + 1];
+  double Mh[MAXP][MAXP];
+  double Mhinv[MAXP][MAXP];
+};
+
+bool build_tables(int p, int Q, Tab1D* t, std::string* err);
+
+// Geometry kind of the local mesh
+enum GeomKind { GEOM_BOX = 0, GEOM_AFFINE = 1, GEOM_TRILINEAR = 2 };
+
+struct MinresWork;   // solver.cu
+struct Comm;         // comm.cu
+
+}  // namespace hdiv
+
+struct hdiv_ctx {
+  int dim = 3, p = 1, Q = 3;
+  hdiv_kind kind = HDIV_GRAD_DIV;
+  hdiv_options opts{};
+  int64_t N[3] = {1, 1, 1};       // global element counts
+  int64_t NL[3] = {1, 1, 1};      // local element counts (last axis = slab thickness)
+  int64_t ez0 = 0, ez1 = 1;       // slab along the last axis
+  int64_t n[3] = {1, 1, 1};       // local subcell counts n_a = NL_a p
+  int64_t E = 1;                  // local elements
+  int64_t nrt = 0, nl2 = 0, nrt_g = 0, nl2_g = 0;
+  int64_t off[3] = {0, 0, 0};     // RT component offsets (local numbering)
+  int geom = hdiv::GEOM_BOX;
+  bool has_z = true;              // (2,2) block nonzero
+  int kernel = 2;                 // 1 general quadrature kernel, 2 affine tile kernel
+  hdiv::Tab1D tab{};
+  hdiv::TabAffine taff{};
+  // device data
+  double* d_vert = nullptr;       // local vertices [layers][(ny+1)][(nx+1)][dim]
+  double* d_coef = nullptr;       // per element: box {cx, cy, cz, z}; general {w, z, 0, 0}
+  double* d_mdiag = nullptr;      // M~ (assembled, interface-summed)
+  double* d_ctil = nullptr;       // C~
+  double* d_c2 = nullptr;         // per element alpha (grad-div) | gamma (Darcy)
+  double* d_sdinv = nullptr;      // 1 / diag(S~)
+  int64_t* d_srow = nullptr;      // S~ CSR (local rows; ghost columns >= nl2 for multi-GPU)
+  int32_t* d_scol = nullptr;
+  double* d_sval = nullptr;
+  int64_t snnz = 0;
+  double* d_scratch = nullptr;    // reduction partials etc.
+  double* d_xbuf = nullptr;       // host-API staging (lazily allocated)
+  double* d_ybuf = nullptr;
+  int rank = 0, nranks = 1;
+  hdiv::Comm* comm = nullptr;
+  hdiv::MinresWork* mw = nullptr;
+};
+
+// error plumbing
+namespace hdiv {
+void set_error(const std::string& s);
+}
+#define HDIV_CUDA_TRY(expr)                                                           \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess) {                                                          \
+      hdiv::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));            \
+      return HDIV_ERR_CUDA;                                                           \
+    }                                                                                 \
+  } while (0)
+
+namespace hdiv {
+// kernel launchers (return cudaGetLastError())
+cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
+                                const int* skip, cudaStream_t s);
+cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
+                                 const int* skip, cudaStream_t s);
+cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s);
+cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
+                            cudaStream_t s);
+cudaError_t launch_div(const hdiv_ctx* h, const double* u, double* yq, cudaStream_t s);
+cudaError_t launch_divT(const hdiv_ctx* h, const double* q, double* yu, cudaStream_t s);
+cudaError_t launch_mass_diag(const hdiv_ctx* h, double* diag, cudaStream_t s);
+cudaError_t launch_ctil(const hdiv_ctx* h, const double* d_c2, double* ctil, cudaStream_t s);
+cudaError_t launch_geometry_check(const hdiv_ctx* h, int* bad, cudaStream_t s);
+cudaError_t launch_div_csr(const hdiv_ctx* h, int64_t* rp, int64_t* col, double* val,
+                           cudaStream_t s);
+hdiv_status build_schur(hdiv_ctx* h, cudaStream_t s);
+cudaError_t launch_schur_export(const hdiv_ctx* h, int64_t* rp, int64_t* col, double* val,
+                                cudaStream_t s);
+cudaError_t launch_spmv(const hdiv_ctx* h, const double* x, double* y, cudaStream_t s);
+hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t s);
+hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit,
+                   hdiv_report* rep, cudaStream_t s);
+void minres_free(hdiv_ctx* h);
+
+// apply modes
+enum { MODE_MASS = 1, MODE_BLOCK = 2 };
+}  // namespace hdiv

@@ -1,0 +1,435 @@
+// solver.cu — block-diagonal preconditioner and MINRES, device resident.
+//
+// P:411-421 Remark: P = diag(tau M~, S^);  P:668 M~^-1 is diagonal scaling;
+// S^-1 = Chebyshev-Jacobi polynomial on S~ (reading A9/A10; the paper uses one AMG V-cycle,
+// P:889, which is NEXT-1).  P:169 / P:663: MINRES; rtol 1e-12 on the preconditioned
+// residual (reading A8).  Recurrence: Elman-Silvester-Wathen preconditioned MINRES
+// (SURVEY §8(c) step 10), written with the unnormalised z (A z/gamma = (A z)/gamma).
+//
+// Per iteration (all on `stream`, captured in a CUDA graph of 6 iterations so the buffer
+// rotation v(3) / w(3) / z(2) is baked into the graph):
+//   apply_block(z) -> Az                      (kernel_affine / kernel_general)
+//   dot(Az, z) partials -> fin_delta          (delta = <Az,z>/gamma^2)
+//   vupd: v_new, z_new_u = v_new_u/(tau M~), partial <z_u, v_u>
+//   Chebyshev steps on v_new_q -> z_new_q, last step partial <z_q, v_q>
+//   scalar: gamma_new, Givens rotation, eta, convergence flag
+//   wupd: w_new, x += c eta w_new
+// Reductions are two-stage with a fixed grid and a fixed-order final sum -> deterministic.
+// Every kernel reads the device `done` flag and returns early once converged.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace hdiv {
+
+
+namespace {
+
+constexpr int RED_BLOCKS = 148 * 4;
+constexpr int RED_NT = 256;
+
+struct MState {
+  double gamma, gamma_old, eta, gamma1, s, s_old, c, c_old, delta;
+  double wz, wa3, wa2, xc, rtol, rel;
+  int done, iters, maxit, breakdown, conv, pad;
+};
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double red[RED_NT / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = (l < RED_NT / 32) ? red[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  return r;   // valid in thread 0
+}
+
+__global__ void __launch_bounds__(RED_NT)
+dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+           double* __restrict__ part, const int* __restrict__ done) {
+  if (done && *done) return;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT)
+    s = fma(a[i], b[i], s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// fixed-order sum of RED_BLOCKS partials by one block
+__device__ __forceinline__ double sum_partials(const double* part) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < RED_BLOCKS; i += RED_NT) s += part[i];
+  return block_sum(s);
+}
+
+__global__ void __launch_bounds__(RED_NT) fin_delta_kernel(const double* part, MState* st) {
+  if (st->done) return;
+  double s = sum_partials(part);
+  if (threadIdx.x == 0) st->delta = s / (st->gamma * st->gamma);
+}
+
+// v_new = Az/g - (delta/g) v - (g/g_old) v_old ; z_new_u = v_new_u / (tau M~)
+__global__ void __launch_bounds__(RED_NT)
+vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
+            const double* __restrict__ v_old, double* __restrict__ v_new,
+            double* __restrict__ z_new, const double* __restrict__ mdiag, double tau,
+            long long nrt, long long n, const MState* __restrict__ st, double* part) {
+  if (st->done) return;
+  const double g = st->gamma, ig = 1.0 / g;
+  const double cd = st->delta * ig, co = g / st->gamma_old;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    double vn = Az[i] * ig - cd * v[i] - co * v_old[i];
+    v_new[i] = vn;
+    if (i < nrt) {
+      double zn = vn / (tau * mdiag[i]);
+      z_new[i] = zn;
+      s = fma(zn, vn, s);
+    }
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// Chebyshev step k (reading A10): r_new = r - S~ d ; d_new = c1 d + c2 Dinv r_new ; y += d_new
+// first==1: y = d = Dinv r / theta (no SpMV).  `last` adds the partial <y, v>.
+__global__ void __launch_bounds__(RED_NT)
+cheb_first_kernel(const double* __restrict__ rin, const double* __restrict__ dinv, double itheta,
+                  double* __restrict__ d, double* __restrict__ y, long long n, int last,
+                  double* part, const int* __restrict__ done) {
+  if (done && *done) return;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    double di = dinv[i] * rin[i] * itheta;
+    d[i] = di;
+    y[i] = di;
+    if (last) s = fma(di, rin[i], s);
+  }
+  if (last && part) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(RED_NT)
+cheb_step_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                 const double* __restrict__ val, const double* rin, double* rout, const double* __restrict__ d, double* __restrict__ dn,
+                 const double* __restrict__ dinv, double* __restrict__ y, double c1, double c2,
+                 long long n, int last, const double* __restrict__ vin, double* part,
+                 const int* __restrict__ done) {
+  if (done && *done) return;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    double sd = 0.0;
+    for (long long t = rp[i]; t < rp[i + 1]; ++t) sd = fma(val[t], d[col[t]], sd);
+    double r = rin[i] - sd;
+    rout[i] = r;
+    double dd = c1 * d[i] + c2 * dinv[i] * r;
+    dn[i] = dd;
+    double yy = y[i] + dd;
+    y[i] = yy;
+    if (last) s = fma(yy, vin[i], s);
+  }
+  if (last && part) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+// scale z_u = v_u / (tau M~)  (plain preconditioner application)
+__global__ void diag_scale_kernel(const double* __restrict__ v, const double* __restrict__ mdiag,
+                                  double tau, double* __restrict__ z, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) z[i] = v[i] / (tau * mdiag[i]);
+}
+
+__global__ void __launch_bounds__(RED_NT)
+init_kernel(const double* part_u, const double* part_q, MState* st, double rtol, int maxit) {
+  double s = sum_partials(part_u);
+  __syncthreads();
+  double t = sum_partials(part_q);
+  if (threadIdx.x == 0) {
+    double g2 = s + t;
+    MState m{};
+    m.rtol = rtol; m.maxit = maxit;
+    m.gamma_old = 1.0; m.c = 1.0; m.c_old = 1.0; m.s = 0.0; m.s_old = 0.0;
+    if (g2 < 0.0) { m.breakdown = 1; m.done = 1; }
+    double g = std::sqrt(g2 > 0 ? g2 : 0.0);
+    m.gamma = g; m.gamma1 = g; m.eta = g; m.rel = 1.0;
+    if (g == 0.0 && !m.breakdown) { m.done = 1; m.conv = 1; m.rel = 0.0; }
+    *st = m;
+  }
+}
+
+__global__ void __launch_bounds__(RED_NT)
+scalar_kernel(const double* part_u, const double* part_q, MState* st) {
+  if (st->done) return;
+  double s = sum_partials(part_u);
+  __syncthreads();
+  double t = sum_partials(part_q);
+  if (threadIdx.x != 0) return;
+  MState m = *st;
+  double g2 = s + t;
+  if (g2 < 0.0) { m.breakdown = 1; m.done = 1; *st = m; return; }
+  const double gn = std::sqrt(g2);
+  const double delta = m.delta, g = m.gamma;
+  const double a0 = m.c * delta - m.c_old * m.s * g;
+  const double a1 = hypot(a0, gn);
+  const double a2 = m.s * delta + m.c_old * m.c * g;
+  const double a3 = m.s_old * g;
+  const double cn = a0 / a1, sn = gn / a1;
+  m.wz = 1.0 / (g * a1);      // w_new = z/g/a1 - (a3/a1) w_old - (a2/a1) w
+  m.wa3 = a3 / a1;
+  m.wa2 = a2 / a1;
+  m.xc = cn * m.eta;          // x += c_new eta w_new
+  m.eta = -sn * m.eta;
+  m.gamma_old = g; m.gamma = gn;
+  m.c_old = m.c; m.c = cn;
+  m.s_old = m.s; m.s = sn;
+  m.iters += 1;
+  m.rel = fabs(m.eta) / m.gamma1;
+  if (fabs(m.eta) <= m.rtol * m.gamma1 || gn == 0.0) { m.conv = 1; m.done = 2; }
+  else if (m.iters >= m.maxit) m.done = 2;
+  *st = m;
+}
+
+// w_new = wz z - wa3 w_old - wa2 w ;  x += xc w_new.  Runs in the iteration that set done=2
+// (the final update), and is skipped once done == 1 is latched by latch_kernel.
+__global__ void __launch_bounds__(RED_NT)
+wupd_kernel(const double* __restrict__ z, const double* __restrict__ w_old,
+            const double* __restrict__ w, double* __restrict__ w_new, double* __restrict__ x,
+            long long n, const MState* __restrict__ st) {
+  if (st->done == 1) return;
+  const double wz = st->wz, wa3 = st->wa3, wa2 = st->wa2, xc = st->xc;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    double wn = wz * z[i] - wa3 * w_old[i] - wa2 * w[i];
+    w_new[i] = wn;
+    x[i] = fma(xc, wn, x[i]);
+  }
+}
+
+__global__ void latch_kernel(MState* st) {
+  if (threadIdx.x == 0 && st->done == 2) st->done = 1;
+}
+
+inline unsigned nb(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
+
+}  // namespace
+
+struct MinresWork {
+  long long n = 0;
+  double* buf = nullptr;           // all vectors
+  double *v[3], *w[3], *z[2], *Az, *r, *d[2];
+  double *part_a, *part_b;
+  MState* st = nullptr;
+  MState* st_host = nullptr;       // pinned
+  std::vector<double> c1, c2;      // Chebyshev step constants
+  double itheta = 0;
+};
+
+static hdiv_status ensure_work(hdiv_ctx* h) {
+  if (h->mw) return HDIV_OK;
+  auto* mw = new MinresWork();
+  h->mw = mw;
+  const long long n = h->nrt + h->nl2, nq = h->nl2;
+  mw->n = n;
+  size_t tot = 9 * (size_t)n + 3 * (size_t)nq + 2 * RED_BLOCKS;
+  HDIV_CUDA_TRY(cudaMalloc(&mw->buf, tot * sizeof(double)));
+  double* p = mw->buf;
+  for (int i = 0; i < 3; ++i) { mw->v[i] = p; p += n; }
+  for (int i = 0; i < 3; ++i) { mw->w[i] = p; p += n; }
+  for (int i = 0; i < 2; ++i) { mw->z[i] = p; p += n; }
+  mw->Az = p; p += n;
+  mw->r = p; p += nq;
+  for (int i = 0; i < 2; ++i) { mw->d[i] = p; p += nq; }
+  mw->part_a = p; p += RED_BLOCKS;
+  mw->part_b = p; p += RED_BLOCKS;
+  HDIV_CUDA_TRY(cudaMalloc(&mw->st, sizeof(MState)));
+  HDIV_CUDA_TRY(cudaMallocHost(&mw->st_host, sizeof(MState)));
+  // Chebyshev constants on [lmax/ratio, lmax], lmax = 2 (reading A10)
+  const int k = h->opts.cheb_degree;
+  const double lmax = 2.0, a = lmax / h->opts.cheb_ratio, b = lmax;
+  const double theta = 0.5 * (a + b), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  mw->itheta = 1.0 / theta;
+  for (int i = 1; i < k; ++i) {
+    double rn = 1.0 / (2.0 * sigma - rho);
+    mw->c1.push_back(rn * rho);
+    mw->c2.push_back(2.0 * rn / delta);
+    rho = rn;
+  }
+  return HDIV_OK;
+}
+
+void minres_free(hdiv_ctx* h) {
+  if (!h->mw) return;
+  cudaFree(h->mw->buf);
+  cudaFree(h->mw->st);
+  cudaFreeHost(h->mw->st_host);
+  delete h->mw;
+  h->mw = nullptr;
+}
+
+// Chebyshev-Jacobi S^-1 applied to vq -> y (uses mw->r, mw->d); partial <y, vq> if part
+static cudaError_t cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
+                              const int* done, cudaStream_t s) {
+  MinresWork* mw = h->mw;
+  const long long n = h->nl2;
+  const int k = h->opts.cheb_degree;
+  cheb_first_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0], y, n,
+                                                  k == 1, part, done);
+  const double* rin = vq;
+  for (int i = 1; i < k; ++i) {
+    cheb_step_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_srow, h->d_scol, h->d_sval, rin, mw->r,
+                                                   mw->d[(i - 1) & 1], mw->d[i & 1], h->d_sdinv,
+                                                   y, mw->c1[i - 1], mw->c2[i - 1], n, i == k - 1,
+                                                   vq, part, done);
+    rin = mw->r;
+  }
+  return cudaGetLastError();
+}
+
+hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t s) {
+  hdiv_status st = ensure_work(h);
+  if (st != HDIV_OK) return st;
+  diag_scale_kernel<<<nb(h->nrt, 256), 256, 0, s>>>(v, h->d_mdiag, h->opts.tau, z, h->nrt);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  HDIV_CUDA_TRY(cheb_apply(h, v + h->nrt, z + h->nrt, nullptr, nullptr, s));
+  return HDIV_OK;
+}
+
+static cudaError_t apply_A(hdiv_ctx* h, const double* x, double* y, const int* skip,
+                           cudaStream_t s);
+
+hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit,
+                   hdiv_report* rep, cudaStream_t s) {
+  hdiv_status stt = ensure_work(h);
+  if (stt != HDIV_OK) return stt;
+  MinresWork* mw = h->mw;
+  const long long n = mw->n, nrt = h->nrt;
+  const int* done = &mw->st->done;
+  cudaEvent_t e0, e1;
+  HDIV_CUDA_TRY(cudaEventCreate(&e0));
+  HDIV_CUDA_TRY(cudaEventCreate(&e1));
+  HDIV_CUDA_TRY(cudaEventRecord(e0, s));
+  // x0 = 0, v0 = 0 (v_old), w0 = w1 = 0, v1 = b, z1 = P^-1 v1, gamma1 = sqrt(<z1, v1>)
+  HDIV_CUDA_TRY(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  HDIV_CUDA_TRY(cudaMemsetAsync(mw->v[0], 0, n * sizeof(double), s));
+  HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[0], 0, n * sizeof(double), s));
+  HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[1], 0, n * sizeof(double), s));
+  HDIV_CUDA_TRY(cudaMemcpyAsync(mw->v[1], b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  {
+    // z_u and partial <z_u, v_u>, then Chebyshev with partial <z_q, v_q>
+    diag_scale_kernel<<<nb(nrt, 256), 256, 0, s>>>(mw->v[1], h->d_mdiag, h->opts.tau, mw->z[0],
+                                                   nrt);
+    dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->z[0], mw->v[1], nrt, mw->part_a, nullptr);
+    HDIV_CUDA_TRY(cheb_apply(h, mw->v[1] + nrt, mw->z[0] + nrt, mw->part_b, nullptr, s));
+    init_kernel<<<1, RED_NT, 0, s>>>(mw->part_a, mw->part_b, mw->st, rtol, maxit);
+    HDIV_CUDA_TRY(cudaGetLastError());
+  }
+  // one iteration j: buffers (v_old, v, v_new) = v[(j-1)%3], v[j%3], v[(j+1)%3]
+  //                  (w_old, w, w_new)  = w[(j-1)%3], w[j%3], w[(j+1)%3]
+  //                  (z, z_new)         = z[(j-1)%2], z[j%2]
+  auto iteration = [&](int j) -> cudaError_t {
+    double* vo = mw->v[(j + 2) % 3];
+    double* vc = mw->v[j % 3];
+    double* vn = mw->v[(j + 1) % 3];
+    double* wo = mw->w[(j + 2) % 3];
+    double* wc = mw->w[j % 3];
+    double* wn = mw->w[(j + 1) % 3];
+    double* zc = mw->z[(j + 1) % 2];
+    double* zn = mw->z[j % 2];
+    cudaError_t e = apply_A(h, zc, mw->Az, done, s);
+    if (e != cudaSuccess) return e;
+    dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, zc, n, mw->part_a, done);
+    fin_delta_kernel<<<1, RED_NT, 0, s>>>(mw->part_a, mw->st);
+    vupd_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
+                                              nrt, n, mw->st, mw->part_a);
+    e = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s);
+    if (e != cudaSuccess) return e;
+    scalar_kernel<<<1, RED_NT, 0, s>>>(mw->part_a, mw->part_b, mw->st);
+    wupd_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(zc, wo, wc, wn, x, n, mw->st);
+    latch_kernel<<<1, 32, 0, s>>>(mw->st);
+    return cudaGetLastError();
+  };
+  // capture 6 iterations (j = 1..6 pattern repeats with period 6)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool use_graph = true;
+  {
+    cudaStream_t cs = s;
+    cudaStreamCaptureStatus cst;
+    if (cudaStreamIsCapturing(cs, &cst) != cudaSuccess || cst != cudaStreamCaptureStatusNone)
+      use_graph = false;
+  }
+  if (use_graph) {
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      use_graph = false;
+    } else {
+      cudaError_t e = cudaSuccess;
+      for (int j = 1; j <= 6 && e == cudaSuccess; ++j) e = iteration(j);
+      cudaError_t ec = cudaStreamEndCapture(s, &graph);
+      if (e != cudaSuccess || ec != cudaSuccess ||
+          cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        use_graph = false;
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        graph = nullptr;
+      }
+    }
+  }
+  int launched = 0;
+  for (;;) {
+    if (use_graph) {
+      HDIV_CUDA_TRY(cudaGraphLaunch(exec, s));
+    } else {
+      for (int j = 1; j <= 6; ++j) {
+        cudaError_t e = iteration(j);
+        if (e != cudaSuccess) { hdiv::set_error(cudaGetErrorString(e)); return HDIV_ERR_CUDA; }
+      }
+    }
+    launched += 6;
+    HDIV_CUDA_TRY(cudaMemcpyAsync(mw->st_host, mw->st, sizeof(MState), cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    if (mw->st_host->done || launched >= maxit + 6) break;
+  }
+  HDIV_CUDA_TRY(cudaEventRecord(e1, s));
+  HDIV_CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  MState m = *mw->st_host;
+  if (rep) {
+    rep->iters = m.iters;
+    rep->converged = m.conv;
+    rep->rel_resid = m.rel;
+    rep->t_solve_ms = ms;
+  }
+  if (m.breakdown) return HDIV_ERR_BREAKDOWN;
+  return HDIV_OK;
+}
+
+cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
+                            cudaStream_t s);   // api.cu
+
+static cudaError_t apply_A(hdiv_ctx* h, const double* x, double* y, const int* skip,
+                           cudaStream_t s) {
+  return apply_block_dev(h, x, y, skip, s);
+}
+
+}  // namespace hdiv

@@ -30,15 +30,23 @@ def _splitmix(z: np.ndarray) -> np.ndarray:
 
 def counter_uniform(seed: int, n: int, offset: int = 0) -> np.ndarray:
     """n uniforms in [0,1): u_i = splitmix64(seed*G + (offset+i+1)*G) >> 11 * 2^-53."""
+    out = np.empty(n, dtype=np.float64)
+    chunk = 1 << 24
     with np.errstate(over="ignore"):
-        idx = np.arange(offset + 1, offset + n + 1, dtype=np.uint64)
         s = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) * _GOLDEN
-        z = _splitmix(s + idx * _GOLDEN)
-    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        for c0 in range(0, n, chunk):
+            c1 = min(n, c0 + chunk)
+            idx = np.arange(offset + c0 + 1, offset + c1 + 1, dtype=np.uint64)
+            z = _splitmix(s + idx * _GOLDEN)
+            out[c0:c1] = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return out
 
 
 def random_vector(n: int, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
-    return lo + (hi - lo) * counter_uniform(seed, n)
+    u = counter_uniform(seed, n)
+    u *= (hi - lo)
+    u += lo
+    return u
 
 
 def cartesian_vertices(dim: int, N, lo=None, hi=None) -> np.ndarray:

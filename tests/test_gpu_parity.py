@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle, element by element, on the
+same seeded inputs (north_star bars: D / CSR structure bit-exact; applies and diagonals 1e-12
+relative per block; S~ values 1e-10; MINRES iteration counts +-1)."""
+import numpy as np
+import pytest
+
+from synth import make_config, random_vector, Problem, cartesian_vertices, graded_two_material
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _rel(a, b):
+    d = np.abs(np.asarray(a) - np.asarray(b)).max()
+    s = np.abs(np.asarray(b)).max()
+    return d / s if s > 0 else d
+
+
+def _gpu(prob, **kw):
+    from paper_2304_12387_b200 import from_problem
+    return from_problem(prob, **kw)
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _host(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# small cases spanning several tiles with ragged tails (tile sizes: p1 8^3, p2 8x8x4,
+# p3 4^3, p4 4x4x2, p5 4x2x2, p6 2^3)
+CASES = [
+    ("c1", None, None, 0),                 # 2D 4x4 p=2 Darcy (config 1), general kernel
+    ("c1", (5, 3), 3, 0),                  # 2D ragged
+    ("c2", (3, 2, 2), 3, 0),               # 3D box, affine tile kernel
+    ("c2", (5, 3, 6), 2, 0),
+    ("c2", (9, 5, 3), 1, 0),
+    ("c2", (5, 3, 3), 4, 0),
+    ("c2", (5, 3, 3), 5, 0),
+    ("c2", (3, 3, 3), 6, 0),
+    ("c2", (5, 3, 3), 4, 1),               # same, forced general kernel
+    ("c3", (3, 2, 3), 2, 0),               # trilinear Darcy gamma = 0, general kernel
+    ("c3", (2, 3, 2), 4, 0),
+    ("c5", (5, 4, 3), 3, 0),               # graded two-material, box kernel
+]
+
+
+def _problem(name, N, p):
+    pr = make_config(name, N=N, p=p)
+    if name == "c2":   # heterogeneous coefficients so per-element weights matter
+        pr.alpha = 10.0 ** random_vector(pr.E, 31)
+        pr.beta = 10.0 ** random_vector(pr.E, 32)
+    return pr
+
+
+@pytest.mark.parametrize("name,N,p,kernel", CASES)
+def test_block_apply_parity(name, N, p, kernel):
+    from oracle import operators
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr, with_schur=False)
+    op = _gpu(pr, kernel=kernel)
+    s = op.sizes
+    assert (s.n_rt, s.n_l2) == (A.n_rt, A.n_l2)
+    x = random_vector(s.n, 7)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL
+    assert _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    # the Z q~ term alone (u = 0), measured separately
+    x0 = x.copy()
+    x0[:s.n_rt] = 0
+    y0 = _host(op.apply_block(_dev(x0)))
+    yo0 = A.apply_block(x0)
+    assert _rel(y0[s.n_rt:], yo0[s.n_rt:]) < TOL
+    # mass, D, D^T separately
+    u = x[:s.n_rt]
+    q = x[s.n_rt:]
+    assert _rel(_host(op.apply_mass(_dev(u))), A.M @ u) < TOL
+    assert np.array_equal(_host(op.apply_div(_dev(u))), A.D @ u) or \
+        _rel(_host(op.apply_div(_dev(u))), A.D @ u) < 1e-15
+    assert _rel(_host(op.apply_divT(_dev(q))), A.D.T @ q) < 1e-15
+    # determinism: bitwise identical repeat
+    y2 = _host(op.apply_block(_dev(x)))
+    assert np.array_equal(y, y2)
+
+
+@pytest.mark.parametrize("name,N,p,kernel", CASES[:8] + CASES[9:])
+def test_setup_objects_parity(name, N, p, kernel):
+    """diag(M) (1e-12), C~, D CSR (bit-exact), S~ CSR structure (bit-exact) and values (1e-10)."""
+    from oracle import operators
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    op = _gpu(pr, kernel=kernel)
+    assert _rel(_host(op.mass_diag()), A.Mdiag) < TOL
+    assert _rel(_host(op.schur_diag_term()), A.Ctil) < TOL
+    rp, col, val = [_host(t) for t in op.div_csr()]
+    assert np.array_equal(rp, A.Dptr) and np.array_equal(col, A.Dcol)
+    assert np.array_equal(val, A.Dval)
+    rp, col, val = [_host(t) for t in op.schur_csr()]
+    S = A.S.tocsr()
+    S.sort_indices()
+    assert np.array_equal(rp, S.indptr) and np.array_equal(col, S.indices)
+    assert _rel(val, S.data) < 1e-10
+    xq = random_vector(A.n_l2, 5)
+    assert _rel(_host(op.apply_schur(_dev(xq))), S @ xq) < 1e-12
+
+
+@pytest.mark.parametrize("name,N,p", [("c1", None, None), ("c2", (2, 2, 2), 2),
+                                      ("c3", (2, 2, 2), 2), ("c2", (3, 2, 2), 3)])
+def test_preconditioner_and_minres_parity(name, N, p):
+    from oracle import operators, solvers
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    op = _gpu(pr, tau=1.0, cheb_degree=4, cheb_ratio=30.0)
+    n = A.n_rt + A.n_l2
+    v = random_vector(n, 3)
+    P = solvers.BlockDiagPrecond(A, tau=1.0, degree=4, ratio=30.0)
+    z = _host(op.apply_precond(_dev(v)))
+    zo = P.apply(v)
+    assert _rel(z[:A.n_rt], zo[:A.n_rt]) < TOL
+    assert _rel(z[A.n_rt:], zo[A.n_rt:]) < 1e-11
+    xs = random_vector(n, 1)
+    b = A.apply_block(xs)
+    xo, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=2000)
+    x, rep = op.minres(_dev(b), rtol=1e-12, maxit=2000)
+    x = _host(x)
+    assert conv_o and rep.converged
+    assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    assert _rel(x, xo) < 1e-9
+
+
+def test_config2_minres_full():
+    """Config 2 (8^3, p=3, grad-div): MINRES to 1e-12, iteration count within +-1 of the oracle,
+    solution against the known x*."""
+    from oracle import operators, solvers
+    pr = make_config("c2")
+    A = operators.Assembled(pr)
+    n = A.n_rt + A.n_l2
+    xs = random_vector(n, 2)
+    b = A.apply_block(xs)
+    P = solvers.BlockDiagPrecond(A)
+    xo, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=3000)
+    op = _gpu(pr)
+    x, rep = op.minres(_dev(b), rtol=1e-12, maxit=3000)
+    assert rep.converged and conv_o
+    assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    assert _rel(_host(x), xs) < 1e-7
+
+
+@pytest.mark.parametrize("name,p", [("c4", 4), ("c3", 4)])
+def test_full_size_sampled_parity(name, p):
+    """BASELINE full sizes (config 4: 128^3 p=4 grad-div; config 3: 64^3 p=4 perturbed Darcy) in
+    the launch configuration bench.py times; sampled outputs computed one by one by the oracle
+    from the element matrices of the touching elements."""
+    from oracle import sample
+    pr = make_config(name)
+    if name == "c4":
+        pr.alpha = 10.0 ** random_vector(pr.E, 41)   # heterogeneous, exercises per-element c_e
+        pr.beta = 10.0 ** random_vector(pr.E, 42)
+    op = _gpu(pr)
+    s = op.sizes
+    x = random_vector(s.n, 9)
+    y = _host(op.apply_block(_dev(x)))
+    rng = np.random.default_rng(0)
+    n_rt, n_l2 = s.n_rt, s.n_l2
+    rt_rows = np.concatenate([[0, n_rt - 1], rng.integers(0, n_rt, 60)])
+    l2_rows = np.concatenate([[0, n_l2 - 1], rng.integers(0, n_l2, 30)])
+    yu, yq = sample.block_apply_rows(pr, x, rt_rows, l2_rows)
+    scale_u = np.abs(yu).max()
+    scale_q = np.abs(yq).max()
+    assert np.abs(y[rt_rows] - yu).max() < TOL * scale_u * 10
+    assert np.abs(y[n_rt + l2_rows] - yq).max() < TOL * scale_q * 10
