@@ -1,0 +1,372 @@
+"""bench.py — BASELINE.json metric: GDOF/s of the fp64 matrix-free H(div) block-operator apply
+(plus MINRES time-to-solve), on synthetic inputs, through libhdiv's C-ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--p 4] [--impl reference]
+
+A step is one block-operator apply y = A x over the whole workload (default
+config 4: 128^3 Cartesian hexes, p = 4, grad-div, 537.7M DOFs; inputs 4.3 GB per vector,
+i.e. much larger than the 126 MB L2, so no flush is needed).  N > 1: element slabs along z,
+one rank per GPU (torchrun), interface reverse-add over NCCL inside each apply; the timed
+region is bracketed by barrier + synchronize and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GDOF/s of matrix-free H(div) block-operator apply, p=2–6; MINRES time-to-solve"
+WORKLOADS = {
+    "c4": "config 4: 3D 128^3 Cartesian hex mesh, RT p / L2 p-1 (default p=4), grad-div "
+          "alpha=beta=1, block-operator apply [M, D^T; D, -W_alpha^-1]",
+    "c3": "config 3: 3D 64^3 randomly perturbed hex mesh, p=4, Darcy eps=10^U(-2,2), gamma=0",
+    "c5": "config 5: graded two-material crooked-pipe analogue, grad-div",
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_problem(cfg: str, p: int):
+    from synth import make_config
+    return make_config(cfg, p=p)
+
+
+def slab_bounds(Nz: int, ws: int, rank: int):
+    base, rem = divmod(Nz, ws)
+    z0 = rank * base + min(rank, rem)
+    return z0, z0 + base + (1 if rank < rem else 0)
+
+
+def sliced_problem_arrays(pr, z0, z1):
+    """Vertex layers z0..z1 and per-element coefficients of the slab (inputs only)."""
+    V = pr.vertices[z0:z1 + 1]
+    Ex = pr.N[0] * pr.N[1]
+    sl = slice(z0 * Ex, z1 * Ex)
+    pick = lambda a: None if a is None else a[sl]
+    return V, pick(pr.alpha), pick(pr.beta), pick(pr.gamma), pick(pr.eps)
+
+
+def build_operator(pr, ws, rank, dist, nccl_id=None):
+    from paper_2304_12387_b200 import HdivOperator
+    if ws == 1:
+        from paper_2304_12387_b200 import from_problem
+        return from_problem(pr)
+    z0, z1 = slab_bounds(pr.N[2], ws, rank)
+    V, a, b, g, e = sliced_problem_arrays(pr, z0, z1)
+    return HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b, gamma=g, eps=e,
+                        slab=(z0, z1), nccl_id=nccl_id, rank=rank, nranks=ws)
+
+
+def time_applies(op, x, y, steps, warmup, dist, torch):
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        op.apply_block(x, y)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        op.apply_block(x, y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def cpu_baseline(pr, budget_s: float = 15.0):
+    """Time the oracle (as it stands) on a bounded sample of the workload's elements."""
+    import numpy as np
+    from oracle import sample
+    from synth import random_vector
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    n = pr.n_rt() + pr.n_l2()
+    E = pr.E
+    x = random_vector(n, 9) if n < 2e8 else None
+    if x is None:   # only the sampled elements' entries are touched; use a cheap stand-in
+        x = np.zeros(n)
+    rng = np.random.default_rng(0)
+    elems = rng.integers(0, E, 100000)
+    t0 = time.perf_counter()
+    done = 0
+    while time.perf_counter() - t0 < budget_s and done < len(elems):
+        sample.element_apply(pr, x, elems[done:done + 8])
+        done += 8
+    dt = time.perf_counter() - t0
+    dofs = n * done / E
+    return {"value": dofs / dt / 1e9, "unit": "GDOF/s", "cores": int(cores), "kind": "oracle",
+            "sample": f"{done} of {E} elements of {pr.name} p={pr.p} (element matrices by "
+                      f"direct quadrature + multiply), {dt:.1f} s, scaled to whole-apply DOFs"}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the oracle, as it stands, on the host cores; rank 0 only."""
+    if rank != 0:
+        return
+    pr = make_problem(args.config, args.p)
+    n = pr.n_rt() + pr.n_l2()
+    per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(pr, budget_s=1.0)
+    vals = [cpu_baseline(pr, budget_s=per_step_budget) for _ in range(args.steps)]
+    v = sorted(x["value"] for x in vals)[len(vals) // 2]
+    cb = dict(vals[0])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GDOF/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": n / (v * 1e9) * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS.get(args.config, args.config), "p": pr.p,
+                       "N_RT": pr.n_rt(), "N_L2": pr.n_l2(),
+                       "note": "each step: oracle element-by-element apply on a bounded "
+                               "sample, scaled to the whole workload"},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--impl", default="hdiv", choices=["hdiv", "reference"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-minres", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if ws > 1:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+        from paper_2304_12387_b200.binding import nccl_unique_id
+        idl = [nccl_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(idl, src=0)
+        nccl_id = idl[0]
+
+    from paper_2304_12387_b200.binding import nccl_unique_id  # noqa: F401 (import check)
+    pr = make_problem(args.config, args.p)
+    n_glob = pr.n_rt() + pr.n_l2()
+    t0 = time.time()
+    op = build_operator(pr, ws, rank, dist, nccl_id)
+    t_setup = time.time() - t0
+    s = op.sizes
+    x = torch.rand(s.n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+
+    clk = ClockSampler(local)
+    clk.start()
+    ms = time_applies(op, x, y, args.steps, args.warmup, dist, torch)
+    clocks = clk.stop()
+    ms_step = ms / args.steps
+    value = n_glob / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (the block-apply kernel: 1 launch per step on one GPU)
+    peak, peak_src = _peaks()
+    E_loc = op.sizes.n_l2 // (pr.p ** pr.dim)
+    alg_bytes = 16 * s.n + 32 * E_loc        # read x, write y, 4 coefficients per element
+    launches = op.apply_launches()
+    achieved = alg_bytes / (ms_step * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        key = f"{args.config}_p{pr.p}"
+        if key in tr and ws == 1:
+            traffic = tr[key]["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "affine_apply_kernel (fused block apply)" if pr.affine else
+                          "general_kernel (quadrature block apply)",
+                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
+
+    # end-to-end through the C-ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        xh = torch.empty(s.n, dtype=torch.float64, pin_memory=True)
+        yh = torch.empty(s.n, dtype=torch.float64, pin_memory=True)
+        xh.copy_(x.cpu())
+        op.apply_block_host(xh, yh)
+        if dist is not None:
+            dist.barrier()
+        t1 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            op.apply_block_host(xh, yh)
+        te = time.perf_counter() - t1
+        if dist is not None:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": n_glob * args.e2e_steps / te / 1e9, "unit": "GDOF/s",
+               "h2d_bytes_per_step": 8 * s.n, "d2h_bytes_per_step": 8 * s.n,
+               "note": "hdiv_apply_block_host: pinned H2D copy + apply + D2H copy per step"}
+        del xh, yh
+
+    result = {"metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws,
+              "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+              "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+              "dtype": "f64", "data": "synthetic",
+              "config": {"workload": WORKLOADS.get(args.config, args.config), "p": pr.p,
+                         "N": list(pr.N), "N_RT": pr.n_rt(), "N_L2": pr.n_l2(),
+                         "global_dofs": n_glob, "parallelism": f"z-slabs x{ws}",
+                         "l2_flush": "inputs larger than L2 (%.2f GB per vector vs 126 MB)"
+                                     % (8 * n_glob / 1e9),
+                         "setup_s": round(t_setup, 2)},
+              "roofline": roofline, "e2e": e2e, "gpu_launches": launches * args.steps,
+              "clocks": clocks}
+
+    del x, y
+    op.close()
+    torch.cuda.empty_cache()
+
+    # p sweep (1 GPU): GDOF/s for p = 2..6 on meshes that fill a similar memory footprint
+    if not args.no_sweep and ws == 1 and args.config == "c4":
+        sweep = {}
+        for p in (2, 3, 4, 5, 6):
+            Nn = {2: 160, 3: 128, 4: 128, 5: 96, 6: 80}[p]
+            from synth import make_config
+            prp = make_config("c4", N=(Nn, Nn, Nn), p=p)
+            opp = build_operator(prp, 1, 0, None)
+            xs = torch.rand(opp.sizes.n, dtype=torch.float64, device="cuda")
+            ys = torch.empty_like(xs)
+            msp = time_applies(opp, xs, ys, 30, 5, None, torch) / 30
+            nn = opp.sizes.n
+            ab = 16 * nn + 32 * prp.E
+            sweep[f"p{p}"] = {"N": Nn, "dofs": nn, "ms": msp, "GDOF_s": nn / msp / 1e6,
+                              "hbm_frac": ab / (msp * 1e-3) / 1e9 / peak}
+            del xs, ys
+            opp.close()
+            torch.cuda.empty_cache()
+        result["sweep"] = sweep
+
+    # MINRES time-to-solve (config 2: 8^3 p=3 grad-div, rtol 1e-12, x0 = 0)
+    if not args.no_minres and ws == 1:
+        from synth import make_config, random_vector
+        pr2 = make_config("c2")
+        op2 = build_operator(pr2, 1, 0, None)
+        xs = torch.from_numpy(random_vector(op2.sizes.n, 2)).cuda()
+        b = op2.apply_block(xs)
+        op2.minres(b, rtol=1e-12, maxit=5000)   # warm-up (graph build)
+        _, rep = op2.minres(b, rtol=1e-12, maxit=5000)
+        result["minres"] = {"workload": "config 2: 8^3 Cartesian, p=3, grad-div alpha=beta=1, "
+                                        "b = A x*, rtol 1e-12 (P:899), x0 = 0",
+                            "iters": rep.iters, "converged": bool(rep.converged),
+                            "time_to_solve_s": rep.t_solve_ms / 1e3,
+                            "preconditioner": "diag(tau M~) + Chebyshev-Jacobi(S~), degree 4"}
+        op2.close()
+
+    if rank == 0 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(pr)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

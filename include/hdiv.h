@@ -144,6 +144,11 @@ hdiv_status hdiv_apply_precond(hdiv_handle h, const double* v, double* z, void* 
 hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double rtol,
                               int maxit, hdiv_report* report, void* stream);
 
+/* Multi-GPU helper: writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the
+ * bytes, e.g. with torch.distributed, before every rank calls hdiv_setup).  NCCL is resolved
+ * at run time (dlopen); HDIV_ERR_NCCL if it is unavailable. */
+hdiv_status hdiv_nccl_unique_id(void* out, int64_t len);
+
 /* Diagnostic, host only (no GPU needed): the library's 1D tables for order p with Q points
  * (reading A3: Q = p+2).  Outputs (caller-owned host arrays): xq[Q], wq[Q] Gauss-Legendre on
  * [0,1]; Bl[Q][p+1] = l_i(x_q); Bh[Q][p] = h_j(x_q); Ml[(p+1)^2], Mh[p^2], Mhinv[p^2]. */

@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
         "hdiv_apply_precond": (C.c_int, [vp, dp, dp, vp]),
         "hdiv_minres_solve": (C.c_int, [vp, dp, dp, C.c_double, C.c_int, C.POINTER(Report), vp]),
         "hdiv_debug_tables": (C.c_int, [C.c_int, C.c_int] + [dp] * 7),
+        "hdiv_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -96,6 +97,14 @@ def _check(code: int):
     if code != 0:
         msg = _lib.hdiv_last_error().decode()
         raise HdivError(code, msg)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from the library (rank 0 creates it and broadcasts the bytes)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    _check(lib.hdiv_nccl_unique_id(C.cast(buf, C.c_void_p), 128))
+    return buf.raw
 
 
 def debug_tables(p: int, Q: int = 0) -> dict:

@@ -59,7 +59,7 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
     objs = [_obj(s) for s in SOURCES]
     if force or todo or not os.path.exists(LIB) or any(
             os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-cudart", "static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-cudart", "static"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,38 +1,226 @@
-// comm.cu — multi-GPU plumbing (element slabs along the last axis, NCCL over NVLink).
-// Round-1 placeholder: the slab path is implemented in the next step; single-GPU never
-// reaches these functions.
+// comm.cu — multi-GPU plumbing: element slabs along the last axis (z in 3D, y in 2D), one
+// rank per GPU, NCCL over NVLink/NVSwitch.
+//
+//  * Interface face plane (the last-axis faces at the slab boundary) is replicated on both
+//    ranks.  After a local apply each rank holds its own partial sum there; comm_reverse_add
+//    exchanges the two partials (ncclSend/ncclRecv in one group) and adds them: a+b = b+a, so
+//    both replicas stay bitwise identical.
+//  * S~ couples L2 cells across the interface (face-neighbour stencil): the SpMV
+//    reads a ghost layer of n_x n_y cells per interface, refreshed by comm_l2_ghosts.
+//  * Dot products: the interface plane is owned by the lower rank (the upper rank masks its
+//    bottom plane); each rank reduces locally in a fixed order, the P scalars are all-gathered
+//    and summed in rank order on every rank -> identical on all ranks, independent of the NCCL
+//    algorithm.
+// NCCL is resolved with dlopen at first use, so libhdiv has no link-time NCCL dependency and
+// shares the copy already loaded by the process (torch's).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
+
+#include <cstring>
 
 #include "internal.h"
 
 namespace hdiv {
 
+namespace {
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl(std::string* err) {
+  if (g_nccl.lib) return true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  void* lib = nullptr;
+  for (const char* n : names) {
+    lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (lib) break;
+  }
+  if (!lib) { *err = std::string("dlopen libnccl failed: ") + dlerror(); return false; }
+#define LOADSYM(field, name)                                                   \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(lib, name));   \
+  if (!g_nccl.field) { *err = std::string("missing NCCL symbol ") + name; return false; }
+  LOADSYM(GetUniqueId, "ncclGetUniqueId");
+  LOADSYM(CommInitRank, "ncclCommInitRank");
+  LOADSYM(CommDestroy, "ncclCommDestroy");
+  LOADSYM(Send, "ncclSend");
+  LOADSYM(Recv, "ncclRecv");
+  LOADSYM(GroupStart, "ncclGroupStart");
+  LOADSYM(GroupEnd, "ncclGroupEnd");
+  LOADSYM(AllGather, "ncclAllGather");
+  LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+  g_nccl.lib = lib;
+  return true;
+}
+
+__global__ void add_planes_kernel(double* lo, const double* rlo, double* hi, const double* rhi,
+                                  long long m) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  if (lo) lo[i] += rlo[i];
+  if (hi) hi[i] += rhi[i];
+}
+
+// cells of the bottom (c = 0 of element layer 0) / top (c = p-1 of the last layer) subcell
+// layer, ordered by subcell (X [, Y]) -> send buffers
+__global__ void pack_l2_layers_kernel(const double* __restrict__ x, double* lo, double* hi,
+                                      long long NLx, long long NLy, long long NLz, int p, int dim,
+                                      long long m) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  if (dim == 3) {
+    long long nx = NLx * p;
+    long long X = i % nx, Y = i / nx;
+    long long ex = X / p, ey = Y / p, a = X % p, b = Y % p;
+    long long pd = (long long)p * p * p;
+    if (lo) lo[i] = x[(ex + NLx * ey) * pd + a + p * b];
+    if (hi) hi[i] = x[(ex + NLx * (ey + NLy * (NLz - 1))) * pd + a + p * (b + p * (p - 1))];
+  } else {
+    long long X = i;
+    long long ex = X / p, a = X % p;
+    long long pd = (long long)p * p;
+    if (lo) lo[i] = x[ex * pd + a];
+    if (hi) hi[i] = x[(ex + NLx * (NLy - 1)) * pd + a + p * (p - 1)];
+  }
+}
+}  // namespace
+
 struct Comm {
   ncclComm_t comm = nullptr;
+  int rank = 0, P = 1;
+  long long plane = 0;      // RT interface plane size (faces)
+  long long lplane = 0;     // L2 ghost layer size (cells)
+  double* buf = nullptr;    // recv_lo, recv_hi (RT) ; send_lo, send_hi (L2)
+  double *rlo, *rhi, *slo, *shi;
 };
 
+static hdiv_status nccl_fail(ncclResult_t r, const char* what) {
+  set_error(std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+  return HDIV_ERR_NCCL;
+}
+
 hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s) {
-  (void)h; (void)id; (void)s;
-  set_error("multi-GPU slabs not built yet");
-  return HDIV_ERR_UNSUPPORTED;
+  (void)s;
+  std::string err;
+  if (!load_nccl(&err)) { set_error(err); return HDIV_ERR_NCCL; }
+  auto* c = new Comm();
+  h->comm = c;
+  c->rank = h->rank;
+  c->P = h->nranks;
+  c->plane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
+  c->lplane = c->plane;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclResult_t r = g_nccl.CommInitRank(&c->comm, c->P, uid, c->rank);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+  HDIV_CUDA_TRY(cudaMalloc(&c->buf, sizeof(double) * 4 * c->plane));
+  c->rlo = c->buf;
+  c->rhi = c->buf + c->plane;
+  c->slo = c->buf + 2 * c->plane;
+  c->shi = c->buf + 3 * c->plane;
+  return HDIV_OK;
 }
 
 void comm_free(hdiv_ctx* h) {
   if (!h->comm) return;
-  if (h->comm->comm) ncclCommDestroy(h->comm->comm);
+  if (h->comm->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm->comm);
+  cudaFree(h->comm->buf);
   delete h->comm;
   h->comm = nullptr;
 }
 
-hdiv_status comm_reverse_add(hdiv_ctx* h, double* y, cudaStream_t s) {
-  (void)h; (void)y; (void)s;
-  return HDIV_ERR_UNSUPPORTED;
+// interface plane pointers of an RT vector (last-axis faces at K = 0 and K = n_last)
+static void planes(const hdiv_ctx* h, double* y, double** lo, double** hi) {
+  const int last = h->dim - 1;
+  const long long plane = h->comm->plane;
+  *lo = (h->rank > 0) ? y + h->off[last] : nullptr;
+  *hi = (h->rank < h->nranks - 1) ? y + h->off[last] + plane * h->n[last] : nullptr;
 }
 
+hdiv_status comm_reverse_add(hdiv_ctx* h, double* y, cudaStream_t s) {
+  Comm* c = h->comm;
+  if (!c) return HDIV_OK;
+  double *lo, *hi;
+  planes(h, y, &lo, &hi);
+  ncclResult_t r = g_nccl.GroupStart();
+  if (lo) {
+    g_nccl.Send(lo, c->plane, ncclDouble, c->rank - 1, c->comm, s);
+    g_nccl.Recv(c->rlo, c->plane, ncclDouble, c->rank - 1, c->comm, s);
+  }
+  if (hi) {
+    g_nccl.Send(hi, c->plane, ncclDouble, c->rank + 1, c->comm, s);
+    g_nccl.Recv(c->rhi, c->plane, ncclDouble, c->rank + 1, c->comm, s);
+  }
+  r = g_nccl.GroupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "reverse-add exchange");
+  add_planes_kernel<<<(unsigned)((c->plane + 255) / 256), 256, 0, s>>>(lo, c->rlo, hi, c->rhi,
+                                                                       c->plane);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  return HDIV_OK;
+}
+
+// refresh the ghost layers stored after the local entries of an L2 vector x[nl2 + 2 lplane]
+hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s) {
+  Comm* c = h->comm;
+  if (!c) return HDIV_OK;
+  const bool down = h->rank > 0, up = h->rank < h->nranks - 1;
+  pack_l2_layers_kernel<<<(unsigned)((c->lplane + 255) / 256), 256, 0, s>>>(
+      x, down ? c->slo : nullptr, up ? c->shi : nullptr, h->NL[0], h->NL[1], h->NL[2], h->p,
+      h->dim, c->lplane);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  double* glo = x + h->nl2;
+  double* ghi = x + h->nl2 + c->lplane;
+  ncclResult_t r = g_nccl.GroupStart();
+  if (down) {
+    g_nccl.Send(c->slo, c->lplane, ncclDouble, c->rank - 1, c->comm, s);
+    g_nccl.Recv(glo, c->lplane, ncclDouble, c->rank - 1, c->comm, s);
+  }
+  if (up) {
+    g_nccl.Send(c->shi, c->lplane, ncclDouble, c->rank + 1, c->comm, s);
+    g_nccl.Recv(ghi, c->lplane, ncclDouble, c->rank + 1, c->comm, s);
+  }
+  r = g_nccl.GroupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "L2 ghost exchange");
+  return HDIV_OK;
+}
+
+// all-gather of k local scalars into glob[P][k] (rank-ordered)
+hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, cudaStream_t s) {
+  Comm* c = h->comm;
+  ncclResult_t r = g_nccl.AllGather(loc, glob, k, ncclDouble, c->comm, s);
+  if (r != ncclSuccess) return nccl_fail(r, "allgather");
+  return HDIV_OK;
+}
+
+// S~ ghost columns are built into the CSR by build_schur (columns nl2 + ...); nothing else.
 hdiv_status comm_setup_schur_ghosts(hdiv_ctx* h, cudaStream_t s) {
   (void)h; (void)s;
-  return HDIV_ERR_UNSUPPORTED;
+  return HDIV_OK;
 }
 
 }  // namespace hdiv
+
+extern "C" hdiv_status hdiv_nccl_unique_id(void* out, int64_t len) {
+  using namespace hdiv;
+  if (!out) { set_error("NULL out"); return HDIV_ERR_NULL; }
+  if (len < (int64_t)sizeof(ncclUniqueId)) { set_error("buffer < 128 bytes"); return HDIV_ERR_SHAPE; }
+  std::string err;
+  if (!load_nccl(&err)) { set_error(err); return HDIV_ERR_NCCL; }
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof(id));
+  return HDIV_OK;
+}

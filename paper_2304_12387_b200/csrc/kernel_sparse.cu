@@ -18,6 +18,7 @@ namespace {
 struct Grid {
   long long NL[3], n[3], off[3];
   int p, dim;
+  long long ghost_lo, ghost_hi;   // first ghost column below / above the slab, -1 if none
   __device__ __forceinline__ long long l2(long long X, long long Y, long long Z) const {
     long long e = (X / p) + NL[0] * ((Y / p) + NL[1] * (Z / p));
     long long a = X % p, b = Y % p, c = Z % p;
@@ -49,6 +50,9 @@ Grid make_grid(const hdiv_ctx* h) {
   Grid g;
   for (int d = 0; d < 3; ++d) { g.NL[d] = h->NL[d]; g.n[d] = h->n[d]; g.off[d] = h->off[d]; }
   g.p = h->p; g.dim = h->dim;
+  const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
+  g.ghost_lo = (h->rank > 0) ? h->nl2 : -1;
+  g.ghost_hi = (h->rank < h->nranks - 1) ? h->nl2 + lplane : -1;
   return g;
 }
 
@@ -120,6 +124,12 @@ __device__ __forceinline__ int faces_of(const Grid& g, long long X, long long Y,
   if (g.dim == 3) {
     face[4] = g.rt(2, X, Y, Z);     nb[4] = Z > 0 ? g.l2(X, Y, Z - 1) : -1;
     face[5] = g.rt(2, X, Y, Z + 1); nb[5] = Z + 1 < g.n[2] ? g.l2(X, Y, Z + 1) : -1;
+    // slab interfaces: the neighbour across is a ghost cell (ordered by subcell X + n_x Y)
+    if (Z == 0 && g.ghost_lo >= 0) nb[4] = g.ghost_lo + X + g.n[0] * Y;
+    if (Z + 1 == g.n[2] && g.ghost_hi >= 0) nb[5] = g.ghost_hi + X + g.n[0] * Y;
+  } else {
+    if (Y == 0 && g.ghost_lo >= 0) nb[2] = g.ghost_lo + X;
+    if (Y + 1 == g.n[1] && g.ghost_hi >= 0) nb[3] = g.ghost_hi + X;
   }
   return nd;
 }

@@ -6,15 +6,16 @@
 // residual (reading A8).  Recurrence: Elman-Silvester-Wathen preconditioned MINRES
 // (SURVEY §8(c) step 10), written with the unnormalised z (A z/gamma = (A z)/gamma).
 //
-// Per iteration (all on `stream`, captured in a CUDA graph of 6 iterations so the buffer
-// rotation v(3) / w(3) / z(2) is baked into the graph):
-//   apply_block(z) -> Az                      (kernel_affine / kernel_general)
-//   dot(Az, z) partials -> fin_delta          (delta = <Az,z>/gamma^2)
+// Per iteration (all on the handle's stream, captured in a CUDA graph of 6 iterations so the
+// buffer rotation v(3) / w(3) / z(2) is baked into the graph):
+//   apply_block(z) -> Az                      (kernel_affine / kernel_general [+ reverse-add])
+//   dot(Az, z) -> local scalar [-> allgather] -> delta = <Az,z>/gamma^2
 //   vupd: v_new, z_new_u = v_new_u/(tau M~), partial <z_u, v_u>
-//   Chebyshev steps on v_new_q -> z_new_q, last step partial <z_q, v_q>
+//   Chebyshev steps on v_new_q -> z_new_q [ghost refresh before each SpMV], partial <z_q, v_q>
 //   scalar: gamma_new, Givens rotation, eta, convergence flag
 //   wupd: w_new, x += c eta w_new
-// Reductions are two-stage with a fixed grid and a fixed-order final sum -> deterministic.
+// Reductions: fixed grid, fixed-order block and partial sums, and (multi-GPU) an all-gather of
+// the per-rank scalars summed in rank order -> deterministic and identical on every rank.
 // Every kernel reads the device `done` flag and returns early once converged.
 #include <cuda_runtime.h>
 
@@ -25,6 +26,8 @@
 
 namespace hdiv {
 
+hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s);
+hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, cudaStream_t s);
 
 namespace {
 
@@ -48,32 +51,49 @@ __device__ __forceinline__ double block_sum(double v) {
     r = (l < RED_NT / 32) ? red[l] : 0.0;
     for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
   }
+  __syncthreads();
   return r;   // valid in thread 0
 }
 
+// partial sums of a.b over [0,n) excluding [ex_lo, ex_hi) (replicated interface plane)
 __global__ void __launch_bounds__(RED_NT)
 dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
-           double* __restrict__ part, const int* __restrict__ done) {
+           long long ex_lo, long long ex_hi, double* __restrict__ part,
+           const int* __restrict__ done) {
   if (done && *done) return;
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
        i += (long long)gridDim.x * RED_NT)
-    s = fma(a[i], b[i], s);
+    if (i < ex_lo || i >= ex_hi) s = fma(a[i], b[i], s);
   s = block_sum(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// fixed-order sum of RED_BLOCKS partials by one block
 __device__ __forceinline__ double sum_partials(const double* part) {
   double s = 0.0;
   for (int i = threadIdx.x; i < RED_BLOCKS; i += RED_NT) s += part[i];
   return block_sum(s);
 }
 
-__global__ void __launch_bounds__(RED_NT) fin_delta_kernel(const double* part, MState* st) {
-  if (st->done) return;
-  double s = sum_partials(part);
-  if (threadIdx.x == 0) st->delta = s / (st->gamma * st->gamma);
+// loc[0] = sum(part_a) (+ sum(part_b))
+__global__ void __launch_bounds__(RED_NT)
+local_reduce_kernel(const double* part_a, const double* part_b, double* loc,
+                    const int* __restrict__ done) {
+  if (done && *done) return;
+  double s = sum_partials(part_a);
+  double t = part_b ? sum_partials(part_b) : 0.0;
+  if (threadIdx.x == 0) loc[0] = s + t;
+}
+
+__device__ __forceinline__ double rank_sum(const double* glob, int P) {
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += glob[r];
+  return s;
+}
+
+__global__ void fin_delta_kernel(const double* glob, int P, MState* st) {
+  if (threadIdx.x != 0 || st->done) return;
+  st->delta = rank_sum(glob, P) / (st->gamma * st->gamma);
 }
 
 // v_new = Az/g - (delta/g) v - (g/g_old) v_old ; z_new_u = v_new_u / (tau M~)
@@ -81,7 +101,8 @@ __global__ void __launch_bounds__(RED_NT)
 vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
             const double* __restrict__ v_old, double* __restrict__ v_new,
             double* __restrict__ z_new, const double* __restrict__ mdiag, double tau,
-            long long nrt, long long n, const MState* __restrict__ st, double* part) {
+            long long nrt, long long n, long long ex_lo, long long ex_hi,
+            const MState* __restrict__ st, double* part) {
   if (st->done) return;
   const double g = st->gamma, ig = 1.0 / g;
   const double cd = st->delta * ig, co = g / st->gamma_old;
@@ -93,15 +114,15 @@ vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
     if (i < nrt) {
       double zn = vn / (tau * mdiag[i]);
       z_new[i] = zn;
-      s = fma(zn, vn, s);
+      if (i < ex_lo || i >= ex_hi) s = fma(zn, vn, s);
     }
   }
   s = block_sum(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// Chebyshev step k (reading A10): r_new = r - S~ d ; d_new = c1 d + c2 Dinv r_new ; y += d_new
-// first==1: y = d = Dinv r / theta (no SpMV).  `last` adds the partial <y, v>.
+// Chebyshev semi-iteration (reading A10).  first: y = d = Dinv r / theta.
+// step: r_new = r - S~ d ; d_new = c1 d + c2 Dinv r_new ; y += d_new.  `last` adds <y, v>.
 __global__ void __launch_bounds__(RED_NT)
 cheb_first_kernel(const double* __restrict__ rin, const double* __restrict__ dinv, double itheta,
                   double* __restrict__ d, double* __restrict__ y, long long n, int last,
@@ -123,7 +144,8 @@ cheb_first_kernel(const double* __restrict__ rin, const double* __restrict__ din
 
 __global__ void __launch_bounds__(RED_NT)
 cheb_step_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                 const double* __restrict__ val, const double* rin, double* rout, const double* __restrict__ d, double* __restrict__ dn,
+                 const double* __restrict__ val, const double* rin, double* rout,
+                 const double* __restrict__ d, double* __restrict__ dn,
                  const double* __restrict__ dinv, double* __restrict__ y, double c1, double c2,
                  long long n, int last, const double* __restrict__ vin, double* part,
                  const int* __restrict__ done) {
@@ -147,40 +169,29 @@ cheb_step_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col
   }
 }
 
-// scale z_u = v_u / (tau M~)  (plain preconditioner application)
 __global__ void diag_scale_kernel(const double* __restrict__ v, const double* __restrict__ mdiag,
                                   double tau, double* __restrict__ z, long long n) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) z[i] = v[i] / (tau * mdiag[i]);
 }
 
-__global__ void __launch_bounds__(RED_NT)
-init_kernel(const double* part_u, const double* part_q, MState* st, double rtol, int maxit) {
-  double s = sum_partials(part_u);
-  __syncthreads();
-  double t = sum_partials(part_q);
-  if (threadIdx.x == 0) {
-    double g2 = s + t;
-    MState m{};
-    m.rtol = rtol; m.maxit = maxit;
-    m.gamma_old = 1.0; m.c = 1.0; m.c_old = 1.0; m.s = 0.0; m.s_old = 0.0;
-    if (g2 < 0.0) { m.breakdown = 1; m.done = 1; }
-    double g = std::sqrt(g2 > 0 ? g2 : 0.0);
-    m.gamma = g; m.gamma1 = g; m.eta = g; m.rel = 1.0;
-    if (g == 0.0 && !m.breakdown) { m.done = 1; m.conv = 1; m.rel = 0.0; }
-    *st = m;
-  }
+__global__ void init_kernel(const double* glob, int P, MState* st, double rtol, int maxit) {
+  if (threadIdx.x != 0) return;
+  double g2 = rank_sum(glob, P);
+  MState m{};
+  m.rtol = rtol; m.maxit = maxit;
+  m.gamma_old = 1.0; m.c = 1.0; m.c_old = 1.0; m.s = 0.0; m.s_old = 0.0;
+  if (g2 < 0.0) { m.breakdown = 1; m.done = 1; }
+  double g = std::sqrt(g2 > 0 ? g2 : 0.0);
+  m.gamma = g; m.gamma1 = g; m.eta = g; m.rel = 1.0;
+  if (g == 0.0 && !m.breakdown) { m.done = 1; m.conv = 1; m.rel = 0.0; }
+  *st = m;
 }
 
-__global__ void __launch_bounds__(RED_NT)
-scalar_kernel(const double* part_u, const double* part_q, MState* st) {
-  if (st->done) return;
-  double s = sum_partials(part_u);
-  __syncthreads();
-  double t = sum_partials(part_q);
-  if (threadIdx.x != 0) return;
+__global__ void scalar_kernel(const double* glob, int P, MState* st) {
+  if (threadIdx.x != 0 || st->done) return;
   MState m = *st;
-  double g2 = s + t;
+  double g2 = rank_sum(glob, P);
   if (g2 < 0.0) { m.breakdown = 1; m.done = 1; *st = m; return; }
   const double gn = std::sqrt(g2);
   const double delta = m.delta, g = m.gamma;
@@ -205,7 +216,7 @@ scalar_kernel(const double* part_u, const double* part_q, MState* st) {
 }
 
 // w_new = wz z - wa3 w_old - wa2 w ;  x += xc w_new.  Runs in the iteration that set done=2
-// (the final update), and is skipped once done == 1 is latched by latch_kernel.
+// (its final update) and is skipped once latch_kernel turned done into 1.
 __global__ void __launch_bounds__(RED_NT)
 wupd_kernel(const double* __restrict__ z, const double* __restrict__ w_old,
             const double* __restrict__ w, double* __restrict__ w_new, double* __restrict__ x,
@@ -232,11 +243,13 @@ struct MinresWork {
   long long n = 0;
   double* buf = nullptr;           // all vectors
   double *v[3], *w[3], *z[2], *Az, *r, *d[2];
-  double *part_a, *part_b;
+  double *part_a, *part_b, *loc, *glob;
   MState* st = nullptr;
   MState* st_host = nullptr;       // pinned
+  cudaStream_t stream = nullptr;   // own non-blocking stream (graph capture needs one)
   std::vector<double> c1, c2;      // Chebyshev step constants
   double itheta = 0;
+  long long ex_lo = 0, ex_hi = 0;  // RT range excluded from dots (replicated plane)
 };
 
 static hdiv_status ensure_work(hdiv_ctx* h) {
@@ -244,20 +257,32 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
   auto* mw = new MinresWork();
   h->mw = mw;
   const long long n = h->nrt + h->nl2, nq = h->nl2;
+  const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
+  const long long nqg = nq + (h->nranks > 1 ? 2 * lplane : 0);   // + ghost layers
   mw->n = n;
-  size_t tot = 9 * (size_t)n + 3 * (size_t)nq + 2 * RED_BLOCKS;
+  size_t tot = 9 * (size_t)n + (size_t)nq + 2 * (size_t)nqg + 2 * RED_BLOCKS + 2 + 2 * h->nranks;
   HDIV_CUDA_TRY(cudaMalloc(&mw->buf, tot * sizeof(double)));
+  HDIV_CUDA_TRY(cudaMemset(mw->buf, 0, tot * sizeof(double)));
   double* p = mw->buf;
   for (int i = 0; i < 3; ++i) { mw->v[i] = p; p += n; }
   for (int i = 0; i < 3; ++i) { mw->w[i] = p; p += n; }
   for (int i = 0; i < 2; ++i) { mw->z[i] = p; p += n; }
   mw->Az = p; p += n;
   mw->r = p; p += nq;
-  for (int i = 0; i < 2; ++i) { mw->d[i] = p; p += nq; }
+  for (int i = 0; i < 2; ++i) { mw->d[i] = p; p += nqg; }
   mw->part_a = p; p += RED_BLOCKS;
   mw->part_b = p; p += RED_BLOCKS;
+  mw->loc = p; p += 2;
+  mw->glob = (h->nranks > 1) ? p : mw->loc;
+  p += 2 * h->nranks;
+  if (h->rank > 0) {   // the lower rank owns the shared interface plane
+    const int last = h->dim - 1;
+    mw->ex_lo = h->off[last];
+    mw->ex_hi = h->off[last] + lplane;
+  }
   HDIV_CUDA_TRY(cudaMalloc(&mw->st, sizeof(MState)));
   HDIV_CUDA_TRY(cudaMallocHost(&mw->st_host, sizeof(MState)));
+  HDIV_CUDA_TRY(cudaStreamCreateWithFlags(&mw->stream, cudaStreamNonBlocking));
   // Chebyshev constants on [lmax/ratio, lmax], lmax = 2 (reading A10)
   const int k = h->opts.cheb_degree;
   const double lmax = 2.0, a = lmax / h->opts.cheb_ratio, b = lmax;
@@ -278,27 +303,35 @@ void minres_free(hdiv_ctx* h) {
   cudaFree(h->mw->buf);
   cudaFree(h->mw->st);
   cudaFreeHost(h->mw->st_host);
+  if (h->mw->stream) cudaStreamDestroy(h->mw->stream);
   delete h->mw;
   h->mw = nullptr;
 }
 
 // Chebyshev-Jacobi S^-1 applied to vq -> y (uses mw->r, mw->d); partial <y, vq> if part
-static cudaError_t cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
+static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
                               const int* done, cudaStream_t s) {
   MinresWork* mw = h->mw;
   const long long n = h->nl2;
   const int k = h->opts.cheb_degree;
   cheb_first_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0], y, n,
                                                   k == 1, part, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
   const double* rin = vq;
   for (int i = 1; i < k; ++i) {
+    double* dprev = mw->d[(i - 1) & 1];
+    if (h->nranks > 1) {
+      hdiv_status st = comm_l2_ghosts(h, dprev, s);
+      if (st != HDIV_OK) return st;
+    }
     cheb_step_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_srow, h->d_scol, h->d_sval, rin, mw->r,
-                                                   mw->d[(i - 1) & 1], mw->d[i & 1], h->d_sdinv,
-                                                   y, mw->c1[i - 1], mw->c2[i - 1], n, i == k - 1,
+                                                   dprev, mw->d[i & 1], h->d_sdinv, y,
+                                                   mw->c1[i - 1], mw->c2[i - 1], n, i == k - 1,
                                                    vq, part, done);
+    HDIV_CUDA_TRY(cudaGetLastError());
     rin = mw->r;
   }
-  return cudaGetLastError();
+  return HDIV_OK;
 }
 
 hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t s) {
@@ -306,23 +339,34 @@ hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t 
   if (st != HDIV_OK) return st;
   diag_scale_kernel<<<nb(h->nrt, 256), 256, 0, s>>>(v, h->d_mdiag, h->opts.tau, z, h->nrt);
   HDIV_CUDA_TRY(cudaGetLastError());
-  HDIV_CUDA_TRY(cheb_apply(h, v + h->nrt, z + h->nrt, nullptr, nullptr, s));
+  return cheb_apply(h, v + h->nrt, z + h->nrt, nullptr, nullptr, s);
+}
+
+// local scalar -> (all-gather) -> glob
+static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
+                                 cudaStream_t s) {
+  MinresWork* mw = h->mw;
+  local_reduce_kernel<<<1, RED_NT, 0, s>>>(pa, pb, mw->loc, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  if (h->nranks > 1) return comm_allgather(h, mw->loc, mw->glob, 1, s);
   return HDIV_OK;
 }
 
-static cudaError_t apply_A(hdiv_ctx* h, const double* x, double* y, const int* skip,
-                           cudaStream_t s);
-
 hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit,
-                   hdiv_report* rep, cudaStream_t s) {
+                   hdiv_report* rep, cudaStream_t caller) {
   hdiv_status stt = ensure_work(h);
   if (stt != HDIV_OK) return stt;
   MinresWork* mw = h->mw;
   const long long n = mw->n, nrt = h->nrt;
   const int* done = &mw->st->done;
+  const int P = h->nranks;
+  // the solve runs on the handle's own (capturable) stream, ordered after `caller`
+  cudaStream_t s = mw->stream;
   cudaEvent_t e0, e1;
   HDIV_CUDA_TRY(cudaEventCreate(&e0));
   HDIV_CUDA_TRY(cudaEventCreate(&e1));
+  HDIV_CUDA_TRY(cudaEventRecord(e0, caller));
+  HDIV_CUDA_TRY(cudaStreamWaitEvent(s, e0, 0));
   HDIV_CUDA_TRY(cudaEventRecord(e0, s));
   // x0 = 0, v0 = 0 (v_old), w0 = w1 = 0, v1 = b, z1 = P^-1 v1, gamma1 = sqrt(<z1, v1>)
   HDIV_CUDA_TRY(cudaMemsetAsync(x, 0, n * sizeof(double), s));
@@ -330,19 +374,19 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
   HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[0], 0, n * sizeof(double), s));
   HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[1], 0, n * sizeof(double), s));
   HDIV_CUDA_TRY(cudaMemcpyAsync(mw->v[1], b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  {
-    // z_u and partial <z_u, v_u>, then Chebyshev with partial <z_q, v_q>
-    diag_scale_kernel<<<nb(nrt, 256), 256, 0, s>>>(mw->v[1], h->d_mdiag, h->opts.tau, mw->z[0],
-                                                   nrt);
-    dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->z[0], mw->v[1], nrt, mw->part_a, nullptr);
-    HDIV_CUDA_TRY(cheb_apply(h, mw->v[1] + nrt, mw->z[0] + nrt, mw->part_b, nullptr, s));
-    init_kernel<<<1, RED_NT, 0, s>>>(mw->part_a, mw->part_b, mw->st, rtol, maxit);
-    HDIV_CUDA_TRY(cudaGetLastError());
-  }
-  // one iteration j: buffers (v_old, v, v_new) = v[(j-1)%3], v[j%3], v[(j+1)%3]
-  //                  (w_old, w, w_new)  = w[(j-1)%3], w[j%3], w[(j+1)%3]
-  //                  (z, z_new)         = z[(j-1)%2], z[j%2]
-  auto iteration = [&](int j) -> cudaError_t {
+  diag_scale_kernel<<<nb(nrt, 256), 256, 0, s>>>(mw->v[1], h->d_mdiag, h->opts.tau, mw->z[0], nrt);
+  dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->z[0], mw->v[1], nrt, mw->ex_lo, mw->ex_hi,
+                                           mw->part_a, nullptr);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  if ((stt = cheb_apply(h, mw->v[1] + nrt, mw->z[0] + nrt, mw->part_b, nullptr, s)) != HDIV_OK)
+    return stt;
+  if ((stt = reduce_scalar(h, mw->part_a, mw->part_b, nullptr, s)) != HDIV_OK) return stt;
+  init_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st, rtol, maxit);
+  HDIV_CUDA_TRY(cudaGetLastError());
+
+  // iteration j: (v_old, v, v_new) = v[(j-1)%3], v[j%3], v[(j+1)%3]; same for w;
+  //              (z, z_new) = z[(j-1)%2], z[j%2]
+  auto iteration = [&](int j) -> hdiv_status {
     double* vo = mw->v[(j + 2) % 3];
     double* vc = mw->v[j % 3];
     double* vn = mw->v[(j + 1) % 3];
@@ -351,43 +395,41 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     double* wn = mw->w[(j + 1) % 3];
     double* zc = mw->z[(j + 1) % 2];
     double* zn = mw->z[j % 2];
-    cudaError_t e = apply_A(h, zc, mw->Az, done, s);
-    if (e != cudaSuccess) return e;
-    dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, zc, n, mw->part_a, done);
-    fin_delta_kernel<<<1, RED_NT, 0, s>>>(mw->part_a, mw->st);
+    HDIV_CUDA_TRY(apply_block_dev(h, zc, mw->Az, done, s));
+    dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_a,
+                                             done);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    hdiv_status st = reduce_scalar(h, mw->part_a, nullptr, done, s);
+    if (st != HDIV_OK) return st;
+    fin_delta_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st);
     vupd_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
-                                              nrt, n, mw->st, mw->part_a);
-    e = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s);
-    if (e != cudaSuccess) return e;
-    scalar_kernel<<<1, RED_NT, 0, s>>>(mw->part_a, mw->part_b, mw->st);
+                                              nrt, n, mw->ex_lo, mw->ex_hi, mw->st, mw->part_a);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    if ((st = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s)) != HDIV_OK) return st;
+    if ((st = reduce_scalar(h, mw->part_a, mw->part_b, done, s)) != HDIV_OK) return st;
+    scalar_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st);
     wupd_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(zc, wo, wc, wn, x, n, mw->st);
     latch_kernel<<<1, 32, 0, s>>>(mw->st);
-    return cudaGetLastError();
+    HDIV_CUDA_TRY(cudaGetLastError());
+    return HDIV_OK;
   };
-  // capture 6 iterations (j = 1..6 pattern repeats with period 6)
+  // capture 6 iterations (the buffer pattern repeats with period 6)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   bool use_graph = true;
-  {
-    cudaStream_t cs = s;
-    cudaStreamCaptureStatus cst;
-    if (cudaStreamIsCapturing(cs, &cst) != cudaSuccess || cst != cudaStreamCaptureStatusNone)
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    use_graph = false;
+    cudaGetLastError();
+  } else {
+    hdiv_status e = HDIV_OK;
+    for (int j = 1; j <= 6 && e == HDIV_OK; ++j) e = iteration(j);
+    cudaError_t ec = cudaStreamEndCapture(s, &graph);
+    if (e != HDIV_OK || ec != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
       use_graph = false;
-  }
-  if (use_graph) {
-    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-      use_graph = false;
-    } else {
-      cudaError_t e = cudaSuccess;
-      for (int j = 1; j <= 6 && e == cudaSuccess; ++j) e = iteration(j);
-      cudaError_t ec = cudaStreamEndCapture(s, &graph);
-      if (e != cudaSuccess || ec != cudaSuccess ||
-          cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
-        use_graph = false;
-        cudaGetLastError();
-        if (graph) cudaGraphDestroy(graph);
-        graph = nullptr;
-      }
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      graph = nullptr;
+      exec = nullptr;
     }
   }
   int launched = 0;
@@ -396,8 +438,8 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
       HDIV_CUDA_TRY(cudaGraphLaunch(exec, s));
     } else {
       for (int j = 1; j <= 6; ++j) {
-        cudaError_t e = iteration(j);
-        if (e != cudaSuccess) { hdiv::set_error(cudaGetErrorString(e)); return HDIV_ERR_CUDA; }
+        hdiv_status e = iteration(j);
+        if (e != HDIV_OK) return e;
       }
     }
     launched += 6;
@@ -406,6 +448,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     if (mw->st_host->done || launched >= maxit + 6) break;
   }
   HDIV_CUDA_TRY(cudaEventRecord(e1, s));
+  HDIV_CUDA_TRY(cudaStreamWaitEvent(caller, e1, 0));
   HDIV_CUDA_TRY(cudaEventSynchronize(e1));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -420,16 +463,11 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     rep->rel_resid = m.rel;
     rep->t_solve_ms = ms;
   }
-  if (m.breakdown) return HDIV_ERR_BREAKDOWN;
+  if (m.breakdown) {
+    set_error("MINRES breakdown: <z, v> < 0");
+    return HDIV_ERR_BREAKDOWN;
+  }
   return HDIV_OK;
-}
-
-cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
-                            cudaStream_t s);   // api.cu
-
-static cudaError_t apply_A(hdiv_ctx* h, const double* x, double* y, const int* skip,
-                           cudaStream_t s) {
-  return apply_block_dev(h, x, y, skip, s);
 }
 
 }  // namespace hdiv
