@@ -10,16 +10,19 @@
 //
 // B200 design:
 //  * one CTA per tile of TXxTYxTZ elements; every DOF is read once from HBM (cp.async into
-//    shared memory) and written once — no atomics, no zero-fill;
+//    shared memory) and written once (streaming stores) — no atomics, no zero fill;
 //  * a face plane shared by two tiles is OWNED by the tile on its + side; that tile
 //    recomputes the - side neighbour element's contribution from a one-element halo of the
 //    single component involved (1/T of one component; neighbours' reads hit L2);
-//  * sum factorisation: two element-local M_h passes, then one line pass along the component
-//    direction that applies c_e M_l element by element, carries the shared-plane sum in a
-//    register and adds D^T q~; one thread owns a whole line, smem row strides are odd, so
-//    the passes are bank-conflict free;
-//  * D u and -Z q~ are accumulated in registers by the thread that owns each cell and stored
-//    coalesced (the L2 DOFs of a tile row are contiguous in HBM).
+//  * per component: one register-blocked pass applies M_h (x) M_h across the two histopolation
+//    directions (P x P block per thread), one line pass applies c_e M_l along the component
+//    direction element by element with the shared-plane sum carried in a register, and D^T q~
+//    is added in the coalesced copy-out;
+//  * tile geometry is compile-time (loops unrolled, constant divisors); partial tiles at the
+//    domain edge are handled with predicates; every smem extent is padded to an odd number of
+//    doubles so that all lane strides are odd -> bank-conflict free;
+//  * D u and -Z q~ accumulate in registers per owned cell; stored coalesced (a tile row of
+//    L2 DOFs is contiguous in HBM).
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -36,27 +39,43 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 constexpr int odd_up(int v) { return (v % 2) ? v : v + 1; }
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+// smem box of component AX: extent (T_AX+1)P+1 along AX (position 0 <-> global plane
+// (e0_AX - 1) P), T P along the others; extents 0 and 1 padded odd.
+template <int P, int TX, int TY, int TZ, int AX>
+struct CG {
+  static constexpr int E0 = (AX == 0) ? (TX + 1) * P + 1 : TX * P;
+  static constexpr int E1 = (AX == 1) ? (TY + 1) * P + 1 : TY * P;
+  static constexpr int E2 = (AX == 2) ? (TZ + 1) * P + 1 : TZ * P;
+  static constexpr int S1 = odd_up(E0);
+  static constexpr int S2 = S1 * odd_up(E1);
+  static constexpr int SIZE = S2 * E2;
+  static constexpr int EA = (AX == 0) ? E0 : (AX == 1) ? E1 : E2;   // extent along AX
+  static constexpr int SA = (AX == 0) ? 1 : (AX == 1) ? S1 : S2;    // stride along AX
+  // the two histopolation axes A1 < A2
+  static constexpr int A1 = (AX == 0) ? 1 : 0;
+  static constexpr int A2 = (AX == 2) ? 1 : 2;
+  static constexpr int SA1 = (A1 == 0) ? 1 : S1;
+  static constexpr int SA2 = (A2 == 1) ? S1 : S2;
+  static constexpr int TA = (AX == 0) ? TX : (AX == 1) ? TY : TZ;
+  static constexpr int TA1 = (A1 == 0) ? TX : TY;
+  static constexpr int TA2 = (A2 == 1) ? TY : TZ;
+};
 
 template <int P, int TX, int TY, int TZ>
 struct Geo {
-  // x-component tile: [K][J][I'], I' in [0,(TX+1)P], I' = 0 <-> global plane (ex0-1)P
-  static constexpr int XI = odd_up((TX + 1) * P + 1), XJ = TY * P, XK = TZ * P;
-  // y-component tile: [K][J'][I]
-  static constexpr int YI = odd_up(TX * P), YJ = (TY + 1) * P + 1, YK = TZ * P;
-  // z-component tile: [K'][J][I]
-  static constexpr int ZI = odd_up(TX * P), ZJ = TY * P, ZK = (TZ + 1) * P + 1;
-  static constexpr int SX = XI * XJ * XK, SY = YI * YJ * YK, SZ = ZI * ZJ * ZK;
   static constexpr int P3 = P * P * P;
   static constexpr int NE = TX * TY * TZ;
   static constexpr int NCELL = NE * P3;
-  static constexpr int RQ = odd_up(P);                 // padded a-row of the Z scratch
-  static constexpr int SZQ = NE * RQ * P * P;
-  static constexpr int SU0 = SX > SY ? (SX > SZ ? SX : SZ) : (SY > SZ ? SY : SZ);
-  static constexpr int SU = SU0 > SZQ ? SU0 : SZQ;
-  static constexpr int HQX = TZ * P * TY * P, HQY = TZ * P * TX * P, HQZ = TY * P * TX * P;
+  static constexpr int RQ = odd_up(P);          // padded a-row of the Z scratch
+  static constexpr int ESZ = RQ * P * P;        // element stride of the Z scratch
+  static constexpr int SU = cmax(cmax(CG<P, TX, TY, TZ, 0>::SIZE, CG<P, TX, TY, TZ, 1>::SIZE),
+                                 cmax(CG<P, TX, TY, TZ, 2>::SIZE, NE * ESZ));
+  static constexpr int HQ0 = TY * P * TZ * P, HQ1 = TX * P * TZ * P, HQ2 = TX * P * TY * P;
   static constexpr int NCO = (TX + 1) * (TY + 1) * (TZ + 1);
   static constexpr size_t smem_doubles(bool block) {
-    return (size_t)SU + (block ? (size_t)NCELL + HQX + HQY + HQZ : 0) + 4 * NCO;
+    return (size_t)SU + (block ? (size_t)NCELL + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
   }
 };
 
@@ -70,127 +89,196 @@ struct AffArgs {
   long long nrt;
   int ntile[3];
   int has_z;
-  const int* skip;   // MINRES done flag (nullptr: never skip)
+  const int* skip;     // MINRES done flag (nullptr: never skip)
 };
 
-template <int P>
-__device__ __forceinline__ void matvec_h(const double (*M)[MAXP], double* v) {
-  double w[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) {
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < P; ++j) s = fma(M[i][j], v[j], s);
-    w[i] = s;
-  }
-#pragma unroll
-  for (int i = 0; i < P; ++i) v[i] = w[i];
-}
+struct TileInfo {
+  int e0[3];    // first element of the tile
+  int m[3];     // valid elements per axis (<= T)
+  int h[3];     // - side halo element present
+  int last[3];  // tile touches the + domain boundary
+};
 
-// In-place element-local contraction along one axis.  Element k of line (i0,i1,blk) lives at
-// s[off + i0*s0 + i1*s1 + blk*sb + k*se]; lanes run over i0 first.
-template <int P, int NT>
-__device__ __forceinline__ void hpass(double* s, const double (*M)[MAXP], int off, int n0,
-                                      int s0, int n1, int s1, int nb, int sb, int se) {
-  const int total = n0 * n1 * nb;
-  for (int it = threadIdx.x; it < total; it += NT) {
-    const int i0 = it % n0;
-    const int r = it / n0;
-    const int i1 = r % n1;
-    const int blk = r / n1;
-    double* b = s + off + i0 * s0 + i1 * s1 + blk * sb;
-    double v[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) v[k] = b[k * se];
-    matvec_h<P>(M, v);
-#pragma unroll
-    for (int k = 0; k < P; ++k) b[k * se] = v[k];
-  }
-}
-
-// Line pass along the component axis AX (0 x, 1 y, 2 z).  Lines are indexed by the two other
-// subcell coordinates (l0 = lane-fast, l1).  Element et (in [-h, m)) covers positions
-// (et+1)P .. (et+1)P+P of the line (stride sl).  Applies c_e M_l, sums the shared planes,
-// adds D^T q~ (BLOCK), writes the owned planes [P, (m+1)P) (+ the last plane if `last`).
+// -------- one component phase (AX) --------------------------------------------------------
 template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK>
-__device__ __forceinline__ void lpass(double* su, const double* sq, const double* hq,
-                                      const double* sco, const TabAffine& tab, int n0, int s0,
-                                      int n1, int s1, int sl, int m, int h, bool last) {
+__device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
+                                          const TabAffine& tab, double* su, const double* sq,
+                                          const double* hq, const double* sco, double* acc) {
+  using C = CG<P, TX, TY, TZ, AX>;
   using G = Geo<P, TX, TY, TZ>;
   constexpr int P3 = G::P3;
-  const int total = n0 * n1;
-  for (int it = threadIdx.x; it < total; it += NT) {
-    const int l0 = it % n0, l1 = it / n0;
-    double* line = su + l0 * s0 + l1 * s1;
-    // other-axis element / local coordinates of this line
-    int e_o0, loc_o0, e_o1, loc_o1;   // (x: J->y, K->z ; y: I->x, K->z ; z: I->x, J->y)
-    e_o0 = l0 / P; loc_o0 = l0 % P;
-    e_o1 = l1 / P; loc_o1 = l1 % P;
-    int ex = 0, ey = 0, ez = 0;
-    // q~ addressing: cell (ex,ey,ez ; a,b,c) -> ((ez*TY+ey)*TX+ex)*P3 + a + P b + P^2 c
-    int qbase = 0, qstep_loc = 1, qstep_el = P3, hqi = 0;
-    if (AX == 0) {
-      ey = e_o0; ez = e_o1;
-      qbase = ((ez * TY + ey) * TX) * P3 + P * loc_o0 + P * P * loc_o1;
-      qstep_loc = 1; qstep_el = P3;
-      hqi = l1 * (TY * P) + l0;
-    } else if (AX == 1) {
-      ex = e_o0; ez = e_o1;
-      qbase = ((ez * TY) * TX + ex) * P3 + loc_o0 + P * P * loc_o1;
-      qstep_loc = P; qstep_el = TX * P3;
-      hqi = l1 * (TX * P) + l0;
-    } else {
-      ex = e_o0; ey = e_o1;
-      qbase = (ey * TX + ex) * P3 + loc_o0 + P * loc_o1;
-      qstep_loc = P * P; qstep_el = TX * TY * P3;
-      hqi = l1 * (TX * P) + l0;
+  constexpr int NQR = (G::NCELL + NT - 1) / NT;
+  const int tid = threadIdx.x;
+  const double* __restrict__ u = a.x;
+  // global extents of the component-AX face grid
+  const long long ext0 = a.n[0] + (AX == 0), ext1 = a.n[1] + (AX == 1);
+  long long gorg[3];   // global subcell coordinate of smem position 0 along each axis
+#pragma unroll
+  for (int d = 0; d < 3; ++d) gorg[d] = (long long)(ti.e0[d] - (d == AX ? 1 : 0)) * P;
+  const int lo_a = ti.h[AX] ? 0 : P;                  // first loaded position along AX
+  const int hi_a = (ti.m[AX] + 1) * P;                // last valid position along AX
+  int hi_o[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) hi_o[d] = ti.m[d] * P;  // valid positions < hi_o (other axes)
+
+  // ---- load (cp.async, 8 B) ----
+  constexpr int NLD = C::E0 * C::E1 * C::E2;
+#pragma unroll 4
+  for (int it = tid; it < NLD; it += NT) {
+    const int i0 = it % C::E0, i1 = (it / C::E0) % C::E1, i2 = it / (C::E0 * C::E1);
+    const int pos[3] = {i0, i1, i2};
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      ok = ok && (d == AX ? (pos[d] >= lo_a && pos[d] <= hi_a) : (pos[d] < hi_o[d]));
+    if (ok) {
+      long long g = a.off[AX] + (gorg[0] + i0) + ext0 * ((gorg[1] + i1) + ext1 * (gorg[2] + i2));
+      cp_async8(su + i0 + C::S1 * i1 + C::S2 * i2, u + g);
     }
-    auto cof = [&](int et) -> double {
-      int cx = (AX == 0) ? et : ex, cy = (AX == 1) ? et : ey, cz = (AX == 2) ? et : ez;
-      return sco[4 * (((cz + 1) * (TY + 1) + (cy + 1)) * (TX + 1) + (cx + 1)) + AX];
-    };
-    double carry = 0.0;
-    if (h) {   // halo element et = -1: only its contribution to plane P
-      double v[P + 1];
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- D u (this component's two faces of every owned cell), from the raw values ----
+  if constexpr (BLOCK) {
 #pragma unroll
-      for (int i = 0; i <= P; ++i) v[i] = line[i * sl];
-      double s = 0.0;
+    for (int k = 0; k < NQR; ++k) {
+      const int i = tid + k * NT;
+      if (i < G::NCELL) {
+        const int e = i / P3, il = i % P3;
+        const int et[3] = {e % TX, (e / TX) % TY, e / (TX * TY)};
+        const int lc[3] = {il % P, (il / P) % P, il / (P * P)};
+        int pos[3];
 #pragma unroll
-      for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], v[j], s);
-      carry = cof(-1) * s;
+        for (int d = 0; d < 3; ++d) pos[d] = et[d] * P + lc[d] + (d == AX ? P : 0);
+        const double* s = su + pos[0] + C::S1 * pos[1] + C::S2 * pos[2];
+        acc[k] += s[C::SA] - s[0];
+      }
     }
-    double qprev = 0.0;   // q~ of the cell on the - side of the current plane
-    if (BLOCK && h) qprev = hq[hqi];
-    for (int et = 0; et < m; ++et) {
-      double* eb = line + (et + 1) * P * sl;
-      double v[P + 1];
+    __syncthreads();
+  }
+
+  // ---- M_h (x) M_h over the two histopolation axes: one P x P block per thread ----
+  constexpr int NH = C::EA * C::TA1 * C::TA2;
+#pragma unroll 2
+  for (int it = tid; it < NH; it += NT) {
+    const int pa = it % C::EA, b1 = (it / C::EA) % C::TA1, b2 = it / (C::EA * C::TA1);
+    double* base = su + pa * C::SA + b1 * P * C::SA1 + b2 * P * C::SA2;
+    double v[P][P];
 #pragma unroll
-      for (int i = 0; i <= P; ++i) v[i] = eb[i * sl];
-      const double c = cof(et);
-      double w[P + 1];
+    for (int k2 = 0; k2 < P; ++k2)
 #pragma unroll
-      for (int i = 0; i <= P; ++i) {
+      for (int k1 = 0; k1 < P; ++k1) v[k2][k1] = base[k1 * C::SA1 + k2 * C::SA2];
+    double w[P][P];
+#pragma unroll
+    for (int k2 = 0; k2 < P; ++k2)
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) {
         double s = 0.0;
 #pragma unroll
-        for (int j = 0; j <= P; ++j) s = fma(tab.Ml[i][j], v[j], s);
-        w[i] = c * s;
+        for (int j = 0; j < P; ++j) s = fma(tab.Mh[k1][j], v[k2][j], s);
+        w[k2][k1] = s;
       }
-      w[0] += carry;
-      if constexpr (BLOCK) {
-        const double* qe = sq + qbase + et * qstep_el;
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1)
+#pragma unroll
+      for (int k2 = 0; k2 < P; ++k2) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) s = fma(tab.Mh[k2][j], w[j][k1], s);
+        base[k1 * C::SA1 + k2 * C::SA2] = s;
+      }
+  }
+  __syncthreads();
+
+  // ---- c_e M_l along AX, element by element, shared planes summed in a register ----
+  constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
+  constexpr int NL = EL1 * EL2;
+  const int m_a = ti.m[AX], h_a = ti.h[AX];
+#pragma unroll 1
+  for (int it = tid; it < NL; it += NT) {
+    const int l1 = it % EL1, l2 = it / EL1;
+    double* line = su + l1 * C::SA1 + l2 * C::SA2;
+    int ec[3];   // element coordinates (in-tile) of this line; ec[AX] set per element
+    ec[C::A1] = l1 / P;
+    ec[C::A2] = l2 / P;
+    auto cof = [&](int eax) -> double {
+      int c3[3] = {ec[0], ec[1], ec[2]};
+      c3[AX] = eax;
+      return sco[4 * (((c3[2] + 1) * (TY + 1) + (c3[1] + 1)) * (TX + 1) + (c3[0] + 1)) + AX];
+    };
+    double carry = 0.0;
+    if (h_a) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], line[j * C::SA], s);
+      carry = cof(-1) * s;
+    }
+#pragma unroll
+    for (int et = 0; et < C::TA; ++et) {
+      if (et < m_a) {
+        double* eb = line + (et + 1) * P * C::SA;
+        double v[P + 1];
+#pragma unroll
+        for (int i = 0; i <= P; ++i) v[i] = eb[i * C::SA];
+        const double c = cof(et);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-          double qc = qe[i * qstep_loc];
-          w[i] += qprev - qc;   // (D^T q)_face = q(- side cell) - q(+ side cell)
-          qprev = qc;
-        }
-      }
+          double s = 0.0;
 #pragma unroll
-      for (int i = 0; i < P; ++i) eb[i * sl] = w[i];
-      carry = w[P];
+          for (int j = 0; j <= P; ++j) s = fma(tab.Ml[i][j], v[j], s);
+          eb[i * C::SA] = (i == 0) ? fma(c, s, carry) : c * s;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], v[j], s);
+        carry = c * s;
+      }
     }
-    if (last) line[(m + 1) * P * sl] = carry + (BLOCK ? qprev : 0.0);
+    if (ti.last[AX]) line[(m_a + 1) * P * C::SA] = carry;
   }
+  __syncthreads();
+
+  // ---- copy-out of the owned planes, + D^T q~ (coalesced, streaming stores) ----
+  constexpr int NOA = C::TA * P + 1;          // candidate owned positions along AX
+  constexpr int NO0 = (AX == 0) ? NOA : C::E0;
+  constexpr int NO1 = (AX == 1) ? NOA : C::E1;
+  constexpr int NO2 = (AX == 2) ? NOA : C::E2;
+  const int own_hi = (m_a + 1) * P + (ti.last[AX] ? 1 : 0);   // exclusive
+#pragma unroll 4
+  for (int it = tid; it < NO0 * NO1 * NO2; it += NT) {
+    const int o0 = it % NO0, o1 = (it / NO0) % NO1, o2 = it / (NO0 * NO1);
+    int pos[3] = {o0, o1, o2};
+    pos[AX] += P;
+    bool ok = pos[AX] < own_hi;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (d != AX) ok = ok && pos[d] < hi_o[d];
+    if (!ok) continue;
+    double v = su[pos[0] + C::S1 * pos[1] + C::S2 * pos[2]];
+    if constexpr (BLOCK) {
+      // face at position pos[AX] separates tile cells cA-1 (- side) and cA (+ side) along AX
+      const int cA = pos[AX] - P;
+      int cc[3] = {pos[0], pos[1], pos[2]};
+      cc[AX] = cA;
+      auto qcell = [&](const int* c3) -> double {
+        const int e = ((c3[2] / P) * TY + c3[1] / P) * TX + c3[0] / P;
+        return sq[e * P3 + (c3[0] % P) + P * ((c3[1] % P) + P * (c3[2] % P))];
+      };
+      if (cA < m_a * P) v -= qcell(cc);
+      if (cA > 0) {
+        cc[AX] = cA - 1;
+        v += qcell(cc);
+      } else if (h_a) {
+        const int o_1 = pos[C::A1], o_2 = pos[C::A2];
+        v += hq[o_2 * C::TA1 * P + o_1];
+      }
+    }
+    const long long g = a.off[AX] + (gorg[0] + pos[0]) +
+                        ext0 * ((gorg[1] + pos[1]) + ext1 * (gorg[2] + pos[2]));
+    __stcs(a.y + g, v);
+  }
+  __syncthreads();
 }
 
 template <int P, int TX, int TY, int TZ, int NT, bool BLOCK>
@@ -198,74 +286,90 @@ __global__ void __launch_bounds__(NT)
 affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
   constexpr int P3 = G::P3;
+  constexpr int NQR = (G::NCELL + NT - 1) / NT;
   if (a.skip && *a.skip) return;
   extern __shared__ double smem[];
   double* su = smem;                                  // component tile / Z scratch
   double* sq = su + G::SU;                            // q~ tile (element-major)
-  double* hqx = sq + (BLOCK ? G::NCELL : 0);          // halo q~ for owned -x planes [K][J]
-  double* hqy = hqx + (BLOCK ? G::HQX : 0);           // [K][I]
-  double* hqz = hqy + (BLOCK ? G::HQY : 0);           // [J][I]
-  double* sco = hqz + (BLOCK ? G::HQZ : 0);           // coefficients [(TZ+1)][(TY+1)][(TX+1)][4]
+  double* hq0 = sq + (BLOCK ? G::NCELL : 0);          // halo q~ for owned -x planes [K][J]
+  double* hq1 = hq0 + (BLOCK ? G::HQ0 : 0);           // [K][I]
+  double* hq2 = hq1 + (BLOCK ? G::HQ1 : 0);           // [J][I]
+  double* sco = hq2 + (BLOCK ? G::HQ2 : 0);           // coefficients [(TZ+1)][(TY+1)][(TX+1)][4]
 
   const int tid = threadIdx.x;
-  int t = blockIdx.x;
-  const int tx = t % a.ntile[0];
-  t /= a.ntile[0];
-  const int ty = t % a.ntile[1];
-  const int tz = t / a.ntile[1];
-  const long long NLx = a.NL[0], NLy = a.NL[1], NLz = a.NL[2];
-  const int ex0 = tx * TX, ey0 = ty * TY, ez0 = tz * TZ;
-  const int mx = (int)min((long long)TX, NLx - ex0);
-  const int my = (int)min((long long)TY, NLy - ey0);
-  const int mz = (int)min((long long)TZ, NLz - ez0);
-  const int hx = ex0 > 0, hy = ey0 > 0, hz = ez0 > 0;
-  const bool lastx = (ex0 + mx == NLx), lasty = (ey0 + my == NLy), lastz = (ez0 + mz == NLz);
-  const long long nx = a.n[0], ny = a.n[1];
-  const double* u = a.x;
+  TileInfo ti;
+  {
+    int t = blockIdx.x;
+    const int tx = t % a.ntile[0];
+    t /= a.ntile[0];
+    const int ty = t % a.ntile[1];
+    const int tz = t / a.ntile[1];
+    const int T3[3] = {TX, TY, TZ};
+    const int tt[3] = {tx, ty, tz};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      ti.e0[d] = tt[d] * T3[d];
+      ti.m[d] = (int)min((long long)T3[d], a.NL[d] - ti.e0[d]);
+      ti.h[d] = ti.e0[d] > 0;
+      ti.last[d] = (ti.e0[d] + ti.m[d] == a.NL[d]);
+    }
+  }
+  const long long NLx = a.NL[0], NLy = a.NL[1];
   const double* q = a.x + a.nrt;
 
   // ---- coefficients of the tile and its - halo ----
   for (int i = tid; i < G::NCO; i += NT) {
-    int ix = i % (TX + 1), iy = (i / (TX + 1)) % (TY + 1), iz = i / ((TX + 1) * (TY + 1));
-    long long ex = ex0 - 1 + ix, ey = ey0 - 1 + iy, ez = ez0 - 1 + iz;
-    if (ex >= 0 && ey >= 0 && ez >= 0 && ex < ex0 + mx && ey < ey0 + my && ez < ez0 + mz) {
-      const double* c = a.coef + 4 * ((ez * NLy + ey) * NLx + ex);
+    const int ix = i % (TX + 1), iy = (i / (TX + 1)) % (TY + 1), iz = i / ((TX + 1) * (TY + 1));
+    const int ex = ti.e0[0] - 1 + ix, ey = ti.e0[1] - 1 + iy, ez = ti.e0[2] - 1 + iz;
+    if (ex >= 0 && ey >= 0 && ez >= 0 && ix <= ti.m[0] && iy <= ti.m[1] && iz <= ti.m[2]) {
+      const double* c = a.coef + 4 * (((long long)ez * NLy + ey) * NLx + ex);
 #pragma unroll
       for (int k = 0; k < 4; ++k) cp_async8(sco + 4 * i + k, c + k);
     }
   }
 
-  constexpr int NQR = (G::NCELL + NT - 1) / NT;
   double acc[NQR];
 #pragma unroll
   for (int k = 0; k < NQR; ++k) acc[k] = 0.0;
 
   if constexpr (BLOCK) {
+#pragma unroll 4
     for (int i = tid; i < G::NCELL; i += NT) {
-      int e = i / P3, il = i % P3;
-      int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-      if (etx < mx && ety < my && etz < mz) {
-        long long ge = ((long long)(ez0 + etz) * NLy + (ey0 + ety)) * NLx + (ex0 + etx);
+      const int e = i / P3, il = i % P3;
+      const int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
+      if (etx < ti.m[0] && ety < ti.m[1] && etz < ti.m[2]) {
+        const long long ge =
+            ((long long)(ti.e0[2] + etz) * NLy + (ti.e0[1] + ety)) * NLx + (ti.e0[0] + etx);
         cp_async8(sq + i, q + ge * P3 + il);
       }
     }
-    if (hx)
-      for (int i = tid; i < my * P * mz * P; i += NT) {
-        int J = i % (my * P), K = i / (my * P);
-        long long ge = ((long long)(ez0 + K / P) * NLy + (ey0 + J / P)) * NLx + (ex0 - 1);
-        cp_async8(hqx + K * (TY * P) + J, q + ge * P3 + (P - 1) + P * ((J % P) + P * (K % P)));
+    // halo q~ of the - neighbour's adjacent cell layer (for D^T at the owned - planes)
+    if (ti.h[0])
+      for (int i = tid; i < G::HQ0; i += NT) {
+        const int J = i % (TY * P), K = i / (TY * P);
+        if (J < ti.m[1] * P && K < ti.m[2] * P) {
+          const long long ge = ((long long)(ti.e0[2] + K / P) * NLy + (ti.e0[1] + J / P)) * NLx +
+                               (ti.e0[0] - 1);
+          cp_async8(hq0 + i, q + ge * P3 + (P - 1) + P * ((J % P) + P * (K % P)));
+        }
       }
-    if (hy)
-      for (int i = tid; i < mx * P * mz * P; i += NT) {
-        int I = i % (mx * P), K = i / (mx * P);
-        long long ge = ((long long)(ez0 + K / P) * NLy + (ey0 - 1)) * NLx + (ex0 + I / P);
-        cp_async8(hqy + K * (TX * P) + I, q + ge * P3 + (I % P) + P * ((P - 1) + P * (K % P)));
+    if (ti.h[1])
+      for (int i = tid; i < G::HQ1; i += NT) {
+        const int I = i % (TX * P), K = i / (TX * P);
+        if (I < ti.m[0] * P && K < ti.m[2] * P) {
+          const long long ge = ((long long)(ti.e0[2] + K / P) * NLy + (ti.e0[1] - 1)) * NLx +
+                               (ti.e0[0] + I / P);
+          cp_async8(hq1 + i, q + ge * P3 + (I % P) + P * ((P - 1) + P * (K % P)));
+        }
       }
-    if (hz)
-      for (int i = tid; i < mx * P * my * P; i += NT) {
-        int I = i % (mx * P), J = i / (mx * P);
-        long long ge = ((long long)(ez0 - 1) * NLy + (ey0 + J / P)) * NLx + (ex0 + I / P);
-        cp_async8(hqz + J * (TX * P) + I, q + ge * P3 + (I % P) + P * ((J % P) + P * (P - 1)));
+    if (ti.h[2])
+      for (int i = tid; i < G::HQ2; i += NT) {
+        const int I = i % (TX * P), J = i / (TX * P);
+        if (I < ti.m[0] * P && J < ti.m[1] * P) {
+          const long long ge = ((long long)(ti.e0[2] - 1) * NLy + (ti.e0[1] + J / P)) * NLx +
+                               (ti.e0[0] + I / P);
+          cp_async8(hq2 + i, q + ge * P3 + (I % P) + P * ((J % P) + P * (P - 1)));
+        }
       }
   }
   cp_async_wait_all();
@@ -273,33 +377,73 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
 
   if constexpr (BLOCK) {
     if (a.has_z) {
-      // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e ; scratch layout [e][c][b][a] with a-row stride RQ
-      constexpr int RQ = G::RQ, EST = RQ * P * P;
+      // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e ; scratch [e][c][b][a], a-row stride RQ (odd)
+      constexpr int RQ = G::RQ, ES = G::ESZ;
+#pragma unroll 4
       for (int i = tid; i < G::NCELL; i += NT) {
-        int e = i / P3, il = i % P3;
-        su[e * EST + (il / P) * RQ + il % P] = sq[i];
+        const int e = i / P3, il = i % P3;
+        su[e * ES + (il / P) * RQ + il % P] = sq[i];
       }
       __syncthreads();
-      // a-lines: lanes over (b,c) rows [stride RQ, odd] then elements
-      hpass<P, NT>(su, tab.Mhinv, 0, P * P, RQ, G::NE, EST, 1, 0, 1);
+      // a-lines then b-lines then c-lines; one line (P values) per thread, in place
+      constexpr int NLN = G::NE * P * P;
+#pragma unroll 2
+      for (int it = tid; it < NLN; it += NT) {   // a-lines: row r = b + P c, lanes over rows
+        const int r = it % (P * P), e = it / (P * P);
+        double* b = su + e * ES + r * RQ;
+        double v[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[k] = b[k];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < P; ++j) s = fma(tab.Mhinv[i][j], v[j], s);
+          b[i] = s;
+        }
+      }
       __syncthreads();
-      // b-lines: lanes over a, then (c, e)
-      hpass<P, NT>(su, tab.Mhinv, 0, P, 1, P * G::NE, RQ * P, 1, 0, RQ);
+#pragma unroll 2
+      for (int it = tid; it < NLN; it += NT) {   // b-lines: (a, c, e), stride RQ
+        const int A = it % P, c = (it / P) % P, e = it / (P * P);
+        double* b = su + e * ES + c * RQ * P + A;
+        double v[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[k] = b[k * RQ];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < P; ++j) s = fma(tab.Mhinv[i][j], v[j], s);
+          b[i * RQ] = s;
+        }
+      }
       __syncthreads();
-      // c-lines: lanes over a, then (b, e) -- i1 = b + P e is not affine in memory, so run
-      // over b explicitly
-      for (int b = 0; b < P; ++b)
-        hpass<P, NT>(su, tab.Mhinv, b * RQ, P, 1, G::NE, EST, 1, 0, RQ * P);
+#pragma unroll 2
+      for (int it = tid; it < NLN; it += NT) {   // c-lines: (a, b, e), stride RQ P
+        const int A = it % P, bb = (it / P) % P, e = it / (P * P);
+        double* b = su + e * ES + bb * RQ + A;
+        double v[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[k] = b[k * RQ * P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < P; ++j) s = fma(tab.Mhinv[i][j], v[j], s);
+          b[i * RQ * P] = s;
+        }
+      }
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < NQR; ++k) {
-        int i = tid + k * NT;
+        const int i = tid + k * NT;
         if (i < G::NCELL) {
-          int e = i / P3, il = i % P3;
-          int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-          if (etx < mx && ety < my && etz < mz) {
-            double z = sco[4 * (((etz + 1) * (TY + 1) + (ety + 1)) * (TX + 1) + (etx + 1)) + 3];
-            acc[k] = -z * su[e * EST + (il / P) * RQ + il % P];
+          const int e = i / P3, il = i % P3;
+          const int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
+          if (etx < ti.m[0] && ety < ti.m[1] && etz < ti.m[2]) {
+            const double z = sco[4 * (((etz + 1) * (TY + 1) + (ety + 1)) * (TX + 1) + (etx + 1)) + 3];
+            acc[k] = -z * su[e * ES + (il / P) * RQ + il % P];
           }
         }
       }
@@ -307,154 +451,31 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     }
   }
 
-  // ======================= x component =======================
-  {
-    constexpr int XI = G::XI, XJ = G::XJ;
-    const int ilo = hx ? 0 : P;
-    const int nI = (mx + 1) * P + 1 - ilo;
-    const int nJ = my * P, nK = mz * P;
-    const long long gI0 = (long long)(ex0 - 1) * P;
-    for (int i = tid; i < nI * nJ * nK; i += NT) {
-      int I = i % nI + ilo, r = i / nI, J = r % nJ, K = r / nJ;
-      long long g = a.off[0] + (gI0 + I) + (nx + 1) * ((long long)(ey0 * P + J) + ny * (ez0 * P + K));
-      cp_async8(su + (K * XJ + J) * XI + I, u + g);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if constexpr (BLOCK) {
-#pragma unroll
-      for (int k = 0; k < NQR; ++k) {
-        int i = tid + k * NT;
-        int e = i / P3, il = i % P3;
-        int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-        if (i < G::NCELL && etx < mx && ety < my && etz < mz) {
-          int A = il % P, B = (il / P) % P, C = il / (P * P);
-          const double* s = su + ((etz * P + C) * XJ + ety * P + B) * XI + (etx + 1) * P + A;
-          acc[k] += s[1] - s[0];
-        }
-      }
-      __syncthreads();
-    }
-    hpass<P, NT>(su, tab.Mh, ilo, nI, 1, nJ, XI, mz, P * XI * XJ, XI * XJ);      // K
-    __syncthreads();
-    hpass<P, NT>(su, tab.Mh, ilo, nI, 1, nK, XI * XJ, my, P * XI, XI);           // J
-    __syncthreads();
-    lpass<P, TX, TY, TZ, NT, 0, BLOCK>(su, sq, hqx, sco, tab, nJ, XI, nK, XI * XJ, 1, mx, hx,
-                                      lastx);
-    __syncthreads();
-    const int nO = mx * P + (lastx ? 1 : 0);
-    for (int i = tid; i < nO * nJ * nK; i += NT) {
-      int I = i % nO + P, r = i / nO, J = r % nJ, K = r / nJ;
-      long long g = a.off[0] + (gI0 + I) + (nx + 1) * ((long long)(ey0 * P + J) + ny * (ez0 * P + K));
-      a.y[g] = su[(K * XJ + J) * XI + I];
-    }
-    __syncthreads();
-  }
-  // ======================= y component =======================
-  {
-    constexpr int YI = G::YI, YJ = G::YJ;
-    const int jlo = hy ? 0 : P;
-    const int nJ = (my + 1) * P + 1 - jlo;
-    const int nI = mx * P, nK = mz * P;
-    const long long gJ0 = (long long)(ey0 - 1) * P;
-    for (int i = tid; i < nI * nJ * nK; i += NT) {
-      int I = i % nI, r = i / nI, J = r % nJ + jlo, K = r / nJ;
-      long long g = a.off[1] + (ex0 * P + I) + nx * ((gJ0 + J) + (ny + 1) * (long long)(ez0 * P + K));
-      cp_async8(su + (K * YJ + J) * YI + I, u + g);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if constexpr (BLOCK) {
-#pragma unroll
-      for (int k = 0; k < NQR; ++k) {
-        int i = tid + k * NT;
-        int e = i / P3, il = i % P3;
-        int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-        if (i < G::NCELL && etx < mx && ety < my && etz < mz) {
-          int A = il % P, B = (il / P) % P, C = il / (P * P);
-          const double* s = su + ((etz * P + C) * YJ + (ety + 1) * P + B) * YI + etx * P + A;
-          acc[k] += s[YI] - s[0];
-        }
-      }
-      __syncthreads();
-    }
-    hpass<P, NT>(su, tab.Mh, jlo * YI, nJ, YI, nK, YI * YJ, mx, P, 1);           // I
-    __syncthreads();
-    hpass<P, NT>(su, tab.Mh, jlo * YI, nI, 1, nJ, YI, mz, P * YI * YJ, YI * YJ);  // K
-    __syncthreads();
-    lpass<P, TX, TY, TZ, NT, 1, BLOCK>(su, sq, hqy, sco, tab, nI, 1, nK, YI * YJ, YI, my, hy,
-                                      lasty);
-    __syncthreads();
-    const int nO = my * P + (lasty ? 1 : 0);
-    for (int i = tid; i < nI * nO * nK; i += NT) {
-      int I = i % nI, r = i / nI, J = r % nO + P, K = r / nO;
-      long long g = a.off[1] + (ex0 * P + I) + nx * ((gJ0 + J) + (ny + 1) * (long long)(ez0 * P + K));
-      a.y[g] = su[(K * YJ + J) * YI + I];
-    }
-    __syncthreads();
-  }
-  // ======================= z component =======================
-  {
-    constexpr int ZI = G::ZI, ZJ = G::ZJ;
-    const int klo = hz ? 0 : P;
-    const int nK = (mz + 1) * P + 1 - klo;
-    const int nI = mx * P, nJ = my * P;
-    const long long gK0 = (long long)(ez0 - 1) * P;
-    for (int i = tid; i < nI * nJ * nK; i += NT) {
-      int I = i % nI, r = i / nI, J = r % nJ, K = r / nJ + klo;
-      long long g = a.off[2] + (ex0 * P + I) + nx * ((long long)(ey0 * P + J) + ny * (gK0 + K));
-      cp_async8(su + (K * ZJ + J) * ZI + I, u + g);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if constexpr (BLOCK) {
-#pragma unroll
-      for (int k = 0; k < NQR; ++k) {
-        int i = tid + k * NT;
-        int e = i / P3, il = i % P3;
-        int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-        if (i < G::NCELL && etx < mx && ety < my && etz < mz) {
-          int A = il % P, B = (il / P) % P, C = il / (P * P);
-          const double* s = su + (((etz + 1) * P + C) * ZJ + ety * P + B) * ZI + etx * P + A;
-          acc[k] += s[ZI * ZJ] - s[0];
-        }
-      }
-      __syncthreads();
-    }
-    hpass<P, NT>(su, tab.Mh, klo * ZI * ZJ, nJ, ZI, nK, ZI * ZJ, mx, P, 1);      // I
-    __syncthreads();
-    hpass<P, NT>(su, tab.Mh, klo * ZI * ZJ, nI, 1, nK, ZI * ZJ, my, P * ZI, ZI);  // J
-    __syncthreads();
-    lpass<P, TX, TY, TZ, NT, 2, BLOCK>(su, sq, hqz, sco, tab, nI, 1, nJ, ZI, ZI * ZJ, mz, hz,
-                                      lastz);
-    __syncthreads();
-    const int nO = mz * P + (lastz ? 1 : 0);
-    for (int i = tid; i < nI * nJ * nO; i += NT) {
-      int I = i % nI, r = i / nI, J = r % nJ, K = r / nJ + P;
-      long long g = a.off[2] + (ex0 * P + I) + nx * ((long long)(ey0 * P + J) + ny * (gK0 + K));
-      a.y[g] = su[(K * ZJ + J) * ZI + I];
-    }
-  }
-  // ======================= L2 block =======================
+  component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, su, sq, hq0, sco, acc);
+  component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, su, sq, hq1, sco, acc);
+  component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, su, sq, hq2, sco, acc);
+
   if constexpr (BLOCK) {
     double* yq = a.y + a.nrt;
 #pragma unroll
     for (int k = 0; k < NQR; ++k) {
-      int i = tid + k * NT;
-      int e = i / P3, il = i % P3;
-      int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-      if (i < G::NCELL && etx < mx && ety < my && etz < mz) {
-        long long ge = ((long long)(ez0 + etz) * NLy + (ey0 + ety)) * NLx + (ex0 + etx);
-        yq[ge * P3 + il] = acc[k];
+      const int i = tid + k * NT;
+      if (i < G::NCELL) {
+        const int e = i / P3, il = i % P3;
+        const int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
+        if (etx < ti.m[0] && ety < ti.m[1] && etz < ti.m[2]) {
+          const long long ge =
+              ((long long)(ti.e0[2] + etz) * NLy + (ti.e0[1] + ety)) * NLx + (ti.e0[0] + etx);
+          __stcs(yq + ge * P3 + il, acc[k]);
+        }
       }
     }
   }
 }
 
-template <int P, int TX, int TY, int TZ, bool BLOCK>
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK>
 cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
-  constexpr int NT = 256;
   using G = Geo<P, TX, TY, TZ>;
   AffArgs a;
   a.x = x; a.y = y; a.coef = h->d_coef;
@@ -483,12 +504,12 @@ template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
                      cudaStream_t s) {
   switch (h->p) {
-    case 1: return launch_t<1, 8, 8, 8, BLOCK>(h, x, y, k, s);
-    case 2: return launch_t<2, 8, 8, 4, BLOCK>(h, x, y, k, s);
-    case 3: return launch_t<3, 4, 4, 4, BLOCK>(h, x, y, k, s);
-    case 4: return launch_t<4, 4, 4, 2, BLOCK>(h, x, y, k, s);
-    case 5: return launch_t<5, 4, 2, 2, BLOCK>(h, x, y, k, s);
-    case 6: return launch_t<6, 2, 2, 2, BLOCK>(h, x, y, k, s);
+    case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
+    case 2: return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
+    case 3: return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+    case 4: return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+    case 5: return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
+    case 6: return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;
 }
