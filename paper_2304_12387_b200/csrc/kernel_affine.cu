@@ -68,14 +68,16 @@ struct Geo {
   static constexpr int P3 = P * P * P;
   static constexpr int NE = TX * TY * TZ;
   static constexpr int NCELL = NE * P3;
-  static constexpr int RQ = odd_up(P);          // padded a-row of the Z scratch
-  static constexpr int ESZ = RQ * P * P;        // element stride of the Z scratch
+  // cell tile (subcell-major, odd-padded): cell (X,Y,Z) at X + Q1 Y + Q2 Z
+  static constexpr int CX = TX * P, CY = TY * P, CZ = TZ * P;
+  static constexpr int Q1 = odd_up(CX), Q2 = Q1 * odd_up(CY);
+  static constexpr int SQSIZE = Q2 * CZ;
   static constexpr int SU = cmax(cmax(CG<P, TX, TY, TZ, 0>::SIZE, CG<P, TX, TY, TZ, 1>::SIZE),
-                                 cmax(CG<P, TX, TY, TZ, 2>::SIZE, NE * ESZ));
-  static constexpr int HQ0 = TY * P * TZ * P, HQ1 = TX * P * TZ * P, HQ2 = TX * P * TY * P;
+                                 cmax(CG<P, TX, TY, TZ, 2>::SIZE, SQSIZE));
+  static constexpr int HQ0 = CY * CZ, HQ1 = CX * CZ, HQ2 = CX * CY;
   static constexpr int NCO = (TX + 1) * (TY + 1) * (TZ + 1);
   static constexpr size_t smem_doubles(bool block) {
-    return (size_t)SU + (block ? (size_t)NCELL + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
+    return (size_t)SU + (block ? (size_t)SQSIZE + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
   }
 };
 
@@ -99,6 +101,48 @@ struct TileInfo {
   int last[3];  // tile touches the + domain boundary
 };
 
+// Row loop: rows (i1 < R1, i2 < R2) of L contiguous entries; lanes run along the row and
+// rows shorter than 16 are packed several per warp.  f(i0, i1, i2) for every entry.
+template <int NT, int L, int R1, int R2, class F>
+__device__ __forceinline__ void rows(F&& f) {
+  static_assert(L <= 32, "row longer than a warp");
+  constexpr int LP = L <= 2 ? 2 : L <= 4 ? 4 : L <= 8 ? 8 : L <= 16 ? 16 : 32;
+  constexpr int RPI = 32 / LP;
+  constexpr int NW = NT / 32;
+  constexpr int NR = R1 * R2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % LP, rs = lane / LP;
+  if (c >= L) return;
+#pragma unroll 2
+  for (int rb = warp * RPI; rb < NR; rb += NW * RPI) {
+    const int r = rb + rs;
+    if (r < NR) f(c, r % R1, r / R1);
+  }
+}
+
+// In-place element-local contraction with a P x P matrix along one axis.  Element k of line
+// (i0, i1, blk) lives at s[off + i0*s0 + i1*s1 + blk*sb + k*se]; lanes run over i0 first.
+template <int P, int NT>
+__device__ __forceinline__ void hpass(double* s, const double (*M)[MAXP], int off, int n0,
+                                      int s0, int n1, int s1, int nb, int sb, int se) {
+  const int total = n0 * n1 * nb;
+#pragma unroll 2
+  for (int it = threadIdx.x; it < total; it += NT) {
+    const int i0 = it % n0, r = it / n0, i1 = r % n1, blk = r / n1;
+    double* b = s + off + i0 * s0 + i1 * s1 + blk * sb;
+    double v[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) v[k] = b[k * se];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < P; ++j) t = fma(M[i][j], v[j], t);
+      b[i * se] = t;
+    }
+  }
+}
+
 // -------- one component phase (AX) --------------------------------------------------------
 template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK>
 __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
@@ -106,51 +150,44 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
                                           const double* hq, const double* sco, double* acc) {
   using C = CG<P, TX, TY, TZ, AX>;
   using G = Geo<P, TX, TY, TZ>;
-  constexpr int P3 = G::P3;
   constexpr int NQR = (G::NCELL + NT - 1) / NT;
   const int tid = threadIdx.x;
-  const double* __restrict__ u = a.x;
-  // global extents of the component-AX face grid
+  // global extents of the component-AX face grid and the tile origin (position 0)
   const long long ext0 = a.n[0] + (AX == 0), ext1 = a.n[1] + (AX == 1);
-  long long gorg[3];   // global subcell coordinate of smem position 0 along each axis
+  const long long ext01 = ext0 * ext1;
+  long long gorg[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) gorg[d] = (long long)(ti.e0[d] - (d == AX ? 1 : 0)) * P;
+  const long long gtile = a.off[AX] + gorg[0] + ext0 * (gorg[1] + ext1 * gorg[2]);
   const int lo_a = ti.h[AX] ? 0 : P;                  // first loaded position along AX
   const int hi_a = (ti.m[AX] + 1) * P;                // last valid position along AX
   int hi_o[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) hi_o[d] = ti.m[d] * P;  // valid positions < hi_o (other axes)
 
-  // ---- load (cp.async, 8 B) ----
-  constexpr int NLD = C::E0 * C::E1 * C::E2;
-#pragma unroll 4
-  for (int it = tid; it < NLD; it += NT) {
-    const int i0 = it % C::E0, i1 = (it / C::E0) % C::E1, i2 = it / (C::E0 * C::E1);
-    const int pos[3] = {i0, i1, i2};
-    bool ok = true;
+  // ---- load (cp.async, 8 B), warp per row ----
+  {
+    const double* ut = a.x + gtile;
+    rows<NT, C::E0, C::E1, C::E2>([&](int i0, int i1, int i2) {
+      const int pos[3] = {i0, i1, i2};
+      bool ok = true;
 #pragma unroll
-    for (int d = 0; d < 3; ++d)
-      ok = ok && (d == AX ? (pos[d] >= lo_a && pos[d] <= hi_a) : (pos[d] < hi_o[d]));
-    if (ok) {
-      long long g = a.off[AX] + (gorg[0] + i0) + ext0 * ((gorg[1] + i1) + ext1 * (gorg[2] + i2));
-      cp_async8(su + i0 + C::S1 * i1 + C::S2 * i2, u + g);
-    }
+      for (int d = 0; d < 3; ++d)
+        ok = ok && (d == AX ? (pos[d] >= lo_a && pos[d] <= hi_a) : (pos[d] < hi_o[d]));
+      if (ok) cp_async8(su + i0 + C::S1 * i1 + C::S2 * i2, ut + (i2 * ext01 + i1 * ext0 + i0));
+    });
   }
   cp_async_wait_all();
   __syncthreads();
 
-  // ---- D u (this component's two faces of every owned cell), from the raw values ----
+  // ---- D u: this component's two faces of every owned cell (subcell order, lanes along X) ----
   if constexpr (BLOCK) {
 #pragma unroll
     for (int k = 0; k < NQR; ++k) {
       const int i = tid + k * NT;
       if (i < G::NCELL) {
-        const int e = i / P3, il = i % P3;
-        const int et[3] = {e % TX, (e / TX) % TY, e / (TX * TY)};
-        const int lc[3] = {il % P, (il / P) % P, il / (P * P)};
-        int pos[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) pos[d] = et[d] * P + lc[d] + (d == AX ? P : 0);
+        int pos[3] = {i % G::CX, (i / G::CX) % G::CY, i / (G::CX * G::CY)};
+        pos[AX] += P;
         const double* s = su + pos[0] + C::S1 * pos[1] + C::S2 * pos[2];
         acc[k] += s[C::SA] - s[0];
       }
@@ -202,17 +239,15 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     int ec[3];   // element coordinates (in-tile) of this line; ec[AX] set per element
     ec[C::A1] = l1 / P;
     ec[C::A2] = l2 / P;
-    auto cof = [&](int eax) -> double {
-      int c3[3] = {ec[0], ec[1], ec[2]};
-      c3[AX] = eax;
-      return sco[4 * (((c3[2] + 1) * (TY + 1) + (c3[1] + 1)) * (TX + 1) + (c3[0] + 1)) + AX];
-    };
+    ec[AX] = 0;
+    const double* cbase = sco + 4 * (((ec[2] + 1) * (TY + 1) + (ec[1] + 1)) * (TX + 1) + (ec[0] + 1)) + AX;
+    constexpr int CSTEP = 4 * ((AX == 0) ? 1 : (AX == 1) ? (TX + 1) : (TX + 1) * (TY + 1));
     double carry = 0.0;
     if (h_a) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], line[j * C::SA], s);
-      carry = cof(-1) * s;
+      carry = cbase[-CSTEP] * s;
     }
 #pragma unroll
     for (int et = 0; et < C::TA; ++et) {
@@ -221,7 +256,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
         double v[P + 1];
 #pragma unroll
         for (int i = 0; i <= P; ++i) v[i] = eb[i * C::SA];
-        const double c = cof(et);
+        const double c = cbase[et * CSTEP];
 #pragma unroll
         for (int i = 0; i < P; ++i) {
           double s = 0.0;
@@ -239,45 +274,35 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
   __syncthreads();
 
-  // ---- copy-out of the owned planes, + D^T q~ (coalesced, streaming stores) ----
+  // ---- copy-out of the owned planes + D^T q~ (warp per row, streaming stores) ----
   constexpr int NOA = C::TA * P + 1;          // candidate owned positions along AX
   constexpr int NO0 = (AX == 0) ? NOA : C::E0;
   constexpr int NO1 = (AX == 1) ? NOA : C::E1;
   constexpr int NO2 = (AX == 2) ? NOA : C::E2;
   const int own_hi = (m_a + 1) * P + (ti.last[AX] ? 1 : 0);   // exclusive
-#pragma unroll 4
-  for (int it = tid; it < NO0 * NO1 * NO2; it += NT) {
-    const int o0 = it % NO0, o1 = (it / NO0) % NO1, o2 = it / (NO0 * NO1);
+  double* yt = a.y + gtile;
+  rows<NT, NO0, NO1, NO2>([&](int o0, int o1, int o2) {
     int pos[3] = {o0, o1, o2};
     pos[AX] += P;
     bool ok = pos[AX] < own_hi;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
       if (d != AX) ok = ok && pos[d] < hi_o[d];
-    if (!ok) continue;
+    if (!ok) return;
     double v = su[pos[0] + C::S1 * pos[1] + C::S2 * pos[2]];
     if constexpr (BLOCK) {
-      // face at position pos[AX] separates tile cells cA-1 (- side) and cA (+ side) along AX
-      const int cA = pos[AX] - P;
+      // the face at pos[AX] separates tile cells cA-1 (- side) and cA (+ side) along AX
       int cc[3] = {pos[0], pos[1], pos[2]};
+      const int cA = pos[AX] - P;
       cc[AX] = cA;
-      auto qcell = [&](const int* c3) -> double {
-        const int e = ((c3[2] / P) * TY + c3[1] / P) * TX + c3[0] / P;
-        return sq[e * P3 + (c3[0] % P) + P * ((c3[1] % P) + P * (c3[2] % P))];
-      };
-      if (cA < m_a * P) v -= qcell(cc);
-      if (cA > 0) {
-        cc[AX] = cA - 1;
-        v += qcell(cc);
-      } else if (h_a) {
-        const int o_1 = pos[C::A1], o_2 = pos[C::A2];
-        v += hq[o_2 * C::TA1 * P + o_1];
-      }
+      const double* qc = sq + cc[0] + G::Q1 * cc[1] + G::Q2 * cc[2];
+      constexpr int QS = (AX == 0) ? 1 : (AX == 1) ? G::Q1 : G::Q2;
+      if (cA < m_a * P) v -= qc[0];
+      if (cA > 0) v += qc[-QS];
+      else if (h_a) v += hq[pos[C::A2] * (C::TA1 * P) + pos[C::A1]];
     }
-    const long long g = a.off[AX] + (gorg[0] + pos[0]) +
-                        ext0 * ((gorg[1] + pos[1]) + ext1 * (gorg[2] + pos[2]));
-    __stcs(a.y + g, v);
-  }
+    __stcs(yt + ((long long)pos[2] * ext01 + pos[1] * ext0 + pos[0]), v);
+  });
   __syncthreads();
 }
 
@@ -287,16 +312,18 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
   constexpr int P3 = G::P3;
   constexpr int NQR = (G::NCELL + NT - 1) / NT;
+  constexpr int NW = NT / 32;
   if (a.skip && *a.skip) return;
   extern __shared__ double smem[];
-  double* su = smem;                                  // component tile / Z scratch
-  double* sq = su + G::SU;                            // q~ tile (element-major)
-  double* hq0 = sq + (BLOCK ? G::NCELL : 0);          // halo q~ for owned -x planes [K][J]
+  double* su = smem;                                  // component tile / Z scratch / y_q staging
+  double* sq = su + G::SU;                            // q~ tile, subcell-major
+  double* hq0 = sq + (BLOCK ? G::SQSIZE : 0);         // halo q~ for owned -x planes [K][J]
   double* hq1 = hq0 + (BLOCK ? G::HQ0 : 0);           // [K][I]
   double* hq2 = hq1 + (BLOCK ? G::HQ1 : 0);           // [J][I]
   double* sco = hq2 + (BLOCK ? G::HQ2 : 0);           // coefficients [(TZ+1)][(TY+1)][(TX+1)][4]
 
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   TileInfo ti;
   {
     int t = blockIdx.x;
@@ -316,6 +343,12 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   }
   const long long NLx = a.NL[0], NLy = a.NL[1];
   const double* q = a.x + a.nrt;
+  auto elem_ok = [&](int ex, int ey, int ez) {
+    return ex < ti.m[0] && ey < ti.m[1] && ez < ti.m[2];
+  };
+  auto gelem = [&](int ex, int ey, int ez) -> long long {
+    return ((long long)(ti.e0[2] + ez) * NLy + (ti.e0[1] + ey)) * NLx + (ti.e0[0] + ex);
+  };
 
   // ---- coefficients of the tile and its - halo ----
   for (int i = tid; i < G::NCO; i += NT) {
@@ -333,20 +366,21 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   for (int k = 0; k < NQR; ++k) acc[k] = 0.0;
 
   if constexpr (BLOCK) {
-#pragma unroll 4
-    for (int i = tid; i < G::NCELL; i += NT) {
-      const int e = i / P3, il = i % P3;
-      const int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-      if (etx < ti.m[0] && ety < ti.m[1] && etz < ti.m[2]) {
-        const long long ge =
-            ((long long)(ti.e0[2] + etz) * NLy + (ti.e0[1] + ety)) * NLx + (ti.e0[0] + etx);
-        cp_async8(sq + i, q + ge * P3 + il);
+    // q~ tile: warp per element, contiguous P^3 run -> subcell-major smem
+    for (int e = warp; e < G::NE; e += NW) {
+      const int ex = e % TX, ey = (e / TX) % TY, ez = e / (TX * TY);
+      if (elem_ok(ex, ey, ez)) {
+        const double* qe = q + gelem(ex, ey, ez) * P3;
+        double* se = sq + ex * P + G::Q1 * (ey * P) + G::Q2 * (ez * P);
+#pragma unroll
+        for (int il = lane; il < P3; il += 32)
+          cp_async8(se + il % P + G::Q1 * ((il / P) % P) + G::Q2 * (il / (P * P)), qe + il);
       }
     }
     // halo q~ of the - neighbour's adjacent cell layer (for D^T at the owned - planes)
     if (ti.h[0])
       for (int i = tid; i < G::HQ0; i += NT) {
-        const int J = i % (TY * P), K = i / (TY * P);
+        const int J = i % G::CY, K = i / G::CY;
         if (J < ti.m[1] * P && K < ti.m[2] * P) {
           const long long ge = ((long long)(ti.e0[2] + K / P) * NLy + (ti.e0[1] + J / P)) * NLx +
                                (ti.e0[0] - 1);
@@ -355,7 +389,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       }
     if (ti.h[1])
       for (int i = tid; i < G::HQ1; i += NT) {
-        const int I = i % (TX * P), K = i / (TX * P);
+        const int I = i % G::CX, K = i / G::CX;
         if (I < ti.m[0] * P && K < ti.m[2] * P) {
           const long long ge = ((long long)(ti.e0[2] + K / P) * NLy + (ti.e0[1] - 1)) * NLx +
                                (ti.e0[0] + I / P);
@@ -364,7 +398,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       }
     if (ti.h[2])
       for (int i = tid; i < G::HQ2; i += NT) {
-        const int I = i % (TX * P), J = i / (TX * P);
+        const int I = i % G::CX, J = i / G::CX;
         if (I < ti.m[0] * P && J < ti.m[1] * P) {
           const long long ge = ((long long)(ti.e0[2] - 1) * NLy + (ti.e0[1] + J / P)) * NLx +
                                (ti.e0[0] + I / P);
@@ -377,74 +411,24 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
 
   if constexpr (BLOCK) {
     if (a.has_z) {
-      // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e ; scratch [e][c][b][a], a-row stride RQ (odd)
-      constexpr int RQ = G::RQ, ES = G::ESZ;
-#pragma unroll 4
-      for (int i = tid; i < G::NCELL; i += NT) {
-        const int e = i / P3, il = i % P3;
-        su[e * ES + (il / P) * RQ + il % P] = sq[i];
-      }
+      // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in su (same subcell-major layout as sq)
+      for (int i = tid; i < G::SQSIZE; i += NT) su[i] = sq[i];
       __syncthreads();
-      // a-lines then b-lines then c-lines; one line (P values) per thread, in place
-      constexpr int NLN = G::NE * P * P;
-#pragma unroll 2
-      for (int it = tid; it < NLN; it += NT) {   // a-lines: row r = b + P c, lanes over rows
-        const int r = it % (P * P), e = it / (P * P);
-        double* b = su + e * ES + r * RQ;
-        double v[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) v[k] = b[k];
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < P; ++j) s = fma(tab.Mhinv[i][j], v[j], s);
-          b[i] = s;
-        }
-      }
+      // X-lines (lanes over Y, odd stride Q1), Y-lines and Z-lines (lanes over X)
+      hpass<P, NT>(su, tab.Mhinv, 0, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
       __syncthreads();
-#pragma unroll 2
-      for (int it = tid; it < NLN; it += NT) {   // b-lines: (a, c, e), stride RQ
-        const int A = it % P, c = (it / P) % P, e = it / (P * P);
-        double* b = su + e * ES + c * RQ * P + A;
-        double v[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) v[k] = b[k * RQ];
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < P; ++j) s = fma(tab.Mhinv[i][j], v[j], s);
-          b[i * RQ] = s;
-        }
-      }
+      hpass<P, NT>(su, tab.Mhinv, 0, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
       __syncthreads();
-#pragma unroll 2
-      for (int it = tid; it < NLN; it += NT) {   // c-lines: (a, b, e), stride RQ P
-        const int A = it % P, bb = (it / P) % P, e = it / (P * P);
-        double* b = su + e * ES + bb * RQ + A;
-        double v[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) v[k] = b[k * RQ * P];
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < P; ++j) s = fma(tab.Mhinv[i][j], v[j], s);
-          b[i * RQ * P] = s;
-        }
-      }
+      hpass<P, NT>(su, tab.Mhinv, 0, G::CX, 1, G::CY, G::Q1, TZ, P * G::Q2, G::Q2);
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < NQR; ++k) {
         const int i = tid + k * NT;
         if (i < G::NCELL) {
-          const int e = i / P3, il = i % P3;
-          const int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-          if (etx < ti.m[0] && ety < ti.m[1] && etz < ti.m[2]) {
-            const double z = sco[4 * (((etz + 1) * (TY + 1) + (ety + 1)) * (TX + 1) + (etx + 1)) + 3];
-            acc[k] = -z * su[e * ES + (il / P) * RQ + il % P];
-          }
+          const int X = i % G::CX, Y = (i / G::CX) % G::CY, Z = i / (G::CX * G::CY);
+          const int ex = X / P, ey = Y / P, ez = Z / P;
+          const double z = sco[4 * (((ez + 1) * (TY + 1) + (ey + 1)) * (TX + 1) + (ex + 1)) + 3];
+          acc[k] = -z * su[X + G::Q1 * Y + G::Q2 * Z];
         }
       }
       __syncthreads();
@@ -456,18 +440,25 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, su, sq, hq2, sco, acc);
 
   if constexpr (BLOCK) {
-    double* yq = a.y + a.nrt;
+    // stage y_q through smem (subcell-major), then store element-contiguous runs
 #pragma unroll
     for (int k = 0; k < NQR; ++k) {
       const int i = tid + k * NT;
       if (i < G::NCELL) {
-        const int e = i / P3, il = i % P3;
-        const int etx = e % TX, ety = (e / TX) % TY, etz = e / (TX * TY);
-        if (etx < ti.m[0] && ety < ti.m[1] && etz < ti.m[2]) {
-          const long long ge =
-              ((long long)(ti.e0[2] + etz) * NLy + (ti.e0[1] + ety)) * NLx + (ti.e0[0] + etx);
-          __stcs(yq + ge * P3 + il, acc[k]);
-        }
+        const int X = i % G::CX, Y = (i / G::CX) % G::CY, Z = i / (G::CX * G::CY);
+        su[X + G::Q1 * Y + G::Q2 * Z] = acc[k];
+      }
+    }
+    __syncthreads();
+    double* yq = a.y + a.nrt;
+    for (int e = warp; e < G::NE; e += NW) {
+      const int ex = e % TX, ey = (e / TX) % TY, ez = e / (TX * TY);
+      if (elem_ok(ex, ey, ez)) {
+        double* ye = yq + gelem(ex, ey, ez) * P3;
+        const double* se = su + ex * P + G::Q1 * (ey * P) + G::Q2 * (ez * P);
+#pragma unroll
+        for (int il = lane; il < P3; il += 32)
+          __stcs(ye + il, se[il % P + G::Q1 * ((il / P) % P) + G::Q2 * (il / (P * P))]);
       }
     }
   }
