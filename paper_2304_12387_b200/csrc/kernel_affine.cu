@@ -25,6 +25,8 @@
 //    L2 DOFs is contiguous in HBM).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace hdiv {
@@ -101,44 +103,57 @@ struct TileInfo {
   int last[3];  // tile touches the + domain boundary
 };
 
-// Row loop: rows (i1 < R1, i2 < R2) of L contiguous entries; lanes run along the row and
-// rows shorter than 16 are packed several per warp.  f(i0, i1, i2) for every entry.
-template <int NT, int L, int R1, int R2, class F>
-__device__ __forceinline__ void rows(F&& f) {
+// Row loops.  The box (i0 < L, i1 < R1, i2 < R2) is contiguous along i0 in both smem and HBM;
+// warps take i2 planes round-robin, lanes run along rows (rows shorter than 16 are packed
+// RPI per warp), and the row loop is unrolled with incremental addresses so each entry costs
+// a predicate, an address add and the access.  act(global_ptr, smem_ptr) per valid entry;
+// ok0(i0) / ok1(i1) / ok2(i2) are the per-axis validity predicates.
+template <int NT, int L, int R1, int R2, int S1, int S2, class GT, class OK0, class OK1,
+          class OK2, class ACT>
+__device__ __forceinline__ void rows(GT* gbase, long long ext0, long long ext01, double* sbase,
+                                     OK0 ok0, OK1 ok1, OK2 ok2, ACT act) {
   static_assert(L <= 32, "row longer than a warp");
   constexpr int LP = L <= 2 ? 2 : L <= 4 ? 4 : L <= 8 ? 8 : L <= 16 ? 16 : 32;
   constexpr int RPI = 32 / LP;
+  constexpr int NJ = (R1 + RPI - 1) / RPI;
   constexpr int NW = NT / 32;
-  constexpr int NR = R1 * R2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LP, rs = lane / LP;
-  if (c >= L) return;
-#pragma unroll 2
-  for (int rb = warp * RPI; rb < NR; rb += NW * RPI) {
-    const int r = rb + rs;
-    if (r < NR) f(c, r % R1, r / R1);
+  if (c >= L || !ok0(c)) return;
+  const long long gstep = RPI * ext0;
+  for (int i2 = warp; i2 < R2; i2 += NW) {
+    if (!ok2(i2)) continue;
+    GT* g = gbase + (i2 * ext01 + rs * ext0 + c);
+    double* s = sbase + (i2 * S2 + rs * S1 + c);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int i1 = j * RPI + rs;
+      if (i1 < R1 && ok1(i1)) act(g, s + j * RPI * S1);
+      g += gstep;
+    }
   }
 }
 
-// In-place element-local contraction with a P x P matrix along one axis.  Element k of line
-// (i0, i1, blk) lives at s[off + i0*s0 + i1*s1 + blk*sb + k*se]; lanes run over i0 first.
+// Element-local contraction with a P x P matrix along one axis, dst <- M src (may alias).
+// Element k of line (i0, i1, blk) lives at off + i0*s0 + i1*s1 + blk*sb + k*se; lanes run
+// over i0 first.
 template <int P, int NT>
-__device__ __forceinline__ void hpass(double* s, const double (*M)[MAXP], int off, int n0,
-                                      int s0, int n1, int s1, int nb, int sb, int se) {
+__device__ __forceinline__ void hpass(const double* src, double* dst, const double (*M)[MAXP],
+                                      int n0, int s0, int n1, int s1, int nb, int sb, int se) {
   const int total = n0 * n1 * nb;
 #pragma unroll 2
   for (int it = threadIdx.x; it < total; it += NT) {
     const int i0 = it % n0, r = it / n0, i1 = r % n1, blk = r / n1;
-    double* b = s + off + i0 * s0 + i1 * s1 + blk * sb;
+    const int o = i0 * s0 + i1 * s1 + blk * sb;
     double v[P];
 #pragma unroll
-    for (int k = 0; k < P; ++k) v[k] = b[k * se];
+    for (int k = 0; k < P; ++k) v[k] = src[o + k * se];
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       double t = 0.0;
 #pragma unroll
       for (int j = 0; j < P; ++j) t = fma(M[i][j], v[j], t);
-      b[i * se] = t;
+      dst[o + i * se] = t;
     }
   }
 }
@@ -161,26 +176,21 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   const long long gtile = a.off[AX] + gorg[0] + ext0 * (gorg[1] + ext1 * gorg[2]);
   const int lo_a = ti.h[AX] ? 0 : P;                  // first loaded position along AX
   const int hi_a = (ti.m[AX] + 1) * P;                // last valid position along AX
-  int hi_o[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) hi_o[d] = ti.m[d] * P;  // valid positions < hi_o (other axes)
+  const int hi0 = ti.m[0] * P, hi1 = ti.m[1] * P, hi2 = ti.m[2] * P;
+  auto okd = [&](int d, int pos) {
+    if (d == AX) return pos >= lo_a && pos <= hi_a;
+    return pos < (d == 0 ? hi0 : d == 1 ? hi1 : hi2);
+  };
 
-  // ---- load (cp.async, 8 B), warp per row ----
-  {
-    const double* ut = a.x + gtile;
-    rows<NT, C::E0, C::E1, C::E2>([&](int i0, int i1, int i2) {
-      const int pos[3] = {i0, i1, i2};
-      bool ok = true;
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-        ok = ok && (d == AX ? (pos[d] >= lo_a && pos[d] <= hi_a) : (pos[d] < hi_o[d]));
-      if (ok) cp_async8(su + i0 + C::S1 * i1 + C::S2 * i2, ut + (i2 * ext01 + i1 * ext0 + i0));
-    });
-  }
+  // ---- load (cp.async, 8 B) ----
+  rows<NT, C::E0, C::E1, C::E2, C::S1, C::S2>(
+      a.x + gtile, ext0, ext01, su, [&](int i) { return okd(0, i); },
+      [&](int i) { return okd(1, i); }, [&](int i) { return okd(2, i); },
+      [&](const double* g, double* s) { cp_async8(s, g); });
   cp_async_wait_all();
   __syncthreads();
 
-  // ---- D u: this component's two faces of every owned cell (subcell order, lanes along X) ----
+  // ---- D u: this component's two faces of every owned cell (subcell order) ----
   if constexpr (BLOCK) {
 #pragma unroll
     for (int k = 0; k < NQR; ++k) {
@@ -228,26 +238,44 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
   __syncthreads();
 
-  // ---- c_e M_l along AX, element by element, shared planes summed in a register ----
+  // ---- c_e M_l along AX element by element (shared-plane sum carried in a register),
+  //      + D^T q~ ; y/z: owned planes stored straight to HBM (lanes run along x: coalesced),
+  //      x: written back to smem for a coalesced copy-out ----
   constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
   constexpr int NL = EL1 * EL2;
+  constexpr int QA1 = (C::A1 == 0) ? 1 : G::Q1;
+  constexpr int QA2 = (C::A2 == 1) ? G::Q1 : G::Q2;
+  constexpr int QS = (AX == 0) ? 1 : (AX == 1) ? G::Q1 : G::Q2;
+  constexpr long long GA1 = 0;   // placeholder to keep the structure explicit
+  (void)GA1;
+  const long long gs1 = (C::A1 == 0) ? 1 : ext0;        // HBM strides along A1, A2, AX
+  const long long gs2 = (C::A2 == 1) ? ext0 : ext01;
+  const long long gsa = (AX == 0) ? 1 : (AX == 1) ? ext0 : ext01;
   const int m_a = ti.m[AX], h_a = ti.h[AX];
+  const int hiA1 = (C::A1 == 0) ? hi0 : hi1, hiA2 = (C::A2 == 1) ? hi1 : hi2;
+  double* yt = a.y + gtile;
 #pragma unroll 1
   for (int it = tid; it < NL; it += NT) {
     const int l1 = it % EL1, l2 = it / EL1;
+    const bool line_ok = l1 < hiA1 && l2 < hiA2;
+    if (AX != 0 && !line_ok) continue;
     double* line = su + l1 * C::SA1 + l2 * C::SA2;
-    int ec[3];   // element coordinates (in-tile) of this line; ec[AX] set per element
+    double* gl = yt + (l1 * gs1 + l2 * gs2);
+    int ec[3];
     ec[C::A1] = l1 / P;
     ec[C::A2] = l2 / P;
     ec[AX] = 0;
-    const double* cbase = sco + 4 * (((ec[2] + 1) * (TY + 1) + (ec[1] + 1)) * (TX + 1) + (ec[0] + 1)) + AX;
+    const double* cbase =
+        sco + 4 * (((ec[2] + 1) * (TY + 1) + (ec[1] + 1)) * (TX + 1) + (ec[0] + 1)) + AX;
     constexpr int CSTEP = 4 * ((AX == 0) ? 1 : (AX == 1) ? (TX + 1) : (TX + 1) * (TY + 1));
-    double carry = 0.0;
+    const double* ql = sq + l1 * QA1 + l2 * QA2;
+    double carry = 0.0, qprev = 0.0;
     if (h_a) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], line[j * C::SA], s);
       carry = cbase[-CSTEP] * s;
+      if (BLOCK) qprev = hq[l2 * EL1 + l1];
     }
 #pragma unroll
     for (int et = 0; et < C::TA; ++et) {
@@ -262,7 +290,14 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
           double s = 0.0;
 #pragma unroll
           for (int j = 0; j <= P; ++j) s = fma(tab.Ml[i][j], v[j], s);
-          eb[i * C::SA] = (i == 0) ? fma(c, s, carry) : c * s;
+          double o = (i == 0) ? fma(c, s, carry) : c * s;
+          if constexpr (BLOCK) {   // (D^T q)_face = q(- side cell) - q(+ side cell)
+            const double qc = ql[(et * P + i) * QS];
+            o += qprev - qc;
+            qprev = qc;
+          }
+          if (AX == 0) eb[i * C::SA] = o;
+          else __stcs(gl + ((et + 1) * P + i) * gsa, o);
         }
         double s = 0.0;
 #pragma unroll
@@ -270,40 +305,24 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
         carry = c * s;
       }
     }
-    if (ti.last[AX]) line[(m_a + 1) * P * C::SA] = carry;
+    if (ti.last[AX]) {
+      const double o = carry + (BLOCK ? qprev : 0.0);
+      if (AX == 0) line[(m_a + 1) * P * C::SA] = o;
+      else __stcs(gl + (m_a + 1) * P * gsa, o);
+    }
   }
   __syncthreads();
 
-  // ---- copy-out of the owned planes + D^T q~ (warp per row, streaming stores) ----
-  constexpr int NOA = C::TA * P + 1;          // candidate owned positions along AX
-  constexpr int NO0 = (AX == 0) ? NOA : C::E0;
-  constexpr int NO1 = (AX == 1) ? NOA : C::E1;
-  constexpr int NO2 = (AX == 2) ? NOA : C::E2;
-  const int own_hi = (m_a + 1) * P + (ti.last[AX] ? 1 : 0);   // exclusive
-  double* yt = a.y + gtile;
-  rows<NT, NO0, NO1, NO2>([&](int o0, int o1, int o2) {
-    int pos[3] = {o0, o1, o2};
-    pos[AX] += P;
-    bool ok = pos[AX] < own_hi;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-      if (d != AX) ok = ok && pos[d] < hi_o[d];
-    if (!ok) return;
-    double v = su[pos[0] + C::S1 * pos[1] + C::S2 * pos[2]];
-    if constexpr (BLOCK) {
-      // the face at pos[AX] separates tile cells cA-1 (- side) and cA (+ side) along AX
-      int cc[3] = {pos[0], pos[1], pos[2]};
-      const int cA = pos[AX] - P;
-      cc[AX] = cA;
-      const double* qc = sq + cc[0] + G::Q1 * cc[1] + G::Q2 * cc[2];
-      constexpr int QS = (AX == 0) ? 1 : (AX == 1) ? G::Q1 : G::Q2;
-      if (cA < m_a * P) v -= qc[0];
-      if (cA > 0) v += qc[-QS];
-      else if (h_a) v += hq[pos[C::A2] * (C::TA1 * P) + pos[C::A1]];
-    }
-    __stcs(yt + ((long long)pos[2] * ext01 + pos[1] * ext0 + pos[0]), v);
-  });
-  __syncthreads();
+  if constexpr (AX == 0) {
+    // ---- copy-out of the owned x planes (coalesced, streaming) ----
+    constexpr int NO0 = TX * P + 1;
+    const int own_hi = m_a * P + (ti.last[0] ? 1 : 0);   // exclusive, relative to position P
+    rows<NT, NO0, C::E1, C::E2, C::S1, C::S2>(
+        yt + P, ext0, ext01, su + P, [&](int i) { return i < own_hi; },
+        [&](int i) { return i < hi1; }, [&](int i) { return i < hi2; },
+        [&](double* g, const double* s) { __stcs(g, *s); });
+    __syncthreads();
+  }
 }
 
 template <int P, int TX, int TY, int TZ, int NT, bool BLOCK>
@@ -412,14 +431,12 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   if constexpr (BLOCK) {
     if (a.has_z) {
       // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in su (same subcell-major layout as sq)
-      for (int i = tid; i < G::SQSIZE; i += NT) su[i] = sq[i];
+      // X-lines (lanes over Y, odd stride Q1; sq -> su), then Y- and Z-lines (lanes over X)
+      hpass<P, NT>(sq, su, tab.Mhinv, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
       __syncthreads();
-      // X-lines (lanes over Y, odd stride Q1), Y-lines and Z-lines (lanes over X)
-      hpass<P, NT>(su, tab.Mhinv, 0, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
+      hpass<P, NT>(su, su, tab.Mhinv, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
       __syncthreads();
-      hpass<P, NT>(su, tab.Mhinv, 0, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
-      __syncthreads();
-      hpass<P, NT>(su, tab.Mhinv, 0, G::CX, 1, G::CY, G::Q1, TZ, P * G::Q2, G::Q2);
+      hpass<P, NT>(su, su, tab.Mhinv, G::CX, 1, G::CY, G::Q1, TZ, P * G::Q2, G::Q2);
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < NQR; ++k) {
@@ -491,16 +508,43 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   return cudaGetLastError();
 }
 
+// Tile shapes per order; variant 0 is the default, HDIV_AFFINE_TILE=<k> selects another (tuning).
+static int tile_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HDIV_AFFINE_TILE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
                      cudaStream_t s) {
+  const int v = tile_variant();
   switch (h->p) {
     case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
-    case 2: return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
-    case 3: return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-    case 4: return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-    case 5: return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
-    case 6: return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+    case 2:
+      if (v == 1) return launch_t<2, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<2, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
+    case 3:
+      if (v == 1) return launch_t<3, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<3, 8, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+    case 4:
+      if (v == 1) return launch_t<4, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<4, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 3) return launch_t<4, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+    case 5:
+      if (v == 1) return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<5, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
+    case 6:
+      if (v == 1) return launch_t<6, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;
 }
