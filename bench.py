@@ -107,28 +107,14 @@ def make_problem(cfg: str, p: int):
     return make_config(cfg, p=p)
 
 
-def slab_bounds(Nz: int, ws: int, rank: int):
-    base, rem = divmod(Nz, ws)
-    z0 = rank * base + min(rank, rem)
-    return z0, z0 + base + (1 if rank < rem else 0)
-
-
-def sliced_problem_arrays(pr, z0, z1):
-    """Vertex layers z0..z1 and per-element coefficients of the slab (inputs only)."""
-    V = pr.vertices[z0:z1 + 1]
-    Ex = pr.N[0] * pr.N[1]
-    sl = slice(z0 * Ex, z1 * Ex)
-    pick = lambda a: None if a is None else a[sl]
-    return V, pick(pr.alpha), pick(pr.beta), pick(pr.gamma), pick(pr.eps)
-
-
 def build_operator(pr, ws, rank, dist, nccl_id=None):
     from paper_2304_12387_b200 import HdivOperator
     if ws == 1:
         from paper_2304_12387_b200 import from_problem
         return from_problem(pr)
-    z0, z1 = slab_bounds(pr.N[2], ws, rank)
-    V, a, b, g, e = sliced_problem_arrays(pr, z0, z1)
+    from paper_2304_12387_b200.slabs import slab_bounds, slab_inputs
+    z0, z1 = slab_bounds(pr.N[pr.dim - 1], ws, rank)
+    V, a, b, g, e = slab_inputs(pr, z0, z1)
     return HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b, gamma=g, eps=e,
                         slab=(z0, z1), nccl_id=nccl_id, rank=rank, nranks=ws)
 
@@ -193,9 +179,9 @@ def run_reference(args, ws, rank):
         return
     pr = make_problem(args.config, args.p)
     n = pr.n_rt() + pr.n_l2()
-    per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step_budget = max(0.2, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_baseline(pr, budget_s=1.0)
+        cpu_baseline(pr, budget_s=min(1.0, per_step_budget))
     vals = [cpu_baseline(pr, budget_s=per_step_budget) for _ in range(args.steps)]
     v = sorted(x["value"] for x in vals)[len(vals) // 2]
     cb = dict(vals[0])

@@ -39,6 +39,13 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 constexpr int odd_up(int v) { return (v % 2) ? v : v + 1; }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -78,8 +85,8 @@ struct Geo {
                                  cmax(CG<P, TX, TY, TZ, 2>::SIZE, SQSIZE));
   static constexpr int HQ0 = CY * CZ, HQ1 = CX * CZ, HQ2 = CX * CY;
   static constexpr int NCO = (TX + 1) * (TY + 1) * (TZ + 1);
-  static constexpr size_t smem_doubles(bool block) {
-    return (size_t)SU + (block ? (size_t)SQSIZE + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
+  static constexpr size_t smem_doubles(bool block) {   // two component buffers (double buffer)
+    return 2 * (size_t)SU + (block ? (size_t)SQSIZE + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
   }
 };
 
@@ -158,22 +165,37 @@ __device__ __forceinline__ void hpass(const double* src, double* dst, const doub
   }
 }
 
-// -------- one component phase (AX) --------------------------------------------------------
-template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK>
-__device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
-                                          const TabAffine& tab, double* su, const double* sq,
-                                          const double* hq, const double* sco, double* acc) {
-  using C = CG<P, TX, TY, TZ, AX>;
+// L2-cell ownership: thread t owns the cell columns (X, Y) = col % CX, col / CX for
+// col = t + j NT (j < JC) and all Z of the tile -> acc[j * CZ + Z]; addresses are a per-column
+// base plus compile-time offsets, and lanes run along X (conflict free).
+template <int P, int TX, int TY, int TZ, int NT>
+struct Own {
   using G = Geo<P, TX, TY, TZ>;
-  constexpr int NQR = (G::NCELL + NT - 1) / NT;
-  const int tid = threadIdx.x;
-  // global extents of the component-AX face grid and the tile origin (position 0)
-  const long long ext0 = a.n[0] + (AX == 0), ext1 = a.n[1] + (AX == 1);
-  const long long ext01 = ext0 * ext1;
-  long long gorg[3];
+  static constexpr int NCOL = G::CX * G::CY;
+  static constexpr int JC = (NCOL + NT - 1) / NT;
+  static constexpr int NACC = JC * G::CZ;
+};
+
+// global tile origin of component AX (position 0 of its smem box) and its face-grid extents
+template <int P, int AX>
+struct CompAddr {
+  long long ext0, ext01, gtile;
+  __device__ __forceinline__ CompAddr(const AffArgs& a, const TileInfo& ti) {
+    ext0 = a.n[0] + (AX == 0);
+    const long long ext1 = a.n[1] + (AX == 1);
+    ext01 = ext0 * ext1;
+    long long gorg[3];
 #pragma unroll
-  for (int d = 0; d < 3; ++d) gorg[d] = (long long)(ti.e0[d] - (d == AX ? 1 : 0)) * P;
-  const long long gtile = a.off[AX] + gorg[0] + ext0 * (gorg[1] + ext1 * gorg[2]);
+    for (int d = 0; d < 3; ++d) gorg[d] = (long long)(ti.e0[d] - (d == AX ? 1 : 0)) * P;
+    gtile = a.off[AX] + gorg[0] + ext0 * (gorg[1] + ext1 * gorg[2]);
+  }
+};
+
+// issue the cp.async loads of component AX's tile (+ - halo) into `su` and commit a group
+template <int P, int TX, int TY, int TZ, int NT, int AX>
+__device__ __forceinline__ void load_component(const AffArgs& a, const TileInfo& ti, double* su) {
+  using C = CG<P, TX, TY, TZ, AX>;
+  const CompAddr<P, AX> ca(a, ti);
   const int lo_a = ti.h[AX] ? 0 : P;                  // first loaded position along AX
   const int hi_a = (ti.m[AX] + 1) * P;                // last valid position along AX
   const int hi0 = ti.m[0] * P, hi1 = ti.m[1] * P, hi2 = ti.m[2] * P;
@@ -181,25 +203,38 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     if (d == AX) return pos >= lo_a && pos <= hi_a;
     return pos < (d == 0 ? hi0 : d == 1 ? hi1 : hi2);
   };
-
-  // ---- load (cp.async, 8 B) ----
   rows<NT, C::E0, C::E1, C::E2, C::S1, C::S2>(
-      a.x + gtile, ext0, ext01, su, [&](int i) { return okd(0, i); },
+      a.x + ca.gtile, ca.ext0, ca.ext01, su, [&](int i) { return okd(0, i); },
       [&](int i) { return okd(1, i); }, [&](int i) { return okd(2, i); },
       [&](const double* g, double* s) { cp_async8(s, g); });
-  cp_async_wait_all();
-  __syncthreads();
+  cp_async_commit();
+}
 
-  // ---- D u: this component's two faces of every owned cell (subcell order) ----
+// -------- one component phase (AX), data already in `su` ------------------------------------
+template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK>
+__device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
+                                          const TabAffine& tab, double* su, const double* sq,
+                                          const double* hq, const double* sco, double* acc) {
+  using C = CG<P, TX, TY, TZ, AX>;
+  using G = Geo<P, TX, TY, TZ>;
+  using O = Own<P, TX, TY, TZ, NT>;
+  const int tid = threadIdx.x;
+  const CompAddr<P, AX> ca(a, ti);
+  const long long ext0 = ca.ext0, ext01 = ca.ext01, gtile = ca.gtile;
+  const int hi0 = ti.m[0] * P, hi1 = ti.m[1] * P, hi2 = ti.m[2] * P;
+
+  // ---- D u: this component's two faces of every owned cell ----
   if constexpr (BLOCK) {
 #pragma unroll
-    for (int k = 0; k < NQR; ++k) {
-      const int i = tid + k * NT;
-      if (i < G::NCELL) {
-        int pos[3] = {i % G::CX, (i / G::CX) % G::CY, i / (G::CX * G::CY)};
+    for (int j = 0; j < O::JC; ++j) {
+      const int col = tid + j * NT;
+      if (col < O::NCOL) {
+        int pos[3] = {col % G::CX, col / G::CX, 0};
         pos[AX] += P;
         const double* s = su + pos[0] + C::S1 * pos[1] + C::S2 * pos[2];
-        acc[k] += s[C::SA] - s[0];
+#pragma unroll
+        for (int z = 0; z < G::CZ; ++z)
+          acc[j * G::CZ + z] += s[z * C::S2 + C::SA] - s[z * C::S2];
       }
     }
     __syncthreads();
@@ -329,13 +364,14 @@ template <int P, int TX, int TY, int TZ, int NT, bool BLOCK>
 __global__ void __launch_bounds__(NT)
 affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
+  using O = Own<P, TX, TY, TZ, NT>;
   constexpr int P3 = G::P3;
-  constexpr int NQR = (G::NCELL + NT - 1) / NT;
   constexpr int NW = NT / 32;
   if (a.skip && *a.skip) return;
   extern __shared__ double smem[];
-  double* su = smem;                                  // component tile / Z scratch / y_q staging
-  double* sq = su + G::SU;                            // q~ tile, subcell-major
+  double* bufA = smem;                                // component buffers (double buffered);
+  double* bufB = smem + G::SU;                        // also Z scratch / y_q staging
+  double* sq = bufB + G::SU;                          // q~ tile, subcell-major
   double* hq0 = sq + (BLOCK ? G::SQSIZE : 0);         // halo q~ for owned -x planes [K][J]
   double* hq1 = hq0 + (BLOCK ? G::HQ0 : 0);           // [K][I]
   double* hq2 = hq1 + (BLOCK ? G::HQ1 : 0);           // [J][I]
@@ -369,7 +405,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     return ((long long)(ti.e0[2] + ez) * NLy + (ti.e0[1] + ey)) * NLx + (ti.e0[0] + ex);
   };
 
-  // ---- coefficients of the tile and its - halo ----
+  // ---- group 0: coefficients of the tile and its - halo, q~ tile, halo q~ ----
   for (int i = tid; i < G::NCO; i += NT) {
     const int ix = i % (TX + 1), iy = (i / (TX + 1)) % (TY + 1), iz = i / ((TX + 1) * (TY + 1));
     const int ex = ti.e0[0] - 1 + ix, ey = ti.e0[1] - 1 + iy, ez = ti.e0[2] - 1 + iz;
@@ -379,11 +415,6 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       for (int k = 0; k < 4; ++k) cp_async8(sco + 4 * i + k, c + k);
     }
   }
-
-  double acc[NQR];
-#pragma unroll
-  for (int k = 0; k < NQR; ++k) acc[k] = 0.0;
-
   if constexpr (BLOCK) {
     // q~ tile: warp per element, contiguous P^3 run -> subcell-major smem
     for (int e = warp; e < G::NE; e += NW) {
@@ -425,45 +456,64 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
         }
       }
   }
-  cp_async_wait_all();
-  __syncthreads();
+  cp_async_commit();
+  // ---- group 1: x component -> A ----
+  load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
 
+  double acc[O::NACC];
+#pragma unroll
+  for (int k = 0; k < O::NACC; ++k) acc[k] = 0.0;
+
+  cp_async_wait_group<1>();
+  __syncthreads();
   if constexpr (BLOCK) {
     if (a.has_z) {
-      // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in su (same subcell-major layout as sq)
-      // X-lines (lanes over Y, odd stride Q1; sq -> su), then Y- and Z-lines (lanes over X)
-      hpass<P, NT>(sq, su, tab.Mhinv, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
+      // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in B (subcell-major like sq):
+      // X-lines (lanes over Y, odd stride Q1; sq -> B), then Y- and Z-lines (lanes over X)
+      hpass<P, NT>(sq, bufB, tab.Mhinv, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
       __syncthreads();
-      hpass<P, NT>(su, su, tab.Mhinv, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
+      hpass<P, NT>(bufB, bufB, tab.Mhinv, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
       __syncthreads();
-      hpass<P, NT>(su, su, tab.Mhinv, G::CX, 1, G::CY, G::Q1, TZ, P * G::Q2, G::Q2);
+      hpass<P, NT>(bufB, bufB, tab.Mhinv, G::CX, 1, G::CY, G::Q1, TZ, P * G::Q2, G::Q2);
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < NQR; ++k) {
-        const int i = tid + k * NT;
-        if (i < G::NCELL) {
-          const int X = i % G::CX, Y = (i / G::CX) % G::CY, Z = i / (G::CX * G::CY);
-          const int ex = X / P, ey = Y / P, ez = Z / P;
-          const double z = sco[4 * (((ez + 1) * (TY + 1) + (ey + 1)) * (TX + 1) + (ex + 1)) + 3];
-          acc[k] = -z * su[X + G::Q1 * Y + G::Q2 * Z];
+      for (int j = 0; j < O::JC; ++j) {
+        const int col = tid + j * NT;
+        if (col < O::NCOL) {
+          const int X = col % G::CX, Y = col / G::CX;
+          const double* sz = sco + 4 * (((Y / P) + 1) * (TX + 1) + (X / P) + 1) + 3;
+          const double* s = bufB + X + G::Q1 * Y;
+#pragma unroll
+          for (int z = 0; z < G::CZ; ++z)
+            acc[j * G::CZ + z] = -sz[4 * (TX + 1) * (TY + 1) * (z / P + 1)] * s[z * G::Q2];
         }
       }
       __syncthreads();
     }
   }
-
-  component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, su, sq, hq0, sco, acc);
-  component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, su, sq, hq1, sco, acc);
-  component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, su, sq, hq2, sco, acc);
+  // ---- group 2: y component -> B ; compute x from A ----
+  load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
+  cp_async_wait_group<1>();
+  __syncthreads();
+  component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, bufA, sq, hq0, sco, acc);
+  // ---- group 3: z component -> A ; compute y from B ----
+  load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
+  cp_async_wait_group<1>();
+  __syncthreads();
+  component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, bufB, sq, hq1, sco, acc);
+  cp_async_wait_group<0>();
+  __syncthreads();
+  component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
 
   if constexpr (BLOCK) {
     // stage y_q through smem (subcell-major), then store element-contiguous runs
 #pragma unroll
-    for (int k = 0; k < NQR; ++k) {
-      const int i = tid + k * NT;
-      if (i < G::NCELL) {
-        const int X = i % G::CX, Y = (i / G::CX) % G::CY, Z = i / (G::CX * G::CY);
-        su[X + G::Q1 * Y + G::Q2 * Z] = acc[k];
+    for (int j = 0; j < O::JC; ++j) {
+      const int col = tid + j * NT;
+      if (col < O::NCOL) {
+        double* s = bufB + (col % G::CX) + G::Q1 * (col / G::CX);
+#pragma unroll
+        for (int z = 0; z < G::CZ; ++z) s[z * G::Q2] = acc[j * G::CZ + z];
       }
     }
     __syncthreads();
@@ -472,7 +522,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       const int ex = e % TX, ey = (e / TX) % TY, ez = e / (TX * TY);
       if (elem_ok(ex, ey, ez)) {
         double* ye = yq + gelem(ex, ey, ez) * P3;
-        const double* se = su + ex * P + G::Q1 * (ey * P) + G::Q2 * (ez * P);
+        const double* se = bufB + ex * P + G::Q1 * (ey * P) + G::Q2 * (ez * P);
 #pragma unroll
         for (int il = lane; il < P3; il += 32)
           __stcs(ye + il, se[il % P + G::Q1 * ((il / P) % P) + G::Q2 * (il / (P * P))]);
