@@ -37,7 +37,8 @@ static void corners(const std::vector<double>& V, int dim, int64_t NLx, int64_t 
 
 cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
                             cudaStream_t s) {
-  cudaError_t e = (h->kernel == 2) ? launch_affine_apply(h, x, y, MODE_BLOCK, skip, s)
+  cudaError_t e = (h->kernel == 2)  ? launch_affine_apply(h, x, y, MODE_BLOCK, skip, s)
+                   : (h->dim == 3) ? launch_trilinear_apply(h, x, y, MODE_BLOCK, skip, s)
                                    : launch_general_apply(h, x, y, MODE_BLOCK, skip, s);
   if (e != cudaSuccess) return e;
   if (h->nranks > 1) {
@@ -363,8 +364,9 @@ hdiv_status hdiv_sizes(hdiv_handle h, int64_t* nrt, int64_t* nl2, int64_t* nrt_g
 hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* yu, void* stream) {
   if (!h || !u || !yu) return fail(HDIV_ERR_NULL, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
-  HDIV_CUDA_TRY(h->kernel == 2 ? launch_affine_apply(h, u, yu, MODE_MASS, nullptr, s)
-                               : launch_general_apply(h, u, yu, MODE_MASS, nullptr, s));
+  HDIV_CUDA_TRY(h->kernel == 2  ? launch_affine_apply(h, u, yu, MODE_MASS, nullptr, s)
+                : (h->dim == 3) ? launch_trilinear_apply(h, u, yu, MODE_MASS, nullptr, s)
+                                : launch_general_apply(h, u, yu, MODE_MASS, nullptr, s));
   if (h->nranks > 1) return comm_reverse_add(h, yu, s);
   return HDIV_OK;
 }

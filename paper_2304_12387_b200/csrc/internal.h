@@ -98,6 +98,8 @@ cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, i
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                  const int* skip, cudaStream_t s);
 cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s);
+cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
+                                   const int* skip, cudaStream_t s);
 cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
                             cudaStream_t s);
 cudaError_t launch_div(const hdiv_ctx* h, const double* u, double* yq, cudaStream_t s);

@@ -241,10 +241,14 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
 
   // ---- M_h (x) M_h over the two histopolation axes: one P x P block per thread ----
-  constexpr int NH = C::EA * C::TA1 * C::TA2;
+  // lanes run along AX (odd stride); the position range is padded to a multiple of 16 so a
+  // half-warp never straddles two blocks (conflict-free 8-byte accesses)
+  constexpr int EAP = (C::EA + 15) / 16 * 16;
+  constexpr int NH = EAP * C::TA1 * C::TA2;
 #pragma unroll 2
   for (int it = tid; it < NH; it += NT) {
-    const int pa = it % C::EA, b1 = (it / C::EA) % C::TA1, b2 = it / (C::EA * C::TA1);
+    const int pa = it % EAP, b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
+    if (pa >= C::EA) continue;
     double* base = su + pa * C::SA + b1 * P * C::SA1 + b2 * P * C::SA2;
     double v[P][P];
 #pragma unroll
@@ -277,12 +281,11 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   //      + D^T q~ ; y/z: owned planes stored straight to HBM (lanes run along x: coalesced),
   //      x: written back to smem for a coalesced copy-out ----
   constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
-  constexpr int NL = EL1 * EL2;
+  constexpr int EL1P = (EL1 + 15) / 16 * 16;   // half-warp aligned lane rows
+  constexpr int NL = EL1P * EL2;
   constexpr int QA1 = (C::A1 == 0) ? 1 : G::Q1;
   constexpr int QA2 = (C::A2 == 1) ? G::Q1 : G::Q2;
   constexpr int QS = (AX == 0) ? 1 : (AX == 1) ? G::Q1 : G::Q2;
-  constexpr long long GA1 = 0;   // placeholder to keep the structure explicit
-  (void)GA1;
   const long long gs1 = (C::A1 == 0) ? 1 : ext0;        // HBM strides along A1, A2, AX
   const long long gs2 = (C::A2 == 1) ? ext0 : ext01;
   const long long gsa = (AX == 0) ? 1 : (AX == 1) ? ext0 : ext01;
@@ -291,7 +294,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   double* yt = a.y + gtile;
 #pragma unroll 1
   for (int it = tid; it < NL; it += NT) {
-    const int l1 = it % EL1, l2 = it / EL1;
+    const int l1 = it % EL1P, l2 = it / EL1P;
+    if (l1 >= EL1) continue;
     const bool line_ok = l1 < hiA1 && l2 < hiA2;
     if (AX != 0 && !line_ok) continue;
     double* line = su + l1 * C::SA1 + l2 * C::SA2;
