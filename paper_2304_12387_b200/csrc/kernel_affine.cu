@@ -370,7 +370,6 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
   using O = Own<P, TX, TY, TZ, NT>;
   constexpr int P3 = G::P3;
-  constexpr int NW = NT / 32;
   if (a.skip && *a.skip) return;
   extern __shared__ double smem[];
   double* bufA = smem;                                // component buffers (double buffered);
@@ -382,7 +381,6 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   double* sco = hq2 + (BLOCK ? G::HQ2 : 0);           // coefficients [(TZ+1)][(TY+1)][(TX+1)][4]
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
   TileInfo ti;
   {
     int t = blockIdx.x;
@@ -420,15 +418,21 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     }
   }
   if constexpr (BLOCK) {
-    // q~ tile: warp per element, contiguous P^3 run -> subcell-major smem
-    for (int e = warp; e < G::NE; e += NW) {
-      const int ex = e % TX, ey = (e / TX) % TY, ez = e / (TX * TY);
-      if (elem_ok(ex, ey, ez)) {
-        const double* qe = q + gelem(ex, ey, ez) * P3;
-        double* se = sq + ex * P + G::Q1 * (ey * P) + G::Q2 * (ez * P);
+    // q~ tile, subcell-major, loaded per owned column (X, Y): lanes run along X (conflict-free
+    // smem writes; HBM runs of P doubles per element)
 #pragma unroll
-        for (int il = lane; il < P3; il += 32)
-          cp_async8(se + il % P + G::Q1 * ((il / P) % P) + G::Q2 * (il / (P * P)), qe + il);
+    for (int j = 0; j < O::JC; ++j) {
+      const int col = tid + j * NT;
+      if (col < O::NCOL) {
+        const int X = col % G::CX, Y = col / G::CX;
+        if (X < ti.m[0] * P && Y < ti.m[1] * P) {
+          const double* qc = q + gelem(X / P, Y / P, 0) * P3 + (X % P) + P * (Y % P);
+          double* sc = sq + X + G::Q1 * Y;
+#pragma unroll
+          for (int z = 0; z < G::CZ; ++z)
+            if (z < ti.m[2] * P)
+              cp_async8(sc + z * G::Q2, qc + (long long)(z / P) * NLx * NLy * P3 + P * P * (z % P));
+        }
       }
     }
     // halo q~ of the - neighbour's adjacent cell layer (for D^T at the owned - planes)
@@ -510,26 +514,20 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
 
   if constexpr (BLOCK) {
-    // stage y_q through smem (subcell-major), then store element-contiguous runs
+    // y_q straight from the accumulators: per owned column, runs of P doubles per element
+    double* yq = a.y + a.nrt;
 #pragma unroll
     for (int j = 0; j < O::JC; ++j) {
       const int col = tid + j * NT;
       if (col < O::NCOL) {
-        double* s = bufB + (col % G::CX) + G::Q1 * (col / G::CX);
+        const int X = col % G::CX, Y = col / G::CX;
+        if (X < ti.m[0] * P && Y < ti.m[1] * P) {
+          double* yc = yq + gelem(X / P, Y / P, 0) * P3 + (X % P) + P * (Y % P);
 #pragma unroll
-        for (int z = 0; z < G::CZ; ++z) s[z * G::Q2] = acc[j * G::CZ + z];
-      }
-    }
-    __syncthreads();
-    double* yq = a.y + a.nrt;
-    for (int e = warp; e < G::NE; e += NW) {
-      const int ex = e % TX, ey = (e / TX) % TY, ez = e / (TX * TY);
-      if (elem_ok(ex, ey, ez)) {
-        double* ye = yq + gelem(ex, ey, ez) * P3;
-        const double* se = bufB + ex * P + G::Q1 * (ey * P) + G::Q2 * (ez * P);
-#pragma unroll
-        for (int il = lane; il < P3; il += 32)
-          __stcs(ye + il, se[il % P + G::Q1 * ((il / P) % P) + G::Q2 * (il / (P * P))]);
+          for (int z = 0; z < G::CZ; ++z)
+            if (z < ti.m[2] * P)
+              __stcs(yc + (long long)(z / P) * NLx * NLy * P3 + P * P * (z % P), acc[j * G::CZ + z]);
+        }
       }
     }
   }
@@ -584,21 +582,21 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
       return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
     case 3:
       if (v == 1) return launch_t<3, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<3, 8, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<3, 8, 4, 2, 128, BLOCK>(h, x, y, k, s);
     case 4:
       if (v == 1) return launch_t<4, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<4, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 3) return launch_t<4, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
-      return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<4, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 5:
-      if (v == 1) return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 1) return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<5, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 6:
       if (v == 1) return launch_t<6, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
-      return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 2) return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;
 }
