@@ -1,15 +1,15 @@
 #!/bin/bash
 # time every tile variant of the box kernel (HDIV_AFFINE_TILE) for p = 2..6
-for v in 0 1 2 3; do
-  HDIV_AFFINE_TILE=$v python - <<'PY'
+for v in 0 1 -1; do
+  HDIV_MARCH_TILE=$v python - <<'PY'
 import os, sys
 sys.path.insert(0, ".")
 import torch
 from synth import make_config
 from paper_2304_12387_b200 import from_problem
-v = os.environ["HDIV_AFFINE_TILE"]
+v = os.environ["HDIV_MARCH_TILE"]
 for p, N in [(2, 160), (3, 128), (4, 128), (5, 96), (6, 80)]:
-    if p in (3, 5, 6, 2) and v == "3":
+    if False:
         continue
     pr = make_config("c4", N=(N, N, N), p=p)
     op = from_problem(pr)

@@ -59,6 +59,33 @@ def _problem(name, N, p):
     return pr
 
 
+# box-kernel variants: z-marching with forced chunk boundaries, and the halo-tile kernel
+VARIANTS = [("c2", (5, 3, 7), 4, {"HDIV_ZCHUNK": "2"}), ("c2", (3, 5, 5), 3, {"HDIV_ZCHUNK": "1"}),
+            ("c2", (5, 4, 6), 2, {"HDIV_ZCHUNK": "4"}), ("c2", (3, 3, 5), 5, {"HDIV_ZCHUNK": "2"}),
+            ("c2", (3, 3, 4), 6, {"HDIV_ZCHUNK": "3"}), ("c2", (9, 5, 5), 1, {"HDIV_ZCHUNK": "2"}),
+            ("c5", (5, 4, 6), 3, {"HDIV_ZCHUNK": "2"}),
+            ("c2", (5, 3, 3), 4, {"HDIV_MARCH_TILE": "-1"}), ("c2", (5, 3, 3), 4, {"HDIV_MARCH_TILE": "1"}),
+            ("c2", (3, 5, 3), 6, {"HDIV_MARCH_TILE": "1", "HDIV_ZCHUNK": "2"})]
+
+
+@pytest.mark.parametrize("name,N,p,env", VARIANTS)
+def test_box_kernel_variants(name, N, p, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    from oracle import operators
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr, with_schur=False)
+    op = _gpu(pr)
+    s = op.sizes
+    x = random_vector(s.n, 17)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL
+    assert _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    u = x[:s.n_rt]
+    assert _rel(_host(op.apply_mass(_dev(u))), A.M @ u) < TOL
+
+
 @pytest.mark.parametrize("name,N,p,kernel", CASES)
 def test_block_apply_parity(name, N, p, kernel):
     from oracle import operators
