@@ -3,19 +3,23 @@
 //   M^e u = sum_q w_q (mw_e / det J_q) J_q^T J_q u_hat(x_q) tested against phi_hat
 //   (P:84 Piola, P:135 eq. matrices), Gauss-Legendre Q = p+2 (reading A3).
 //
-// One CTA per element, all three components advanced together so a sum-factorisation stage
-// costs one barrier: 3 forward contractions (B_l / B_h tables), the pointwise G_q = w mw
-// J^T J / det J (J from per-element column factors: dT/dx_hat depends on (y_hat,z_hat) only,
-// etc., so the three columns are tabulated on the Q^2 faces once), 3 transposed contractions,
-// then D^T q~ and the scatter (fp64 atomics on element-boundary faces onto a zeroed y, plain
-// stores inside).  All extents are compile-time.  Z (constant-J elements only) and D u are
-// element-local.  Bound: FP64 issue.
+// One CTA (64 threads) per element; the three components advance together so every
+// sum-factorisation stage costs one barrier.  Each contraction is a register-blocked line
+// pass: a thread loads the NIN inputs of one line, applies the 1D table (B_l / B_h, compile-
+// time indices -> constant-bank operands) and writes the NO outputs, i.e. ~(NIN+NO)/(NIN NO)
+// shared-memory accesses per FMA.  All smem arrays use odd-padded strides (lanes run over an
+// odd stride -> conflict free).  The trilinear Jacobian columns are tabulated on the Q^2 point
+// pairs (dT/dx_hat depends on (y_hat, z_hat) only, etc.).  Element-boundary faces are
+// accumulated with fp64 atomics onto a zeroed y (0 + a + b: order independent), interior
+// faces stored.  Z (constant-J elements only) and D u are element-local.
 #include <cuda_runtime.h>
 
 #include "internal.h"
 
 namespace hdiv {
 namespace {
+
+constexpr int odd_up(int v) { return (v % 2) ? v : v + 1; }
 
 struct TriArgs {
   const double* x;      // [u ; q]  (MASS: u)
@@ -30,42 +34,87 @@ struct TriArgs {
   const int* skip;
 };
 
-// out(i0,i1,i2) = sum_t T[o][t] in(.. t at axis AX ..); in extents (N0,N1,N2), out extent NO
-// along AX; T(o, t) = tab[o*SO + t*ST].  Thread-strided over the outputs.
-template <int NT, int N0, int N1, int N2, int AX, int NO, int SO, int ST>
-__device__ __forceinline__ void contract(const double* in, double* out, const double* tab) {
+// padded layout of a (D0, D1, D2) array
+template <int D0, int D1, int D2>
+struct Lay {
+  static constexpr int S1 = odd_up(D0), S2 = S1 * odd_up(D1), SIZE = S2 * D2;
+};
+
+enum { TB_L = 0, TB_H = 1, TB_HI = 2 };   // B_l, B_h, M_h^-1
+
+template <int KIND, bool FWD>
+__device__ __forceinline__ double tcoef(const Tab1D& tab, int o, int t) {
+  if (KIND == TB_HI) return tab.Mhinv[o][t];
+  if (FWD) return (KIND == TB_L) ? tab.Bl[o][t] : tab.Bh[o][t];   // T(o=q, t=i) = B[q][i]
+  return (KIND == TB_L) ? tab.Bl[t][o] : tab.Bh[t][o];            // T(o=i, t=q) = B[q][i]
+}
+
+// line contraction along AX: in (N0,N1,N2) layout LI -> out (.. NO at AX ..) layout LO
+template <int NT, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI, class LO>
+__device__ __forceinline__ void lines(const double* in, double* out, const Tab1D& tab) {
   constexpr int NIN = (AX == 0) ? N0 : (AX == 1) ? N1 : N2;
-  constexpr int E0 = (AX == 0) ? NO : N0;
-  constexpr int E1 = (AX == 1) ? NO : N1;
-  constexpr int E2 = (AX == 2) ? NO : N2;
-  constexpr int TOT = E0 * E1 * E2;
-  constexpr int SIN = (AX == 0) ? 1 : (AX == 1) ? N0 : N0 * N1;
-#pragma unroll 2
-  for (int it = threadIdx.x; it < TOT; it += NT) {
-    const int o0 = it % E0, r = it / E0, o1 = r % E1, o2 = r / E1;
-    const int o = (AX == 0) ? o0 : (AX == 1) ? o1 : o2;
-    const double* b = in + (AX == 0 ? 0 : o0) + (AX == 1 ? 0 : o1 * N0) + (AX == 2 ? 0 : o2 * N0 * N1);
-    double s = 0.0;
+  // the two other axes (lanes over the first: odd stride)
+  constexpr int B0 = (AX == 0) ? N1 : N0;
+  constexpr int B1 = (AX == 2) ? N1 : N2;
+  constexpr int SI_A = (AX == 0) ? 1 : (AX == 1) ? LI::S1 : LI::S2;
+  constexpr int SI_0 = (AX == 0) ? LI::S1 : 1;
+  constexpr int SI_1 = (AX == 2) ? LI::S1 : LI::S2;
+  constexpr int SO_A = (AX == 0) ? 1 : (AX == 1) ? LO::S1 : LO::S2;
+  constexpr int SO_0 = (AX == 0) ? LO::S1 : 1;
+  constexpr int SO_1 = (AX == 2) ? LO::S1 : LO::S2;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < B0 * B1; it += NT) {
+    const int b0 = it % B0, b1 = it / B0;
+    const double* pi = in + b0 * SI_0 + b1 * SI_1;
+    double* po = out + b0 * SO_0 + b1 * SO_1;
+    double v[NIN];
 #pragma unroll
-    for (int t = 0; t < NIN; ++t) s = fma(tab[o * SO + t * ST], b[t * SIN], s);
-    out[it] = s;
+    for (int t = 0; t < NIN; ++t) v[t] = pi[t * SI_A];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < NIN; ++t) s = fma(tcoef<KIND, FWD>(tab, o, t), v[t], s);
+      po[o * SO_A] = s;
+    }
   }
 }
 
+template <int P>
+struct TG {   // per-component layouts at every stage
+  static constexpr int Q = P + 2;
+  using U0 = Lay<P + 1, P, P>;  using U1 = Lay<P, P + 1, P>;  using U2 = Lay<P, P, P + 1>;
+  using A0 = Lay<Q, P, P>;      using A1 = Lay<Q, P + 1, P>;  using A2 = Lay<Q, P, P + 1>;
+  using B0 = Lay<Q, Q, P>;      using B1 = Lay<Q, Q, P>;      using B2 = Lay<Q, Q, P + 1>;
+  using V = Lay<Q, Q, Q>;
+  using L2 = Lay<P, P, P>;
+  static constexpr int SU = U2::SIZE;     // largest of U0..U2 (padded)
+  static constexpr int SA = A2::SIZE > A1::SIZE ? A2::SIZE : A1::SIZE;
+  static constexpr int SB = B2::SIZE;
+  static constexpr int SV = V::SIZE;
+  static constexpr int SL = L2::SIZE;
+};
+
 template <int P, int NT, bool BLOCK>
 __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_constant__ Tab1D tab) {
+  using T = TG<P>;
   constexpr int Q = P + 2;
   constexpr int NQ = Q * Q * Q;
-  constexpr int NC = (P + 1) * P * P;
   constexpr int P3 = P * P * P;
   if (a.skip && *a.skip) return;
-  __shared__ double sBl[Q * (P + 1)], sBh[Q * P], sw[Q], sx[Q], sMhi[P * P];
   __shared__ double sX[8 * 3];
   __shared__ double sJ[3][Q * Q][3];   // column factors: sJ[c][pair][d] = dT_d/dx_hat_c
-  __shared__ double su[3 * NC];        // inputs / outputs per component
-  __shared__ double sT1[3 * NQ], sT2[3 * NQ];
-  double* const sV = sT1;              // V is live only while T1 is dead (F3 .. B1)
-  __shared__ double sq[BLOCK ? P3 : 1], sy[BLOCK ? P3 : 1], sz1[BLOCK ? P3 : 1], sz2[BLOCK ? P3 : 1];
+  // lifetimes: su (load..F1, B3..scatter) / sB (F2..F3, B1..B2) share region R1;
+  //            sA (F1..F2, B2..B3) / sV (F3..B1) share region R2
+  constexpr int R1 = (3 * T::SU > 3 * T::SB) ? 3 * T::SU : 3 * T::SB;
+  constexpr int R2 = (3 * T::SA > 3 * T::SV) ? 3 * T::SA : 3 * T::SV;
+  __shared__ double sreg[R1 + R2];
+  double* const su[3] = {sreg, sreg + T::SU, sreg + 2 * T::SU};
+  double* const sB[3] = {sreg, sreg + T::SB, sreg + 2 * T::SB};
+  double* const sA[3] = {sreg + R1, sreg + R1 + T::SA, sreg + R1 + 2 * T::SA};
+  double* const sV[3] = {sreg + R1, sreg + R1 + T::SV, sreg + R1 + 2 * T::SV};
+  __shared__ double sq[BLOCK ? T::SL : 1], sy[BLOCK ? P3 : 1], sz1[BLOCK ? T::SL : 1],
+      sz2[BLOCK ? T::SL : 1];
   __shared__ double scoef[2];
 
   const int tid = threadIdx.x;
@@ -74,10 +123,6 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   const int ex = (int)(e % NLx), ey = (int)((e / NLx) % NLy), ez = (int)(e / (NLx * NLy));
   const long long nx = a.n[0], ny = a.n[1];
 
-  for (int i = tid; i < Q * (P + 1); i += NT) sBl[i] = tab.Bl[i / (P + 1)][i % (P + 1)];
-  for (int i = tid; i < Q * P; i += NT) sBh[i] = tab.Bh[i / P][i % P];
-  for (int i = tid; i < Q; i += NT) { sw[i] = tab.wq[i]; sx[i] = tab.xq[i]; }
-  for (int i = tid; i < P * P; i += NT) sMhi[i] = tab.Mhinv[i / P][i % P];
   if (tid < 2) scoef[tid] = a.coef[4 * e + tid];
   for (int i = tid; i < 24; i += NT) {
     const int v = i / 3, d = i % 3;
@@ -85,33 +130,42 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
                         (ex + (v & 1));
     sX[i] = a.vert[g * 3 + d];
   }
-  // gather u (component c, local (i,j,k), i fastest; extent P+1 along c)
-  for (int i = tid; i < 3 * NC; i += NT) {
-    const int c = i / NC, l = i % NC;
-    int li, lj, lk;
-    long long g;
-    if (c == 0) {
-      li = l % (P + 1); lj = (l / (P + 1)) % P; lk = l / ((P + 1) * P);
-      g = a.off[0] + (ex * P + li) + (nx + 1) * ((ey * P + lj) + ny * (long long)(ez * P + lk));
-    } else if (c == 1) {
-      li = l % P; lj = (l / P) % (P + 1); lk = l / (P * (P + 1));
-      g = a.off[1] + (ex * P + li) + nx * ((ey * P + lj) + (ny + 1) * (long long)(ez * P + lk));
-    } else {
-      li = l % P; lj = (l / P) % P; lk = l / (P * P);
-      g = a.off[2] + (ex * P + li) + nx * ((ey * P + lj) + ny * (long long)(ez * P + lk));
+  // gather u: component c, local (i,j,k) i fastest, extent P+1 along c, padded layout
+  {
+    constexpr int NC = (P + 1) * P * P;
+    for (int i = tid; i < 3 * NC; i += NT) {
+      const int c = i / NC, l = i % NC;
+      int li, lj, lk, so;
+      long long g;
+      if (c == 0) {
+        li = l % (P + 1); lj = (l / (P + 1)) % P; lk = l / ((P + 1) * P);
+        g = a.off[0] + (ex * P + li) + (nx + 1) * ((ey * P + lj) + ny * (long long)(ez * P + lk));
+        so = li + T::U0::S1 * lj + T::U0::S2 * lk;
+      } else if (c == 1) {
+        li = l % P; lj = (l / P) % (P + 1); lk = l / (P * (P + 1));
+        g = a.off[1] + (ex * P + li) + nx * ((ey * P + lj) + (ny + 1) * (long long)(ez * P + lk));
+        so = li + T::U1::S1 * lj + T::U1::S2 * lk;
+      } else {
+        li = l % P; lj = (l / P) % P; lk = l / (P * P);
+        g = a.off[2] + (ex * P + li) + nx * ((ey * P + lj) + ny * (long long)(ez * P + lk));
+        so = li + T::U2::S1 * lj + T::U2::S2 * lk;
+      }
+      su[c][so] = a.x[g];
     }
-    su[i] = a.x[g];
   }
   if constexpr (BLOCK) {
     const double* q = a.x + a.nrt;
-    for (int i = tid; i < P3; i += NT) sq[i] = q[e * P3 + i];
+    for (int i = tid; i < P3; i += NT) {
+      const int A = i % P, B = (i / P) % P, C = i / (P * P);
+      sq[A + T::L2::S1 * B + T::L2::S2 * C] = q[e * P3 + i];
+    }
   }
   __syncthreads();
 
-  // column factors of the trilinear Jacobian on the Q x Q point pairs
+  // trilinear Jacobian column factors on the Q x Q point pairs
   for (int i = tid; i < 3 * Q * Q * 3; i += NT) {
     const int c = i / (Q * Q * 3), r = i % (Q * Q * 3), pr = r / 3, d = r % 3;
-    const double s = sx[pr % Q], t = sx[pr / Q];
+    const double s = tab.xq[pr % Q], t = tab.xq[pr / Q];
     auto X = [&](int va, int vb, int vc) { return sX[(va + 2 * vb + 4 * vc) * 3 + d]; };
     double v;
     if (c == 0)        // (s,t) = (y,z)
@@ -125,34 +179,35 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
           (1 - s) * t * (X(0, 1, 1) - X(0, 1, 0)) + s * t * (X(1, 1, 1) - X(1, 1, 0));
     sJ[c][pr][d] = v;
   }
-  // forward stage 1 (axis 0) for the 3 components, + D u and Z stage 1
-  contract<NT, P + 1, P, P, 0, Q, P + 1, 1>(su, sT1, sBl);
-  contract<NT, P, P + 1, P, 0, Q, P, 1>(su + NC, sT1 + NQ, sBh);
-  contract<NT, P, P, P + 1, 0, Q, P, 1>(su + 2 * NC, sT1 + 2 * NQ, sBh);
+  // ---- forward: axis 0, 1, 2 (3 components per stage), + D u and Z q~ ----
+  lines<NT, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0>(su[0], sA[0], tab);
+  lines<NT, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1>(su[1], sA[1], tab);
+  lines<NT, P, P, P + 1, 0, Q, TB_H, true, typename T::U2, typename T::A2>(su[2], sA[2], tab);
   if constexpr (BLOCK) {
     for (int i = tid; i < P3; i += NT) {
       const int A = i % P, B = (i / P) % P, C = i / (P * P);
-      double d = su[(A + 1) + (P + 1) * (B + P * C)] - su[A + (P + 1) * (B + P * C)];
-      d += su[NC + A + P * ((B + 1) + (P + 1) * C)] - su[NC + A + P * (B + (P + 1) * C)];
-      d += su[2 * NC + A + P * (B + P * (C + 1))] - su[2 * NC + A + P * (B + P * C)];
-      sy[i] = d;
+      const double* u0 = su[0] + A + T::U0::S1 * B + T::U0::S2 * C;
+      const double* u1 = su[1] + A + T::U1::S1 * B + T::U1::S2 * C;
+      const double* u2 = su[2] + A + T::U2::S1 * B + T::U2::S2 * C;
+      sy[i] = (u0[1] - u0[0]) + (u1[T::U1::S1] - u1[0]) + (u2[T::U2::S2] - u2[0]);
     }
-    if (a.has_z) contract<NT, P, P, P, 0, P, P, 1>(sq, sz1, sMhi);
+    if (a.has_z)
+      lines<NT, P, P, P, 0, P, TB_HI, true, typename T::L2, typename T::L2>(sq, sz1, tab);
   }
   __syncthreads();
-  // forward stage 2 (axis 1)
-  contract<NT, Q, P, P, 1, Q, P, 1>(sT1, sT2, sBh);
-  contract<NT, Q, P + 1, P, 1, Q, P + 1, 1>(sT1 + NQ, sT2 + NQ, sBl);
-  contract<NT, Q, P, P + 1, 1, Q, P, 1>(sT1 + 2 * NQ, sT2 + 2 * NQ, sBh);
-  if constexpr (BLOCK) if (a.has_z) contract<NT, P, P, P, 1, P, P, 1>(sz1, sz2, sMhi);
+  lines<NT, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0>(sA[0], sB[0], tab);
+  lines<NT, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1>(sA[1], sB[1], tab);
+  lines<NT, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2>(sA[2], sB[2], tab);
+  if constexpr (BLOCK)
+    if (a.has_z) lines<NT, P, P, P, 1, P, TB_HI, true, typename T::L2, typename T::L2>(sz1, sz2, tab);
   __syncthreads();
-  // forward stage 3 (axis 2)
-  contract<NT, Q, Q, P, 2, Q, P, 1>(sT2, sV, sBh);
-  contract<NT, Q, Q, P, 2, Q, P, 1>(sT2 + NQ, sV + NQ, sBh);
-  contract<NT, Q, Q, P + 1, 2, Q, P + 1, 1>(sT2 + 2 * NQ, sV + 2 * NQ, sBl);
-  if constexpr (BLOCK) if (a.has_z) contract<NT, P, P, P, 2, P, P, 1>(sz2, sz1, sMhi);
+  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V>(sB[0], sV[0], tab);
+  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V>(sB[1], sV[1], tab);
+  lines<NT, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V>(sB[2], sV[2], tab);
+  if constexpr (BLOCK)
+    if (a.has_z) lines<NT, P, P, P, 2, P, TB_HI, true, typename T::L2, typename T::L2>(sz2, sz1, tab);
   __syncthreads();
-  // pointwise G_q = w_q mw / det J  J^T J
+  // ---- pointwise G_q = w_q mw / det J  J^T J ----
   const double mw = scoef[0];
   for (int qi = tid; qi < NQ; qi += NT) {
     const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
@@ -161,65 +216,75 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     const double* c2 = sJ[2][qx + Q * qy];
     const double det = c0[0] * (c1[1] * c2[2] - c1[2] * c2[1]) - c1[0] * (c0[1] * c2[2] - c0[2] * c2[1]) +
                        c2[0] * (c0[1] * c1[2] - c0[2] * c1[1]);
-    const double s = sw[qx] * sw[qy] * sw[qz] * mw / det;
-    const double u0 = sV[qi], u1 = sV[NQ + qi], u2 = sV[2 * NQ + qi];
+    const double s = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] * mw / det;
+    const int o = qx + T::V::S1 * qy + T::V::S2 * qz;
+    const double u0 = sV[0][o], u1 = sV[1][o], u2 = sV[2][o];
     double Ju[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) Ju[d] = c0[d] * u0 + c1[d] * u1 + c2[d] * u2;
-    sV[qi] = s * (c0[0] * Ju[0] + c0[1] * Ju[1] + c0[2] * Ju[2]);
-    sV[NQ + qi] = s * (c1[0] * Ju[0] + c1[1] * Ju[1] + c1[2] * Ju[2]);
-    sV[2 * NQ + qi] = s * (c2[0] * Ju[0] + c2[1] * Ju[1] + c2[2] * Ju[2]);
+    sV[0][o] = s * (c0[0] * Ju[0] + c0[1] * Ju[1] + c0[2] * Ju[2]);
+    sV[1][o] = s * (c1[0] * Ju[0] + c1[1] * Ju[1] + c1[2] * Ju[2]);
+    sV[2][o] = s * (c2[0] * Ju[0] + c2[1] * Ju[1] + c2[2] * Ju[2]);
   }
   __syncthreads();
-  // backward stage 1 (axis 2): T(o=k, t=q) = B[q][k]
-  contract<NT, Q, Q, Q, 2, P, 1, P>(sV, sT2, sBh);
-  contract<NT, Q, Q, Q, 2, P, 1, P>(sV + NQ, sT2 + NQ, sBh);
-  contract<NT, Q, Q, Q, 2, P + 1, 1, P + 1>(sV + 2 * NQ, sT2 + 2 * NQ, sBl);
+  // ---- backward: axis 2, 1, 0 ----
+  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B0>(sV[0], sB[0], tab);
+  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B1>(sV[1], sB[1], tab);
+  lines<NT, Q, Q, Q, 2, P + 1, TB_L, false, typename T::V, typename T::B2>(sV[2], sB[2], tab);
   __syncthreads();
-  contract<NT, Q, Q, P, 1, P, 1, P>(sT2, sT1, sBh);
-  contract<NT, Q, Q, P, 1, P + 1, 1, P + 1>(sT2 + NQ, sT1 + NQ, sBl);
-  contract<NT, Q, Q, P + 1, 1, P, 1, P>(sT2 + 2 * NQ, sT1 + 2 * NQ, sBh);
+  lines<NT, Q, Q, P, 1, P, TB_H, false, typename T::B0, typename T::A0>(sB[0], sA[0], tab);
+  lines<NT, Q, Q, P, 1, P + 1, TB_L, false, typename T::B1, typename T::A1>(sB[1], sA[1], tab);
+  lines<NT, Q, Q, P + 1, 1, P, TB_H, false, typename T::B2, typename T::A2>(sB[2], sA[2], tab);
   __syncthreads();
-  contract<NT, Q, P, P, 0, P + 1, 1, P + 1>(sT1, su, sBl);
-  contract<NT, Q, P + 1, P, 0, P, 1, P>(sT1 + NQ, su + NC, sBh);
-  contract<NT, Q, P, P + 1, 0, P, 1, P>(sT1 + 2 * NQ, su + 2 * NC, sBh);
+  lines<NT, Q, P, P, 0, P + 1, TB_L, false, typename T::A0, typename T::U0>(sA[0], su[0], tab);
+  lines<NT, Q, P + 1, P, 0, P, TB_H, false, typename T::A1, typename T::U1>(sA[1], su[1], tab);
+  lines<NT, Q, P, P + 1, 0, P, TB_H, false, typename T::A2, typename T::U2>(sA[2], su[2], tab);
   __syncthreads();
-  // D^T q~ and scatter
-  for (int i = tid; i < 3 * NC; i += NT) {
-    const int c = i / NC, l = i % NC;
-    int li, lj, lk, ic;
-    long long g;
-    if (c == 0) {
-      li = l % (P + 1); lj = (l / (P + 1)) % P; lk = l / ((P + 1) * P); ic = li;
-      g = a.off[0] + (ex * P + li) + (nx + 1) * ((ey * P + lj) + ny * (long long)(ez * P + lk));
-    } else if (c == 1) {
-      li = l % P; lj = (l / P) % (P + 1); lk = l / (P * (P + 1)); ic = lj;
-      g = a.off[1] + (ex * P + li) + nx * ((ey * P + lj) + (ny + 1) * (long long)(ez * P + lk));
-    } else {
-      li = l % P; lj = (l / P) % P; lk = l / (P * P); ic = lk;
-      g = a.off[2] + (ex * P + li) + nx * ((ey * P + lj) + ny * (long long)(ez * P + lk));
+  // ---- D^T q~ and scatter ----
+  {
+    constexpr int NC = (P + 1) * P * P;
+    for (int i = tid; i < 3 * NC; i += NT) {
+      const int c = i / NC, l = i % NC;
+      int li, lj, lk, ic, so;
+      long long g;
+      if (c == 0) {
+        li = l % (P + 1); lj = (l / (P + 1)) % P; lk = l / ((P + 1) * P); ic = li;
+        g = a.off[0] + (ex * P + li) + (nx + 1) * ((ey * P + lj) + ny * (long long)(ez * P + lk));
+        so = li + T::U0::S1 * lj + T::U0::S2 * lk;
+      } else if (c == 1) {
+        li = l % P; lj = (l / P) % (P + 1); lk = l / (P * (P + 1)); ic = lj;
+        g = a.off[1] + (ex * P + li) + nx * ((ey * P + lj) + (ny + 1) * (long long)(ez * P + lk));
+        so = li + T::U1::S1 * lj + T::U1::S2 * lk;
+      } else {
+        li = l % P; lj = (l / P) % P; lk = l / (P * P); ic = lk;
+        g = a.off[2] + (ex * P + li) + nx * ((ey * P + lj) + ny * (long long)(ez * P + lk));
+        so = li + T::U2::S1 * lj + T::U2::S2 * lk;
+      }
+      double v = su[c][so];
+      if constexpr (BLOCK) {
+        const int cstep = (c == 0) ? 1 : (c == 1) ? T::L2::S1 : T::L2::S2;
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;   // the + side cell when ic < P
+        if (ic > 0) v += sq[cell - cstep];
+        if (ic < P) v -= sq[cell];
+      }
+      if (ic == 0 || ic == P) atomicAdd(a.y + g, v);
+      else a.y[g] = v;
     }
-    double v = su[i];
-    if constexpr (BLOCK) {
-      const int cstep = (c == 0) ? 1 : (c == 1) ? P : P * P;
-      const int cell = li + P * (lj + P * lk);   // valid when ic < P (the + side cell)
-      if (ic > 0) v += sq[cell - cstep];
-      if (ic < P) v -= sq[cell];
-    }
-    if (ic == 0 || ic == P) atomicAdd(a.y + g, v);
-    else a.y[g] = v;
   }
   if constexpr (BLOCK) {
     double* yq = a.y + a.nrt;
     const double z = scoef[1];
-    for (int i = tid; i < P3; i += NT) yq[e * P3 + i] = a.has_z ? sy[i] - z * sz1[i] : sy[i];
+    for (int i = tid; i < P3; i += NT) {
+      const int A = i % P, B = (i / P) % P, C = i / (P * P);
+      yq[e * P3 + i] = a.has_z ? sy[i] - z * sz1[A + T::L2::S1 * B + T::L2::S2 * C] : sy[i];
+    }
   }
 }
 
 template <int P, bool BLOCK>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
-  constexpr int NT = 128;
+  constexpr int NT = 64;
   TriArgs a;
   a.x = x; a.y = y; a.vert = h->d_vert; a.coef = h->d_coef;
   for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
