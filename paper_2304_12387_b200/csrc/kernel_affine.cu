@@ -85,8 +85,8 @@ struct Geo {
                                  cmax(CG<P, TX, TY, TZ, 2>::SIZE, SQSIZE));
   static constexpr int HQ0 = CY * CZ, HQ1 = CX * CZ, HQ2 = CX * CY;
   static constexpr int NCO = (TX + 1) * (TY + 1) * (TZ + 1);
-  static constexpr size_t smem_doubles(bool block) {   // two component buffers (double buffer)
-    return 2 * (size_t)SU + (block ? (size_t)SQSIZE + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
+  static constexpr size_t smem_doubles(bool block, bool db = true) {   // db: double buffer
+    return (db ? 2 : 1) * (size_t)SU + (block ? (size_t)SQSIZE + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
   }
 };
 
@@ -364,7 +364,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
 }
 
-template <int P, int TX, int TY, int TZ, int NT, bool BLOCK>
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB>
 __global__ void __launch_bounds__(NT)
 affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
@@ -372,8 +372,8 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   constexpr int P3 = G::P3;
   if (a.skip && *a.skip) return;
   extern __shared__ double smem[];
-  double* bufA = smem;                                // component buffers (double buffered);
-  double* bufB = smem + G::SU;                        // also Z scratch / y_q staging
+  double* bufA = smem;                                // component buffers (DB: double buffered;
+  double* bufB = DB ? smem + G::SU : smem;            // else one buffer, more CTAs per SM)
   double* sq = bufB + G::SU;                          // q~ tile, subcell-major
   double* hq0 = sq + (BLOCK ? G::SQSIZE : 0);         // halo q~ for owned -x planes [K][J]
   double* hq1 = hq0 + (BLOCK ? G::HQ0 : 0);           // [K][I]
@@ -465,14 +465,15 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       }
   }
   cp_async_commit();
-  // ---- group 1: x component -> A ----
-  load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
+  // ---- group 1 (DB): x component -> A, overlapping the Z passes (scratch B) ----
+  if constexpr (DB) load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
 
   double acc[O::NACC];
 #pragma unroll
   for (int k = 0; k < O::NACC; ++k) acc[k] = 0.0;
 
-  cp_async_wait_group<1>();
+  if constexpr (DB) cp_async_wait_group<1>();
+  else cp_async_wait_group<0>();
   __syncthreads();
   if constexpr (BLOCK) {
     if (a.has_z) {
@@ -499,19 +500,34 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       __syncthreads();
     }
   }
-  // ---- group 2: y component -> B ; compute x from A ----
-  load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
-  cp_async_wait_group<1>();
-  __syncthreads();
-  component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, bufA, sq, hq0, sco, acc);
-  // ---- group 3: z component -> A ; compute y from B ----
-  load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
-  cp_async_wait_group<1>();
-  __syncthreads();
-  component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, bufB, sq, hq1, sco, acc);
-  cp_async_wait_group<0>();
-  __syncthreads();
-  component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
+  if constexpr (DB) {
+    // ---- group 2: y component -> B ; compute x from A ----
+    load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
+    cp_async_wait_group<1>();
+    __syncthreads();
+    component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    // ---- group 3: z component -> A ; compute y from B ----
+    load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
+    cp_async_wait_group<1>();
+    __syncthreads();
+    component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, bufB, sq, hq1, sco, acc);
+    cp_async_wait_group<0>();
+    __syncthreads();
+    component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
+  } else {
+    load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
+    cp_async_wait_group<0>();
+    __syncthreads();
+    component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufA);
+    cp_async_wait_group<0>();
+    __syncthreads();
+    component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, bufA, sq, hq1, sco, acc);
+    load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
+    cp_async_wait_group<0>();
+    __syncthreads();
+    component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
+  }
 
   if constexpr (BLOCK) {
     // y_q straight from the accumulators: per owned column, runs of P doubles per element
@@ -533,7 +549,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   }
 }
 
-template <int P, int TX, int TY, int TZ, int NT, bool BLOCK>
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true>
 cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
   using G = Geo<P, TX, TY, TZ>;
@@ -546,8 +562,8 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ntile[2] = (int)((h->NL[2] + TZ - 1) / TZ);
   a.has_z = h->has_z ? 1 : 0;
   a.skip = skip;
-  const size_t smem = G::smem_doubles(BLOCK) * sizeof(double);
-  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK>;
+  const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
+  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB>;
   static bool attr_done = false;   // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -912,12 +928,10 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.nrt = h->nrt;
   a.ntile[0] = (int)((h->NL[0] + TX - 1) / TX);
   a.ntile[1] = (int)((h->NL[1] + TY - 1) / TY);
-  // z chunk: enough CTAs for >= 8 per SM, chunks of at least 4 layers
+  // z chunk: 32 layers (r01 sweep), shortened when that leaves fewer than ~4 CTAs per SM
   const long long cols = (long long)a.ntile[0] * a.ntile[1];
-  long long nch = (148LL * 8 + cols - 1) / cols;
-  if (nch < 1) nch = 1;
-  int zc = (int)((h->NL[2] + nch - 1) / nch);
-  if (zc < 4) zc = 4;
+  int zc = 32;
+  while (zc > 4 && cols * ((h->NL[2] + zc - 1) / zc) < 148LL * 4) zc /= 2;
   const char* e = getenv("HDIV_ZCHUNK");
   if (e) zc = atoi(e);
   if (zc > h->NL[2]) zc = (int)h->NL[2];
@@ -944,15 +958,18 @@ static int tile_variant() {
   return e ? atoi(e) : 0;
 }
 
-static int march_variant() {   // -1 selects the halo-tile kernel instead of z-marching
+// Default per order from the r01 sweeps (profiles/): z-marching wins at p = 3, 5; the halo-tile
+// kernel at p = 1, 2, 4, 6.  HDIV_MARCH_TILE=-1 forces halo tiles, >= 0 a marching variant.
+static int march_variant(int p) {
   const char* e = getenv("HDIV_MARCH_TILE");
-  return e ? atoi(e) : 0;
+  if (e) return atoi(e);
+  return (p == 3) ? 0 : (p == 5) ? 1 : -1;
 }
 
 template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
                      cudaStream_t s) {
-  const int mv = march_variant();
+  const int mv = march_variant(h->p);
   if (mv >= 0) {
     switch (h->p) {
       case 1: return launch_m<1, 8, 8, 128, BLOCK>(h, x, y, k, s);
@@ -974,29 +991,38 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
     }
     return cudaErrorInvalidValue;
   }
+  // halo-tile variants: 0..3 double-buffered shapes, 4/5 single-buffered (more CTAs per SM)
   const int v = tile_variant();
   switch (h->p) {
     case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
     case 2:
       if (v == 1) return launch_t<2, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<2, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
+      if (v == 4) return launch_t<2, 8, 4, 4, 128, BLOCK, false>(h, x, y, k, s);
       return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
     case 3:
       if (v == 1) return launch_t<3, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 4) return launch_t<3, 8, 4, 2, 128, BLOCK, false>(h, x, y, k, s);
       return launch_t<3, 8, 4, 2, 128, BLOCK>(h, x, y, k, s);
     case 4:
       if (v == 1) return launch_t<4, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 3) return launch_t<4, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 4) return launch_t<4, 4, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 5) return launch_t<4, 4, 4, 2, 128, BLOCK, false>(h, x, y, k, s);
       return launch_t<4, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 5:
       if (v == 1) return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<5, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 4) return launch_t<5, 2, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 5) return launch_t<5, 4, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
       return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 6:
       if (v == 1) return launch_t<6, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
+      if (v == 4) return launch_t<6, 2, 2, 1, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 5) return launch_t<6, 2, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
       return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;

@@ -109,10 +109,10 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   constexpr int R1 = (3 * T::SU > 3 * T::SB) ? 3 * T::SU : 3 * T::SB;
   constexpr int R2 = (3 * T::SA > 3 * T::SV) ? 3 * T::SA : 3 * T::SV;
   __shared__ double sreg[R1 + R2];
-  double* const su[3] = {sreg, sreg + T::SU, sreg + 2 * T::SU};
-  double* const sB[3] = {sreg, sreg + T::SB, sreg + 2 * T::SB};
-  double* const sA[3] = {sreg + R1, sreg + R1 + T::SA, sreg + R1 + 2 * T::SA};
-  double* const sV[3] = {sreg + R1, sreg + R1 + T::SV, sreg + R1 + 2 * T::SV};
+#define su(c) (sreg + (c) * T::SU)
+#define sB(c) (sreg + (c) * T::SB)
+#define sA(c) (sreg + R1 + (c) * T::SA)
+#define sV(c) (sreg + R1 + (c) * T::SV)
   __shared__ double sq[BLOCK ? T::SL : 1], sy[BLOCK ? P3 : 1], sz1[BLOCK ? T::SL : 1],
       sz2[BLOCK ? T::SL : 1];
   __shared__ double scoef[2];
@@ -130,27 +130,22 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
                         (ex + (v & 1));
     sX[i] = a.vert[g * 3 + d];
   }
-  // gather u: component c, local (i,j,k) i fastest, extent P+1 along c, padded layout
+  // gather u per component (compile-time extents, i fastest; padded smem layouts)
   {
-    constexpr int NC = (P + 1) * P * P;
-    for (int i = tid; i < 3 * NC; i += NT) {
-      const int c = i / NC, l = i % NC;
-      int li, lj, lk, so;
-      long long g;
-      if (c == 0) {
-        li = l % (P + 1); lj = (l / (P + 1)) % P; lk = l / ((P + 1) * P);
-        g = a.off[0] + (ex * P + li) + (nx + 1) * ((ey * P + lj) + ny * (long long)(ez * P + lk));
-        so = li + T::U0::S1 * lj + T::U0::S2 * lk;
-      } else if (c == 1) {
-        li = l % P; lj = (l / P) % (P + 1); lk = l / (P * (P + 1));
-        g = a.off[1] + (ex * P + li) + nx * ((ey * P + lj) + (ny + 1) * (long long)(ez * P + lk));
-        so = li + T::U1::S1 * lj + T::U1::S2 * lk;
-      } else {
-        li = l % P; lj = (l / P) % P; lk = l / (P * P);
-        g = a.off[2] + (ex * P + li) + nx * ((ey * P + lj) + ny * (long long)(ez * P + lk));
-        so = li + T::U2::S1 * lj + T::U2::S2 * lk;
-      }
-      su[c][so] = a.x[g];
+    const long long gx = a.off[0] + (long long)ex * P + (nx + 1) * ((long long)ey * P + ny * (long long)ez * P);
+    const long long gy = a.off[1] + (long long)ex * P + nx * ((long long)ey * P + (ny + 1) * (long long)ez * P);
+    const long long gz = a.off[2] + (long long)ex * P + nx * ((long long)ey * P + ny * (long long)ez * P);
+    for (int l = tid; l < (P + 1) * P * P; l += NT) {
+      const int li = l % (P + 1), lj = (l / (P + 1)) % P, lk = l / ((P + 1) * P);
+      su(0)[li + T::U0::S1 * lj + T::U0::S2 * lk] = a.x[gx + li + (nx + 1) * (lj + ny * lk)];
+    }
+    for (int l = tid; l < (P + 1) * P * P; l += NT) {
+      const int li = l % P, lj = (l / P) % (P + 1), lk = l / (P * (P + 1));
+      su(1)[li + T::U1::S1 * lj + T::U1::S2 * lk] = a.x[gy + li + nx * (lj + (ny + 1) * lk)];
+    }
+    for (int l = tid; l < (P + 1) * P * P; l += NT) {
+      const int li = l % P, lj = (l / P) % P, lk = l / (P * P);
+      su(2)[li + T::U2::S1 * lj + T::U2::S2 * lk] = a.x[gz + li + nx * (lj + ny * lk)];
     }
   }
   if constexpr (BLOCK) {
@@ -180,30 +175,30 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     sJ[c][pr][d] = v;
   }
   // ---- forward: axis 0, 1, 2 (3 components per stage), + D u and Z q~ ----
-  lines<NT, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0>(su[0], sA[0], tab);
-  lines<NT, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1>(su[1], sA[1], tab);
-  lines<NT, P, P, P + 1, 0, Q, TB_H, true, typename T::U2, typename T::A2>(su[2], sA[2], tab);
+  lines<NT, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0>(su(0), sA(0), tab);
+  lines<NT, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1>(su(1), sA(1), tab);
+  lines<NT, P, P, P + 1, 0, Q, TB_H, true, typename T::U2, typename T::A2>(su(2), sA(2), tab);
   if constexpr (BLOCK) {
     for (int i = tid; i < P3; i += NT) {
       const int A = i % P, B = (i / P) % P, C = i / (P * P);
-      const double* u0 = su[0] + A + T::U0::S1 * B + T::U0::S2 * C;
-      const double* u1 = su[1] + A + T::U1::S1 * B + T::U1::S2 * C;
-      const double* u2 = su[2] + A + T::U2::S1 * B + T::U2::S2 * C;
+      const double* u0 = su(0) + A + T::U0::S1 * B + T::U0::S2 * C;
+      const double* u1 = su(1) + A + T::U1::S1 * B + T::U1::S2 * C;
+      const double* u2 = su(2) + A + T::U2::S1 * B + T::U2::S2 * C;
       sy[i] = (u0[1] - u0[0]) + (u1[T::U1::S1] - u1[0]) + (u2[T::U2::S2] - u2[0]);
     }
     if (a.has_z)
       lines<NT, P, P, P, 0, P, TB_HI, true, typename T::L2, typename T::L2>(sq, sz1, tab);
   }
   __syncthreads();
-  lines<NT, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0>(sA[0], sB[0], tab);
-  lines<NT, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1>(sA[1], sB[1], tab);
-  lines<NT, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2>(sA[2], sB[2], tab);
+  lines<NT, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0>(sA(0), sB(0), tab);
+  lines<NT, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1>(sA(1), sB(1), tab);
+  lines<NT, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2>(sA(2), sB(2), tab);
   if constexpr (BLOCK)
     if (a.has_z) lines<NT, P, P, P, 1, P, TB_HI, true, typename T::L2, typename T::L2>(sz1, sz2, tab);
   __syncthreads();
-  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V>(sB[0], sV[0], tab);
-  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V>(sB[1], sV[1], tab);
-  lines<NT, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V>(sB[2], sV[2], tab);
+  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V>(sB(0), sV(0), tab);
+  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V>(sB(1), sV(1), tab);
+  lines<NT, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V>(sB(2), sV(2), tab);
   if constexpr (BLOCK)
     if (a.has_z) lines<NT, P, P, P, 2, P, TB_HI, true, typename T::L2, typename T::L2>(sz2, sz1, tab);
   __syncthreads();
@@ -218,57 +213,66 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
                        c2[0] * (c0[1] * c1[2] - c0[2] * c1[1]);
     const double s = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] * mw / det;
     const int o = qx + T::V::S1 * qy + T::V::S2 * qz;
-    const double u0 = sV[0][o], u1 = sV[1][o], u2 = sV[2][o];
+    const double u0 = sV(0)[o], u1 = sV(1)[o], u2 = sV(2)[o];
     double Ju[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) Ju[d] = c0[d] * u0 + c1[d] * u1 + c2[d] * u2;
-    sV[0][o] = s * (c0[0] * Ju[0] + c0[1] * Ju[1] + c0[2] * Ju[2]);
-    sV[1][o] = s * (c1[0] * Ju[0] + c1[1] * Ju[1] + c1[2] * Ju[2]);
-    sV[2][o] = s * (c2[0] * Ju[0] + c2[1] * Ju[1] + c2[2] * Ju[2]);
+    sV(0)[o] = s * (c0[0] * Ju[0] + c0[1] * Ju[1] + c0[2] * Ju[2]);
+    sV(1)[o] = s * (c1[0] * Ju[0] + c1[1] * Ju[1] + c1[2] * Ju[2]);
+    sV(2)[o] = s * (c2[0] * Ju[0] + c2[1] * Ju[1] + c2[2] * Ju[2]);
   }
   __syncthreads();
   // ---- backward: axis 2, 1, 0 ----
-  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B0>(sV[0], sB[0], tab);
-  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B1>(sV[1], sB[1], tab);
-  lines<NT, Q, Q, Q, 2, P + 1, TB_L, false, typename T::V, typename T::B2>(sV[2], sB[2], tab);
+  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B0>(sV(0), sB(0), tab);
+  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B1>(sV(1), sB(1), tab);
+  lines<NT, Q, Q, Q, 2, P + 1, TB_L, false, typename T::V, typename T::B2>(sV(2), sB(2), tab);
   __syncthreads();
-  lines<NT, Q, Q, P, 1, P, TB_H, false, typename T::B0, typename T::A0>(sB[0], sA[0], tab);
-  lines<NT, Q, Q, P, 1, P + 1, TB_L, false, typename T::B1, typename T::A1>(sB[1], sA[1], tab);
-  lines<NT, Q, Q, P + 1, 1, P, TB_H, false, typename T::B2, typename T::A2>(sB[2], sA[2], tab);
+  lines<NT, Q, Q, P, 1, P, TB_H, false, typename T::B0, typename T::A0>(sB(0), sA(0), tab);
+  lines<NT, Q, Q, P, 1, P + 1, TB_L, false, typename T::B1, typename T::A1>(sB(1), sA(1), tab);
+  lines<NT, Q, Q, P + 1, 1, P, TB_H, false, typename T::B2, typename T::A2>(sB(2), sA(2), tab);
   __syncthreads();
-  lines<NT, Q, P, P, 0, P + 1, TB_L, false, typename T::A0, typename T::U0>(sA[0], su[0], tab);
-  lines<NT, Q, P + 1, P, 0, P, TB_H, false, typename T::A1, typename T::U1>(sA[1], su[1], tab);
-  lines<NT, Q, P, P + 1, 0, P, TB_H, false, typename T::A2, typename T::U2>(sA[2], su[2], tab);
+  lines<NT, Q, P, P, 0, P + 1, TB_L, false, typename T::A0, typename T::U0>(sA(0), su(0), tab);
+  lines<NT, Q, P + 1, P, 0, P, TB_H, false, typename T::A1, typename T::U1>(sA(1), su(1), tab);
+  lines<NT, Q, P, P + 1, 0, P, TB_H, false, typename T::A2, typename T::U2>(sA(2), su(2), tab);
   __syncthreads();
-  // ---- D^T q~ and scatter ----
+  // ---- D^T q~ and scatter (per component; boundary faces by atomics) ----
   {
-    constexpr int NC = (P + 1) * P * P;
-    for (int i = tid; i < 3 * NC; i += NT) {
-      const int c = i / NC, l = i % NC;
-      int li, lj, lk, ic, so;
-      long long g;
-      if (c == 0) {
-        li = l % (P + 1); lj = (l / (P + 1)) % P; lk = l / ((P + 1) * P); ic = li;
-        g = a.off[0] + (ex * P + li) + (nx + 1) * ((ey * P + lj) + ny * (long long)(ez * P + lk));
-        so = li + T::U0::S1 * lj + T::U0::S2 * lk;
-      } else if (c == 1) {
-        li = l % P; lj = (l / P) % (P + 1); lk = l / (P * (P + 1)); ic = lj;
-        g = a.off[1] + (ex * P + li) + nx * ((ey * P + lj) + (ny + 1) * (long long)(ez * P + lk));
-        so = li + T::U1::S1 * lj + T::U1::S2 * lk;
-      } else {
-        li = l % P; lj = (l / P) % P; lk = l / (P * P); ic = lk;
-        g = a.off[2] + (ex * P + li) + nx * ((ey * P + lj) + ny * (long long)(ez * P + lk));
-        so = li + T::U2::S1 * lj + T::U2::S2 * lk;
-      }
-      double v = su[c][so];
+    const long long gx = a.off[0] + (long long)ex * P + (nx + 1) * ((long long)ey * P + ny * (long long)ez * P);
+    const long long gy = a.off[1] + (long long)ex * P + nx * ((long long)ey * P + (ny + 1) * (long long)ez * P);
+    const long long gz = a.off[2] + (long long)ex * P + nx * ((long long)ey * P + ny * (long long)ez * P);
+    auto put = [&](double* g, double v, int ic) {
+      if (ic == 0 || ic == P) atomicAdd(g, v);
+      else *g = v;
+    };
+    for (int l = tid; l < (P + 1) * P * P; l += NT) {
+      const int li = l % (P + 1), lj = (l / (P + 1)) % P, lk = l / ((P + 1) * P);
+      double v = su(0)[li + T::U0::S1 * lj + T::U0::S2 * lk];
       if constexpr (BLOCK) {
-        const int cstep = (c == 0) ? 1 : (c == 1) ? T::L2::S1 : T::L2::S2;
-        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;   // the + side cell when ic < P
-        if (ic > 0) v += sq[cell - cstep];
-        if (ic < P) v -= sq[cell];
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;
+        if (li > 0) v += sq[cell - 1];
+        if (li < P) v -= sq[cell];
       }
-      if (ic == 0 || ic == P) atomicAdd(a.y + g, v);
-      else a.y[g] = v;
+      put(a.y + gx + li + (nx + 1) * (lj + ny * lk), v, li);
+    }
+    for (int l = tid; l < (P + 1) * P * P; l += NT) {
+      const int li = l % P, lj = (l / P) % (P + 1), lk = l / (P * (P + 1));
+      double v = su(1)[li + T::U1::S1 * lj + T::U1::S2 * lk];
+      if constexpr (BLOCK) {
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;
+        if (lj > 0) v += sq[cell - T::L2::S1];
+        if (lj < P) v -= sq[cell];
+      }
+      put(a.y + gy + li + nx * (lj + (ny + 1) * lk), v, lj);
+    }
+    for (int l = tid; l < (P + 1) * P * P; l += NT) {
+      const int li = l % P, lj = (l / P) % P, lk = l / (P * P);
+      double v = su(2)[li + T::U2::S1 * lj + T::U2::S2 * lk];
+      if constexpr (BLOCK) {
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;
+        if (lk > 0) v += sq[cell - T::L2::S2];
+        if (lk < P) v -= sq[cell];
+      }
+      put(a.y + gz + li + nx * (lj + ny * lk), v, lk);
     }
   }
   if constexpr (BLOCK) {

@@ -1,16 +1,14 @@
 #!/bin/bash
-# time every tile variant of the box kernel (HDIV_AFFINE_TILE) for p = 2..6
-for v in -1; do
-  HDIV_MARCH_TILE=$v python - <<'PY'
+# halo-tile kernel variants (HDIV_MARCH_TILE=-1, HDIV_AFFINE_TILE=v), p = 2..6
+for v in 0 1 2 4 5; do
+  HDIV_MARCH_TILE=-1 HDIV_AFFINE_TILE=$v python - <<'PY'
 import os, sys
 sys.path.insert(0, ".")
 import torch
 from synth import make_config
 from paper_2304_12387_b200 import from_problem
-v = os.environ["HDIV_MARCH_TILE"]
+v = os.environ["HDIV_AFFINE_TILE"]
 for p, N in [(2, 160), (3, 128), (4, 128), (5, 96), (6, 80)]:
-    if False:
-        continue
     pr = make_config("c4", N=(N, N, N), p=p)
     op = from_problem(pr)
     x = torch.rand(op.sizes.n, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
@@ -22,7 +20,7 @@ for p, N in [(2, 160), (3, 128), (4, 128), (5, 96), (6, 80)]:
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     n = op.sizes.n
-    print(f"variant {v} p={p} N={N}: {ms:.3f} ms {n/ms/1e6:.1f} GDOF/s {16*n/ms/1e6/6534.8*100:.1f}% HBM", flush=True)
+    print(f"halo variant {v} p={p} N={N}: {ms:.3f} ms {n/ms/1e6:.1f} GDOF/s {16*n/ms/1e6/6534.8*100:.1f}% HBM", flush=True)
     op.close(); del x, y; torch.cuda.empty_cache()
 PY
 done
