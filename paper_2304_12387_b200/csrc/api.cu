@@ -86,6 +86,8 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_srow);
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
+  cudaFree(h->d_ecol);
+  cudaFree(h->d_eval);
   cudaFree(h->d_scratch);
   cudaFree(h->d_xbuf);
   cudaFree(h->d_ybuf);

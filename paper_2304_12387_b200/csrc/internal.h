@@ -69,6 +69,8 @@ struct hdiv_ctx {
   int64_t* d_srow = nullptr;      // S~ CSR (local rows; ghost columns >= nl2 for multi-GPU)
   int32_t* d_scol = nullptr;
   double* d_sval = nullptr;
+  int32_t* d_ecol = nullptr;      // S~ as SELL-32, fixed width 2d+1 (padding: col=row, val=0)
+  double* d_eval = nullptr;
   int64_t snnz = 0;
   double* d_scratch = nullptr;    // reduction partials etc.
   double* d_xbuf = nullptr;       // host-API staging (lazily allocated)

@@ -49,6 +49,12 @@ __device__ __forceinline__ void cp_async_wait_group() {
 
 constexpr int odd_up(int v) { return (v % 2) ? v : v + 1; }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
+// x component: 1 = store the owned planes straight from the line pass (per-lane runs along x;
+// full sectors merge in L2), 0 = write back to smem + coalesced copy-out
+#ifndef HDIV_X_DIRECT
+#define HDIV_X_DIRECT 1
+#endif
+constexpr bool kXDirect = HDIV_X_DIRECT;
 
 // smem box of component AX: extent (T_AX+1)P+1 along AX (position 0 <-> global plane
 // (e0_AX - 1) P), T P along the others; extents 0 and 1 padded odd.
@@ -232,9 +238,19 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
         int pos[3] = {col % G::CX, col / G::CX, 0};
         pos[AX] += P;
         const double* s = su + pos[0] + C::S1 * pos[1] + C::S2 * pos[2];
+        if constexpr (AX == 2) {   // walk up the column: each z face read once
+          double lo = s[0];
 #pragma unroll
-        for (int z = 0; z < G::CZ; ++z)
-          acc[j * G::CZ + z] += s[z * C::S2 + C::SA] - s[z * C::S2];
+          for (int z = 0; z < G::CZ; ++z) {
+            const double hi = s[(z + 1) * C::S2];
+            acc[j * G::CZ + z] += hi - lo;
+            lo = hi;
+          }
+        } else {
+#pragma unroll
+          for (int z = 0; z < G::CZ; ++z)
+            acc[j * G::CZ + z] += s[z * C::S2 + C::SA] - s[z * C::S2];
+        }
       }
     }
     __syncthreads();
@@ -297,7 +313,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     const int l1 = it % EL1P, l2 = it / EL1P;
     if (l1 >= EL1) continue;
     const bool line_ok = l1 < hiA1 && l2 < hiA2;
-    if (AX != 0 && !line_ok) continue;
+    if ((AX != 0 || kXDirect) && !line_ok) continue;
     double* line = su + l1 * C::SA1 + l2 * C::SA2;
     double* gl = yt + (l1 * gs1 + l2 * gs2);
     int ec[3];
@@ -335,7 +351,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
             o += qprev - qc;
             qprev = qc;
           }
-          if (AX == 0) eb[i * C::SA] = o;
+          if (AX == 0 && !kXDirect) eb[i * C::SA] = o;
           else __stcs(gl + ((et + 1) * P + i) * gsa, o);
         }
         double s = 0.0;
@@ -346,13 +362,13 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     }
     if (ti.last[AX]) {
       const double o = carry + (BLOCK ? qprev : 0.0);
-      if (AX == 0) line[(m_a + 1) * P * C::SA] = o;
+      if (AX == 0 && !kXDirect) line[(m_a + 1) * P * C::SA] = o;
       else __stcs(gl + (m_a + 1) * P * gsa, o);
     }
   }
   __syncthreads();
 
-  if constexpr (AX == 0) {
+  if constexpr (AX == 0 && !kXDirect) {
     // ---- copy-out of the owned x planes (coalesced, streaming) ----
     constexpr int NO0 = TX * P + 1;
     const int own_hi = m_a * P + (ti.last[0] ? 1 : 0);   // exclusive, relative to position P
@@ -483,8 +499,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       __syncthreads();
       hpass<P, NT>(bufB, bufB, tab.Mhinv, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
       __syncthreads();
-      hpass<P, NT>(bufB, bufB, tab.Mhinv, G::CX, 1, G::CY, G::Q1, TZ, P * G::Q2, G::Q2);
-      __syncthreads();
+      // Z-lines in registers: every thread owns whole z-columns of cells
 #pragma unroll
       for (int j = 0; j < O::JC; ++j) {
         const int col = tid + j * NT;
@@ -493,8 +508,19 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
           const double* sz = sco + 4 * (((Y / P) + 1) * (TX + 1) + (X / P) + 1) + 3;
           const double* s = bufB + X + G::Q1 * Y;
 #pragma unroll
-          for (int z = 0; z < G::CZ; ++z)
-            acc[j * G::CZ + z] = -sz[4 * (TX + 1) * (TY + 1) * (z / P + 1)] * s[z * G::Q2];
+          for (int zb = 0; zb < TZ; ++zb) {
+            double v[P];
+#pragma unroll
+            for (int k = 0; k < P; ++k) v[k] = s[(zb * P + k) * G::Q2];
+            const double ze = sz[4 * (TX + 1) * (TY + 1) * (zb + 1)];
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              double t = 0.0;
+#pragma unroll
+              for (int k = 0; k < P; ++k) t = fma(tab.Mhinv[i][k], v[k], t);
+              acc[j * G::CZ + zb * P + i] = -ze * t;
+            }
+          }
         }
       }
       __syncthreads();
@@ -953,9 +979,11 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
 }
 
 // Tile shapes per order; variant 0 is the default, HDIV_AFFINE_TILE=<k> selects another (tuning).
-static int tile_variant() {
+// halo-tile shape per order (r01 sweeps, profiles/): HDIV_AFFINE_TILE overrides
+static int tile_variant(int p) {
   const char* e = getenv("HDIV_AFFINE_TILE");
-  return e ? atoi(e) : 0;
+  if (e) return atoi(e);
+  return (p == 3) ? 4 : (p == 6) ? 5 : 0;
 }
 
 // Default per order from the r01 sweeps (profiles/): z-marching wins at p = 3, 5; the halo-tile
@@ -963,7 +991,7 @@ static int tile_variant() {
 static int march_variant(int p) {
   const char* e = getenv("HDIV_MARCH_TILE");
   if (e) return atoi(e);
-  return (p == 3) ? 0 : (p == 5) ? 1 : -1;
+  return (p == 5) ? 1 : -1;
 }
 
 template <bool BLOCK>
@@ -992,7 +1020,7 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
     return cudaErrorInvalidValue;
   }
   // halo-tile variants: 0..3 double-buffered shapes, 4/5 single-buffered (more CTAs per SM)
-  const int v = tile_variant();
+  const int v = tile_variant(h->p);
   switch (h->p) {
     case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
     case 2:

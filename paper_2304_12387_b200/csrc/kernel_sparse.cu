@@ -174,6 +174,21 @@ __global__ void schur_fill_kernel(Grid g, const double* __restrict__ mdiag,
   sdinv[i] = 1.0 / d;
 }
 
+// CSR -> SELL-32 with fixed width W: entry (row, k) at (row/32)*32*W + k*32 + row%32
+__global__ void sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ c,
+                            const double* __restrict__ v, int32_t* ec, double* ev, long long n,
+                            int W) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long base = (i / 32) * 32 * W + (i % 32);
+  const long long r0 = rp[i], r1 = rp[i + 1];
+  for (int k = 0; k < W; ++k) {
+    const long long t = r0 + k;
+    ec[base + 32 * k] = (t < r1) ? c[t] : (int32_t)i;
+    ev[base + 32 * k] = (t < r1) ? v[t] : 0.0;
+  }
+}
+
 __global__ void schur_export_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ c,
                                     const double* __restrict__ v, int64_t* rp_o, int64_t* c_o,
                                     double* v_o, long long nl2) {
@@ -306,6 +321,16 @@ hdiv_status build_schur(hdiv_ctx* h, cudaStream_t s) {
   HDIV_CUDA_TRY(cudaMalloc(&h->d_sdinv, sizeof(double) * (n > 0 ? n : 1)));
   schur_fill_kernel<<<nblocks(n, 256), 256, 0, s>>>(g, h->d_mdiag, h->d_ctil, h->d_srow,
                                                     h->d_scol, h->d_sval, h->d_sdinv, n);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  // sliced-ELL copy used by the SpMV inside S^-1 (coalesced slot loads)
+  const int W = 2 * h->dim + 1;
+  const long long ns = (n + 31) / 32;
+  HDIV_CUDA_TRY(cudaMalloc(&h->d_ecol, sizeof(int32_t) * ns * 32 * W));
+  HDIV_CUDA_TRY(cudaMalloc(&h->d_eval, sizeof(double) * ns * 32 * W));
+  HDIV_CUDA_TRY(cudaMemsetAsync(h->d_ecol, 0, sizeof(int32_t) * ns * 32 * W, s));
+  HDIV_CUDA_TRY(cudaMemsetAsync(h->d_eval, 0, sizeof(double) * ns * 32 * W, s));
+  sell_kernel<<<nblocks(n, 256), 256, 0, s>>>(h->d_srow, h->d_scol, h->d_sval, h->d_ecol,
+                                              h->d_eval, n, W);
   HDIV_CUDA_TRY(cudaGetLastError());
   return HDIV_OK;
 }

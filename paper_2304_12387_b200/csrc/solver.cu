@@ -142,9 +142,11 @@ cheb_first_kernel(const double* __restrict__ rin, const double* __restrict__ din
   }
 }
 
+// S~ d with S~ in SELL-32 of width W (padding slots: col = row, val = 0)
+template <int W>
 __global__ void __launch_bounds__(RED_NT)
-cheb_step_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                 const double* __restrict__ val, const double* rin, double* rout,
+cheb_step_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                 const double* rin, double* rout,
                  const double* __restrict__ d, double* __restrict__ dn,
                  const double* __restrict__ dinv, double* __restrict__ y, double c1, double c2,
                  long long n, int last, const double* __restrict__ vin, double* part,
@@ -153,8 +155,10 @@ cheb_step_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
        i += (long long)gridDim.x * RED_NT) {
+    const long long base = (i >> 5) * (32 * W) + (i & 31);
     double sd = 0.0;
-    for (long long t = rp[i]; t < rp[i + 1]; ++t) sd = fma(val[t], d[col[t]], sd);
+#pragma unroll
+    for (int k = 0; k < W; ++k) sd = fma(eval[base + 32 * k], d[ecol[base + 32 * k]], sd);
     double r = rin[i] - sd;
     rout[i] = r;
     double dd = c1 * d[i] + c2 * dinv[i] * r;
@@ -324,10 +328,16 @@ static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* 
       hdiv_status st = comm_l2_ghosts(h, dprev, s);
       if (st != HDIV_OK) return st;
     }
-    cheb_step_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_srow, h->d_scol, h->d_sval, rin, mw->r,
-                                                   dprev, mw->d[i & 1], h->d_sdinv, y,
-                                                   mw->c1[i - 1], mw->c2[i - 1], n, i == k - 1,
-                                                   vq, part, done);
+    if (h->dim == 3)
+      cheb_step_kernel<7><<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
+                                                        mw->d[i & 1], h->d_sdinv, y,
+                                                        mw->c1[i - 1], mw->c2[i - 1], n,
+                                                        i == k - 1, vq, part, done);
+    else
+      cheb_step_kernel<5><<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
+                                                        mw->d[i & 1], h->d_sdinv, y,
+                                                        mw->c1[i - 1], mw->c2[i - 1], n,
+                                                        i == k - 1, vq, part, done);
     HDIV_CUDA_TRY(cudaGetLastError());
     rin = mw->r;
   }
