@@ -256,14 +256,35 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     __syncthreads();
   }
 
-  // ---- M_h (x) M_h over the two histopolation axes: one P x P block per thread ----
-  // lanes run along AX (odd stride); the position range is padded to a multiple of 16 so a
-  // half-warp never straddles two blocks (conflict-free 8-byte accesses)
-  constexpr int EAP = (C::EA + 15) / 16 * 16;
+  // ---- halo element: only its contribution to the shared plane is needed, and by
+  //      linearity c_h sum_j M_l[P][j] (M_h (x) M_h) u_j = c_h (M_h (x) M_h) sum_j M_l[P][j] u_j,
+  //      so the raw halo planes are combined first into position P-1 (one plane to transform)
+  constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
+  constexpr int EL1P = (EL1 + 15) / 16 * 16;   // half-warp aligned lane rows
+  const int m_a = ti.m[AX], h_a = ti.h[AX];
+  if (h_a) {
+#pragma unroll 1
+    for (int it = tid; it < EL1P * EL2; it += NT) {
+      const int l1 = it % EL1P, l2 = it / EL1P;
+      if (l1 >= EL1) continue;
+      double* line = su + l1 * C::SA1 + l2 * C::SA2;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], line[j * C::SA], s);
+      line[(P - 1) * C::SA] = s;
+    }
+    __syncthreads();
+  }
+
+  // ---- M_h (x) M_h over the two histopolation axes: one P x P block per thread, positions
+  //      P-1 (combined halo) .. (T+1)P; lanes run along AX (odd stride), the position range
+  //      padded to a multiple of 16 so a half-warp never straddles two blocks ----
+  constexpr int EAH = C::EA - (P - 1);
+  constexpr int EAP = (EAH + 15) / 16 * 16;
   constexpr int NH = EAP * C::TA1 * C::TA2;
 #pragma unroll 2
   for (int it = tid; it < NH; it += NT) {
-    const int pa = it % EAP, b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
+    const int pa = it % EAP + (P - 1), b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
     if (pa >= C::EA) continue;
     double* base = su + pa * C::SA + b1 * P * C::SA1 + b2 * P * C::SA2;
     double v[P][P];
@@ -296,8 +317,6 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   // ---- c_e M_l along AX element by element (shared-plane sum carried in a register),
   //      + D^T q~ ; y/z: owned planes stored straight to HBM (lanes run along x: coalesced),
   //      x: written back to smem for a coalesced copy-out ----
-  constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
-  constexpr int EL1P = (EL1 + 15) / 16 * 16;   // half-warp aligned lane rows
   constexpr int NL = EL1P * EL2;
   constexpr int QA1 = (C::A1 == 0) ? 1 : G::Q1;
   constexpr int QA2 = (C::A2 == 1) ? G::Q1 : G::Q2;
@@ -305,7 +324,6 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   const long long gs1 = (C::A1 == 0) ? 1 : ext0;        // HBM strides along A1, A2, AX
   const long long gs2 = (C::A2 == 1) ? ext0 : ext01;
   const long long gsa = (AX == 0) ? 1 : (AX == 1) ? ext0 : ext01;
-  const int m_a = ti.m[AX], h_a = ti.h[AX];
   const int hiA1 = (C::A1 == 0) ? hi0 : hi1, hiA2 = (C::A2 == 1) ? hi1 : hi2;
   double* yt = a.y + gtile;
 #pragma unroll 1
@@ -325,11 +343,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     constexpr int CSTEP = 4 * ((AX == 0) ? 1 : (AX == 1) ? (TX + 1) : (TX + 1) * (TY + 1));
     const double* ql = sq + l1 * QA1 + l2 * QA2;
     double carry = 0.0, qprev = 0.0;
-    if (h_a) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j <= P; ++j) s = fma(tab.Ml[P][j], line[j * C::SA], s);
-      carry = cbase[-CSTEP] * s;
+    if (h_a) {   // transformed combined halo plane (position P-1)
+      carry = cbase[-CSTEP] * line[(P - 1) * C::SA];
       if (BLOCK) qprev = hq[l2 * EL1 + l1];
     }
 #pragma unroll
