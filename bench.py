@@ -344,6 +344,19 @@ def main():
                             "time_to_solve_s": rep.t_solve_ms / 1e3,
                             "preconditioner": "diag(tau M~) + Chebyshev-Jacobi(S~), degree 4"}
         op2.close()
+        del xs, b
+        torch.cuda.empty_cache()
+        if args.config == "c4":
+            # per-iteration device cost of the whole MINRES iteration at the bench workload
+            op4 = build_operator(pr, 1, 0, None)
+            b4 = torch.rand(op4.sizes.n, dtype=torch.float64, device="cuda")
+            op4.minres(b4, rtol=1e-30, maxit=6)
+            _, r4 = op4.minres(b4, rtol=1e-30, maxit=30)
+            result["minres"]["c4_ms_per_iteration"] = r4.t_solve_ms / max(r4.iters, 1)
+            result["minres"]["c4_iterations_timed"] = r4.iters
+            op4.close()
+            del b4
+            torch.cuda.empty_cache()
 
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(pr)

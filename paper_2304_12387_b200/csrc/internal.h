@@ -24,6 +24,11 @@ struct Tab1D {
   double Ml[MAXP + 1][MAXP + 1];        // 1D masses B^T W B
   double Mh[MAXP][MAXP];
   double Mhinv[MAXP][MAXP];
+  // Gauss-Legendre nodal basis of Q_{p-1} (p GL points g_b) for the local CG of W^-1
+  // (P:606): BG[q][b] = L_b(x_q), HG[a][b] = integral over subinterval a of L_b
+  // (histopolation coefficients of L_b, i.e. the change of basis GL-nodal -> histopolation)
+  double BG[MAXQ][MAXP];
+  double HG[MAXP][MAXP];
 };
 
 // Small table set for the affine (axis-aligned box) kernels.

@@ -40,13 +40,32 @@ struct Lay {
   static constexpr int S1 = odd_up(D0), S2 = S1 * odd_up(D1), SIZE = S2 * D2;
 };
 
-enum { TB_L = 0, TB_H = 1, TB_HI = 2 };   // B_l, B_h, M_h^-1
+// 1D tables: B_l, B_h, M_h^-1, GL-nodal basis at the quadrature points (BG), its square
+// (diagonal of W in the GL basis), the change of basis GL-nodal -> histopolation (HG) and HG^T
+enum { TB_L = 0, TB_H = 1, TB_HI = 2, TB_G = 3, TB_G2 = 4, TB_HG = 5, TB_HGT = 6 };
 
 template <int KIND, bool FWD>
 __device__ __forceinline__ double tcoef(const Tab1D& tab, int o, int t) {
   if (KIND == TB_HI) return tab.Mhinv[o][t];
+  if (KIND == TB_HG) return tab.HG[o][t];
+  if (KIND == TB_HGT) return tab.HG[t][o];
+  if (KIND == TB_G) return FWD ? tab.BG[o][t] : tab.BG[t][o];
+  if (KIND == TB_G2) return FWD ? tab.BG[o][t] * tab.BG[o][t] : tab.BG[t][o] * tab.BG[t][o];
   if (FWD) return (KIND == TB_L) ? tab.Bl[o][t] : tab.Bh[o][t];   // T(o=q, t=i) = B[q][i]
   return (KIND == TB_L) ? tab.Bl[t][o] : tab.Bh[t][o];            // T(o=i, t=q) = B[q][i]
+}
+
+// sum over the CTA of a per-thread value (all threads return the total)
+template <int NT>
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) s += red[w];
+  __syncthreads();
+  return s;
 }
 
 // line contraction along AX: in (N0,N1,N2) layout LI -> out (.. NO at AX ..) layout LO
@@ -186,21 +205,15 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       const double* u2 = su(2) + A + T::U2::S1 * B + T::U2::S2 * C;
       sy[i] = (u0[1] - u0[0]) + (u1[T::U1::S1] - u1[0]) + (u2[T::U2::S2] - u2[0]);
     }
-    if (a.has_z)
-      lines<NT, P, P, P, 0, P, TB_HI, true, typename T::L2, typename T::L2>(sq, sz1, tab);
   }
   __syncthreads();
   lines<NT, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0>(sA(0), sB(0), tab);
   lines<NT, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1>(sA(1), sB(1), tab);
   lines<NT, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2>(sA(2), sB(2), tab);
-  if constexpr (BLOCK)
-    if (a.has_z) lines<NT, P, P, P, 1, P, TB_HI, true, typename T::L2, typename T::L2>(sz1, sz2, tab);
   __syncthreads();
   lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V>(sB(0), sV(0), tab);
   lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V>(sB(1), sV(1), tab);
   lines<NT, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V>(sB(2), sV(2), tab);
-  if constexpr (BLOCK)
-    if (a.has_z) lines<NT, P, P, P, 2, P, TB_HI, true, typename T::L2, typename T::L2>(sz2, sz1, tab);
   __syncthreads();
   // ---- pointwise G_q = w_q mw / det J  J^T J ----
   const double mw = scoef[0];
@@ -276,6 +289,109 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     }
   }
   if constexpr (BLOCK) {
+    if (a.has_z) {
+      // ---- Z q~ = s_e W_1^-1 q~ (s_e = 1/alpha | gamma) by a fused
+      //      element-local PCG in the Gauss-Legendre nodal basis with Jacobi preconditioning
+      //      (P:606-609): W_h^-1 = H W_g^-1 H^T, W_g = H^T W_h H, H = HG^{(x)3}.
+      //      W_g v = B_G^T diag(w_q / det J_q) B_G v by sum factorisation (Q = p+2 points).
+      using GA = Lay<Q, P, P>;
+      using GB = Lay<Q, Q, P>;
+      using GV = Lay<Q, Q, Q>;
+      using L2 = typename T::L2;
+      __syncthreads();   // sreg is free: the mass part is done
+      double* ta = sreg;
+      double* tb = ta + GA::SIZE;
+      double* tv = tb + GB::SIZE;
+      double* gq = tv + GV::SIZE;        // w_q / det J_q (GV layout)
+      double* vz = gq + GV::SIZE;        // CG iterate (GL basis)
+      double* vp = vz + L2::SIZE;        // search direction
+      double* vap = vp + L2::SIZE;       // W_g p
+      double* vr = sz2;                  // residual
+      double* vd = sz1;                  // diag(W_g), later the result
+      __shared__ double red[NT / 32];
+      for (int qi = tid; qi < NQ; qi += NT) {
+        const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
+        const double* c0 = sJ[0][qy + Q * qz];
+        const double* c1 = sJ[1][qx + Q * qz];
+        const double* c2 = sJ[2][qx + Q * qy];
+        const double det = c0[0] * (c1[1] * c2[2] - c1[2] * c2[1]) -
+                           c1[0] * (c0[1] * c2[2] - c0[2] * c2[1]) +
+                           c2[0] * (c0[1] * c1[2] - c0[2] * c1[1]);
+        gq[qx + GV::S1 * qy + GV::S2 * qz] = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] / det;
+      }
+      // r = H^T q~ ; d = diag(W_g) = (B_G^2)^T g
+      lines<NT, P, P, P, 0, P, TB_HGT, true, L2, L2>(sq, vz, tab);
+      __syncthreads();
+      lines<NT, P, P, P, 1, P, TB_HGT, true, L2, L2>(vz, vap, tab);
+      lines<NT, Q, Q, Q, 2, P, TB_G2, false, GV, GB>(gq, tb, tab);
+      __syncthreads();
+      lines<NT, P, P, P, 2, P, TB_HGT, true, L2, L2>(vap, vr, tab);
+      lines<NT, Q, Q, P, 1, P, TB_G2, false, GB, GA>(tb, ta, tab);
+      __syncthreads();
+      lines<NT, Q, P, P, 0, P, TB_G2, false, GA, L2>(ta, vd, tab);
+      __syncthreads();
+      // z = 0, p = D^-1 r
+      double rs = 0.0;
+      for (int i = tid; i < P3; i += NT) {
+        const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
+        vz[o] = 0.0;
+        const double s = vr[o] / vd[o];
+        vp[o] = s;
+        rs += vr[o] * s;
+      }
+      rs = cta_sum<NT>(rs, red);
+      const double rs0 = rs;
+      for (int it = 0; it < 40 && rs > 1e-30 * rs0 && rs > 0.0; ++it) {
+        // ap = W_g p
+        lines<NT, P, P, P, 0, Q, TB_G, true, L2, GA>(vp, ta, tab);
+        __syncthreads();
+        lines<NT, Q, P, P, 1, Q, TB_G, true, GA, GB>(ta, tb, tab);
+        __syncthreads();
+        lines<NT, Q, Q, P, 2, Q, TB_G, true, GB, GV>(tb, tv, tab);
+        __syncthreads();
+        for (int qi = tid; qi < NQ; qi += NT) {
+          const int o = qi % Q + GV::S1 * ((qi / Q) % Q) + GV::S2 * (qi / (Q * Q));
+          tv[o] *= gq[o];
+        }
+        __syncthreads();
+        lines<NT, Q, Q, Q, 2, P, TB_G, false, GV, GB>(tv, tb, tab);
+        __syncthreads();
+        lines<NT, Q, Q, P, 1, P, TB_G, false, GB, GA>(tb, ta, tab);
+        __syncthreads();
+        lines<NT, Q, P, P, 0, P, TB_G, false, GA, L2>(ta, vap, tab);
+        __syncthreads();
+        double pap = 0.0;
+        for (int i = tid; i < P3; i += NT) {
+          const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
+          pap += vp[o] * vap[o];
+        }
+        pap = cta_sum<NT>(pap, red);
+        const double al = rs / pap;
+        double rsn = 0.0;
+        for (int i = tid; i < P3; i += NT) {
+          const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
+          vz[o] += al * vp[o];
+          const double r = vr[o] - al * vap[o];
+          vr[o] = r;
+          rsn += r * (r / vd[o]);
+        }
+        rsn = cta_sum<NT>(rsn, red);
+        const double be = rsn / rs;
+        for (int i = tid; i < P3; i += NT) {
+          const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
+          vp[o] = vr[o] / vd[o] + be * vp[o];
+        }
+        rs = rsn;
+        __syncthreads();
+      }
+      // y = H z (histopolation basis) -> sz1
+      lines<NT, P, P, P, 0, P, TB_HG, true, L2, L2>(vz, vap, tab);
+      __syncthreads();
+      lines<NT, P, P, P, 1, P, TB_HG, true, L2, L2>(vap, vp, tab);
+      __syncthreads();
+      lines<NT, P, P, P, 2, P, TB_HG, true, L2, L2>(vp, sz1, tab);
+      __syncthreads();
+    }
     double* yq = a.y + a.nrt;
     const double z = scoef[1];
     for (int i = tid; i < P3; i += NT) {

@@ -149,6 +149,28 @@ bool build_tables(int p, int Q, Tab1D* t, std::string* err) {
       t->Mh[i][j] = s;
     }
   if (!invert_spd(p, &t->Mh[0][0], &t->Mhinv[0][0])) { *err = "M_h singular"; return false; }
+  // GL-nodal basis on the p-point Gauss rule
+  double g[MAXP + 2], gw[MAXP + 2];
+  gauss(p, g, gw);
+  for (int q = 0; q < Q; ++q) {
+    double L[MAXP + 1], dL[MAXP + 1];
+    lagrange(p, g, t->xq[q], L, dL);
+    for (int b = 0; b < p; ++b) t->BG[q][b] = L[b];
+  }
+  // HG[a][b] = integral_{xi_a}^{xi_{a+1}} L_b, by a (p+1)-point Gauss rule per subinterval
+  double sx[MAXP + 2], sw[MAXP + 2];
+  gauss(p + 1, sx, sw);
+  for (int a = 0; a < p; ++a)
+    for (int b = 0; b < p; ++b) {
+      double s = 0.0;
+      for (int k = 0; k <= p; ++k) {
+        const double x = xi[a] + (xi[a + 1] - xi[a]) * sx[k];
+        double L[MAXP + 1], dL[MAXP + 1];
+        lagrange(p, g, x, L, dL);
+        s += (xi[a + 1] - xi[a]) * sw[k] * L[b];
+      }
+      t->HG[a][b] = s;
+    }
   return true;
 }
 

@@ -48,10 +48,24 @@ CASES = [
     ("c3", (3, 2, 3), 2, 0),               # trilinear Darcy gamma = 0, general kernel
     ("c3", (2, 3, 2), 4, 0),
     ("c5", (5, 4, 3), 3, 0),               # graded two-material, box kernel
+    ("c3gd", (3, 2, 2), 2, 0),             # trilinear grad-div: W_alpha^-1 by the local CG
+    ("c3gd", (2, 2, 3), 4, 0),
+    ("c3gd", (2, 2, 2), 6, 0),
+    ("c3g", (3, 2, 2), 3, 0),              # trilinear Darcy gamma > 0 (config 3b)
+    ("c3g", (2, 2, 2), 5, 0),
 ]
 
 
 def _problem(name, N, p):
+    if name in ("c3gd", "c3g"):   # config-3 meshes with a nonzero (2,2) block (NEXT-2)
+        pr = make_config("c3", N=N, p=p)
+        if name == "c3gd":
+            pr.kind = "grad_div"
+            pr.alpha = 10.0 ** random_vector(pr.E, 33)
+            pr.beta = 10.0 ** random_vector(pr.E, 34)
+        else:
+            pr.gamma = 10.0 ** random_vector(pr.E, 35)
+        return pr
     pr = make_config(name, N=N, p=p)
     if name == "c2":   # heterogeneous coefficients so per-element weights matter
         pr.alpha = 10.0 ** random_vector(pr.E, 31)
@@ -139,7 +153,8 @@ def test_setup_objects_parity(name, N, p, kernel):
 
 
 @pytest.mark.parametrize("name,N,p", [("c1", None, None), ("c2", (2, 2, 2), 2),
-                                      ("c3", (2, 2, 2), 2), ("c2", (3, 2, 2), 3)])
+                                      ("c3", (2, 2, 2), 2), ("c2", (3, 2, 2), 3),
+                                      ("c3gd", (2, 2, 2), 3), ("c3g", (2, 2, 2), 2)])
 def test_preconditioner_and_minres_parity(name, N, p):
     from oracle import operators, solvers
     pr = _problem(name, N, p)
