@@ -155,6 +155,11 @@ hdiv_status hdiv_nccl_unique_id(void* out, int64_t len);
 hdiv_status hdiv_debug_tables(int p, int Q, double* xq, double* wq, double* Bl, double* Bh,
                               double* Ml, double* Mh, double* Mhinv);
 
+/* Diagnostic, host only: the Gauss-Legendre nodal tables of the W^-1 local CG.
+ * BG[Q][p] = L_b(x_q) (L_b the Lagrange basis on the p-point Gauss rule, x_q the Q-point rule);
+ * HG[p][p] with HG[a][b] = integral of L_b over GLL subinterval a.  Caller-owned host arrays. */
+hdiv_status hdiv_debug_gl_tables(int p, int Q, double* BG, double* HG);
+
 #ifdef __cplusplus
 }
 #endif

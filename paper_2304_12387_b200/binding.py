@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
         "hdiv_apply_precond": (C.c_int, [vp, dp, dp, vp]),
         "hdiv_minres_solve": (C.c_int, [vp, dp, dp, C.c_double, C.c_int, C.POINTER(Report), vp]),
         "hdiv_debug_tables": (C.c_int, [C.c_int, C.c_int] + [dp] * 7),
+        "hdiv_debug_gl_tables": (C.c_int, [C.c_int, C.c_int, dp, dp]),
         "hdiv_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
     }
     for name, (res, args) in sig.items():
@@ -116,6 +117,16 @@ def debug_tables(p: int, Q: int = 0) -> dict:
            "Mhinv": np.zeros((p, p))}
     _check(lib.hdiv_debug_tables(p, Q, *[C.c_void_p(out[k].ctypes.data) for k in
                                          ("xq", "wq", "Bl", "Bh", "Ml", "Mh", "Mhinv")]))
+    return out
+
+
+def debug_gl_tables(p: int, Q: int = 0) -> dict:
+    """Host-only: the Gauss-Legendre nodal tables of the W^-1 local CG (no GPU needed)."""
+    lib = load_library()
+    Q = Q or p + 2
+    out = {"BG": np.zeros((Q, p)), "HG": np.zeros((p, p))}
+    _check(lib.hdiv_debug_gl_tables(p, Q, C.c_void_p(out["BG"].ctypes.data),
+                                    C.c_void_p(out["HG"].ctypes.data)))
     return out
 
 

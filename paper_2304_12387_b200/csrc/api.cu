@@ -467,6 +467,17 @@ hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double 
   return minres(h, b, x, rtol, maxit, rep, (cudaStream_t)stream);
 }
 
+hdiv_status hdiv_debug_gl_tables(int p, int Q, double* BG, double* HG) {
+  Tab1D t;
+  std::string err;
+  if (!build_tables(p, Q, &t, &err)) return fail(HDIV_ERR_INVALID_ORDER, err);
+  for (int q = 0; q < Q; ++q)
+    for (int b = 0; b < p; ++b) if (BG) BG[q * p + b] = t.BG[q][b];
+  for (int a = 0; a < p; ++a)
+    for (int b = 0; b < p; ++b) if (HG) HG[a * p + b] = t.HG[a][b];
+  return HDIV_OK;
+}
+
 hdiv_status hdiv_debug_tables(int p, int Q, double* xq, double* wq, double* Bl, double* Bh,
                               double* Ml, double* Mh, double* Mhinv) {
   Tab1D t;

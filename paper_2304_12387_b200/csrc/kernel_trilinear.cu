@@ -107,7 +107,8 @@ struct TG {   // per-component layouts at every stage
   using B0 = Lay<Q, Q, P>;      using B1 = Lay<Q, Q, P>;      using B2 = Lay<Q, Q, P + 1>;
   using V = Lay<Q, Q, Q>;
   using L2 = Lay<P, P, P>;
-  static constexpr int SU = U2::SIZE;     // largest of U0..U2 (padded)
+  static constexpr int SU = (U0::SIZE > U1::SIZE ? (U0::SIZE > U2::SIZE ? U0::SIZE : U2::SIZE)
+                                                  : (U1::SIZE > U2::SIZE ? U1::SIZE : U2::SIZE));
   static constexpr int SA = A2::SIZE > A1::SIZE ? A2::SIZE : A1::SIZE;
   static constexpr int SB = B2::SIZE;
   static constexpr int SV = V::SIZE;

@@ -101,3 +101,20 @@ def test_library_tables_match_oracle(lib, p):
     assert np.abs(t["Ml"] - Ml).max() < 1e-14
     assert np.abs(t["Mh"] - Mh).max() < 1e-12 * np.abs(Mh).max()
     assert np.abs(t["Mhinv"] @ Mh - np.eye(p)).max() < 1e-12
+
+
+@pytest.mark.parametrize("p", range(1, 7))
+def test_library_gl_tables(lib, p):
+    """Tables of the W^-1 local CG (NEXT-2): the GL-nodal basis spans the same Q_{p-1} as the
+    histopolation basis, so B_G = B_h HG; and with the exact Q-point rule the GL-nodal mass is
+    diagonal (the GL weights), so HG W_g^-1 HG^T equals the oracle's M_h^-1."""
+    from paper_2304_12387_b200.binding import debug_gl_tables
+    from oracle import basis1d
+    g = debug_gl_tables(p)
+    xq, wq = basis1d.gl_rule(p + 2)
+    Bh = basis1d.histopolation(p, xq)
+    assert np.abs(g["BG"] - Bh @ g["HG"]).max() < 1e-12
+    Wg = g["BG"].T @ np.diag(wq) @ g["BG"]
+    assert np.abs(Wg - np.diag(np.diag(Wg))).max() < 1e-13
+    Mh = Bh.T @ np.diag(wq) @ Bh
+    assert np.abs(g["HG"] @ np.linalg.inv(Wg) @ g["HG"].T - np.linalg.inv(Mh)).max() < 1e-9

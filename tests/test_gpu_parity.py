@@ -47,10 +47,15 @@ CASES = [
     ("c2", (5, 3, 3), 4, 1),               # same, forced general kernel
     ("c3", (3, 2, 3), 2, 0),               # trilinear Darcy gamma = 0, general kernel
     ("c3", (2, 3, 2), 4, 0),
+    ("c3", (3, 2, 2), 3, 0),               # odd orders: padded layouts differ (U0 largest)
+    ("c3", (3, 3, 2), 1, 0),
+    ("c3", (2, 2, 2), 5, 0),
     ("c5", (5, 4, 3), 3, 0),               # graded two-material, box kernel
     ("c3gd", (3, 2, 2), 2, 0),             # trilinear grad-div: W_alpha^-1 by the local CG
     ("c3gd", (2, 2, 3), 4, 0),
     ("c3gd", (2, 2, 2), 6, 0),
+    ("c3gd", (2, 3, 2), 1, 0),
+    ("c3gd", (2, 2, 2), 5, 0),
     ("c3g", (3, 2, 2), 3, 0),              # trilinear Darcy gamma > 0 (config 3b)
     ("c3g", (2, 2, 2), 5, 0),
 ]
