@@ -27,6 +27,7 @@
 
 #include <cstdlib>
 
+#include "affine_layouts.h"
 #include "internal.h"
 
 namespace hdiv {
@@ -57,14 +58,20 @@ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr bool kXDirect = HDIV_X_DIRECT;
 
 // smem box of component AX: extent (T_AX+1)P+1 along AX (position 0 <-> global plane
-// (e0_AX - 1) P), T P along the others; extents 0 and 1 padded odd.
+// (e0_AX - 1) P), T P along the others.  Strides: the generated per-tile layout
+// (affine_layouts.h, fewest modelled bank-conflict wavefronts), else extents 0 and 1 padded odd.
 template <int P, int TX, int TY, int TZ, int AX>
 struct CG {
+  static constexpr int LI = find_tile_layout(P, TX, TY, TZ);
   static constexpr int E0 = (AX == 0) ? (TX + 1) * P + 1 : TX * P;
   static constexpr int E1 = (AX == 1) ? (TY + 1) * P + 1 : TY * P;
   static constexpr int E2 = (AX == 2) ? (TZ + 1) * P + 1 : TZ * P;
-  static constexpr int S1 = odd_up(E0);
-  static constexpr int S2 = S1 * odd_up(E1);
+  static constexpr int S1 = LI >= 0 ? kTileLayouts[LI].S[AX][0] : odd_up(E0);
+  static constexpr int S2 = LI >= 0 ? kTileLayouts[LI].S[AX][1] : S1 * odd_up(E1);
+  static_assert(S1 >= E0 && S2 >= S1 * E1, "component layout overlaps");
+  // lane maps: M_l / halo lines and M_h (x) M_h positions padded to half-warps or packed
+  static constexpr bool PADL = LI >= 0 ? kTileLayouts[LI].padL[AX] != 0 : true;
+  static constexpr bool PADA = LI >= 0 ? kTileLayouts[LI].padA[AX] != 0 : true;
   static constexpr int SIZE = S2 * E2;
   static constexpr int EA = (AX == 0) ? E0 : (AX == 1) ? E1 : E2;   // extent along AX
   static constexpr int SA = (AX == 0) ? 1 : (AX == 1) ? S1 : S2;    // stride along AX
@@ -85,7 +92,10 @@ struct Geo {
   static constexpr int NCELL = NE * P3;
   // cell tile (subcell-major, odd-padded): cell (X,Y,Z) at X + Q1 Y + Q2 Z
   static constexpr int CX = TX * P, CY = TY * P, CZ = TZ * P;
-  static constexpr int Q1 = odd_up(CX), Q2 = Q1 * odd_up(CY);
+  static constexpr int LI = find_tile_layout(P, TX, TY, TZ);
+  static constexpr int Q1 = LI >= 0 ? kTileLayouts[LI].Q[0] : odd_up(CX);
+  static constexpr int Q2 = LI >= 0 ? kTileLayouts[LI].Q[1] : Q1 * odd_up(CY);
+  static_assert(Q1 >= CX && Q2 >= Q1 * CY, "q tile layout overlaps");
   static constexpr int SQSIZE = Q2 * CZ;
   static constexpr int SU = cmax(cmax(CG<P, TX, TY, TZ, 0>::SIZE, CG<P, TX, TY, TZ, 1>::SIZE),
                                  cmax(CG<P, TX, TY, TZ, 2>::SIZE, SQSIZE));
@@ -217,7 +227,7 @@ __device__ __forceinline__ void load_component(const AffArgs& a, const TileInfo&
 }
 
 // -------- one component phase (AX), data already in `su` ------------------------------------
-template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK>
+template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK, bool XD = kXDirect>
 __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
                                           const TabAffine& tab, double* su, const double* sq,
                                           const double* hq, const double* sco, double* acc) {
@@ -260,7 +270,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   //      linearity c_h sum_j M_l[P][j] (M_h (x) M_h) u_j = c_h (M_h (x) M_h) sum_j M_l[P][j] u_j,
   //      so the raw halo planes are combined first into position P-1 (one plane to transform)
   constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
-  constexpr int EL1P = (EL1 + 15) / 16 * 16;   // half-warp aligned lane rows
+  constexpr int EL1P = C::PADL ? (EL1 + 15) / 16 * 16 : EL1;   // half-warp aligned lane rows
   const int m_a = ti.m[AX], h_a = ti.h[AX];
   if (h_a) {
 #pragma unroll 1
@@ -280,28 +290,28 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   //      P-1 (combined halo) .. (T+1)P; lanes run along AX (odd stride), the position range
   //      padded to a multiple of 16 so a half-warp never straddles two blocks ----
   constexpr int EAH = C::EA - (P - 1);
-  constexpr int EAP = (EAH + 15) / 16 * 16;
+  constexpr int EAP = C::PADA ? (EAH + 15) / 16 * 16 : EAH;
   constexpr int NH = EAP * C::TA1 * C::TA2;
 #pragma unroll 2
   for (int it = tid; it < NH; it += NT) {
     const int pa = it % EAP + (P - 1), b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
     if (pa >= C::EA) continue;
     double* base = su + pa * C::SA + b1 * P * C::SA1 + b2 * P * C::SA2;
-    double v[P][P];
-#pragma unroll
-    for (int k2 = 0; k2 < P; ++k2)
-#pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) v[k2][k1] = base[k1 * C::SA1 + k2 * C::SA2];
+    // row by row: only one input row and the P x P intermediate are live (register pressure)
     double w[P][P];
 #pragma unroll
-    for (int k2 = 0; k2 < P; ++k2)
+    for (int k2 = 0; k2 < P; ++k2) {
+      double v[P];
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) v[k1] = base[k1 * C::SA1 + k2 * C::SA2];
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) {
         double s = 0.0;
 #pragma unroll
-        for (int j = 0; j < P; ++j) s = fma(tab.Mh[k1][j], v[k2][j], s);
+        for (int j = 0; j < P; ++j) s = fma(tab.Mh[k1][j], v[j], s);
         w[k2][k1] = s;
       }
+    }
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1)
 #pragma unroll
@@ -331,7 +341,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     const int l1 = it % EL1P, l2 = it / EL1P;
     if (l1 >= EL1) continue;
     const bool line_ok = l1 < hiA1 && l2 < hiA2;
-    if ((AX != 0 || kXDirect) && !line_ok) continue;
+    if ((AX != 0 || XD) && !line_ok) continue;
     double* line = su + l1 * C::SA1 + l2 * C::SA2;
     double* gl = yt + (l1 * gs1 + l2 * gs2);
     int ec[3];
@@ -366,7 +376,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
             o += qprev - qc;
             qprev = qc;
           }
-          if (AX == 0 && !kXDirect) eb[i * C::SA] = o;
+          if (AX == 0 && !XD) eb[i * C::SA] = o;
           else __stcs(gl + ((et + 1) * P + i) * gsa, o);
         }
         double s = 0.0;
@@ -377,13 +387,13 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     }
     if (ti.last[AX]) {
       const double o = carry + (BLOCK ? qprev : 0.0);
-      if (AX == 0 && !kXDirect) line[(m_a + 1) * P * C::SA] = o;
+      if (AX == 0 && !XD) line[(m_a + 1) * P * C::SA] = o;
       else __stcs(gl + (m_a + 1) * P * gsa, o);
     }
   }
   __syncthreads();
 
-  if constexpr (AX == 0 && !kXDirect) {
+  if constexpr (AX == 0 && !XD) {
     // ---- copy-out of the owned x planes (coalesced, streaming) ----
     constexpr int NO0 = TX * P + 1;
     const int own_hi = m_a * P + (ti.last[0] ? 1 : 0);   // exclusive, relative to position P
@@ -395,8 +405,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
 }
 
-template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB>
-__global__ void __launch_bounds__(NT)
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB, int MINB, bool XD>
+__global__ void __launch_bounds__(NT, MINB)
 affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
   using O = Own<P, TX, TY, TZ, NT>;
@@ -439,14 +449,12 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   };
 
   // ---- group 0: coefficients of the tile and its - halo, q~ tile, halo q~ ----
-  for (int i = tid; i < G::NCO; i += NT) {
+  for (int l = tid; l < 4 * G::NCO; l += NT) {   // lanes over (slot, k): contiguous runs
+    const int i = l >> 2, k = l & 3;
     const int ix = i % (TX + 1), iy = (i / (TX + 1)) % (TY + 1), iz = i / ((TX + 1) * (TY + 1));
     const int ex = ti.e0[0] - 1 + ix, ey = ti.e0[1] - 1 + iy, ez = ti.e0[2] - 1 + iz;
-    if (ex >= 0 && ey >= 0 && ez >= 0 && ix <= ti.m[0] && iy <= ti.m[1] && iz <= ti.m[2]) {
-      const double* c = a.coef + 4 * (((long long)ez * NLy + ey) * NLx + ex);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) cp_async8(sco + 4 * i + k, c + k);
-    }
+    if (ex >= 0 && ey >= 0 && ez >= 0 && ix <= ti.m[0] && iy <= ti.m[1] && iz <= ti.m[2])
+      cp_async8(sco + l, a.coef + 4 * (((long long)ez * NLy + ey) * NLx + ex) + k);
   }
   if constexpr (BLOCK) {
     // q~ tile, subcell-major, loaded per owned column (X, Y): lanes run along X (conflict-free
@@ -546,28 +554,28 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD>(a, ti, tab, bufA, sq, hq0, sco, acc);
     // ---- group 3: z component -> A ; compute y from B ----
     load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, bufB, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD>(a, ti, tab, bufB, sq, hq1, sco, acc);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD>(a, ti, tab, bufA, sq, hq2, sco, acc);
   } else {
     load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD>(a, ti, tab, bufA, sq, hq0, sco, acc);
     load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK>(a, ti, tab, bufA, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD>(a, ti, tab, bufA, sq, hq1, sco, acc);
     load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD>(a, ti, tab, bufA, sq, hq2, sco, acc);
   }
 
   if constexpr (BLOCK) {
@@ -590,7 +598,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   }
 }
 
-template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true>
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true, int MINB = 0, bool XD = kXDirect>
 cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
   using G = Geo<P, TX, TY, TZ>;
@@ -604,7 +612,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.has_z = h->has_z ? 1 : 0;
   a.skip = skip;
   const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
-  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB>;
+  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD>;
   static bool attr_done = false;   // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -998,15 +1006,20 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
 static int tile_variant(int p) {
   const char* e = getenv("HDIV_AFFINE_TILE");
   if (e) return atoi(e);
-  return (p == 3) ? 4 : (p == 6) ? 5 : 0;
+  // r01 sweeps with the generated layouts (profiles/r01_variant_sweep_v*.txt): single-buffered
+  // tiles (more CTAs per SM) win at p = 3..6, double-buffered at p = 1, 2; at p = 5, 6 the x
+  // component is written back through shared memory (coalesced copy-out), at p = 3 a
+  // 160-thread CTA owns one cell column per thread
+  return (p == 3) ? 7 : (p == 4) ? 4 : (p == 5 || p == 6) ? 10 : 0;
 }
 
-// Default per order from the r01 sweeps (profiles/): z-marching wins at p = 3, 5; the halo-tile
-// kernel at p = 1, 2, 4, 6.  HDIV_MARCH_TILE=-1 forces halo tiles, >= 0 a marching variant.
+// The z-marching kernel is correct at every order but no longer the fastest anywhere (same
+// sweep); HDIV_MARCH_TILE >= 0 selects a marching variant, -1 (default) the halo tiles.
 static int march_variant(int p) {
   const char* e = getenv("HDIV_MARCH_TILE");
   if (e) return atoi(e);
-  return (p == 5) ? 1 : -1;
+  (void)p;
+  return -1;
 }
 
 template <bool BLOCK>
@@ -1034,7 +1047,8 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
     }
     return cudaErrorInvalidValue;
   }
-  // halo-tile variants: 0..3 double-buffered shapes, 4/5 single-buffered (more CTAs per SM)
+  // halo-tile variants: 0..3 double-buffered shapes, 4/5 single-buffered (more CTAs per SM),
+  // 6/7 other CTA sizes, 8/9 register caps (__launch_bounds__ min blocks), 10 x copy-out
   const int v = tile_variant(h->p);
   switch (h->p) {
     case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
@@ -1042,11 +1056,16 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
       if (v == 1) return launch_t<2, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<2, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
       if (v == 4) return launch_t<2, 8, 4, 4, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 6) return launch_t<2, 8, 8, 4, 256, BLOCK>(h, x, y, k, s);
       return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
     case 3:
       if (v == 1) return launch_t<3, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 4) return launch_t<3, 8, 4, 2, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 6) return launch_t<3, 8, 4, 2, 288, BLOCK, false>(h, x, y, k, s);
+      if (v == 7) return launch_t<3, 4, 4, 2, 160, BLOCK, false>(h, x, y, k, s);
+      if (v == 8) return launch_t<3, 8, 4, 2, 128, BLOCK, false, 6>(h, x, y, k, s);
+      if (v == 10) return launch_t<3, 4, 4, 2, 160, BLOCK, false, 0, false>(h, x, y, k, s);
       return launch_t<3, 8, 4, 2, 128, BLOCK>(h, x, y, k, s);
     case 4:
       if (v == 1) return launch_t<4, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
@@ -1054,18 +1073,33 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
       if (v == 3) return launch_t<4, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 4) return launch_t<4, 4, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
       if (v == 5) return launch_t<4, 4, 4, 2, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 6) return launch_t<4, 4, 4, 2, 256, BLOCK, false>(h, x, y, k, s);
+      if (v == 7) return launch_t<4, 2, 2, 2, 64, BLOCK, false>(h, x, y, k, s);
+      if (v == 8) return launch_t<4, 4, 2, 2, 128, BLOCK, false, 8>(h, x, y, k, s);
+      if (v == 9) return launch_t<4, 4, 2, 2, 128, BLOCK, false, 7>(h, x, y, k, s);
+      if (v == 10) return launch_t<4, 4, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
       return launch_t<4, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 5:
       if (v == 1) return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<5, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 4) return launch_t<5, 2, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
       if (v == 5) return launch_t<5, 4, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 6) return launch_t<5, 4, 2, 2, 224, BLOCK, false>(h, x, y, k, s);
+      if (v == 7) return launch_t<5, 2, 2, 1, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 8) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 6>(h, x, y, k, s);
+      if (v == 9) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 5>(h, x, y, k, s);
+      if (v == 10) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
       return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 6:
       if (v == 1) return launch_t<6, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 2) return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
       if (v == 4) return launch_t<6, 2, 2, 1, 128, BLOCK, false>(h, x, y, k, s);
       if (v == 5) return launch_t<6, 2, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
+      if (v == 6) return launch_t<6, 2, 2, 2, 160, BLOCK, false>(h, x, y, k, s);
+      if (v == 7) return launch_t<6, 4, 2, 2, 288, BLOCK, false>(h, x, y, k, s);
+      if (v == 8) return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3>(h, x, y, k, s);
+      if (v == 10) return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3, false>(h, x, y, k, s);
+      if (v == 9) return launch_t<6, 2, 2, 2, 128, BLOCK, false, 4>(h, x, y, k, s);
       return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;

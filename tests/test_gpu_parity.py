@@ -84,7 +84,13 @@ VARIANTS = [("c2", (5, 3, 7), 4, {"HDIV_ZCHUNK": "2"}), ("c2", (3, 5, 5), 3, {"H
             ("c2", (3, 3, 4), 6, {"HDIV_ZCHUNK": "3"}), ("c2", (9, 5, 5), 1, {"HDIV_ZCHUNK": "2"}),
             ("c5", (5, 4, 6), 3, {"HDIV_ZCHUNK": "2"}),
             ("c2", (5, 3, 3), 4, {"HDIV_MARCH_TILE": "-1"}), ("c2", (5, 3, 3), 4, {"HDIV_MARCH_TILE": "1"}),
-            ("c2", (3, 5, 3), 6, {"HDIV_MARCH_TILE": "1", "HDIV_ZCHUNK": "2"})]
+            ("c2", (3, 5, 3), 6, {"HDIV_MARCH_TILE": "1", "HDIV_ZCHUNK": "2"}),
+            # generated layouts with packed lane maps, other CTA sizes, register caps, x copy-out
+            ("c2", (9, 5, 3), 3, {"HDIV_AFFINE_TILE": "7"}), ("c2", (9, 5, 3), 3, {"HDIV_AFFINE_TILE": "6"}),
+            ("c2", (5, 3, 3), 4, {"HDIV_AFFINE_TILE": "9"}), ("c2", (5, 5, 3), 4, {"HDIV_AFFINE_TILE": "10"}),
+            ("c2", (5, 3, 3), 5, {"HDIV_AFFINE_TILE": "10"}), ("c5", (5, 3, 3), 5, {"HDIV_AFFINE_TILE": "6"}),
+            ("c2", (3, 3, 3), 6, {"HDIV_AFFINE_TILE": "10"}), ("c2", (3, 3, 5), 6, {"HDIV_AFFINE_TILE": "8"}),
+            ("c2", (5, 3, 3), 6, {"HDIV_AFFINE_TILE": "7"}), ("c2", (9, 9, 5), 2, {"HDIV_AFFINE_TILE": "6"})]
 
 
 @pytest.mark.parametrize("name,N,p,env", VARIANTS)
