@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,6 +88,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
   cudaFree(h->d_ecol);
+  cudaFree(h->d_minv);
   cudaFree(h->d_eval);
   cudaFree(h->d_scratch);
   cudaFree(h->d_xbuf);
@@ -342,6 +344,10 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     if (cs != HDIV_OK) { hdiv_destroy(h); return cs; }
   }
   {
+    // SpMV inside S^-1: the SELL-32 copy of S~ (default, fastest measured: profiles/) or the
+    // matrix-free face stencil (HDIV_CHEB_STENCIL=1)
+    const char* ev = getenv("HDIV_CHEB_STENCIL");
+    h->cheb_sell = !(ev && atoi(ev) != 0);
     hdiv_status ss = build_schur(h, s);
     if (ss != HDIV_OK) { hdiv_destroy(h); return ss; }
     if (nranks > 1) {

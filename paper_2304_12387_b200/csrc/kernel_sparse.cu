@@ -189,6 +189,11 @@ __global__ void sell_kernel(const int64_t* __restrict__ rp, const int32_t* __res
   }
 }
 
+__global__ void recip_kernel(const double* __restrict__ a, double* __restrict__ r, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) r[i] = 1.0 / a[i];
+}
+
 __global__ void schur_export_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ c,
                                     const double* __restrict__ v, int64_t* rp_o, int64_t* c_o,
                                     double* v_o, long long nl2) {
@@ -322,6 +327,12 @@ hdiv_status build_schur(hdiv_ctx* h, cudaStream_t s) {
   schur_fill_kernel<<<nblocks(n, 256), 256, 0, s>>>(g, h->d_mdiag, h->d_ctil, h->d_srow,
                                                     h->d_scol, h->d_sval, h->d_sdinv, n);
   HDIV_CUDA_TRY(cudaGetLastError());
+  if (!h->cheb_sell) {   // face weights 1/M~ of the matrix-free S~ stencil used inside S^-1
+    HDIV_CUDA_TRY(cudaMalloc(&h->d_minv, sizeof(double) * (h->nrt > 0 ? h->nrt : 1)));
+    recip_kernel<<<nblocks(h->nrt, 256), 256, 0, s>>>(h->d_mdiag, h->d_minv, h->nrt);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    return HDIV_OK;
+  }
   // sliced-ELL copy used by the SpMV inside S^-1 (coalesced slot loads)
   const int W = 2 * h->dim + 1;
   const long long ns = (n + 31) / 32;

@@ -31,7 +31,7 @@ hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, 
 
 namespace {
 
-constexpr int RED_BLOCKS = 148 * 4;
+constexpr int RED_BLOCKS = 148 * 8;   // 8 x 256 threads per SM: bytes in flight
 constexpr int RED_NT = 256;
 
 struct MState {
@@ -164,6 +164,104 @@ cheb_step_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ ev
     double dd = c1 * d[i] + c2 * dinv[i] * r;
     dn[i] = dd;
     double yy = y[i] + dd;
+    y[i] = yy;
+    if (last) s = fma(yy, vin[i], s);
+  }
+  if (last && part) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+// The same Chebyshev step with S~ applied matrix-free from its definition (P:463-473 entry
+// formula): S~_ii = C~_ii + sum_{k in F(i)} w_k, S~_ij = -w_k across interior face k, with the
+// face weights w_k = 1/M~_kk.  Reads per row: C~_i, the 2d face weights (each shared by two
+// rows), the neighbours' d (cache hits) instead of 2d+1 (col, val) pairs.  The diagonal is summed
+// in the same face order as the CSR rows (-x,+x,-y,+y,-z,+z), so diag and 1/diag match it.
+// One thread per element row of P cells along x: the index arithmetic is amortised over the
+// row, the row's x faces are P+1 contiguous weights and its y/z faces P contiguous ones.
+struct StencilGeo {
+  long long n[3], off[3], nl2, ghost_lo, ghost_hi;   // ghost_*: first ghost row or -1
+  int NL[3];
+  unsigned long long mx, my;                         // ceil(2^64 / NL0), ceil(2^64 / NL1)
+};
+
+__device__ __forceinline__ unsigned fdiv(unsigned v, unsigned long long m) {
+  return m ? (unsigned)__umul64hi((unsigned long long)v, m) : v;   // m = 0 <-> divisor 1
+}
+
+template <int DIM, int P>
+__global__ void __launch_bounds__(RED_NT, 6)
+cheb_stencil_kernel(StencilGeo g, const double* __restrict__ minv, const double* __restrict__ ctil,
+                    const double* rin, double* rout, const double* __restrict__ d,
+                    double* __restrict__ dn, double* __restrict__ y, double c1, double c2,
+                    int last, const double* __restrict__ vin, double* part,
+                    const int* __restrict__ done) {
+  if (done && *done) return;
+  constexpr int PD = (DIM == 3) ? P * P * P : P * P;
+  const long long n0 = g.n[0], n1 = g.n[1];
+  const long long rowx = (long long)g.NL[0] * PD;      // one element row along y
+  const long long lay = rowx * g.NL[1];                // one element layer along z
+  double s = 0.0;
+  // one thread per cell, lanes over consecutive cells (coalesced vectors); all divisions are
+  // by compile-time constants or by multiply-high
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < g.nl2;
+       i += (long long)gridDim.x * RED_NT) {
+    const unsigned e = (unsigned)(i / PD);
+    const int il = (int)(i - (long long)e * PD);
+    const int a = il % P, b = (il / P) % P, c = (DIM == 3) ? il / (P * P) : 0;
+    const unsigned t = fdiv(e, g.mx);
+    const int ex = (int)(e - t * (unsigned)g.NL[0]);
+    int ey, ez;
+    if constexpr (DIM == 3) {
+      const unsigned u = fdiv(t, g.my);
+      ey = (int)(t - u * (unsigned)g.NL[1]);
+      ez = (int)u;
+    } else {
+      ey = (int)t;
+      ez = 0;
+    }
+    const long long X = (long long)ex * P + a, Y = (long long)ey * P + b, Z = (long long)ez * P + c;
+    const long long fx = g.off[0] + X + (n0 + 1) * (DIM == 3 ? Y + n1 * Z : Y);
+    const long long fy = g.off[1] + X + n0 * (DIM == 3 ? Y + (n1 + 1) * Z : Y);
+    const double w0 = minv[fx], w1 = minv[fx + 1], w2 = minv[fy], w3 = minv[fy + n0];
+    double w4 = 0.0, w5 = 0.0;
+    if constexpr (DIM == 3) {
+      const long long fz = g.off[2] + X + n0 * (Y + n1 * Z);
+      w4 = minv[fz];
+      w5 = minv[fz + n0 * n1];
+    }
+    double diag = ctil[i];
+    diag += w0;
+    diag += w1;
+    diag += w2;
+    diag += w3;
+    if constexpr (DIM == 3) {
+      diag += w4;
+      diag += w5;
+    }
+    const double di = d[i];
+    double sd = diag * di;
+    if (X > 0) sd -= w0 * d[a > 0 ? i - 1 : i - PD + (P - 1)];
+    if (X + 1 < n0) sd -= w1 * d[a < P - 1 ? i + 1 : i + PD - (P - 1)];
+    if constexpr (DIM == 3) {
+      if (Y > 0) sd -= w2 * d[b > 0 ? i - P : i - rowx + P * (P - 1)];
+      if (Y + 1 < n1) sd -= w3 * d[b < P - 1 ? i + P : i + rowx - P * (P - 1)];
+      if (Z > 0) sd -= w4 * d[c > 0 ? i - P * P : i - lay + P * P * (P - 1)];
+      else if (g.ghost_lo >= 0) sd -= w4 * d[g.ghost_lo + X + n0 * Y];
+      if (Z + 1 < g.n[2]) sd -= w5 * d[c < P - 1 ? i + P * P : i + lay - P * P * (P - 1)];
+      else if (g.ghost_hi >= 0) sd -= w5 * d[g.ghost_hi + X + n0 * Y];
+    } else {
+      if (Y > 0) sd -= w2 * d[b > 0 ? i - P : i - rowx + P * (P - 1)];
+      else if (g.ghost_lo >= 0) sd -= w2 * d[g.ghost_lo + X];
+      if (Y + 1 < n1) sd -= w3 * d[b < P - 1 ? i + P : i + rowx - P * (P - 1)];
+      else if (g.ghost_hi >= 0) sd -= w3 * d[g.ghost_hi + X];
+    }
+    const double r = rin[i] - sd;
+    rout[i] = r;
+    const double dd = c1 * di + c2 * (1.0 / diag) * r;
+    dn[i] = dd;
+    const double yy = y[i] + dd;
     y[i] = yy;
     if (last) s = fma(yy, vin[i], s);
   }
@@ -312,6 +410,42 @@ void minres_free(hdiv_ctx* h) {
   h->mw = nullptr;
 }
 
+template <int DIM, int P>
+static cudaError_t stencil_p(const hdiv_ctx* h, const StencilGeo& g, const double* rin,
+                             double* rout, const double* d, double* dn, double* y, double c1,
+                             double c2, int last, const double* vin, double* part, const int* done,
+                             cudaStream_t s) {
+  cheb_stencil_kernel<DIM, P><<<RED_BLOCKS, RED_NT, 0, s>>>(g, h->d_minv, h->d_ctil, rin, rout, d,
+                                                            dn, y, c1, c2, last, vin, part, done);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_cheb_stencil(const hdiv_ctx* h, const double* rin, double* rout,
+                                       const double* d, double* dn, double* y, double c1,
+                                       double c2, int last, const double* vin, double* part,
+                                       const int* done, cudaStream_t s) {
+  StencilGeo g;
+  for (int a = 0; a < 3; ++a) { g.n[a] = h->n[a]; g.off[a] = h->off[a]; g.NL[a] = (int)h->NL[a]; }
+  g.nl2 = h->nl2;
+  const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
+  g.ghost_lo = (h->rank > 0) ? h->nl2 : -1;
+  g.ghost_hi = (h->rank < h->nranks - 1) ? h->nl2 + lplane : -1;
+  // exact 32-bit division by multiply-high: q = umulhi64(v, ceil(2^64 / D)) for v, D < 2^32
+  auto magic = [](unsigned long long D) {
+    return D <= 1 ? 0ull : (~0ull) / D + 1ull;
+  };
+  g.mx = magic((unsigned long long)h->NL[0]);
+  g.my = magic((unsigned long long)h->NL[1]);
+#define HDIV_STENCIL_CASE(DD, PP) \
+  if (h->dim == DD && h->p == PP) return stencil_p<DD, PP>(h, g, rin, rout, d, dn, y, c1, c2, last, vin, part, done, s);
+  HDIV_STENCIL_CASE(3, 1) HDIV_STENCIL_CASE(3, 2) HDIV_STENCIL_CASE(3, 3)
+  HDIV_STENCIL_CASE(3, 4) HDIV_STENCIL_CASE(3, 5) HDIV_STENCIL_CASE(3, 6)
+  HDIV_STENCIL_CASE(2, 1) HDIV_STENCIL_CASE(2, 2) HDIV_STENCIL_CASE(2, 3)
+  HDIV_STENCIL_CASE(2, 4) HDIV_STENCIL_CASE(2, 5) HDIV_STENCIL_CASE(2, 6)
+#undef HDIV_STENCIL_CASE
+  return cudaErrorInvalidValue;
+}
+
 // Chebyshev-Jacobi S^-1 applied to vq -> y (uses mw->r, mw->d); partial <y, vq> if part
 static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
                               const int* done, cudaStream_t s) {
@@ -328,7 +462,11 @@ static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* 
       hdiv_status st = comm_l2_ghosts(h, dprev, s);
       if (st != HDIV_OK) return st;
     }
-    if (h->dim == 3)
+    if (!h->cheb_sell) {
+      cudaError_t e = launch_cheb_stencil(h, rin, mw->r, dprev, mw->d[i & 1], y, mw->c1[i - 1],
+                                          mw->c2[i - 1], i == k - 1, vq, part, done, s);
+      HDIV_CUDA_TRY(e);
+    } else if (h->dim == 3)
       cheb_step_kernel<7><<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
                                                         mw->d[i & 1], h->d_sdinv, y,
                                                         mw->c1[i - 1], mw->c2[i - 1], n,

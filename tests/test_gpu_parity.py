@@ -229,3 +229,22 @@ def test_full_size_sampled_parity(name, p):
     scale_q = np.abs(yq).max()
     assert np.abs(y[rt_rows] - yu).max() < TOL * scale_u * 10
     assert np.abs(y[n_rt + l2_rows] - yq).max() < TOL * scale_q * 10
+
+
+@pytest.mark.parametrize("name,N,p", [("c1", None, None), ("c2", (3, 2, 2), 3), ("c5", (5, 4, 3), 2)])
+def test_preconditioner_sell_path(name, N, p, monkeypatch):
+    """The Chebyshev SpMV through the SELL-32 copy of the assembled S~ (default) and through
+    the matrix-free face stencil (HDIV_CHEB_STENCIL=1) both match the oracle's S^-1."""
+    from oracle import operators, solvers
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    P = solvers.BlockDiagPrecond(A, tau=1.0, degree=4, ratio=30.0)
+    v = random_vector(A.n_rt + A.n_l2, 13)
+    zo = P.apply(v)
+    for stencil in ("0", "1"):
+        monkeypatch.setenv("HDIV_CHEB_STENCIL", stencil)
+        op = _gpu(pr, tau=1.0, cheb_degree=4, cheb_ratio=30.0)
+        z = _host(op.apply_precond(_dev(v)))
+        eu, eq = _rel(z[:A.n_rt], zo[:A.n_rt]), _rel(z[A.n_rt:], zo[A.n_rt:])
+        op.close()
+        assert eu < TOL and eq < 1e-11, (stencil, eu, eq)
