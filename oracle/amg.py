@@ -1,0 +1,127 @@
+"""AMG V-cycle approximation of S~^-1 (oracle; test infrastructure only — the product path never
+imports this module).  NEXT-1 of SURVEY §8.
+
+Paper: the Schur-complement block of the preconditioner is approximated by one AMG V-cycle
+("one V-cycle of AMG"), hypre BoomerAMG on the GPU with l1-Jacobi smoothing
+(P:900-901), Galerkin coarse operators.  The paper does not fix the coarsening,
+interpolation, sweeps or coarse solve (reading A9).  Reading A9b (this build):
+
+  * coarsening: deterministic aggregation of the structured subcell grid of the L2 space into
+    3 x 3 (x 3) blocks (the last block of an axis may be shorter; an axis of extent 1 stays 1);
+  * interpolation: smoothed aggregation, P = (I - omega D^-1 A) P_tent, P_tent the 0/1 aggregate
+    indicator, omega = 4 / (3 lam), lam = max_i sum_j |a_ij| / a_ii (Gershgorin bound of D^-1 A);
+  * coarse operators: Galerkin A_c = P^T A P;
+  * smoother: l1-Jacobi, x <- x + D_l1^-1 (b - A x), D_l1 = diag(sum_j |a_ij|), nu sweeps before
+    and nu after the coarse correction (symmetric, so the V-cycle is SPD);
+  * coarsest level (<= max_coarse unknowns, or no axis left to coarsen): exact solve.
+
+With 3-wide aggregates and a distance-1 smoother the coarse operators of a 7-point (5-point)
+fine operator are 27-point (9-point) on the coarse grid, and stay so on every level.
+
+Everything below is the plain algorithm with scipy sparse products: no fusion, no reordering.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+
+def l2_cell_coords(dim, N, p):
+    """Subcell coordinates (X, Y[, Z]) of every L2 row in the element-contiguous numbering
+    e p^d + a + p b (+ p^2 c), e = ex + N_x (ey + N_y ez)."""
+    nl = p ** dim
+    E = int(np.prod(N[:dim]))
+    i = np.arange(E * nl, dtype=np.int64)
+    e, il = i // nl, i % nl
+    ex = e % N[0]
+    X = ex * p + il % p
+    if dim == 2:
+        ey = e // N[0]
+        Y = ey * p + il // p
+        return np.stack([X, Y], axis=1)
+    ey = (e // N[0]) % N[1]
+    ez = e // (N[0] * N[1])
+    Y = ey * p + (il // p) % p
+    Z = ez * p + il // (p * p)
+    return np.stack([X, Y, Z], axis=1)
+
+
+class Level:
+    def __init__(self, A, dims, coords):
+        self.A = A.tocsr()
+        self.dims = tuple(int(d) for d in dims)
+        self.coords = coords
+        self.D = self.A.diagonal().copy()
+        self.l1 = np.asarray(abs(self.A).sum(axis=1)).ravel()
+        self.P = None
+        self.omega = None
+
+
+def _coarse_grid(dims, agg):
+    return tuple((d + agg - 1) // agg for d in dims)
+
+
+def build_hierarchy(S, coords, dims, agg=3, max_coarse=512, max_levels=25, coarse_solve=True):
+    """Levels l = 0..L with A_0 = S; coords: the grid coordinates of the rows of S.
+    coarse_solve=False skips the coarsest inverse (tests on singular operators)."""
+    levels = [Level(S, dims, coords)]
+    while True:
+        lv = levels[-1]
+        n = lv.A.shape[0]
+        cd = _coarse_grid(lv.dims, agg)
+        if n <= max_coarse or cd == lv.dims or len(levels) >= max_levels:
+            break
+        # aggregate of each row and the lexicographic coarse numbering (x fastest)
+        cc = lv.coords // agg
+        J = cc[:, 0].copy()
+        stride = 1
+        for a in range(1, len(cd)):
+            stride *= cd[a - 1]
+            J += stride * cc[:, a]
+        nc = int(np.prod(cd))
+        Pt = sp.csr_matrix((np.ones(n), (np.arange(n), J)), shape=(n, nc))
+        lam = float(np.max(lv.l1 / lv.D))
+        lv.omega = 4.0 / (3.0 * lam)
+        lv.P = (Pt - lv.omega * (sp.diags(1.0 / lv.D) @ (lv.A @ Pt))).tocsr()
+        Ac = (lv.P.T @ lv.A @ lv.P).tocsr()
+        # coarse coordinates in the coarse numbering
+        ci = np.arange(nc, dtype=np.int64)
+        ccoords = []
+        rem = ci
+        for a in range(len(cd)):
+            ccoords.append(rem % cd[a])
+            rem = rem // cd[a]
+        levels.append(Level(Ac, cd, np.stack(ccoords, axis=1)))
+    if coarse_solve:
+        levels[-1].Ainv = np.linalg.inv(levels[-1].A.toarray())
+    return levels
+
+
+def vcycle(levels, b, nu=1, l=0):
+    """One V-cycle x ~ A_l^-1 b from x = 0 (the approximation of S~^-1 when l = 0)."""
+    lv = levels[l]
+    if l == len(levels) - 1:
+        return lv.Ainv @ b
+    dl1inv = 1.0 / lv.l1
+    x = np.zeros_like(b)
+    for _ in range(nu):                       # pre-smoothing, l1-Jacobi
+        x = x + dl1inv * (b - lv.A @ x)
+    r = b - lv.A @ x                          # residual
+    ec = vcycle(levels, lv.P.T @ r, nu, l + 1)   # restrict, coarse correction
+    x = x + lv.P @ ec                         # prolongate
+    for _ in range(nu):                       # post-smoothing
+        x = x + dl1inv * (b - lv.A @ x)
+    return x
+
+
+class AMGSchur:
+    """S^-1 = one V-cycle on S~ (drop-in for the Chebyshev polynomial in BlockDiagPrecond)."""
+
+    def __init__(self, asm, nu=2, max_coarse=512):
+        coords = l2_cell_coords(asm.dim, asm.N, asm.p)
+        dims = tuple(int(asm.N[a]) * asm.p for a in range(asm.dim))
+        self.levels = build_hierarchy(asm.S, coords, dims, max_coarse=max_coarse)
+        self.nu = nu
+
+    def __call__(self, r):
+        return vcycle(self.levels, r, self.nu)

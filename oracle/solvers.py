@@ -37,8 +37,13 @@ def chebyshev_jacobi(S, r, degree: int, ratio: float, lam_max: float = 2.0):
 class BlockDiagPrecond:
     """P^-1 = diag((tau M~)^-1, S^-1)."""
 
-    def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, exact_schur=False, exact_blocks=False):
+    def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, exact_schur=False, exact_blocks=False,
+                 schur="chebyshev", amg_nu=2, amg_max_coarse=512):
         self.asm, self.tau, self.degree, self.ratio = asm, tau, degree, ratio
+        self.amg = None
+        if schur == "amg":   # NEXT-1: one AMG V-cycle on S~ (P:889-891, reading A9b)
+            from .amg import AMGSchur
+            self.amg = AMGSchur(asm, nu=amg_nu, max_coarse=amg_max_coarse)
         self.n_rt = asm.n_rt
         self.exact_schur = exact_schur
         self.exact_blocks = exact_blocks
@@ -65,6 +70,8 @@ class BlockDiagPrecond:
             zu = vu / (self.tau * self.asm.Mdiag)
             if self.exact_schur:
                 zq = self._lu.solve(vq)
+            elif self.amg is not None:
+                zq = self.amg(vq)
             else:
                 zq = chebyshev_jacobi(self.asm.S, vq, self.degree, self.ratio)
         return np.concatenate([zu, zq])

@@ -93,6 +93,8 @@ ALPHA_OUT, BETA_OUT = 1.88e-3, 2000.0  # P:915 outer region
 def _graded_axis(breaks, n: int, ratio: float = 1.35) -> np.ndarray:
     breaks = np.unique(np.asarray(breaks, float))
     L = np.diff(breaks)
+    if n < len(L):   # every interface plane must be a mesh plane
+        raise ValueError(f"graded axis needs at least {len(L)} intervals, got {n}")
     want = L / L.sum() * n
     m = np.maximum(np.floor(want).astype(int), 1)
     while m.sum() < n:

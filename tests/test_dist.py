@@ -113,7 +113,7 @@ def _worker(rank, world, port, cases, q):
 
 
 @pytest.mark.parametrize("cases", [[("c2", (2, 3, 4), 2), ("c1", (3, 4), 2), ("c3", (2, 2, 3), 2),
-                                    ("c5", (3, 2, 5), 1)]])
+                                    ("c5", (5, 5, 4), 1)]])
 def test_slab_decomposition_world2(cases):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")

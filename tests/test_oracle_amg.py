@@ -1,0 +1,126 @@
+"""Pins for the oracle's AMG V-cycle (NEXT-1, reading A9b): closed forms of the 1D smoothed-
+aggregation prolongator and Galerkin operator, stencil-width and constant-preservation
+invariants, SPD-ness, single-level exactness and h-robust contraction."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import amg
+
+
+def _poisson(dims, neumann=False):
+    """7/5/3-point Laplacian (unit weights) on a structured grid, x fastest; Dirichlet-like
+    rows keep the full diagonal 2d unless neumann (zero row sums)."""
+    d = len(dims)
+    n = int(np.prod(dims))
+    idx = np.arange(n).reshape(dims[::-1])
+    rows, cols, vals = [], [], []
+    diag = np.zeros(n)
+    for a in range(d):
+        ax = d - 1 - a
+        lo = np.take(idx, range(0, dims[a] - 1), axis=ax).ravel()
+        hi = np.take(idx, range(1, dims[a]), axis=ax).ravel()
+        rows += [lo, hi]; cols += [hi, lo]; vals += [-np.ones(lo.size)] * 2
+        if neumann:
+            np.add.at(diag, lo, 1.0); np.add.at(diag, hi, 1.0)
+    if not neumann:
+        diag[:] = 2.0 * d
+    A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(n, n)) + sp.diags(diag)
+    coords = np.stack(np.meshgrid(*[np.arange(m) for m in dims], indexing="ij"), -1)
+    coords = coords.transpose(list(range(d))[::-1] + [d]).reshape(n, d)
+    return A.tocsr(), coords
+
+
+def test_1d_prolongator_and_galerkin_closed_form():
+    # tridiag(-1, 2, -1): D = 2, Gershgorin lam = 2 -> omega = 2/3; interior SA column is the
+    # hat (1/3, 2/3, 1, 2/3, 1/3) and P^T A P = (1/3) tridiag(-1, 2, -1)
+    A, c = _poisson((27,))
+    lv = amg.build_hierarchy(A, c, (27,), max_coarse=2)
+    assert abs(lv[0].omega - 2.0 / 3.0) < 1e-15
+    col = lv[0].P[:, 4].toarray().ravel()          # aggregate {12, 13, 14}
+    ref = np.zeros(27)
+    ref[11:16] = [1 / 3, 2 / 3, 1, 2 / 3, 1 / 3]
+    assert np.abs(col - ref).max() < 1e-15
+    Ac = lv[1].A.toarray()
+    for J in range(2, 7):
+        row = np.zeros(9)
+        row[J - 1:J + 2] = [-1 / 3, 2 / 3, -1 / 3]
+        assert np.abs(Ac[J] - row).max() < 1e-14
+
+
+@pytest.mark.parametrize("dims", [(10, 9, 8), (13, 7)])
+def test_coarse_stencils_stay_compact_and_symmetric(dims):
+    A, c = _poisson(dims)
+    lv = amg.build_hierarchy(A, c, dims, max_coarse=8)
+    assert len(lv) >= 2
+    for k in range(1, len(lv)):
+        Ak = lv[k].A.tocoo()
+        assert abs(Ak - Ak.T).max() < 1e-13 * abs(Ak).max()
+        ci, cj = lv[k].coords[Ak.row], lv[k].coords[Ak.col]
+        assert np.abs(ci - cj).max() <= 1                    # 27-point (9-point) coarse stencil
+        assert np.diff(lv[k].A.indptr).max() <= 3 ** len(dims)
+
+
+def test_constants_preserved_on_neumann_laplacian():
+    # zero row sums: P 1 = 1 - omega D^-1 A 1 = 1, so every Galerkin level keeps A_l 1 = 0
+    dims = (12, 10, 9)
+    A, c = _poisson(dims, neumann=True)
+    assert np.abs(A @ np.ones(A.shape[0])).max() == 0
+    lv = amg.build_hierarchy(A, c, dims, max_coarse=20, coarse_solve=False)
+    for k in range(len(lv) - 1):
+        nc = lv[k + 1].A.shape[0]
+        assert np.abs(lv[k].P @ np.ones(nc) - 1.0).max() < 1e-13
+        assert np.abs(lv[k + 1].A @ np.ones(nc)).max() < 1e-12 * abs(lv[k + 1].A).max()
+
+
+def test_single_level_is_exact_and_vcycle_spd():
+    from synth import make_config
+    from oracle import operators
+    asm = operators.Assembled(make_config("c2", N=(2, 2, 2), p=2))
+    big = amg.AMGSchur(asm, max_coarse=10 ** 6)
+    assert len(big.levels) == 1
+    r = np.random.default_rng(0).standard_normal(asm.n_l2)
+    assert np.abs(big(r) - np.linalg.solve(asm.S.toarray(), r)).max() < 1e-10 * np.abs(big(r)).max()
+    ml = amg.AMGSchur(asm, max_coarse=4)
+    assert len(ml.levels) >= 2
+    B = np.stack([ml(e) for e in np.eye(asm.n_l2)], axis=1)
+    assert np.abs(B - B.T).max() < 1e-12 * np.abs(B).max()
+    assert np.linalg.eigvalsh(0.5 * (B + B.T)).min() > 0
+
+
+def _contraction(dims, its=25, nu=2):
+    A, c = _poisson(dims)
+    lv = amg.build_hierarchy(A, c, dims, max_coarse=64)
+    x = np.random.default_rng(1).standard_normal(A.shape[0])
+    rate = 0.0
+    for _ in range(its):   # power iteration on the error propagator I - B A
+        y = x - amg.vcycle(lv, A @ x, nu)
+        rate = np.linalg.norm(y) / np.linalg.norm(x)
+        x = y / np.linalg.norm(y)
+    return rate
+
+
+def test_vcycle_contraction_is_h_robust():
+    # 3D Poisson, 2 l1-Jacobi sweeps: ~0.71 at 18^3 and ~0.76 at 36^3 (3 and 4 levels); a
+    # wrong omega, a missing smoothing step or a transposed P pushes it to >= 0.9
+    r1 = _contraction((18, 18, 18))
+    r2 = _contraction((36, 36, 36))
+    assert r1 < 0.8 and r2 < 0.8, (r1, r2)
+    assert r2 < r1 + 0.1, (r1, r2)
+    assert _contraction((18, 18, 18), nu=1) > r1      # more smoothing contracts more
+
+
+def test_minres_with_amg_beats_chebyshev_on_config2():
+    from synth import make_config, random_vector
+    from oracle import operators, solvers
+    asm = operators.Assembled(make_config("c2"))
+    n = asm.n_rt + asm.n_l2
+    b = asm.apply_block(random_vector(n, 2))
+    its = {}
+    for schur in ("chebyshev", "amg"):
+        P = solvers.BlockDiagPrecond(asm, schur=schur, amg_nu=2)
+        x, it, conv, _ = solvers.minres(asm.apply_block, P.apply, b, rtol=1e-10, maxit=3000)
+        assert conv
+        its[schur] = it
+    assert its["amg"] < its["chebyshev"], its

@@ -8,7 +8,7 @@ from synth import make_config, random_vector
 
 
 @pytest.mark.parametrize("name,N,p", [("c1", (3, 2), 2), ("c2", (2, 3, 2), 2), ("c3", (2, 2, 2), 3),
-                                      ("c5", (3, 3, 3), 2)])
+                                      ("c5", (5, 5, 3), 2)])
 def test_sampled_rows_match_assembly(name, N, p):
     pr = make_config(name, N=N, p=p)
     A = operators.Assembled(pr, with_schur=False)
