@@ -73,7 +73,13 @@ typedef struct {
   int cheb_degree;     /* S^-1 = Chebyshev-Jacobi polynomial degree on S~; <= 0 => 4 (A10)   */
   double cheb_ratio;   /* interval [2/ratio, 2]; <= 0 => 30                                  */
   int kernel;          /* 0 auto, 1 force the general quadrature kernel, 2 force affine tile */
+  int schur_solver;    /* S^-1: HDIV_SCHUR_CHEBYSHEV (0, reading A10) or HDIV_SCHUR_AMG (1):  */
+                       /* one smoothed-aggregation V-cycle (reading A9b; 1 rank)  */
+  int amg_sweeps;      /* l1-Jacobi sweeps before and after the coarse correction; <= 0 => 2 */
+  int amg_max_coarse;  /* dense solve once a level has <= this many rows; <= 0 => 512        */
 } hdiv_options;
+
+enum { HDIV_SCHUR_CHEBYSHEV = 0, HDIV_SCHUR_AMG = 1 };
 
 typedef struct {
   int iters;           /* first j with |eta_j| <= rtol * gamma_1 (reading A8)         */
@@ -158,6 +164,15 @@ hdiv_status hdiv_debug_tables(int p, int Q, double* xq, double* wq, double* Bl, 
 /* Diagnostic, host only: the Gauss-Legendre nodal tables of the W^-1 local CG.
  * BG[Q][p] = L_b(x_q) (L_b the Lagrange basis on the p-point Gauss rule, x_q the Q-point rule);
  * HG[p][p] with HG[a][b] = integral of L_b over GLL subinterval a.  Caller-owned host arrays. */
+/* AMG hierarchy introspection (parity tests): number of levels, and for level l the grid
+ * extents dims[3] (level 0: the subcell grid), rows n, prolongator weight omega, and (levels
+ * >= 1) a copy of the 3^d-point stencil into the caller's DEVICE buffer st[3^d][n] (offset
+ * k = (dx+1) + 3(dy+1) + 9(dz+1), lexicographic x-fastest rows; NULL skips the copy).
+ * HDIV_ERR_UNSUPPORTED if the handle has no AMG hierarchy. */
+hdiv_status hdiv_amg_levels(hdiv_handle h, int* nlevels);
+hdiv_status hdiv_amg_level(hdiv_handle h, int level, int64_t* dims, int64_t* n, double* omega,
+                           double* st, void* stream);
+
 hdiv_status hdiv_debug_gl_tables(int p, int Q, double* BG, double* HG);
 
 #ifdef __cplusplus

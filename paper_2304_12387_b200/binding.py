@@ -40,7 +40,11 @@ class Coeffs(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("tau", C.c_double), ("cheb_degree", C.c_int), ("cheb_ratio", C.c_double),
-                ("kernel", C.c_int)]
+                ("kernel", C.c_int), ("schur_solver", C.c_int), ("amg_sweeps", C.c_int),
+                ("amg_max_coarse", C.c_int)]
+
+
+SCHUR_SOLVERS = {"chebyshev": 0, "amg": 1}
 
 
 class Report(C.Structure):
@@ -84,6 +88,10 @@ def load_library(path: str = LIB_PATH):
         "hdiv_minres_solve": (C.c_int, [vp, dp, dp, C.c_double, C.c_int, C.POINTER(Report), vp]),
         "hdiv_debug_tables": (C.c_int, [C.c_int, C.c_int] + [dp] * 7),
         "hdiv_debug_gl_tables": (C.c_int, [C.c_int, C.c_int, dp, dp]),
+        "hdiv_amg_levels": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+        "hdiv_amg_level": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_void_p,
+                                     C.c_void_p]),
         "hdiv_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
     }
     for name, (res, args) in sig.items():
@@ -154,6 +162,7 @@ class HdivOperator:
 
     def __init__(self, dim, N, p, kind, vertices=None, alpha=None, beta=None, gamma=None,
                  eps=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
+                 schur="chebyshev", amg_sweeps=2, amg_max_coarse=512,
                  slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
         import torch
         self.lib = load_library()
@@ -174,7 +183,8 @@ class HdivOperator:
         md = MeshDesc(dim, N[0], N[1], N[2] if dim == 3 else 1, z0, z1, _dptr(V))
         a_, b_, g_, e_ = arr(alpha), arr(beta), arr(gamma), arr(eps)
         co = Coeffs(_dptr(a_), _dptr(b_), _dptr(g_), _dptr(e_), 1.0, 1.0, 0.0, 1.0)
-        op = Options(tau, cheb_degree, cheb_ratio, kernel)
+        op = Options(tau, cheb_degree, cheb_ratio, kernel, SCHUR_SOLVERS[schur], amg_sweeps,
+                     amg_max_coarse)
         h = C.c_void_p()
         idbuf = None
         if nccl_id is not None:
@@ -315,6 +325,26 @@ class HdivOperator:
         _check(self.lib.hdiv_minres_solve(self.h, self._ptr(b, n), self._ptr(x, n), rtol, maxit,
                                           C.byref(rep), self._stream_handle(stream)))
         return x, rep
+
+    def amg_levels(self) -> int:
+        n = C.c_int()
+        _check(self.lib.hdiv_amg_levels(self.h, C.byref(n)))
+        return n.value
+
+    def amg_level(self, level: int):
+        """(dims, omega, stencil) of AMG level `level`; stencil [3^d][n] (None for level 0)."""
+        torch = self._torch
+        dims = (C.c_int64 * 3)()
+        n, om = C.c_int64(), C.c_double()
+        _check(self.lib.hdiv_amg_level(self.h, level, dims, C.byref(n), C.byref(om), None, None))
+        st = None
+        if level > 0:
+            ns = 27 if self.dim == 3 else 9
+            st = torch.empty((ns, n.value), dtype=torch.float64, device="cuda")
+            _check(self.lib.hdiv_amg_level(self.h, level, dims, C.byref(n), C.byref(om),
+                                           C.c_void_p(st.data_ptr()),
+                                           self._stream_handle(None)))
+        return tuple(dims), om.value, st
 
     def close(self):
         if getattr(self, "h", None):

@@ -1,0 +1,752 @@
+// amg.cu — NEXT-1: one algebraic-multigrid V-cycle as S^-1 (the paper's Schur preconditioner,
+// P:889-891 "one V-cycle of AMG"; l1-Jacobi smoothing P:900-901; Galerkin coarse
+// operators).  The paper leaves coarsening, interpolation, sweeps and coarse solve open
+// (reading A9); this build fixes them as reading A9b, identical in oracle/amg.py:
+//
+//   aggregates   3 x 3 (x 3) blocks of the structured subcell grid (deterministic)
+//   P            (I - omega D^-1 A) P_tent,  omega = 4 / (3 max_i sum_j |a_ij| / a_ii)
+//   A_{l+1}      P^T A_l P   (27-point / 9-point on every coarse level)
+//   smoother     nu sweeps of l1-Jacobi before and after the coarse correction
+//   coarsest     <= max_coarse unknowns: dense inverse (host Gauss-Jordan at setup)
+//
+// B200 layout: level 0 is S~ itself (SELL-32 copy for the SpMVs, its 7-point face form for the
+// setup); levels >= 1 are structured stencils stored as [3^d][n] (SoA: coalesced per offset),
+// lexicographic x-fastest numbering.  P and P^T are never stored: P e = inject(e) - omega D^-1 A
+// inject(e) and P^T r = aggregate-sum(r - omega A D^-1 r) reuse the level's SpMV.  The Galerkin
+// product is formed matrix-free per coarse row (one CTA: phi_I on the 5^d box, A phi_I on 7^d,
+// (I - omega A D^-1) A phi_I on 9^d, summed per neighbouring aggregate), no SpGEMM.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace hdiv {
+
+struct AmgLevel {
+  int dim = 3;
+  long long d[3] = {1, 1, 1};   // grid extents
+  long long n = 0;
+  double* st = nullptr;         // [3^dim][n] stencil (levels >= 1)
+  double* dinv = nullptr;       // 1 / a_ii
+  double* dl1inv = nullptr;     // 1 / sum_j |a_ij|
+  double omega = 0.0;           // prolongator smoothing weight (levels with a coarser one)
+  double *xa = nullptr, *xb = nullptr, *r = nullptr, *sv = nullptr;
+  double *b = nullptr, *e = nullptr;   // levels >= 1: restricted rhs, coarse correction
+};
+
+struct AmgHier {
+  std::vector<AmgLevel> L;
+  int32_t* agg0 = nullptr;      // level-0 row -> level-1 aggregate
+  double* cinv = nullptr;       // dense inverse of the coarsest operator [nc][nc]
+  long long nc = 0;
+  int nu = 2;
+  double* red = nullptr;        // reduction scratch
+};
+
+namespace {
+
+constexpr int ANT = 256;
+constexpr int ABLK = 148 * 8;
+
+// ---- level-0 operator: S~ in its 7/5-point face form, L2 element-major rows ----
+struct Op0 {
+  long long n[3], off[3], NL[3];
+  int p, dim;
+  const double* mdiag;
+  const double* ctil;
+  __device__ __forceinline__ long long idx(long long X, long long Y, long long Z) const {
+    long long e = (X / p) + NL[0] * ((Y / p) + NL[1] * (Z / p));
+    long long a = X % p, b = Y % p, c = Z % p;
+    if (dim == 2) return e * p * p + a + p * b;
+    return e * p * p * p + a + p * (b + p * c);
+  }
+  __device__ __forceinline__ bool in(long long X, long long Y, long long Z) const {
+    return X >= 0 && Y >= 0 && Z >= 0 && X < n[0] && Y < n[1] && (dim == 2 ? Z == 0 : Z < n[2]);
+  }
+  __device__ __forceinline__ void coords(long long r, long long* X, long long* Y,
+                                         long long* Z) const {
+    const long long pd = (dim == 2) ? (long long)p * p : (long long)p * p * p;
+    const long long e = r / pd, il = r % pd;
+    const long long ex = e % NL[0], ey = (e / NL[0]) % NL[1];
+    const long long ez = (dim == 3) ? e / (NL[0] * NL[1]) : 0;
+    *X = ex * p + il % p;
+    *Y = ey * p + (il / p) % p;
+    *Z = (dim == 3) ? ez * p + il / (p * p) : 0;
+  }
+  // a[k], k = (dx+1) + 3(dy+1) (+ 9(dz+1)): the row of S~ at cell (X,Y,Z); zeros elsewhere
+  __device__ __forceinline__ void row(long long X, long long Y, long long Z, double* a) const {
+    const int NS = (dim == 3) ? 27 : 9;
+    for (int k = 0; k < NS; ++k) a[k] = 0.0;
+    const int C = (dim == 3) ? 13 : 4;
+    long long f[6];
+    int nf;
+    if (dim == 3) {
+      f[0] = off[0] + X + (n[0] + 1) * (Y + n[1] * Z);
+      f[1] = f[0] + 1;
+      f[2] = off[1] + X + n[0] * (Y + (n[1] + 1) * Z);
+      f[3] = f[2] + n[0];
+      f[4] = off[2] + X + n[0] * (Y + n[1] * Z);
+      f[5] = f[4] + n[0] * n[1];
+      nf = 6;
+    } else {
+      f[0] = off[0] + X + (n[0] + 1) * Y;
+      f[1] = f[0] + 1;
+      f[2] = off[1] + X + n[0] * Y;
+      f[3] = f[2] + n[0];
+      nf = 4;
+    }
+    double d = ctil[idx(X, Y, Z)];
+    const int step[3] = {1, 3, 9};
+    const long long ext[3] = {n[0], n[1], n[2]};
+    const long long crd[3] = {X, Y, Z};
+    for (int k = 0; k < nf; ++k) {
+      const double w = 1.0 / mdiag[f[k]];
+      d += w;
+      const int ax = k >> 1;
+      const bool up = k & 1;
+      const bool has = up ? (crd[ax] + 1 < ext[ax]) : (crd[ax] > 0);
+      if (has) a[C + (up ? step[ax] : -step[ax])] = -w;
+    }
+    a[C] = d;
+  }
+};
+
+// ---- level >= 1: stored structured stencil ----
+struct OpS {
+  long long d[3], n;
+  int dim;
+  const double* st;
+  __device__ __forceinline__ long long idx(long long X, long long Y, long long Z) const {
+    return X + d[0] * (Y + d[1] * Z);
+  }
+  __device__ __forceinline__ bool in(long long X, long long Y, long long Z) const {
+    return X >= 0 && Y >= 0 && Z >= 0 && X < d[0] && Y < d[1] && Z < d[2];
+  }
+  __device__ __forceinline__ void coords(long long r, long long* X, long long* Y,
+                                         long long* Z) const {
+    *X = r % d[0];
+    *Y = (r / d[0]) % d[1];
+    *Z = r / (d[0] * d[1]);
+  }
+  __device__ __forceinline__ void row(long long X, long long Y, long long Z, double* a) const {
+    const int NS = (dim == 3) ? 27 : 9;
+    const long long i = idx(X, Y, Z);
+    for (int k = 0; k < NS; ++k) a[k] = st[k * n + i];
+  }
+};
+
+// stencil slot k -> offset: k = (dx+1) + 3(dy+1) (+ 9(dz+1) in 3D)
+template <int DIM>
+__device__ __forceinline__ void off_of(int k, int* dx, int* dy, int* dz) {
+  *dx = k % 3 - 1;
+  *dy = (k / 3) % 3 - 1;
+  *dz = (DIM == 3) ? k / 9 - 1 : 0;
+}
+
+// diag / l1 / Gershgorin ratio per row; part[block] = max ratio of the block
+template <class Op>
+__global__ void __launch_bounds__(ANT) level_diag_kernel(Op A, long long nrow, double* dinv,
+                                                        double* dl1inv, double* part) {
+  __shared__ double red[ANT / 32];
+  double mx = 0.0;
+  const int NS = (A.dim == 3) ? 27 : 9;
+  for (long long r = blockIdx.x * (long long)ANT + threadIdx.x; r < nrow;
+       r += (long long)gridDim.x * ANT) {
+    long long X, Y, Z;
+    A.coords(r, &X, &Y, &Z);
+    double a[27];
+    A.row(X, Y, Z, a);
+    double l1 = 0.0;
+    for (int k = 0; k < NS; ++k) l1 += fabs(a[k]);
+    const double dg = a[NS / 2];
+    dinv[r] = 1.0 / dg;
+    dl1inv[r] = 1.0 / l1;
+    mx = fmax(mx, l1 / dg);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < ANT / 32; ++w) m = fmax(m, red[w]);
+    part[blockIdx.x] = m;
+  }
+}
+
+// Galerkin row I of A_c = P^T A P (one CTA per coarse point; DIM 2 or 3)
+template <int DIM, class Op>
+__global__ void __launch_bounds__(128) rap_kernel(Op A, const double* __restrict__ dinv,
+                                                  long long cd0, long long cd1, long long cd2,
+                                                  double omega, double* __restrict__ stc) {
+  constexpr int B5 = (DIM == 3) ? 125 : 25, B7 = (DIM == 3) ? 343 : 49, B9 = (DIM == 3) ? 729 : 81;
+  constexpr int NS = (DIM == 3) ? 27 : 9;
+  __shared__ double phi[B5], psi[B7], chi[B7], xi[B9];
+  const long long nc = cd0 * cd1 * cd2;
+  const long long I = blockIdx.x;
+  const long long IX = I % cd0, IY = (I / cd0) % cd1, IZ = (DIM == 3) ? I / (cd0 * cd1) : 0;
+  const long long ox = 3 * IX, oy = 3 * IY, oz = 3 * IZ;   // aggregate origin (fine coords)
+  auto inagg = [&](long long X, long long Y, long long Z) {
+    return X >= ox && X < ox + 3 && Y >= oy && Y < oy + 3 && (DIM == 2 || (Z >= oz && Z < oz + 3));
+  };
+  auto box = [&](int t, int w, long long lo, long long* X, long long* Y, long long* Z) {
+    *X = ox + lo + t % w;
+    *Y = oy + lo + (t / w) % w;
+    *Z = (DIM == 3) ? oz + lo + t / (w * w) : 0;
+  };
+  auto bidx = [&](long long X, long long Y, long long Z, int w, long long lo) -> int {
+    const long long x = X - ox - lo, y = Y - oy - lo, z = (DIM == 3) ? Z - oz - lo : 0;
+    if (x < 0 || y < 0 || z < 0 || x >= w || y >= w || z >= w) return -1;
+    return (int)(x + w * (y + w * z));
+  };
+  double a[27];
+  // phi_I = (I - omega D^-1 A) 1_agg(I) on the 5^d box [o-1, o+3]
+  for (int t = threadIdx.x; t < B5; t += blockDim.x) {
+    long long X, Y, Z;
+    box(t, 5, -1, &X, &Y, &Z);
+    double v = 0.0;
+    if (A.in(X, Y, Z)) {
+      A.row(X, Y, Z, a);
+      double sacc = 0.0;
+      for (int k = 0; k < NS; ++k) {
+        int dx, dy, dz;
+        off_of<DIM>(k, &dx, &dy, &dz);
+        if (inagg(X + dx, Y + dy, Z + dz) && A.in(X + dx, Y + dy, Z + dz)) sacc += a[k];
+      }
+      v = (inagg(X, Y, Z) ? 1.0 : 0.0) - omega * dinv[A.idx(X, Y, Z)] * sacc;
+    }
+    phi[t] = v;
+  }
+  __syncthreads();
+  // psi = A phi on the 7^d box [o-2, o+4]; chi = D^-1 psi
+  for (int t = threadIdx.x; t < B7; t += blockDim.x) {
+    long long X, Y, Z;
+    box(t, 7, -2, &X, &Y, &Z);
+    double v = 0.0, c = 0.0;
+    if (A.in(X, Y, Z)) {
+      A.row(X, Y, Z, a);
+      for (int k = 0; k < NS; ++k) {
+        int dx, dy, dz;
+        off_of<DIM>(k, &dx, &dy, &dz);
+        const int q = bidx(X + dx, Y + dy, Z + dz, 5, -1);
+        if (q >= 0 && a[k] != 0.0) v += a[k] * phi[q];
+      }
+      c = dinv[A.idx(X, Y, Z)] * v;
+    }
+    psi[t] = v;
+    chi[t] = c;
+  }
+  __syncthreads();
+  // xi = psi - omega A chi on the 9^d box [o-3, o+5]
+  for (int t = threadIdx.x; t < B9; t += blockDim.x) {
+    long long X, Y, Z;
+    box(t, 9, -3, &X, &Y, &Z);
+    double v = 0.0;
+    if (A.in(X, Y, Z)) {
+      A.row(X, Y, Z, a);
+      double ac = 0.0;
+      for (int k = 0; k < NS; ++k) {
+        int dx, dy, dz;
+        off_of<DIM>(k, &dx, &dy, &dz);
+        const int q = bidx(X + dx, Y + dy, Z + dz, 7, -2);
+        if (q >= 0 && a[k] != 0.0) ac += a[k] * chi[q];
+      }
+      const int q0 = bidx(X, Y, Z, 7, -2);
+      v = (q0 >= 0 ? psi[q0] : 0.0) - omega * ac;
+    }
+    xi[t] = v;
+  }
+  __syncthreads();
+  // A_c[I][J] = sum of xi over aggregate J = I + delta
+  for (int k = threadIdx.x; k < NS; k += blockDim.x) {
+    int dx, dy, dz;
+    off_of<DIM>(k, &dx, &dy, &dz);
+    const long long JX = IX + dx, JY = IY + dy, JZ = IZ + dz;
+    double v = 0.0;
+    if (JX >= 0 && JY >= 0 && JZ >= 0 && JX < cd0 && JY < cd1 && JZ < cd2) {
+      for (int cz = 0; cz < (DIM == 3 ? 3 : 1); ++cz)
+        for (int cy = 0; cy < 3; ++cy)
+          for (int cx = 0; cx < 3; ++cx) {
+            const long long X = 3 * JX + cx, Y = 3 * JY + cy, Z = (DIM == 3) ? 3 * JZ + cz : 0;
+            if (!A.in(X, Y, Z)) continue;
+            const int q = bidx(X, Y, Z, 9, -3);
+            v += xi[q];
+          }
+    }
+    stc[k * nc + I] = v;
+  }
+}
+
+// level-0 row -> aggregate (lexicographic coarse numbering)
+__global__ void agg0_kernel(Op0 A, long long cd0, long long cd1, int32_t* agg, long long nrow) {
+  long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= nrow) return;
+  const long long pd = (A.dim == 2) ? (long long)A.p * A.p : (long long)A.p * A.p * A.p;
+  const long long e = r / pd, il = r % pd;
+  const long long ex = e % A.NL[0], ey = (e / A.NL[0]) % A.NL[1];
+  const long long ez = (A.dim == 3) ? e / (A.NL[0] * A.NL[1]) : 0;
+  const long long X = ex * A.p + il % A.p, Y = ey * A.p + (il / A.p) % A.p;
+  const long long Z = (A.dim == 3) ? ez * A.p + il / (A.p * A.p) : 0;
+  (void)X;
+  agg[r] = (int32_t)(X / 3 + cd0 * (Y / 3 + cd1 * (Z / 3)));
+}
+
+// ---- V-cycle kernels.  SpMV access: level 0 through SELL-32 (width W), levels >= 1 stencil ----
+struct SellA {
+  const int32_t* col;
+  const double* val;
+  int W;
+  template <class F>
+  __device__ __forceinline__ double dot(long long i, F f) const {
+    const long long base = (i >> 5) * (32LL * W) + (i & 31);
+    double s = 0.0;
+    for (int k = 0; k < W; ++k) s = fma(val[base + 32 * k], f(col[base + 32 * k]), s);
+    return s;
+  }
+};
+
+struct StA {
+  long long d[3], n;
+  int dim;
+  const double* st;
+  template <class F>
+  __device__ __forceinline__ double dot(long long i, F f) const {
+    const long long X = i % d[0], Y = (i / d[0]) % d[1], Z = i / (d[0] * d[1]);
+    const int NS = (dim == 3) ? 27 : 9;
+    double s = 0.0;
+    for (int k = 0; k < NS; ++k) {
+      const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = (dim == 3) ? k / 9 - 1 : 0;
+      const long long x = X + dx, y = Y + dy, z = Z + dz;
+      if (x < 0 || y < 0 || z < 0 || x >= d[0] || y >= d[1] || z >= d[2]) continue;
+      s = fma(st[k * n + i], f(x + d[0] * (y + d[1] * z)), s);
+    }
+    return s;
+  }
+  __device__ __forceinline__ long long agg(long long j, long long cd0, long long cd1) const {
+    const long long X = j % d[0], Y = (j / d[0]) % d[1], Z = j / (d[0] * d[1]);
+    return X / 3 + cd0 * (Y / 3 + cd1 * (Z / 3));
+  }
+};
+
+#define AMG_LOOP(n) \
+  for (long long i = blockIdx.x * (long long)ANT + threadIdx.x; i < (n); i += (long long)gridDim.x * ANT)
+
+// x_out = x_in + Dl1^-1 (b - A x_in); x_in = nullptr means x_in = Dl1^-1 b (first sweep from 0)
+template <class Acc>
+__global__ void __launch_bounds__(ANT) jacobi_kernel(Acc A, long long n, const double* __restrict__ b,
+                                                     const double* __restrict__ xin,
+                                                     double* __restrict__ xout,
+                                                     const double* __restrict__ dl1inv,
+                                                     const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(n) {
+    double ax, xi;
+    if (xin) {
+      ax = A.dot(i, [&](long long j) { return xin[j]; });
+      xi = xin[i];
+    } else {
+      ax = A.dot(i, [&](long long j) { return dl1inv[j] * b[j]; });
+      xi = dl1inv[i] * b[i];
+    }
+    xout[i] = xi + dl1inv[i] * (b[i] - ax);
+  }
+}
+
+__global__ void __launch_bounds__(ANT) scale_kernel(long long n, const double* __restrict__ b,
+                                                    const double* __restrict__ dl1inv,
+                                                    double* __restrict__ x,
+                                                    const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(n) x[i] = dl1inv[i] * b[i];
+}
+
+// s = r - omega A D^-1 r with r = b - A x  (computed in two passes: r then s)
+template <class Acc>
+__global__ void __launch_bounds__(ANT) resid_kernel(Acc A, long long n, const double* __restrict__ b,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ r,
+                                                    const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(n) r[i] = b[i] - A.dot(i, [&](long long j) { return x[j]; });
+}
+
+template <class Acc>
+__global__ void __launch_bounds__(ANT) smooth_r_kernel(Acc A, long long n,
+                                                       const double* __restrict__ r,
+                                                       const double* __restrict__ dinv, double omega,
+                                                       double* __restrict__ s,
+                                                       const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(n) s[i] = r[i] - omega * A.dot(i, [&](long long j) { return dinv[j] * r[j]; });
+}
+
+// b_c[I] = sum over aggregate I of s (level 0: element-major fine rows)
+__global__ void __launch_bounds__(ANT) aggsum0_kernel(Op0 A, long long cd0, long long cd1,
+                                                      long long nc, const double* __restrict__ s,
+                                                      double* __restrict__ bc,
+                                                      const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(nc) {
+    const long long IX = i % cd0, IY = (i / cd0) % cd1, IZ = (A.dim == 3) ? i / (cd0 * cd1) : 0;
+    double v = 0.0;
+    for (int cz = 0; cz < (A.dim == 3 ? 3 : 1); ++cz)
+      for (int cy = 0; cy < 3; ++cy)
+        for (int cx = 0; cx < 3; ++cx) {
+          const long long X = 3 * IX + cx, Y = 3 * IY + cy, Z = 3 * IZ + cz;
+          if (A.in(X, Y, Z)) v += s[A.idx(X, Y, Z)];
+        }
+    bc[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(ANT) aggsumS_kernel(long long d0, long long d1, long long d2,
+                                                      long long cd0, long long cd1, long long nc,
+                                                      int dim, const double* __restrict__ s,
+                                                      double* __restrict__ bc,
+                                                      const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(nc) {
+    const long long IX = i % cd0, IY = (i / cd0) % cd1, IZ = (dim == 3) ? i / (cd0 * cd1) : 0;
+    double v = 0.0;
+    for (int cz = 0; cz < (dim == 3 ? 3 : 1); ++cz)
+      for (int cy = 0; cy < 3; ++cy)
+        for (int cx = 0; cx < 3; ++cx) {
+          const long long X = 3 * IX + cx, Y = 3 * IY + cy, Z = 3 * IZ + cz;
+          if (X < d0 && Y < d1 && Z < d2) v += s[X + d0 * (Y + d1 * Z)];
+        }
+    bc[i] = v;
+  }
+}
+
+// x_out = x + e_f - omega D^-1 A e_f,  e_f(j) = e_c[agg(j)]
+template <class Acc, class Agg>
+__global__ void __launch_bounds__(ANT) prolong_kernel(Acc A, Agg agg, long long n,
+                                                      const double* __restrict__ x,
+                                                      const double* __restrict__ ec,
+                                                      const double* __restrict__ dinv, double omega,
+                                                      double* __restrict__ xout,
+                                                      const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(n) {
+    const double ae = A.dot(i, [&](long long j) { return ec[agg(j)]; });
+    xout[i] = x[i] + ec[agg(i)] - omega * dinv[i] * ae;
+  }
+}
+
+struct Agg0 {
+  const int32_t* a;
+  __device__ __forceinline__ long long operator()(long long j) const { return a[j]; }
+};
+struct AggS {
+  long long d0, d1, cd0, cd1;
+  __device__ __forceinline__ long long operator()(long long j) const {
+    const long long X = j % d0, Y = (j / d0) % d1, Z = j / (d0 * d1);
+    return X / 3 + cd0 * (Y / 3 + cd1 * (Z / 3));
+  }
+};
+
+// coarsest: x = A^-1 b (dense, one CTA)
+__global__ void __launch_bounds__(ANT) coarse_kernel(const double* __restrict__ cinv, long long nc,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ x,
+                                                     const int* __restrict__ done) {
+  if (done && *done) return;
+  for (long long i = threadIdx.x; i < nc; i += ANT) {
+    double s = 0.0;
+    for (long long j = 0; j < nc; ++j) s = fma(cinv[i * nc + j], b[j], s);
+    x[i] = s;
+  }
+}
+
+inline unsigned nbk(long long n) {
+  long long b = (n + ANT - 1) / ANT;
+  return (unsigned)std::max(1LL, std::min<long long>(b, ABLK));
+}
+
+Op0 make_op0(const hdiv_ctx* h) {
+  Op0 o;
+  for (int a = 0; a < 3; ++a) { o.n[a] = h->n[a]; o.off[a] = h->off[a]; o.NL[a] = h->NL[a]; }
+  if (h->dim == 2) o.n[2] = 1;
+  o.p = h->p;
+  o.dim = h->dim;
+  o.mdiag = h->d_mdiag;
+  o.ctil = h->d_ctil;
+  return o;
+}
+
+OpS make_ops(const AmgLevel& L) {
+  OpS o;
+  for (int a = 0; a < 3; ++a) o.d[a] = L.d[a];
+  o.n = L.n;
+  o.dim = L.dim;
+  o.st = L.st;
+  return o;
+}
+
+StA make_sta(const AmgLevel& L) {
+  StA o;
+  for (int a = 0; a < 3; ++a) o.d[a] = L.d[a];
+  o.n = L.n;
+  o.dim = L.dim;
+  o.st = L.st;
+  return o;
+}
+
+// Gauss-Jordan inverse with partial pivoting (host, coarsest level only)
+bool invert_dense(std::vector<double>& A, long long n) {
+  std::vector<double> Inv(n * n, 0.0);
+  for (long long i = 0; i < n; ++i) Inv[i * n + i] = 1.0;
+  for (long long c = 0; c < n; ++c) {
+    long long piv = c;
+    for (long long r = c + 1; r < n; ++r)
+      if (std::fabs(A[r * n + c]) > std::fabs(A[piv * n + c])) piv = r;
+    if (A[piv * n + c] == 0.0) return false;
+    if (piv != c)
+      for (long long j = 0; j < n; ++j) {
+        std::swap(A[c * n + j], A[piv * n + j]);
+        std::swap(Inv[c * n + j], Inv[piv * n + j]);
+      }
+    const double d = A[c * n + c];
+    for (long long j = 0; j < n; ++j) { A[c * n + j] /= d; Inv[c * n + j] /= d; }
+    for (long long r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = A[r * n + c];
+      if (f == 0.0) continue;
+      for (long long j = 0; j < n; ++j) { A[r * n + j] -= f * A[c * n + j]; Inv[r * n + j] -= f * Inv[c * n + j]; }
+    }
+  }
+  A.swap(Inv);
+  return true;
+}
+
+}  // namespace
+
+void amg_free(hdiv_ctx* h) {
+  if (!h->amg) return;
+  for (auto& L : h->amg->L) {
+    cudaFree(L.st); cudaFree(L.dinv); cudaFree(L.dl1inv);
+    cudaFree(L.xa); cudaFree(L.xb); cudaFree(L.r); cudaFree(L.sv); cudaFree(L.b); cudaFree(L.e);
+  }
+  cudaFree(h->amg->agg0);
+  cudaFree(h->amg->cinv);
+  cudaFree(h->amg->red);
+  delete h->amg;
+  h->amg = nullptr;
+}
+
+hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
+  if (h->nranks > 1) {
+    set_error("AMG Schur preconditioner: single-rank only in this build");
+    return HDIV_ERR_UNSUPPORTED;
+  }
+  auto* H = new AmgHier();
+  h->amg = H;
+  H->nu = h->opts.amg_sweeps;
+  HDIV_CUDA_TRY(cudaMalloc(&H->red, sizeof(double) * ABLK));
+  std::vector<double> part(ABLK);
+  const int dim = h->dim;
+  const int NS = (dim == 3) ? 27 : 9;
+  // level 0
+  {
+    AmgLevel L;
+    L.dim = dim;
+    L.d[0] = h->n[0]; L.d[1] = h->n[1]; L.d[2] = (dim == 3) ? h->n[2] : 1;
+    L.n = h->nl2;
+    HDIV_CUDA_TRY(cudaMalloc(&L.dinv, sizeof(double) * L.n));
+    HDIV_CUDA_TRY(cudaMalloc(&L.dl1inv, sizeof(double) * L.n));
+    HDIV_CUDA_TRY(cudaMemsetAsync(H->red, 0, sizeof(double) * ABLK, s));
+    level_diag_kernel<Op0><<<ABLK, ANT, 0, s>>>(make_op0(h), L.n, L.dinv, L.dl1inv, H->red);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    HDIV_CUDA_TRY(cudaMemcpyAsync(part.data(), H->red, sizeof(double) * ABLK, cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    double mx = 0.0;
+    for (double v : part) mx = std::max(mx, v);
+    L.omega = 4.0 / (3.0 * mx);
+    H->L.push_back(L);
+  }
+  for (;;) {
+    AmgLevel& F = H->L.back();
+    long long cd[3] = {(F.d[0] + 2) / 3, (F.d[1] + 2) / 3, (dim == 3) ? (F.d[2] + 2) / 3 : 1};
+    const bool same = cd[0] == F.d[0] && cd[1] == F.d[1] && cd[2] == F.d[2];
+    if (F.n <= h->opts.amg_max_coarse || same || H->L.size() >= 25) break;
+    AmgLevel Cl;
+    Cl.dim = dim;
+    for (int a = 0; a < 3; ++a) Cl.d[a] = cd[a];
+    Cl.n = cd[0] * cd[1] * cd[2];
+    HDIV_CUDA_TRY(cudaMalloc(&Cl.st, sizeof(double) * NS * Cl.n));
+    const bool first = H->L.size() == 1;
+    if (dim == 3) {
+      if (first) rap_kernel<3, Op0><<<(unsigned)Cl.n, 128, 0, s>>>(make_op0(h), F.dinv, cd[0], cd[1], cd[2], F.omega, Cl.st);
+      else rap_kernel<3, OpS><<<(unsigned)Cl.n, 128, 0, s>>>(make_ops(F), F.dinv, cd[0], cd[1], cd[2], F.omega, Cl.st);
+    } else {
+      if (first) rap_kernel<2, Op0><<<(unsigned)Cl.n, 128, 0, s>>>(make_op0(h), F.dinv, cd[0], cd[1], cd[2], F.omega, Cl.st);
+      else rap_kernel<2, OpS><<<(unsigned)Cl.n, 128, 0, s>>>(make_ops(F), F.dinv, cd[0], cd[1], cd[2], F.omega, Cl.st);
+    }
+    HDIV_CUDA_TRY(cudaGetLastError());
+    if (first) {
+      HDIV_CUDA_TRY(cudaMalloc(&H->agg0, sizeof(int32_t) * F.n));
+      agg0_kernel<<<(unsigned)((F.n + 255) / 256), 256, 0, s>>>(make_op0(h), cd[0], cd[1], H->agg0, F.n);
+      HDIV_CUDA_TRY(cudaGetLastError());
+    }
+    HDIV_CUDA_TRY(cudaMalloc(&Cl.dinv, sizeof(double) * Cl.n));
+    HDIV_CUDA_TRY(cudaMalloc(&Cl.dl1inv, sizeof(double) * Cl.n));
+    HDIV_CUDA_TRY(cudaMemsetAsync(H->red, 0, sizeof(double) * ABLK, s));
+    level_diag_kernel<OpS><<<ABLK, ANT, 0, s>>>(make_ops(Cl), Cl.n, Cl.dinv, Cl.dl1inv, H->red);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    HDIV_CUDA_TRY(cudaMemcpyAsync(part.data(), H->red, sizeof(double) * ABLK, cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    double mx = 0.0;
+    for (double v : part) mx = std::max(mx, v);
+    Cl.omega = 4.0 / (3.0 * mx);
+    H->L.push_back(Cl);
+  }
+  // work vectors
+  for (size_t l = 0; l < H->L.size(); ++l) {
+    AmgLevel& L = H->L[l];
+    const size_t b = sizeof(double) * L.n;
+    HDIV_CUDA_TRY(cudaMalloc(&L.xa, b));
+    HDIV_CUDA_TRY(cudaMalloc(&L.xb, b));
+    HDIV_CUDA_TRY(cudaMalloc(&L.r, b));
+    HDIV_CUDA_TRY(cudaMalloc(&L.sv, b));
+    if (l > 0) {
+      HDIV_CUDA_TRY(cudaMalloc(&L.b, b));
+      HDIV_CUDA_TRY(cudaMalloc(&L.e, b));
+    }
+  }
+  // coarsest dense inverse
+  AmgLevel& Lc = H->L.back();
+  const long long nc = Lc.n;
+  if (nc > 8192) {
+    set_error("AMG coarsest level too large for the dense solve (raise amg_max_coarse coverage)");
+    return HDIV_ERR_UNSUPPORTED;
+  }
+  std::vector<double> Ad(nc * nc, 0.0);
+  if (H->L.size() == 1) {   // the fine operator itself: from the CSR of S~
+    std::vector<int64_t> rp(nc + 1);
+    HDIV_CUDA_TRY(cudaMemcpyAsync(rp.data(), h->d_srow, sizeof(int64_t) * (nc + 1), cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int32_t> col(rp[nc]);
+    std::vector<double> val(rp[nc]);
+    HDIV_CUDA_TRY(cudaMemcpyAsync(col.data(), h->d_scol, sizeof(int32_t) * rp[nc], cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaMemcpyAsync(val.data(), h->d_sval, sizeof(double) * rp[nc], cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    for (long long i = 0; i < nc; ++i)
+      for (int64_t t = rp[i]; t < rp[i + 1]; ++t) Ad[i * nc + col[t]] = val[t];
+  } else {
+    std::vector<double> st(NS * nc);
+    HDIV_CUDA_TRY(cudaMemcpyAsync(st.data(), Lc.st, sizeof(double) * NS * nc, cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    for (long long i = 0; i < nc; ++i) {
+      const long long X = i % Lc.d[0], Y = (i / Lc.d[0]) % Lc.d[1], Z = i / (Lc.d[0] * Lc.d[1]);
+      for (int k = 0; k < NS; ++k) {
+        const long long x = X + k % 3 - 1, y = Y + (k / 3) % 3 - 1;
+        const long long z = Z + ((dim == 3) ? k / 9 - 1 : 0);
+        if (x < 0 || y < 0 || z < 0 || x >= Lc.d[0] || y >= Lc.d[1] || z >= Lc.d[2]) continue;
+        Ad[i * nc + (x + Lc.d[0] * (y + Lc.d[1] * z))] = st[k * nc + i];
+      }
+    }
+  }
+  if (!invert_dense(Ad, nc)) {
+    set_error("AMG: singular coarsest operator");
+    return HDIV_ERR_BREAKDOWN;
+  }
+  H->nc = nc;
+  HDIV_CUDA_TRY(cudaMalloc(&H->cinv, sizeof(double) * nc * nc));
+  HDIV_CUDA_TRY(cudaMemcpyAsync(H->cinv, Ad.data(), sizeof(double) * nc * nc, cudaMemcpyHostToDevice, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  return HDIV_OK;
+}
+
+// one V-cycle at level l: x = B_l b (x written, b read)
+static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, const int* done,
+                          cudaStream_t s) {
+  AmgHier* H = h->amg;
+  AmgLevel& L = H->L[l];
+  if (l + 1 == H->L.size()) {
+    coarse_kernel<<<1, ANT, 0, s>>>(H->cinv, L.n, b, x, done);
+    return cudaGetLastError() == cudaSuccess ? HDIV_OK : HDIV_ERR_CUDA;
+  }
+  AmgLevel& C = H->L[l + 1];
+  const int nu = H->nu;
+  const long long n = L.n;
+  const unsigned g = nbk(n);
+  SellA sa{h->d_ecol, h->d_eval, 2 * h->dim + 1};
+  StA sta = make_sta(L);
+  const bool lev0 = (l == 0);
+  // buffers: pre-smoothing ping-pong in xa/xb, final post-smoothing output in x
+  double* cur = L.xa;
+  double* nxt = L.xb;
+  auto jac = [&](const double* xin, double* xout) {
+    if (lev0) jacobi_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, b, xin, xout, L.dl1inv, done);
+    else jacobi_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, xin, xout, L.dl1inv, done);
+  };
+  if (nu >= 1) {
+    scale_kernel<<<g, ANT, 0, s>>>(n, b, L.dl1inv, cur, done);
+    for (int k = 1; k < nu; ++k) { jac(cur, nxt); std::swap(cur, nxt); }
+  } else {
+    HDIV_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(double) * n, s));
+  }
+  // r = b - A x ; s = r - omega A D^-1 r ; b_c = aggregate sums of s
+  if (lev0) {
+    resid_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, b, cur, L.r, done);
+    smooth_r_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, L.r, L.dinv, L.omega, L.sv, done);
+    aggsum0_kernel<<<nbk(C.n), ANT, 0, s>>>(make_op0(h), C.d[0], C.d[1], C.n, L.sv, C.b, done);
+  } else {
+    resid_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, cur, L.r, done);
+    smooth_r_kernel<StA><<<g, ANT, 0, s>>>(sta, n, L.r, L.dinv, L.omega, L.sv, done);
+    aggsumS_kernel<<<nbk(C.n), ANT, 0, s>>>(L.d[0], L.d[1], L.d[2], C.d[0], C.d[1], C.n, L.dim,
+                                            L.sv, C.b, done);
+  }
+  HDIV_CUDA_TRY(cudaGetLastError());
+  // coarse correction e_c = B_{l+1} b_c
+  hdiv_status st = vcycle(h, l + 1, C.b, C.e, done, s);
+  if (st != HDIV_OK) return st;
+  const double* ecv = C.e;
+  // prolongate: cur + P e_c -> nxt
+  if (lev0)
+    prolong_kernel<SellA, Agg0><<<g, ANT, 0, s>>>(sa, Agg0{H->agg0}, n, cur, ecv, L.dinv, L.omega, nxt, done);
+  else
+    prolong_kernel<StA, AggS><<<g, ANT, 0, s>>>(sta, AggS{L.d[0], L.d[1], C.d[0], C.d[1]}, n, cur,
+                                                ecv, L.dinv, L.omega, nxt, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  std::swap(cur, nxt);
+  // post-smoothing; the last sweep writes x
+  if (nu == 0) {
+    HDIV_CUDA_TRY(cudaMemcpyAsync(x, cur, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  for (int k = 0; k < nu; ++k) {
+    double* out = (k == nu - 1) ? x : nxt;
+    jac(cur, out);
+    if (k < nu - 1) std::swap(cur, nxt);
+  }
+  HDIV_CUDA_TRY(cudaGetLastError());
+  return HDIV_OK;
+}
+
+hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s) {
+  if (!h->amg) {
+    set_error("AMG hierarchy missing");
+    return HDIV_ERR_UNSUPPORTED;
+  }
+  return vcycle(h, 0, b, x, done, s);
+}
+
+int amg_num_levels(const hdiv_ctx* h) { return h->amg ? (int)h->amg->L.size() : 0; }
+
+hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, double* omega,
+                           const double** st) {
+  if (!h->amg || l < 0 || l >= (int)h->amg->L.size()) {
+    set_error("AMG level out of range");
+    return HDIV_ERR_SHAPE;
+  }
+  const AmgLevel& L = h->amg->L[l];
+  for (int a = 0; a < 3; ++a) dims[a] = L.d[a];
+  *n = L.n;
+  *omega = L.omega;
+  *st = L.st;
+  return HDIV_OK;
+}
+
+}  // namespace hdiv

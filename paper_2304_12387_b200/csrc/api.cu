@@ -89,6 +89,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_sval);
   cudaFree(h->d_ecol);
   cudaFree(h->d_minv);
+  amg_free(h);
   cudaFree(h->d_eval);
   cudaFree(h->d_scratch);
   cudaFree(h->d_xbuf);
@@ -125,6 +126,17 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->opts.cheb_degree = (opts && opts->cheb_degree > 0) ? opts->cheb_degree : 4;
   h->opts.cheb_ratio = (opts && opts->cheb_ratio > 0) ? opts->cheb_ratio : 30.0;
   h->opts.kernel = opts ? opts->kernel : 0;
+  h->opts.schur_solver = opts ? opts->schur_solver : HDIV_SCHUR_CHEBYSHEV;
+  h->opts.amg_sweeps = (opts && opts->amg_sweeps > 0) ? opts->amg_sweeps : 2;
+  h->opts.amg_max_coarse = (opts && opts->amg_max_coarse > 0) ? opts->amg_max_coarse : 512;
+  if (h->opts.schur_solver != HDIV_SCHUR_CHEBYSHEV && h->opts.schur_solver != HDIV_SCHUR_AMG) {
+    delete h;
+    return fail(HDIV_ERR_SHAPE, "schur_solver must be HDIV_SCHUR_CHEBYSHEV or HDIV_SCHUR_AMG");
+  }
+  if (h->opts.schur_solver == HDIV_SCHUR_AMG && nranks > 1) {
+    delete h;
+    return fail(HDIV_ERR_UNSUPPORTED, "AMG Schur preconditioner is single-rank in this build");
+  }
   for (int d = 0; d < 3; ++d) { h->N[d] = N[d]; h->NL[d] = N[d]; }
   h->ez0 = mesh->ez_begin; h->ez1 = mesh->ez_end;
   h->NL[last] = h->ez1 - h->ez0;
@@ -354,6 +366,10 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
       ss = comm_setup_schur_ghosts(h, s);
       if (ss != HDIV_OK) { hdiv_destroy(h); return ss; }
     }
+    if (h->opts.schur_solver == HDIV_SCHUR_AMG) {
+      ss = amg_setup(h, s);
+      if (ss != HDIV_OK) { hdiv_destroy(h); return ss; }
+    }
   }
   SETUP_TRY(cudaStreamSynchronize(s));
   SETUP_TRY(cudaGetLastError());
@@ -471,6 +487,28 @@ hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double 
   if (!h || !b || !x) return fail(HDIV_ERR_NULL, "NULL argument");
   if (maxit < 1) return fail(HDIV_ERR_SHAPE, "maxit < 1");
   return minres(h, b, x, rtol, maxit, rep, (cudaStream_t)stream);
+}
+
+hdiv_status hdiv_amg_levels(hdiv_handle h, int* nlevels) {
+  if (!h || !nlevels) return fail(HDIV_ERR_NULL, "NULL argument");
+  if (!h->amg) return fail(HDIV_ERR_UNSUPPORTED, "handle has no AMG hierarchy");
+  *nlevels = amg_num_levels(h);
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_amg_level(hdiv_handle h, int level, int64_t* dims, int64_t* n, double* omega,
+                           double* st, void* stream) {
+  if (!h || !dims || !n || !omega) return fail(HDIV_ERR_NULL, "NULL argument");
+  if (!h->amg) return fail(HDIV_ERR_UNSUPPORTED, "handle has no AMG hierarchy");
+  const double* src = nullptr;
+  hdiv_status st_ = amg_level_info(h, level, dims, n, omega, &src);
+  if (st_ != HDIV_OK) return st_;
+  if (st && src) {
+    const int NS = (h->dim == 3) ? 27 : 9;
+    HDIV_CUDA_TRY(cudaMemcpyAsync(st, src, sizeof(double) * NS * (*n), cudaMemcpyDeviceToDevice,
+                                  (cudaStream_t)stream));
+  }
+  return HDIV_OK;
 }
 
 hdiv_status hdiv_debug_gl_tables(int p, int Q, double* BG, double* HG) {

@@ -45,6 +45,7 @@ enum GeomKind { GEOM_BOX = 0, GEOM_AFFINE = 1, GEOM_TRILINEAR = 2 };
 
 struct MinresWork;   // solver.cu
 struct Comm;         // comm.cu
+struct AmgHier;      // amg.cu
 
 }  // namespace hdiv
 
@@ -85,6 +86,7 @@ struct hdiv_ctx {
   int rank = 0, nranks = 1;
   hdiv::Comm* comm = nullptr;
   hdiv::MinresWork* mw = nullptr;
+  hdiv::AmgHier* amg = nullptr;   // NEXT-1 hierarchy when opts.schur_solver == HDIV_SCHUR_AMG
 };
 
 // error plumbing
@@ -126,6 +128,12 @@ hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t 
 hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit,
                    hdiv_report* rep, cudaStream_t s);
 void minres_free(hdiv_ctx* h);
+hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s);
+void amg_free(hdiv_ctx* h);
+hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s);
+int amg_num_levels(const hdiv_ctx* h);
+hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, double* omega,
+                           const double** st);
 
 // apply modes
 enum { MODE_MASS = 1, MODE_BLOCK = 2 };

@@ -450,6 +450,15 @@ static cudaError_t launch_cheb_stencil(const hdiv_ctx* h, const double* rin, dou
 static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
                               const int* done, cudaStream_t s) {
   MinresWork* mw = h->mw;
+  if (h->opts.schur_solver == HDIV_SCHUR_AMG) {   // NEXT-1: one V-cycle
+    hdiv_status st = amg_vcycle(h, vq, y, done, s);
+    if (st != HDIV_OK) return st;
+    if (part) {
+      dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(y, vq, h->nl2, 0, 0, part, done);
+      HDIV_CUDA_TRY(cudaGetLastError());
+    }
+    return HDIV_OK;
+  }
   const long long n = h->nl2;
   const int k = h->opts.cheb_degree;
   cheb_first_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0], y, n,

@@ -248,3 +248,63 @@ def test_preconditioner_sell_path(name, N, p, monkeypatch):
         eu, eq = _rel(z[:A.n_rt], zo[:A.n_rt]), _rel(z[A.n_rt:], zo[A.n_rt:])
         op.close()
         assert eu < TOL and eq < 1e-11, (stencil, eu, eq)
+
+
+# ---- NEXT-1: AMG V-cycle for S^-1 (reading A9b) ----
+AMG_CASES = [("c2", (5, 4, 3), 3, 16), ("c1", (6, 5), 2, 8), ("c3", (4, 3, 3), 2, 20),
+             ("c5", (5, 5, 3), 2, 30)]
+
+
+@pytest.mark.parametrize("name,N,p,mc", AMG_CASES)
+def test_amg_hierarchy_parity(name, N, p, mc):
+    """Level extents, prolongator weights and Galerkin coarse operators (27/9-point stencils,
+    formed matrix-free per coarse row on the GPU) against the oracle's scipy P^T A P."""
+    from oracle import operators, amg
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    P = amg.AMGSchur(A, nu=2, max_coarse=mc)
+    op = _gpu(pr, schur="amg", amg_max_coarse=mc)
+    assert op.amg_levels() == len(P.levels)
+    for l, lv in enumerate(P.levels):
+        dims, omega, st = op.amg_level(l)
+        assert tuple(dims[:pr.dim]) == lv.dims
+        if lv.omega is not None:
+            assert abs(omega - lv.omega) < 1e-14 * lv.omega
+        if l == 0:
+            continue
+        st = _host(st)
+        n = st.shape[1]
+        ref = lv.A.toarray()
+        dense = np.zeros((n, n))
+        d = lv.dims + (1,) * (3 - len(lv.dims))
+        for i in range(n):
+            X, Y, Z = i % d[0], (i // d[0]) % d[1], i // (d[0] * d[1])
+            for k in range(st.shape[0]):
+                dx, dy, dz = k % 3 - 1, (k // 3) % 3 - 1, (k // 9 - 1) if pr.dim == 3 else 0
+                x, y, z = X + dx, Y + dy, Z + dz
+                if 0 <= x < d[0] and 0 <= y < d[1] and 0 <= z < d[2]:
+                    dense[i, x + d[0] * (y + d[1] * z)] = st[k, i]
+                else:
+                    assert st[k, i] == 0.0
+        assert _rel(dense, ref) < 1e-11
+
+
+@pytest.mark.parametrize("name,N,p,mc", AMG_CASES)
+def test_amg_precond_and_minres_parity(name, N, p, mc):
+    from oracle import operators, solvers
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    P = solvers.BlockDiagPrecond(A, schur="amg", amg_nu=2, amg_max_coarse=mc)
+    op = _gpu(pr, schur="amg", amg_max_coarse=mc)
+    n = A.n_rt + A.n_l2
+    v = random_vector(n, 23)
+    z = _host(op.apply_precond(_dev(v)))
+    zo = P.apply(v)
+    assert _rel(z[:A.n_rt], zo[:A.n_rt]) < TOL
+    assert _rel(z[A.n_rt:], zo[A.n_rt:]) < 1e-11
+    b = A.apply_block(random_vector(n, 1))
+    xo, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=2000)
+    x, rep = op.minres(_dev(b), rtol=1e-12, maxit=2000)
+    assert conv_o and rep.converged
+    assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    assert _rel(_host(x), xo) < 1e-9
