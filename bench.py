@@ -329,34 +329,52 @@ def main():
             torch.cuda.empty_cache()
         result["sweep"] = sweep
 
-    # MINRES time-to-solve (config 2: 8^3 p=3 grad-div, rtol 1e-12, x0 = 0)
+    # MINRES time-to-solve (config 2: 8^3 p=3 grad-div, rtol 1e-12, x0 = 0) with both S^-1
+    # (Chebyshev-Jacobi, reading A10; one AMG V-cycle, P:889-891 / reading A9b), and at the
+    # bench workload (config 4) the AMG solve to 1e-12 plus the per-iteration cost of both
     if not args.no_minres and ws == 1:
         from synth import make_config, random_vector
+        from paper_2304_12387_b200 import from_problem
         pr2 = make_config("c2")
-        op2 = build_operator(pr2, 1, 0, None)
-        xs = torch.from_numpy(random_vector(op2.sizes.n, 2)).cuda()
-        b = op2.apply_block(xs)
-        op2.minres(b, rtol=1e-12, maxit=5000)   # warm-up (graph build)
-        _, rep = op2.minres(b, rtol=1e-12, maxit=5000)
-        result["minres"] = {"workload": "config 2: 8^3 Cartesian, p=3, grad-div alpha=beta=1, "
-                                        "b = A x*, rtol 1e-12 (P:899), x0 = 0",
-                            "iters": rep.iters, "converged": bool(rep.converged),
-                            "time_to_solve_s": rep.t_solve_ms / 1e3,
-                            "preconditioner": "diag(tau M~) + Chebyshev-Jacobi(S~), degree 4"}
-        op2.close()
-        del xs, b
-        torch.cuda.empty_cache()
-        if args.config == "c4":
-            # per-iteration device cost of the whole MINRES iteration at the bench workload
-            op4 = build_operator(pr, 1, 0, None)
-            b4 = torch.rand(op4.sizes.n, dtype=torch.float64, device="cuda")
-            op4.minres(b4, rtol=1e-30, maxit=6)
-            _, r4 = op4.minres(b4, rtol=1e-30, maxit=30)
-            result["minres"]["c4_ms_per_iteration"] = r4.t_solve_ms / max(r4.iters, 1)
-            result["minres"]["c4_iterations_timed"] = r4.iters
-            op4.close()
-            del b4
+        mres = {"workload": "config 2: 8^3 Cartesian, p=3, grad-div alpha=beta=1, "
+                            "b = A x*, rtol 1e-12 (P:899), x0 = 0"}
+        for schur in ("chebyshev", "amg"):
+            op2 = from_problem(pr2, schur=schur)
+            xs = torch.from_numpy(random_vector(op2.sizes.n, 2)).cuda()
+            b = op2.apply_block(xs)
+            op2.minres(b, rtol=1e-12, maxit=5000)   # warm-up (graph build)
+            _, rep = op2.minres(b, rtol=1e-12, maxit=5000)
+            key = "" if schur == "chebyshev" else "amg_"
+            mres[key + "iters"] = rep.iters
+            mres[key + "converged"] = bool(rep.converged)
+            mres[key + "time_to_solve_s"] = rep.t_solve_ms / 1e3
+            op2.close()
+            del xs, b
             torch.cuda.empty_cache()
+        mres["preconditioner"] = "diag(tau M~) + Chebyshev-Jacobi(S~), degree 4"
+        mres["amg_preconditioner"] = ("diag(tau M~) + one smoothed-aggregation V-cycle on S~ "
+                                      "(3^3 aggregates, 2+2 l1-Jacobi sweeps, Galerkin)")
+        result["minres"] = mres
+        if args.config == "c4":
+            for schur in ("chebyshev", "amg"):
+                op4 = from_problem(pr, schur=schur)
+                n4 = op4.sizes.n
+                xs4 = torch.rand(n4, dtype=torch.float64, device="cuda") * 2 - 1
+                b4 = op4.apply_block(xs4)
+                op4.minres(b4, rtol=1e-30, maxit=6)
+                _, r4 = op4.minres(b4, rtol=1e-30, maxit=30)
+                key = "c4_" if schur == "chebyshev" else "c4_amg_"
+                mres[key + "ms_per_iteration"] = r4.t_solve_ms / max(r4.iters, 1)
+                if schur == "amg":   # the full solve at the bench workload (537.7M DOFs)
+                    x4, r5 = op4.minres(b4, rtol=1e-12, maxit=1000)
+                    mres["c4_amg_iters"] = r5.iters
+                    mres["c4_amg_converged"] = bool(r5.converged)
+                    mres["c4_amg_time_to_solve_s"] = r5.t_solve_ms / 1e3
+                    mres["c4_amg_solution_err"] = ((x4 - xs4).abs().max() / xs4.abs().max()).item()
+                    del x4
+                op4.close()
+                del b4, xs4
+                torch.cuda.empty_cache()
 
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(pr)
