@@ -107,6 +107,46 @@ def make_problem(cfg: str, p: int):
     return make_config(cfg, p=p)
 
 
+# V100 local-CG solve times for 100 applies of W^-1 (Table dg-mass-inv), context
+_PAPER_WINV_S = {1: 0.1937, 2: 0.0841, 3: 0.0556, 4: 0.0598, 5: 0.0697, 6: 0.0770}
+
+
+def winv_bench(torch):
+    import numpy as np
+    from synth import make_config, random_vector
+    from paper_2304_12387_b200 import from_problem
+    out = {"workload": "W^-1 q (the (2,2) block) by the fused element-local CG in the GL-nodal "
+                       "basis; config-3 jittered hex mesh sized to ~1.7e6 L2 DOFs, grad-div "
+                       "alpha = 1 (Z = W^-1); 100 applies (Table dg-mass-inv shape, P:773-822)",
+           "paper_v100_context": "P:792-794 local-CG solve x100: " +
+                                 ", ".join(f"p{p} {t} s" for p, t in _PAPER_WINV_S.items())}
+    for p in range(1, 7):
+        ne = max(2, int(round((1.7e6 / p ** 3) ** (1.0 / 3.0))))
+        pr = make_config("c3", N=(ne, ne, ne), p=p)
+        pr.kind = "grad_div"
+        pr.alpha = np.ones(pr.E)
+        pr.beta = np.ones(pr.E)
+        op = from_problem(pr)
+        q = torch.from_numpy(random_vector(op.sizes.n_l2, 5)).cuda()
+        y = torch.empty_like(q)
+        for _ in range(3):
+            op.apply_z(q, y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for _ in range(100):
+            op.apply_z(q, y)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        n = op.sizes.n_l2
+        out[f"p{p}"] = {"N": ne, "l2_dofs": n, "solve_x100_s": t, "GDOF_s": 100 * n / t / 1e9}
+        op.close()
+        del q, y
+        torch.cuda.empty_cache()
+    return out
+
+
 def build_operator(pr, ws, rank, dist, nccl_id=None):
     from paper_2304_12387_b200 import HdivOperator
     if ws == 1:
@@ -375,6 +415,11 @@ def main():
                 op4.close()
                 del b4, xs4
                 torch.cuda.empty_cache()
+
+    # W^-1 benchmark of Table dg-mass-inv (NEXT-2): ~1.7e6 L2 DOFs on a jittered
+    # hex mesh, 100 applications of the (2,2)-block inverse by the fused element-local CG
+    if not args.no_minres and ws == 1:
+        result["winv"] = winv_bench(torch)
 
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(pr)

@@ -118,6 +118,11 @@ hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* y_u, void* s
  * (P:207-211).  x, y: [n_rt + n_l2].  Multi-GPU: includes the interface
  * reverse-add over NCCL. */
 hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* stream);
+/* y_q = Z q: the (2,2) block alone, Z = W_alpha^-1 (grad-div) or gamma_e W^-1 (Darcy, piecewise-
+ * constant gamma), P:235-238, P:535-553 — on every 3D geometry through the element-local CG in
+ * the Gauss-Legendre nodal basis (exact Kronecker case converges in one
+ * step).  q, y_q: DEVICE [n_l2].  3D only (HDIV_ERR_UNSUPPORTED in 2D). */
+hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y_q, void* stream);
 /* Same as hdiv_apply_block with HOST x, y (pinned or pageable): H2D copy, apply, D2H copy on
  * `stream`; blocks until y is on the host (end-to-end path). */
 hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* x_host, double* y_host,

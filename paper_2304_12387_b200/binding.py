@@ -89,6 +89,7 @@ def load_library(path: str = LIB_PATH):
         "hdiv_debug_tables": (C.c_int, [C.c_int, C.c_int] + [dp] * 7),
         "hdiv_debug_gl_tables": (C.c_int, [C.c_int, C.c_int, dp, dp]),
         "hdiv_amg_levels": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+        "hdiv_apply_z": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
         "hdiv_amg_level": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
                                      C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_void_p,
                                      C.c_void_p]),
@@ -242,6 +243,14 @@ class HdivOperator:
         y = self.empty(s.n_rt) if y is None else y
         _check(self.lib.hdiv_apply_divT(self.h, self._ptr(q, s.n_l2), self._ptr(y, s.n_rt),
                                         self._stream_handle(stream)))
+        return y
+
+    def apply_z(self, q, y=None, stream=None):
+        """y = Z q, the (2,2) block alone (3D; element-local CG for W^-1)."""
+        s = self.sizes
+        y = self.empty(s.n_l2) if y is None else y
+        _check(self.lib.hdiv_apply_z(self.h, self._ptr(q, s.n_l2), self._ptr(y, s.n_l2),
+                                     self._stream_handle(stream)))
         return y
 
     def apply_block(self, x, y=None, stream=None):

@@ -89,6 +89,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_sval);
   cudaFree(h->d_ecol);
   cudaFree(h->d_minv);
+  cudaFree(h->d_zcoef);
   amg_free(h);
   cudaFree(h->d_eval);
   cudaFree(h->d_scratch);
@@ -326,6 +327,15 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   SETUP_TRY(cudaMalloc(&h->d_vert, sizeof(double) * V.size()));
   SETUP_TRY(cudaMalloc(&h->d_coef, sizeof(double) * 4 * E));
   SETUP_TRY(cudaMalloc(&h->d_c2, sizeof(double) * E));
+  if (dim == 3) {   // {mass weight, s_e} for the Z-only path (any geometry)
+    std::vector<double> zc(4 * E, 0.0);
+    for (int64_t e = 0; e < E; ++e) {
+      zc[4 * e] = mw[e];
+      zc[4 * e + 1] = (kind == HDIV_GRAD_DIV) ? 1.0 / c2[e] : c2[e];
+    }
+    SETUP_TRY(cudaMalloc(&h->d_zcoef, sizeof(double) * 4 * E));
+    SETUP_TRY(cudaMemcpy(h->d_zcoef, zc.data(), sizeof(double) * 4 * E, cudaMemcpyHostToDevice));
+  }
   SETUP_TRY(cudaMalloc(&h->d_mdiag, sizeof(double) * h->nrt));
   SETUP_TRY(cudaMalloc(&h->d_ctil, sizeof(double) * h->nl2));
   SETUP_TRY(cudaMemcpyAsync(h->d_vert, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, s));
@@ -414,6 +424,13 @@ hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* yu, void* st
 hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* stream) {
   if (!h || !x || !y) return fail(HDIV_ERR_NULL, "NULL argument");
   HDIV_CUDA_TRY(apply_block_dev(h, x, y, nullptr, (cudaStream_t)stream));
+  return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y, void* stream) {
+  if (!h || !q || !y) return fail(HDIV_ERR_NULL, "NULL argument");
+  if (h->dim != 3) return fail(HDIV_ERR_UNSUPPORTED, "apply_z is 3D only");
+  HDIV_CUDA_TRY(launch_trilinear_apply(h, q, y, MODE_ZONLY, nullptr, (cudaStream_t)stream));
   return HDIV_OK;
 }
 

@@ -71,6 +71,7 @@ struct hdiv_ctx {
   double* d_mdiag = nullptr;      // M~ (assembled, interface-summed)
   double* d_ctil = nullptr;       // C~
   double* d_c2 = nullptr;         // per element alpha (grad-div) | gamma (Darcy)
+  double* d_zcoef = nullptr;      // 3D: per element {mass weight, s_e = 1/alpha | gamma, 0, 0}
   double* d_sdinv = nullptr;      // 1 / diag(S~)
   int64_t* d_srow = nullptr;      // S~ CSR (local rows; ghost columns >= nl2 for multi-GPU)
   int32_t* d_scol = nullptr;
@@ -136,5 +137,5 @@ hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, 
                            const double** st);
 
 // apply modes
-enum { MODE_MASS = 1, MODE_BLOCK = 2 };
+enum { MODE_MASS = 1, MODE_BLOCK = 2, MODE_ZONLY = 3 };
 }  // namespace hdiv

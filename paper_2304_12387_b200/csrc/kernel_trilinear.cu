@@ -115,8 +115,10 @@ struct TG {   // per-component layouts at every stage
   static constexpr int SL = L2::SIZE;
 };
 
-template <int P, int NT, bool BLOCK>
+// MODE 0: y_u = M u ; 1: block apply ; 2: y = Z q only (the (2,2) block, W^-1 benchmark)
+template <int P, int NT, int MODE>
 __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_constant__ Tab1D tab) {
+  constexpr bool BLOCK = (MODE == 1), ZONLY = (MODE == 2), HASQ = (MODE >= 1);
   using T = TG<P>;
   constexpr int Q = P + 2;
   constexpr int NQ = Q * Q * Q;
@@ -133,8 +135,8 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
 #define sB(c) (sreg + (c) * T::SB)
 #define sA(c) (sreg + R1 + (c) * T::SA)
 #define sV(c) (sreg + R1 + (c) * T::SV)
-  __shared__ double sq[BLOCK ? T::SL : 1], sy[BLOCK ? P3 : 1], sz1[BLOCK ? T::SL : 1],
-      sz2[BLOCK ? T::SL : 1];
+  __shared__ double sq[HASQ ? T::SL : 1], sy[BLOCK ? P3 : 1], sz1[HASQ ? T::SL : 1],
+      sz2[HASQ ? T::SL : 1];
   __shared__ double scoef[2];
 
   const int tid = threadIdx.x;
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     sX[i] = a.vert[g * 3 + d];
   }
   // gather u per component (compile-time extents, i fastest; padded smem layouts)
-  {
+  if constexpr (!ZONLY) {
     const long long gx = a.off[0] + (long long)ex * P + (nx + 1) * ((long long)ey * P + ny * (long long)ez * P);
     const long long gy = a.off[1] + (long long)ex * P + nx * ((long long)ey * P + (ny + 1) * (long long)ez * P);
     const long long gz = a.off[2] + (long long)ex * P + nx * ((long long)ey * P + ny * (long long)ez * P);
@@ -168,8 +170,8 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       su(2)[li + T::U2::S1 * lj + T::U2::S2 * lk] = a.x[gz + li + nx * (lj + ny * lk)];
     }
   }
-  if constexpr (BLOCK) {
-    const double* q = a.x + a.nrt;
+  if constexpr (HASQ) {
+    const double* q = ZONLY ? a.x : a.x + a.nrt;
     for (int i = tid; i < P3; i += NT) {
       const int A = i % P, B = (i / P) % P, C = i / (P * P);
       sq[A + T::L2::S1 * B + T::L2::S2 * C] = q[e * P3 + i];
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
           (1 - s) * t * (X(0, 1, 1) - X(0, 1, 0)) + s * t * (X(1, 1, 1) - X(1, 1, 0));
     sJ[c][pr][d] = v;
   }
+  if constexpr (!ZONLY) {
   // ---- forward: axis 0, 1, 2 (3 components per stage), + D u and Z q~ ----
   lines<NT, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0>(su(0), sA(0), tab);
   lines<NT, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1>(su(1), sA(1), tab);
@@ -289,8 +292,9 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       put(a.y + gz + li + nx * (lj + ny * lk), v, lk);
     }
   }
-  if constexpr (BLOCK) {
-    if (a.has_z) {
+  }  // !ZONLY
+  if constexpr (HASQ) {
+    if (ZONLY || a.has_z) {
       // ---- Z q~ = s_e W_1^-1 q~ (s_e = 1/alpha | gamma) by a fused
       //      element-local PCG in the Gauss-Legendre nodal basis with Jacobi preconditioning
       //      (P:606-609): W_h^-1 = H W_g^-1 H^T, W_g = H^T W_h H, H = HG^{(x)3}.
@@ -393,38 +397,146 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       lines<NT, P, P, P, 2, P, TB_HG, true, L2, L2>(vp, sz1, tab);
       __syncthreads();
     }
-    double* yq = a.y + a.nrt;
     const double z = scoef[1];
-    for (int i = tid; i < P3; i += NT) {
-      const int A = i % P, B = (i / P) % P, C = i / (P * P);
-      yq[e * P3 + i] = a.has_z ? sy[i] - z * sz1[A + T::L2::S1 * B + T::L2::S2 * C] : sy[i];
+    if constexpr (ZONLY) {
+      for (int i = tid; i < P3; i += NT) {
+        const int A = i % P, B = (i / P) % P, C = i / (P * P);
+        a.y[e * P3 + i] = z * sz1[A + T::L2::S1 * B + T::L2::S2 * C];
+      }
+    } else {
+      double* yq = a.y + a.nrt;
+      for (int i = tid; i < P3; i += NT) {
+        const int A = i % P, B = (i / P) % P, C = i / (P * P);
+        yq[e * P3 + i] = a.has_z ? sy[i] - z * sz1[A + T::L2::S1 * B + T::L2::S2 * C] : sy[i];
+      }
     }
   }
 }
 
-template <int P, bool BLOCK>
+// Z q for p <= 2: one thread per element assembles W^e = sum_q (w_q / det J_q) psi psi^T
+// (P^3 x P^3, P:117/P:135 with the histopolation tensor basis) and solves it by Cholesky in
+// registers — the paper's "explicit inverse for p <= 2" regime, where a
+// 64-thread CTA per element would leave most lanes idle.
+template <int P>
+__global__ void __launch_bounds__(128) tri_z_direct_kernel(const TriArgs a,
+                                                           const __grid_constant__ Tab1D tab,
+                                                           long long E) {
+  constexpr int Q = P + 2, N = P * P * P;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const long long NLx = a.NL[0], NLy = a.NL[1];
+  const long long ex = e % NLx, ey = (e / NLx) % NLy, ez = e / (NLx * NLy);
+  double X[8][3];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const long long g = ((ez + (v >> 2)) * (NLy + 1) + (ey + ((v >> 1) & 1))) * (NLx + 1) + (ex + (v & 1));
+#pragma unroll
+    for (int d = 0; d < 3; ++d) X[v][d] = a.vert[g * 3 + d];
+  }
+  double W[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) W[i][j] = 0.0;
+#pragma unroll 1
+  for (int qz = 0; qz < Q; ++qz)
+#pragma unroll 1
+    for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        const double xh = tab.xq[qx], yh = tab.xq[qy], zh = tab.xq[qz];
+        double J[3][3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          J[d][0] = (1 - yh) * (1 - zh) * (X[1][d] - X[0][d]) + yh * (1 - zh) * (X[3][d] - X[2][d]) +
+                    (1 - yh) * zh * (X[5][d] - X[4][d]) + yh * zh * (X[7][d] - X[6][d]);
+          J[d][1] = (1 - xh) * (1 - zh) * (X[2][d] - X[0][d]) + xh * (1 - zh) * (X[3][d] - X[1][d]) +
+                    (1 - xh) * zh * (X[6][d] - X[4][d]) + xh * zh * (X[7][d] - X[5][d]);
+          J[d][2] = (1 - xh) * (1 - yh) * (X[4][d] - X[0][d]) + xh * (1 - yh) * (X[5][d] - X[1][d]) +
+                    (1 - xh) * yh * (X[6][d] - X[2][d]) + xh * yh * (X[7][d] - X[3][d]);
+        }
+        const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                           J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                           J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+        const double g = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] / det;
+        double phi[N];
+#pragma unroll
+        for (int c = 0; c < P; ++c)
+#pragma unroll
+          for (int b = 0; b < P; ++b)
+#pragma unroll
+            for (int aa = 0; aa < P; ++aa)
+              phi[aa + P * (b + P * c)] = tab.Bh[qx][aa] * tab.Bh[qy][b] * tab.Bh[qz][c];
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) W[i][j] = fma(g * phi[i], phi[j], W[i][j]);
+      }
+  // Cholesky (lower) in place, then forward / backward substitution
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double d = W[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= W[j][k] * W[j][k];
+    d = sqrt(d);
+    W[j][j] = d;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      double v = W[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= W[i][k] * W[j][k];
+      W[i][j] = v / d;
+    }
+  }
+  double y[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = a.x[e * N + i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v -= W[i][k] * y[k];
+    y[i] = v / W[i][i];
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    double v = y[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) v -= W[k][i] * y[k];
+    y[i] = v / W[i][i];
+  }
+  const double z = a.coef[4 * e + 1];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a.y[e * N + i] = z * y[i];
+}
+
+template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
   constexpr int NT = 64;
   TriArgs a;
-  a.x = x; a.y = y; a.vert = h->d_vert; a.coef = h->d_coef;
+  a.x = x; a.y = y;
+  a.vert = h->d_vert;
+  a.coef = (MODE == 2) ? h->d_zcoef : h->d_coef;
   for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
   a.nrt = h->nrt;
   a.has_z = h->has_z ? 1 : 0;
   a.skip = skip;
-  tri_kernel<P, NT, BLOCK><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
+  if constexpr (MODE == 2 && P <= 2) {
+    tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
+    return cudaGetLastError();
+  }
+  tri_kernel<P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
 }
 
-template <bool BLOCK>
+template <int MODE>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k, cudaStream_t s) {
   switch (h->p) {
-    case 1: return launch_p<1, BLOCK>(h, x, y, k, s);
-    case 2: return launch_p<2, BLOCK>(h, x, y, k, s);
-    case 3: return launch_p<3, BLOCK>(h, x, y, k, s);
-    case 4: return launch_p<4, BLOCK>(h, x, y, k, s);
-    case 5: return launch_p<5, BLOCK>(h, x, y, k, s);
-    case 6: return launch_p<6, BLOCK>(h, x, y, k, s);
+    case 1: return launch_p<1, MODE>(h, x, y, k, s);
+    case 2: return launch_p<2, MODE>(h, x, y, k, s);
+    case 3: return launch_p<3, MODE>(h, x, y, k, s);
+    case 4: return launch_p<4, MODE>(h, x, y, k, s);
+    case 5: return launch_p<5, MODE>(h, x, y, k, s);
+    case 6: return launch_p<6, MODE>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -434,10 +546,11 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
 // y (RT part zeroed here) = M u  /  [M u + D^T q ; D u - Z q], 3D, any trilinear geometry
 cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                    const int* skip, cudaStream_t s) {
+  if (mode == MODE_ZONLY) return dispatch<2>(h, x, y, skip, s);   // y (L2) fully written
   cudaError_t e = cudaMemsetAsync(y, 0, sizeof(double) * h->nrt, s);
   if (e != cudaSuccess) return e;
-  if (mode == MODE_BLOCK) return dispatch<true>(h, x, y, skip, s);
-  return dispatch<false>(h, x, y, skip, s);
+  if (mode == MODE_BLOCK) return dispatch<1>(h, x, y, skip, s);
+  return dispatch<0>(h, x, y, skip, s);
 }
 
 }  // namespace hdiv

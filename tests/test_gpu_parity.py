@@ -308,3 +308,15 @@ def test_amg_precond_and_minres_parity(name, N, p, mc):
     assert conv_o and rep.converged
     assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
     assert _rel(_host(x), xo) < 1e-9
+
+
+@pytest.mark.parametrize("name,N,p", [("c3gd", (3, 2, 2), 2), ("c3gd", (2, 2, 3), 5), ("c3g", (2, 3, 2), 4),
+                                      ("c2", (3, 2, 2), 3), ("c5", (5, 5, 3), 1)])
+def test_apply_z_parity(name, N, p):
+    """Z q alone (W^-1 through the local CG on any 3D geometry) against the oracle's Cholesky."""
+    from oracle import operators
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr, with_schur=False)
+    op = _gpu(pr)
+    q = random_vector(A.n_l2, 29)
+    assert _rel(_host(op.apply_z(_dev(q))), A.apply_Z(q)) < TOL
