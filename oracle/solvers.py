@@ -140,3 +140,95 @@ def minres(apply_A, apply_Pinv, b, rtol=1e-12, maxit=1000):
             conv = True
             break
     return x, it, conv, hist
+
+
+# --------------------------------------------------------------------------------------------
+# NEXT-4: block-triangular preconditioner + GMRES (P:423-438 Remark).
+class BlockTriPrecond:
+    """B = [tau M~, D^T; 0, -S^]  (upper block-triangular, P:427-433 with the sign of this
+    build's A = [M, D^T; D, -Z], whose Schur complement is -(Z + D M^-1 D^T) = -S).
+    B^-1 v:  z_q = -S^-1 v_q ;  z_u = (tau M~)^-1 (v_u - D^T z_q).
+    With exact blocks (M, S) B^-1 A has the single eigenvalue 1 and a degree-2 minimal
+    polynomial, so GMRES converges in at most two iterations."""
+
+    def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, schur="chebyshev", exact_blocks=False,
+                 amg_nu=2, amg_max_coarse=512):
+        self.asm, self.tau = asm, tau
+        self.diag = BlockDiagPrecond(asm, tau=tau, degree=degree, ratio=ratio, schur=schur,
+                                     exact_blocks=exact_blocks, amg_nu=amg_nu,
+                                     amg_max_coarse=amg_max_coarse)
+        self.exact_blocks = exact_blocks
+        self.n_rt = asm.n_rt
+
+    def apply(self, v):
+        vu, vq = v[: self.n_rt], v[self.n_rt:]
+        d = self.diag
+        if self.exact_blocks:
+            zq = -np.linalg.solve(d.Sfull, vq)
+            zu = np.linalg.solve(self.tau * d.Mfull, vu - self.asm.D.T @ zq)
+        else:
+            zq = -d.apply(np.concatenate([np.zeros(self.n_rt), vq]))[self.n_rt:]
+            zu = (vu - self.asm.D.T @ zq) / (self.tau * self.asm.Mdiag)
+        return np.concatenate([zu, zq])
+
+
+def gmres(apply_A, apply_Binv, b, rtol=1e-12, restart=30, maxit=1000):
+    """Right-preconditioned restarted GMRES(m), x0 = 0 (Saad, Iterative Methods, Alg. 9.5):
+    Arnoldi on A B^-1 with classical Gram-Schmidt applied twice, Givens rotations on the
+    Hessenberg matrix; stops when the residual of the least-squares problem |g_{j+1}| (= the
+    true residual norm ||b - A x|| in exact arithmetic, right preconditioning) <= rtol ||b||.
+    Returns x, total iterations, converged, residual history."""
+    n = len(b)
+    x = np.zeros(n)
+    bnorm = float(np.linalg.norm(b))
+    if bnorm == 0.0:
+        return x, 0, True, [0.0]
+    hist = [1.0]
+    it = 0
+    while it < maxit:
+        r = b - apply_A(x)
+        beta = float(np.linalg.norm(r))
+        if beta <= rtol * bnorm:
+            return x, it, True, hist
+        m = restart
+        V = np.zeros((m + 1, n))
+        H = np.zeros((m + 1, m))
+        cs, sn = np.zeros(m), np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        V[0] = r / beta
+        k = 0
+        conv = False
+        for j in range(m):
+            w = apply_A(apply_Binv(V[j]))
+            for _ in range(2):                      # CGS2
+                h = V[: j + 1] @ w
+                w = w - V[: j + 1].T @ h
+                H[: j + 1, j] += h
+            H[j + 1, j] = float(np.linalg.norm(w))
+            if H[j + 1, j] > 0.0:
+                V[j + 1] = w / H[j + 1, j]
+            for i in range(j):                       # previous rotations
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = math.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = H[j, j] / den, H[j + 1, j] / den
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            it += 1
+            k = j + 1
+            hist.append(abs(g[j + 1]) / bnorm)
+            if abs(g[j + 1]) <= rtol * bnorm or it >= maxit:
+                conv = abs(g[j + 1]) <= rtol * bnorm
+                break
+        # x += B^-1 V_k y,  H[:k,:k] y = g[:k]  (back substitution)
+        y = np.zeros(k)
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:k]) / H[i, i]
+        x = x + apply_Binv(V[:k].T @ y)
+        if conv:
+            return x, it, True, hist
+    return x, it, False, hist
