@@ -155,6 +155,19 @@ hdiv_status hdiv_apply_precond(hdiv_handle h, const double* v, double* z, void* 
 hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double rtol,
                               int maxit, hdiv_report* report, void* stream);
 
+/* NEXT-4 (P:423-438 Remark): z = B^-1 v with the block upper-triangular preconditioner
+ * B = [tau M~, D^T; 0, -S^] (S^-1 per options.schur_solver):  z_q = -S^-1 v_q,
+ * z_u = (tau M~)^-1 (v_u - D^T z_q).  v, z: DEVICE [n_rt + n_l2].  Single rank. */
+hdiv_status hdiv_apply_precond_tri(hdiv_handle h, const double* v, double* z, void* stream);
+
+/* NEXT-4: right-preconditioned restarted GMRES(restart) with B above, x0 = 0;
+ * Arnoldi with classical Gram-Schmidt applied twice, Givens rotations; stops when the
+ * least-squares residual (the true residual norm, right preconditioning) <= rtol ||b||.
+ * restart <= 64; the (restart+1) basis vectors are allocated on first use (8 (restart+1) n
+ * bytes).  Synchronous (host-driven Hessenberg algebra).  Single rank. */
+hdiv_status hdiv_gmres_solve(hdiv_handle h, const double* b, double* x, double rtol, int maxit,
+                             int restart, hdiv_report* report, void* stream);
+
 /* Multi-GPU helper: writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the
  * bytes, e.g. with torch.distributed, before every rank calls hdiv_setup).  NCCL is resolved
  * at run time (dlopen); HDIV_ERR_NCCL if it is unavailable. */

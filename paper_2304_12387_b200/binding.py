@@ -90,6 +90,9 @@ def load_library(path: str = LIB_PATH):
         "hdiv_debug_gl_tables": (C.c_int, [C.c_int, C.c_int, dp, dp]),
         "hdiv_amg_levels": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
         "hdiv_apply_z": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "hdiv_apply_precond_tri": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "hdiv_gmres_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                       C.c_int, C.POINTER(Report), C.c_void_p]),
         "hdiv_amg_level": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
                                      C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_void_p,
                                      C.c_void_p]),
@@ -333,6 +336,23 @@ class HdivOperator:
         rep = Report()
         _check(self.lib.hdiv_minres_solve(self.h, self._ptr(b, n), self._ptr(x, n), rtol, maxit,
                                           C.byref(rep), self._stream_handle(stream)))
+        return x, rep
+
+    def apply_precond_tri(self, v, z=None, stream=None):
+        """z = B^-1 v, B = [tau M~, D^T; 0, -S^] (NEXT-4)."""
+        n = self.sizes.n
+        z = self.empty(n) if z is None else z
+        _check(self.lib.hdiv_apply_precond_tri(self.h, self._ptr(v, n), self._ptr(z, n),
+                                               self._stream_handle(stream)))
+        return z
+
+    def gmres(self, b, x=None, rtol=1e-12, maxit=1000, restart=30, stream=None):
+        """Right-preconditioned GMRES(restart) with the block-triangular preconditioner."""
+        n = self.sizes.n
+        x = self.empty(n) if x is None else x
+        rep = Report()
+        _check(self.lib.hdiv_gmres_solve(self.h, self._ptr(b, n), self._ptr(x, n), rtol, maxit,
+                                         restart, C.byref(rep), self._stream_handle(stream)))
         return x, rep
 
     def amg_levels(self) -> int:

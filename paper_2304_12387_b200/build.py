@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-diag-suppress", "177", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["tables.cpp", "kernel_affine.cu", "kernel_general.cu", "kernel_trilinear.cu", "kernel_sparse.cu", "amg.cu",
+SOURCES = ["tables.cpp", "kernel_affine.cu", "kernel_general.cu", "kernel_trilinear.cu", "kernel_sparse.cu", "amg.cu", "gmres.cu",
            "solver.cu", "comm.cu", "api.cu"]
 
 

@@ -91,6 +91,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_minv);
   cudaFree(h->d_zcoef);
   amg_free(h);
+  gmres_free(h);
   cudaFree(h->d_eval);
   cudaFree(h->d_scratch);
   cudaFree(h->d_xbuf);
@@ -432,6 +433,19 @@ hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y, void* stream
   if (h->dim != 3) return fail(HDIV_ERR_UNSUPPORTED, "apply_z is 3D only");
   HDIV_CUDA_TRY(launch_trilinear_apply(h, q, y, MODE_ZONLY, nullptr, (cudaStream_t)stream));
   return HDIV_OK;
+}
+
+hdiv_status hdiv_apply_precond_tri(hdiv_handle h, const double* v, double* z, void* stream) {
+  if (!h || !v || !z) return fail(HDIV_ERR_NULL, "NULL argument");
+  return apply_precond_tri(h, v, z, (cudaStream_t)stream);
+}
+
+hdiv_status hdiv_gmres_solve(hdiv_handle h, const double* b, double* x, double rtol, int maxit,
+                             int restart, hdiv_report* report, void* stream) {
+  if (!h || !b || !x) return fail(HDIV_ERR_NULL, "NULL argument");
+  if (!(rtol > 0) || maxit < 1 || restart < 1 || restart > 64)
+    return fail(HDIV_ERR_SHAPE, "gmres: rtol > 0, maxit >= 1, 1 <= restart <= 64 required");
+  return gmres(h, b, x, rtol, maxit, restart, report, (cudaStream_t)stream);
 }
 
 hdiv_status hdiv_apply_launches(hdiv_handle h, int* n) {

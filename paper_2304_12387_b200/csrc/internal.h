@@ -46,6 +46,7 @@ enum GeomKind { GEOM_BOX = 0, GEOM_AFFINE = 1, GEOM_TRILINEAR = 2 };
 struct MinresWork;   // solver.cu
 struct Comm;         // comm.cu
 struct AmgHier;      // amg.cu
+struct GmresWork;    // gmres.cu
 
 }  // namespace hdiv
 
@@ -88,6 +89,7 @@ struct hdiv_ctx {
   hdiv::Comm* comm = nullptr;
   hdiv::MinresWork* mw = nullptr;
   hdiv::AmgHier* amg = nullptr;   // NEXT-1 hierarchy when opts.schur_solver == HDIV_SCHUR_AMG
+  hdiv::GmresWork* gw = nullptr;  // NEXT-4 Krylov basis (lazily allocated)
 };
 
 // error plumbing
@@ -129,6 +131,11 @@ hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t 
 hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit,
                    hdiv_report* rep, cudaStream_t s);
 void minres_free(hdiv_ctx* h);
+hdiv_status schur_inv_apply(hdiv_ctx* h, const double* vq, double* y, cudaStream_t s);
+hdiv_status apply_precond_tri(hdiv_ctx* h, const double* v, double* z, cudaStream_t s);
+hdiv_status gmres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit, int restart,
+                  hdiv_report* rep, cudaStream_t s);
+void gmres_free(hdiv_ctx* h);
 hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s);
 void amg_free(hdiv_ctx* h);
 hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s);

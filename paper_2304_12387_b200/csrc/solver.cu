@@ -499,6 +499,13 @@ hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t 
   return cheb_apply(h, v + h->nrt, z + h->nrt, nullptr, nullptr, s);
 }
 
+// y = S^-1 vq (Chebyshev or AMG per options), for other solvers (GMRES)
+hdiv_status schur_inv_apply(hdiv_ctx* h, const double* vq, double* y, cudaStream_t s) {
+  hdiv_status st = ensure_work(h);
+  if (st != HDIV_OK) return st;
+  return cheb_apply(h, vq, y, nullptr, nullptr, s);
+}
+
 // local scalar -> (all-gather) -> glob
 static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
                                  cudaStream_t s) {

@@ -320,3 +320,29 @@ def test_apply_z_parity(name, N, p):
     op = _gpu(pr)
     q = random_vector(A.n_l2, 29)
     assert _rel(_host(op.apply_z(_dev(q))), A.apply_Z(q)) < TOL
+
+
+
+# ---- NEXT-4: block-triangular preconditioner + GMRES ----
+@pytest.mark.parametrize("name,N,p,schur", [("c1", None, None, "chebyshev"), ("c2", (3, 2, 2), 3, "chebyshev"),
+                                            ("c3", (2, 2, 2), 2, "amg"), ("c5", (5, 5, 3), 1, "amg")])
+def test_gmres_triangular_parity(name, N, p, schur):
+    from oracle import operators, solvers
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    mc = 16
+    B = solvers.BlockTriPrecond(A, schur=schur, amg_max_coarse=mc)
+    op = _gpu(pr, schur=schur, amg_max_coarse=mc)
+    n = A.n_rt + A.n_l2
+    v = random_vector(n, 41)
+    z = _host(op.apply_precond_tri(_dev(v)))
+    zo = B.apply(v)
+    assert _rel(z[:A.n_rt], zo[:A.n_rt]) < 1e-11
+    assert _rel(z[A.n_rt:], zo[A.n_rt:]) < 1e-11
+    b = A.apply_block(random_vector(n, 43))
+    xo, it_o, conv_o, _ = solvers.gmres(A.apply_block, B.apply, b, rtol=1e-10, restart=20,
+                                        maxit=2000)
+    x, rep = op.gmres(_dev(b), rtol=1e-10, maxit=2000, restart=20)
+    assert conv_o and rep.converged
+    assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    assert _rel(_host(x), xo) < 1e-7
