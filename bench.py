@@ -395,6 +395,24 @@ def main():
         mres["amg_preconditioner"] = ("diag(tau M~) + one smoothed-aggregation V-cycle on S~ "
                                       "(3^3 aggregates, 2+2 l1-Jacobi sweeps, Galerkin)")
         result["minres"] = mres
+        # NEXT-4: GMRES(30) + block-triangular vs MINRES + block-diagonal (both with the AMG
+        # S^-1) on config 5 at p=4 (graded two-material, 3.7M DOFs)
+        pr5 = make_config("c5", p=4)
+        op5 = from_problem(pr5, schur="amg")
+        xs5 = torch.from_numpy(random_vector(op5.sizes.n, 5)).cuda()
+        b5 = op5.apply_block(xs5)
+        _, rm = op5.minres(b5, rtol=1e-12, maxit=5000)
+        _, rg = op5.gmres(b5, rtol=1e-12, maxit=5000, restart=30)
+        result["gmres"] = {"workload": "config 5 (24x24x25 graded two-material, p=4, grad-div), "
+                                       "S^-1 = AMG V-cycle, rtol 1e-12, x0 = 0",
+                           "gmres_tri_iters": rg.iters, "gmres_tri_time_s": rg.t_solve_ms / 1e3,
+                           "gmres_converged": bool(rg.converged),
+                           "minres_diag_iters": rm.iters, "minres_diag_time_s": rm.t_solve_ms / 1e3,
+                           "note": "GMRES stops on the true residual (right preconditioning), "
+                                   "MINRES on the preconditioned residual (reading A8)"}
+        op5.close()
+        del xs5, b5
+        torch.cuda.empty_cache()
         if args.config == "c4":
             for schur in ("chebyshev", "amg"):
                 op4 = from_problem(pr, schur=schur)
