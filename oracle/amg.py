@@ -61,9 +61,12 @@ def _coarse_grid(dims, agg):
     return tuple((d + agg - 1) // agg for d in dims)
 
 
-def build_hierarchy(S, coords, dims, agg=3, max_coarse=512, max_levels=25, coarse_solve=True):
+def build_hierarchy(S, coords, dims, agg=3, max_coarse=512, max_levels=25, coarse_solve=True,
+                    pin=False):
     """Levels l = 0..L with A_0 = S; coords: the grid coordinates of the rows of S.
-    coarse_solve=False skips the coarsest inverse (tests on singular operators)."""
+    coarse_solve=False skips the coarsest inverse (tests on singular operators).
+    pin=True (singular S~ of the pure-Neumann problem, NEXT-3, reading A21): the coarsest
+    solve inverts A_L with its last row and column replaced by the identity's."""
     levels = [Level(S, dims, coords)]
     while True:
         lv = levels[-1]
@@ -93,7 +96,12 @@ def build_hierarchy(S, coords, dims, agg=3, max_coarse=512, max_levels=25, coars
             rem = rem // cd[a]
         levels.append(Level(Ac, cd, np.stack(ccoords, axis=1)))
     if coarse_solve:
-        levels[-1].Ainv = np.linalg.inv(levels[-1].A.toarray())
+        Ad = levels[-1].A.toarray()
+        if pin:
+            Ad[-1, :] = 0.0
+            Ad[:, -1] = 0.0
+            Ad[-1, -1] = 1.0
+        levels[-1].Ainv = np.linalg.inv(Ad)
     return levels
 
 
@@ -117,10 +125,10 @@ def vcycle(levels, b, nu=1, l=0):
 class AMGSchur:
     """S^-1 = one V-cycle on S~ (drop-in for the Chebyshev polynomial in BlockDiagPrecond)."""
 
-    def __init__(self, asm, nu=2, max_coarse=512):
+    def __init__(self, asm, nu=2, max_coarse=512, pin=False):
         coords = l2_cell_coords(asm.dim, asm.N, asm.p)
         dims = tuple(int(asm.N[a]) * asm.p for a in range(asm.dim))
-        self.levels = build_hierarchy(asm.S, coords, dims, max_coarse=max_coarse)
+        self.levels = build_hierarchy(asm.S, coords, dims, max_coarse=max_coarse, pin=pin)
         self.nu = nu
 
     def __call__(self, r):

@@ -6,6 +6,10 @@ P:451-456 eq.(approx-schur): M~ = diag(M_beta), W~ = diag(W_alpha), S~ = W~^-1 +
 P:466-471 eq.(approx-schur-entries) entry formula of S~
 P:555  Darcy: W^-1 W_gamma W^-1 approximated by the product of the (reciprocal) diagonals
 P:886  S~ via the sparse triple product D M~^-1 D^T
+NEXT-3 (reading A21): essential flux conditions on whole domain sides by
+elimination — identity rows/columns for the prescribed RT DOFs (u_b), which are dropped from
+D's columns and from the face sets F(i) of S~; M~ = 1 there (the diagonal of the eliminated
+(1,1) block).
 
 Everything is assembled from dense element matrices computed by direct
 quadrature (fem.py); library primitives used: scipy.sparse products,
@@ -79,14 +83,23 @@ class Assembled:
                                shape=(self.n_rt, self.n_rt))
         I, J, A = space.divergence_csr(dim, N, p)
         self.D = sp.csr_matrix((A, J, I), shape=(self.n_l2, self.n_rt))
-        self.Dptr, self.Dcol, self.Dval = I, J, A
+        self.Dptr, self.Dcol, self.Dval = I, J, A   # Algorithm 1's D (unmasked)
+        # essential flux sides (NEXT-3): A_hat = [[F M F + B, F D^T], [D F, -Z]], F = diag(free),
+        # B = diag(essential)
+        self.essential = int(getattr(prob, "essential", 0) or 0)
+        self.ess = space.essential_rt_mask(dim, N, p, self.essential)
+        if self.ess.any():
+            Fm = sp.diags((~self.ess).astype(float))
+            self.M = (Fm @ self.M @ Fm + sp.diags(self.ess.astype(float))).tocsr()
+            self.D = (self.D @ Fm).tocsr()
         self.Mdiag = self.M.diagonal().copy()                 # M~
         if prob.kind == "grad_div":
             self.Ctil = 1.0 / self.Wdiag                     # W~^-1
         else:
             self.Ctil = self.Wgdiag / self.Wdiag ** 2        # diag(W)^-1 diag(W_g) diag(W)^-1
         if with_schur:
-            self.S = schur_entry_formula(self.Dptr, self.Dcol, self.Dval, self.Mdiag, self.Ctil)
+            self.S = schur_entry_formula(self.Dptr, self.Dcol, self.Dval, self.Mdiag, self.Ctil,
+                                         skip=self.ess)
 
     # --- block operator -------------------------------
     def apply_Z(self, q):
@@ -111,11 +124,17 @@ class Assembled:
                          [self.D.toarray(), -Zd]])
 
 
-def schur_entry_formula(Dptr, Dcol, Dval, Mdiag, Ctil) -> sp.csr_matrix:
+def schur_entry_formula(Dptr, Dcol, Dval, Mdiag, Ctil, skip=None) -> sp.csr_matrix:
     """S~ from eq.(approx-schur-entries) (P:466-471):
     S_ii = C~_ii + sum_{k in F(i)} 1/M~_kk ; S_ij = -1/M~_kk if i, j share face k.
-    F(i) and the cells of a face are read off the incidence D; columns sorted."""
+    F(i) and the cells of a face are read off the incidence D; columns sorted.
+    skip: faces removed from every F(i) (eliminated essential-flux DOFs, NEXT-3)."""
     n_l2 = len(Dptr) - 1
+    if skip is not None and np.any(skip):
+        keep = ~skip[Dcol]
+        Dcol, Dval = Dcol[keep], Dval[keep]
+        cnt = np.add.reduceat(keep.astype(np.int64), Dptr[:-1]) if len(keep) else np.zeros(0, np.int64)
+        Dptr = np.concatenate([[0], np.cumsum(cnt)])
     cells_of_face = {}
     for i in range(n_l2):
         for t in range(Dptr[i], Dptr[i + 1]):

@@ -38,12 +38,19 @@ class BlockDiagPrecond:
     """P^-1 = diag((tau M~)^-1, S^-1)."""
 
     def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, exact_schur=False, exact_blocks=False,
-                 schur="chebyshev", amg_nu=2, amg_max_coarse=512):
+                 schur="chebyshev", amg_nu=2, amg_max_coarse=512, project_mean=None):
         self.asm, self.tau, self.degree, self.ratio = asm, tau, degree, ratio
+        # NEXT-3 (P:1038-1040): with pure-Neumann (all-essential flux) Darcy and gamma = 0 the
+        # Schur complement is singular with the constants as nullspace, so every application of
+        # S^-1 is followed by an orthogonalization step: subtract the plain mean of the
+        # coefficient vector (reading A11/A21)
+        if project_mean is None:
+            project_mean = bool(getattr(asm.prob, "project_mean", False))
+        self.project_mean = project_mean
         self.amg = None
         if schur == "amg":   # NEXT-1: one AMG V-cycle on S~ (P:889-891, reading A9b)
             from .amg import AMGSchur
-            self.amg = AMGSchur(asm, nu=amg_nu, max_coarse=amg_max_coarse)
+            self.amg = AMGSchur(asm, nu=amg_nu, max_coarse=amg_max_coarse, pin=project_mean)
         self.n_rt = asm.n_rt
         self.exact_schur = exact_schur
         self.exact_blocks = exact_blocks
@@ -74,6 +81,8 @@ class BlockDiagPrecond:
                 zq = self.amg(vq)
             else:
                 zq = chebyshev_jacobi(self.asm.S, vq, self.degree, self.ratio)
+            if self.project_mean:
+                zq = zq - zq.mean()
         return np.concatenate([zu, zq])
 
 
@@ -156,7 +165,7 @@ class BlockTriPrecond:
         self.asm, self.tau = asm, tau
         self.diag = BlockDiagPrecond(asm, tau=tau, degree=degree, ratio=ratio, schur=schur,
                                      exact_blocks=exact_blocks, amg_nu=amg_nu,
-                                     amg_max_coarse=amg_max_coarse)
+                                     amg_max_coarse=amg_max_coarse, project_mean=False)
         self.exact_blocks = exact_blocks
         self.n_rt = asm.n_rt
 

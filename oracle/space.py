@@ -129,3 +129,26 @@ def divergence_csr(dim, N, p):
             Aval[2 * dim * i + k] = s_loc * s_glob
     Iptr[n_l2] = 2 * dim * n_l2
     return Iptr, Jcol, Aval
+
+
+def essential_rt_mask(dim, N, p, sides: int) -> np.ndarray:
+    """Boolean mask of the RT DOFs on the domain sides selected by the bitmask `sides`
+    (bit 2a: the side x_a = min, bit 2a+1: x_a = max; a = 0..dim-1) — the faces where the
+    normal flux u.n is prescribed (essential flux condition, SPE10 P:1035; NEXT-3).
+    In the canonical numbering a face of component c lies on a side of axis c iff its
+    subcell-face coordinate along c is 0 or n_c."""
+    s = sizes(dim, N, p)
+    n, offs = s["n"], s["offs"]
+    mask = np.zeros(s["n_rt"], dtype=bool)
+    for c in range(dim):
+        ext = [n[a] + (1 if a == c else 0) for a in range(dim)]
+        cnt = int(np.prod(ext))
+        idx = np.arange(cnt, dtype=np.int64)
+        # coordinate along c of face r (x fastest)
+        stride = int(np.prod(ext[:c])) if c > 0 else 1
+        coord = (idx // stride) % ext[c]
+        if sides >> (2 * c) & 1:
+            mask[offs[c] + idx[coord == 0]] = True
+        if sides >> (2 * c + 1) & 1:
+            mask[offs[c] + idx[coord == n[c]]] = True
+    return mask

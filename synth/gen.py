@@ -149,6 +149,9 @@ class Problem:
     gamma: Optional[np.ndarray] = None   # Darcy     W_gamma,         per element
     affine: bool = True                  # axis-aligned boxes (generator knows it)
     Q: int = 0                           # 0 -> p+2 (A3)
+    essential: int = 0                   # essential-flux sides bitmask (bit 2a: x_a = min,
+                                         # bit 2a+1: x_a = max), NEXT-3
+    project_mean: bool = False           # orthogonalize after every S^-1
     extra: dict = field(default_factory=dict)
 
     @property
@@ -170,7 +173,7 @@ class Problem:
         return self.E * self.p ** self.dim
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
+CONFIG_NAMES = ("c1", "c2", "c3", "c3s", "c4", "c5")
 
 
 def make_config(name: str, N=None, p=None, seed: int = 0) -> Problem:
@@ -194,6 +197,10 @@ def make_config(name: str, N=None, p=None, seed: int = 0) -> Problem:
         eps = 10.0 ** (-2.0 + 4.0 * counter_uniform(4 + seed, E))
         return Problem("c3", 3, N, p, "darcy", perturbed_vertices(N, 0.2, 3 + seed),
                        eps=eps, gamma=np.zeros(E), affine=False)
+    if name == "c3s":  # SPE10-shaped: c3 with u.n prescribed on every side, gamma = 0,
+        pr = make_config("c3", N=N, p=p, seed=seed)   # singular S~ -> projection
+        pr.name, pr.essential, pr.project_mean = "c3s", (1 << (2 * pr.dim)) - 1, True
+        return pr
     if name == "c4":   # 3D 128^3, p=4, grad-div alpha=beta=1
         N = tuple(N or (128, 128, 128))
         p = p or 4
