@@ -156,6 +156,7 @@ def build_operator(pr, ws, rank, dist, nccl_id=None):
     z0, z1 = slab_bounds(pr.N[pr.dim - 1], ws, rank)
     V, a, b, g, e = slab_inputs(pr, z0, z1)
     return HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b, gamma=g, eps=e,
+                        essential=pr.essential, project_mean=pr.project_mean,
                         slab=(z0, z1), nccl_id=nccl_id, rank=rank, nranks=ws)
 
 

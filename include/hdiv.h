@@ -77,6 +77,20 @@ typedef struct {
                        /* one smoothed-aggregation V-cycle (reading A9b; 1 rank)  */
   int amg_sweeps;      /* l1-Jacobi sweeps before and after the coarse correction; <= 0 => 2 */
   int amg_max_coarse;  /* dense solve once a level has <= this many rows; <= 0 => 512        */
+  /* NEXT-3 (reading A21).  essential_sides: bitmask of domain sides whose RT
+   * DOFs carry an essential (prescribed-flux) condition, eliminated by identity rows and
+   * columns: bit 2a = side x_a = min, bit 2a+1 = side x_a = max (a = 0..dim-1; global sides —
+   * with slabs the library applies the last-axis bits only on the first / last rank).  In
+   * every apply the eliminated DOFs act as zero inputs and their outputs are the identity
+   * (y_b = x_b in hdiv_apply_block / hdiv_apply_mass, 0 in hdiv_apply_divT); M~ = 1 there
+   * and they are dropped from the face sets F(i) of S~.  The caller lifts inhomogeneous
+   * data into b.  0 = natural conditions everywhere (A11). */
+  int essential_sides;
+  /* project_mean != 0: every application of S^-1 is followed by the orthogonalization step
+   * of P:1038-1040 (subtract the mean of the coefficient vector, reading A11) and the AMG
+   * coarsest solve pins its last unknown — for the singular pure-Neumann Darcy problem
+   * (all sides essential, gamma = 0). */
+  int project_mean;
 } hdiv_options;
 
 enum { HDIV_SCHUR_CHEBYSHEV = 0, HDIV_SCHUR_AMG = 1 };
@@ -110,7 +124,8 @@ hdiv_status hdiv_sizes(hdiv_handle h, int64_t* n_rt_local, int64_t* n_l2_local,
 
 /* y_u = M_beta u  (sum-factorised).  u, y_u: [n_rt]. */
 hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* y_u, void* stream);
-/* y_q = D u  (topological +-1).  u: [n_rt], y_q: [n_l2]. */
+/* y_q = D u  (topological +-1).  u: [n_rt], y_q: [n_l2].  Eliminated
+ * essential DOFs (options.essential_sides) act as zero (the (2,1) block D F of A). */
 hdiv_status hdiv_apply_div(hdiv_handle h, const double* u, double* y_q, void* stream);
 /* y_u = D^T q  .  q: [n_l2], y_u: [n_rt]. */
 hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* y_u, void* stream);
@@ -143,7 +158,8 @@ hdiv_status hdiv_assemble_schur_csr(hdiv_handle h, int64_t* row_ptr, int64_t* co
                                     double* val, void* stream);
 /* y = S~ x (the SpMV used inside S^-1).  x, y: [n_l2]. */
 hdiv_status hdiv_apply_schur(hdiv_handle h, const double* x, double* y, void* stream);
-/* D in CSR by Algorithm 1: row_ptr[n_l2+1] (= 2d i), col[2d n_l2], val. */
+/* D in CSR by Algorithm 1: row_ptr[n_l2+1] (= 2d i), col[2d n_l2], val.  Always
+ * the unmasked incidence (essential_sides does not change it). */
 hdiv_status hdiv_export_div_csr(hdiv_handle h, int64_t* row_ptr, int64_t* col, double* val,
                                 void* stream);
 /* z = P^-1 v with P = diag(tau M~, S^), S^-1 = Chebyshev-Jacobi on S~. */

@@ -41,7 +41,8 @@ class Coeffs(C.Structure):
 class Options(C.Structure):
     _fields_ = [("tau", C.c_double), ("cheb_degree", C.c_int), ("cheb_ratio", C.c_double),
                 ("kernel", C.c_int), ("schur_solver", C.c_int), ("amg_sweeps", C.c_int),
-                ("amg_max_coarse", C.c_int)]
+                ("amg_max_coarse", C.c_int), ("essential_sides", C.c_int),
+                ("project_mean", C.c_int)]
 
 
 SCHUR_SOLVERS = {"chebyshev": 0, "amg": 1}
@@ -166,8 +167,8 @@ class HdivOperator:
 
     def __init__(self, dim, N, p, kind, vertices=None, alpha=None, beta=None, gamma=None,
                  eps=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
-                 schur="chebyshev", amg_sweeps=2, amg_max_coarse=512,
-                 slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
+                 schur="chebyshev", amg_sweeps=2, amg_max_coarse=512, essential=0,
+                 project_mean=False, slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
         import torch
         self.lib = load_library()
         self._torch = torch
@@ -188,7 +189,7 @@ class HdivOperator:
         a_, b_, g_, e_ = arr(alpha), arr(beta), arr(gamma), arr(eps)
         co = Coeffs(_dptr(a_), _dptr(b_), _dptr(g_), _dptr(e_), 1.0, 1.0, 0.0, 1.0)
         op = Options(tau, cheb_degree, cheb_ratio, kernel, SCHUR_SOLVERS[schur], amg_sweeps,
-                     amg_max_coarse)
+                     amg_max_coarse, int(essential), int(bool(project_mean)))
         h = C.c_void_p()
         idbuf = None
         if nccl_id is not None:
@@ -389,5 +390,7 @@ class HdivOperator:
 
 def from_problem(prob, **kw) -> HdivOperator:
     """Build an operator from a synth.Problem (inputs only)."""
+    kw.setdefault("essential", getattr(prob, "essential", 0))
+    kw.setdefault("project_mean", getattr(prob, "project_mean", False))
     return HdivOperator(prob.dim, prob.N, prob.p, prob.kind, vertices=prob.vertices,
                         alpha=prob.alpha, beta=prob.beta, gamma=prob.gamma, eps=prob.eps, **kw)

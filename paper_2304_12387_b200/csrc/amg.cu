@@ -55,6 +55,7 @@ constexpr int ABLK = 148 * 8;
 struct Op0 {
   long long n[3], off[3], NL[3];
   int p, dim;
+  int ess;               // eliminated essential sides (NEXT-3): their faces are not in F(i)
   const double* mdiag;
   const double* ctil;
   __device__ __forceinline__ long long idx(long long X, long long Y, long long Z) const {
@@ -103,11 +104,12 @@ struct Op0 {
     const long long ext[3] = {n[0], n[1], n[2]};
     const long long crd[3] = {X, Y, Z};
     for (int k = 0; k < nf; ++k) {
-      const double w = 1.0 / mdiag[f[k]];
-      d += w;
       const int ax = k >> 1;
       const bool up = k & 1;
       const bool has = up ? (crd[ax] + 1 < ext[ax]) : (crd[ax] > 0);
+      if (!has && ((ess >> k) & 1)) continue;   // k = 2 axis + side: the ess bit layout
+      const double w = 1.0 / mdiag[f[k]];
+      d += w;
       if (has) a[C + (up ? step[ax] : -step[ax])] = -w;
     }
     a[C] = d;
@@ -471,6 +473,7 @@ Op0 make_op0(const hdiv_ctx* h) {
   if (h->dim == 2) o.n[2] = 1;
   o.p = h->p;
   o.dim = h->dim;
+  o.ess = h->ess;
   o.mdiag = h->d_mdiag;
   o.ctil = h->d_ctil;
   return o;
@@ -647,6 +650,13 @@ hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
         Ad[i * nc + (x + Lc.d[0] * (y + Lc.d[1] * z))] = st[k * nc + i];
       }
     }
+  }
+  if (h->opts.project_mean) {   // singular pure-Neumann S~ (NEXT-3, reading A21): pin the
+    for (long long i = 0; i < nc; ++i) {   // last unknown (identity row and column)
+      Ad[(nc - 1) * nc + i] = 0.0;
+      Ad[i * nc + (nc - 1)] = 0.0;
+    }
+    Ad[(nc - 1) * nc + (nc - 1)] = 1.0;
   }
   if (!invert_dense(Ad, nc)) {
     set_error("AMG: singular coarsest operator");

@@ -42,6 +42,11 @@ cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* 
                    : (h->dim == 3) ? launch_trilinear_apply(h, x, y, MODE_BLOCK, skip, s)
                                    : launch_general_apply(h, x, y, MODE_BLOCK, skip, s);
   if (e != cudaSuccess) return e;
+  // eliminated essential faces: identity rows (the box kernel writes them itself)
+  if (h->ess && h->kernel != 2) {
+    e = launch_ess_fixup(h, x, y, 0.0, skip, s);
+    if (e != cudaSuccess) return e;
+  }
   if (h->nranks > 1) {
     if (comm_reverse_add(h, y, s) != HDIV_OK) return cudaErrorUnknown;
   }
@@ -131,6 +136,12 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->opts.schur_solver = opts ? opts->schur_solver : HDIV_SCHUR_CHEBYSHEV;
   h->opts.amg_sweeps = (opts && opts->amg_sweeps > 0) ? opts->amg_sweeps : 2;
   h->opts.amg_max_coarse = (opts && opts->amg_max_coarse > 0) ? opts->amg_max_coarse : 512;
+  h->opts.essential_sides = opts ? opts->essential_sides : 0;
+  h->opts.project_mean = opts ? (opts->project_mean != 0) : 0;
+  if (h->opts.essential_sides < 0 || h->opts.essential_sides >= (1 << (2 * dim))) {
+    delete h;
+    return fail(HDIV_ERR_SHAPE, "essential_sides: bits 0..2 dim - 1 only");
+  }
   if (h->opts.schur_solver != HDIV_SCHUR_CHEBYSHEV && h->opts.schur_solver != HDIV_SCHUR_AMG) {
     delete h;
     return fail(HDIV_ERR_SHAPE, "schur_solver must be HDIV_SCHUR_CHEBYSHEV or HDIV_SCHUR_AMG");
@@ -144,6 +155,12 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->NL[last] = h->ez1 - h->ez0;
   if (dim == 2) h->NL[2] = 1;
   for (int d = 0; d < 3; ++d) h->n[d] = (d < dim) ? h->NL[d] * p : 1;
+  {   // local eliminated sides: the last axis' sides only where the slab meets the boundary
+    int ess = h->opts.essential_sides;
+    if (h->ez0 > 0) ess &= ~(1 << (2 * last));
+    if (h->ez1 < N[last]) ess &= ~(1 << (2 * last + 1));
+    h->ess = ess;
+  }
   h->E = h->NL[0] * h->NL[1] * h->NL[2];
   auto rt_count = [&](const int64_t* n) -> int64_t {
     if (dim == 2) return (n[0] + 1) * n[1] + n[0] * (n[1] + 1);
@@ -358,6 +375,7 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     }
   }
   SETUP_TRY(launch_mass_diag(h, h->d_mdiag, s));
+  if (h->ess) SETUP_TRY(launch_ess_fixup(h, nullptr, h->d_mdiag, 1.0, nullptr, s));   // M~_b = 1
   SETUP_TRY(launch_ctil(h, h->d_c2, h->d_ctil, s));
   SETUP_TRY(cudaMemcpyAsync(h->d_coef, coef.data(), sizeof(double) * 4 * E, cudaMemcpyHostToDevice, s));
   if (nranks > 1) {
@@ -404,6 +422,7 @@ hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* yu, void* st
   HDIV_CUDA_TRY(h->kernel == 2  ? launch_affine_apply(h, u, yu, MODE_MASS, nullptr, s)
                 : (h->dim == 3) ? launch_trilinear_apply(h, u, yu, MODE_MASS, nullptr, s)
                                 : launch_general_apply(h, u, yu, MODE_MASS, nullptr, s));
+  if (h->ess && h->kernel != 2) HDIV_CUDA_TRY(launch_ess_fixup(h, u, yu, 0.0, nullptr, s));
   if (h->nranks > 1) return comm_reverse_add(h, yu, s);
   return HDIV_OK;
 }
@@ -450,7 +469,9 @@ hdiv_status hdiv_gmres_solve(hdiv_handle h, const double* b, double* x, double r
 
 hdiv_status hdiv_apply_launches(hdiv_handle h, int* n) {
   if (!h || !n) return fail(HDIV_ERR_NULL, "NULL argument");
-  *n = (h->kernel == 2) ? 1 : 1;   // general path: one kernel (+ a memset node)
+  // one fused kernel (+ a memset node on the quadrature paths, + the identity-row fixup of
+  // eliminated essential faces there)
+  *n = 1 + ((h->ess && h->kernel != 2) ? 1 : 0);
   return HDIV_OK;
 }
 

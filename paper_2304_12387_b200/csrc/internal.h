@@ -85,6 +85,10 @@ struct hdiv_ctx {
   double* d_scratch = nullptr;    // reduction partials etc.
   double* d_xbuf = nullptr;       // host-API staging (lazily allocated)
   double* d_ybuf = nullptr;
+  // NEXT-3: essential (eliminated) RT sides of THIS rank's slab, bit 2a = side x_a = min of
+  // the local grid, bit 2a+1 = max (the last-axis bits only where the slab touches the domain
+  // boundary); 0 = natural everywhere
+  int ess = 0;
   int rank = 0, nranks = 1;
   hdiv::Comm* comm = nullptr;
   hdiv::MinresWork* mw = nullptr;
@@ -145,4 +149,13 @@ hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, 
 
 // apply modes
 enum { MODE_MASS = 1, MODE_BLOCK = 2, MODE_ZONLY = 3 };
+
+// NEXT-3: is the face of component c at subcell-face coordinate idx (along c) on an
+// eliminated side?  ess: local side bitmask (hdiv_ctx::ess), n_c: local subcells along c
+__host__ __device__ __forceinline__ bool face_masked(int ess, int c, long long idx, long long n_c) {
+  return ((ess >> (2 * c)) & 1 && idx == 0) || ((ess >> (2 * c + 1)) & 1 && idx == n_c);
+}
+// y_b = x_b on the eliminated faces (x == nullptr: y_b = cval)
+cudaError_t launch_ess_fixup(const hdiv_ctx* h, const double* x, double* y, double cval,
+                             const int* skip, cudaStream_t s);
 }  // namespace hdiv

@@ -116,6 +116,7 @@ struct AffArgs {
   long long nrt;
   int ntile[3];
   int has_z;
+  int ess;             // eliminated essential sides (NEXT-3), local bitmask (0: none)
   const int* skip;     // MINRES done flag (nullptr: never skip)
 };
 
@@ -238,6 +239,20 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   const CompAddr<P, AX> ca(a, ti);
   const long long ext0 = ca.ext0, ext01 = ca.ext01, gtile = ca.gtile;
   const int hi0 = ti.m[0] * P, hi1 = ti.m[1] * P, hi2 = ti.m[2] * P;
+  constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
+
+  // ---- NEXT-3: eliminated essential planes act as zero inputs (the tile's first plane when
+  //      it starts at the domain's - side, its last when it ends at the + side) ----
+  const bool ess_lo = ((a.ess >> (2 * AX)) & 1) && ti.e0[AX] == 0;
+  const bool ess_hi = ((a.ess >> (2 * AX + 1)) & 1) && ti.last[AX];
+  if (ess_lo || ess_hi) {   // block-uniform
+    for (int it = tid; it < EL1 * EL2; it += NT) {
+      double* line = su + (it % EL1) * C::SA1 + (it / EL1) * C::SA2;
+      if (ess_lo) line[P * C::SA] = 0.0;
+      if (ess_hi) line[(ti.m[AX] + 1) * P * C::SA] = 0.0;
+    }
+    __syncthreads();
+  }
 
   // ---- D u: this component's two faces of every owned cell ----
   if constexpr (BLOCK) {
@@ -269,7 +284,6 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   // ---- halo element: only its contribution to the shared plane is needed, and by
   //      linearity c_h sum_j M_l[P][j] (M_h (x) M_h) u_j = c_h (M_h (x) M_h) sum_j M_l[P][j] u_j,
   //      so the raw halo planes are combined first into position P-1 (one plane to transform)
-  constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
   constexpr int EL1P = C::PADL ? (EL1 + 15) / 16 * 16 : EL1;   // half-warp aligned lane rows
   const int m_a = ti.m[AX], h_a = ti.h[AX];
   if (h_a) {
@@ -376,6 +390,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
             o += qprev - qc;
             qprev = qc;
           }
+          if (i == 0 && et == 0 && ess_lo)   // identity row of the eliminated plane
+            o = a.x[gtile + (l1 * gs1 + l2 * gs2) + P * gsa];
           if (AX == 0 && !XD) eb[i * C::SA] = o;
           else __stcs(gl + ((et + 1) * P + i) * gsa, o);
         }
@@ -386,7 +402,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
       }
     }
     if (ti.last[AX]) {
-      const double o = carry + (BLOCK ? qprev : 0.0);
+      const double o = ess_hi ? a.x[gtile + (l1 * gs1 + l2 * gs2) + (m_a + 1) * P * gsa]
+                              : carry + (BLOCK ? qprev : 0.0);
       if (AX == 0 && !XD) line[(m_a + 1) * P * C::SA] = o;
       else __stcs(gl + (m_a + 1) * P * gsa, o);
     }
@@ -610,6 +627,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ntile[1] = (int)((h->NL[1] + TY - 1) / TY);
   a.ntile[2] = (int)((h->NL[2] + TZ - 1) / TZ);
   a.has_z = h->has_z ? 1 : 0;
+  a.ess = h->ess;
   a.skip = skip;
   const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
   auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD>;
@@ -986,6 +1004,7 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
   if (zc > h->NL[2]) zc = (int)h->NL[2];
   a.ntile[2] = (int)((h->NL[2] + zc - 1) / zc);
   a.has_z = h->has_z ? 1 : 0;
+  a.ess = 0;   // the marching kernel is not dispatched with eliminated sides
   a.skip = skip;
   const size_t smem = M::smem_doubles(BLOCK) * sizeof(double);
   auto kern = affine_march_kernel<P, TX, TY, NT, BLOCK>;
@@ -1026,7 +1045,7 @@ template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
                      cudaStream_t s) {
   const int mv = march_variant(h->p);
-  if (mv >= 0) {
+  if (mv >= 0 && !h->ess) {
     switch (h->p) {
       case 1: return launch_m<1, 8, 8, 128, BLOCK>(h, x, y, k, s);
       case 2:

@@ -32,6 +32,7 @@ struct GenArgs {
   long long off[3];
   long long nrt;
   int has_z;
+  int ess;              // eliminated essential sides (NEXT-3): zero inputs, outputs skipped
   const int* skip;
 };
 
@@ -133,7 +134,13 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
       int c = i / NC, l = i % NC;
       int n0 = ext(c, 0), n1 = ext(c, 1);
       int ii = l % n0, jj = (l / n0) % n1, kk = (DIM == 3) ? l / (n0 * n1) : 0;
-      su[i] = a.x[gidx(c, ii, jj, kk)];
+      double v = a.x[gidx(c, ii, jj, kk)];
+      if (a.ess) {   // eliminated essential face: acts as zero (NEXT-3)
+        const long long gi = (c == 0) ? (long long)ex * P + ii : (c == 1) ? (long long)ey * P + jj
+                                                                         : (long long)ez * P + kk;
+        if (face_masked(a.ess, c, gi, a.n[c])) v = 0.0;
+      }
+      su[i] = v;
     }
   }
   if constexpr (BLOCK) {
@@ -313,8 +320,13 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
           }
         }
         long long g = gidx(c, ii, jj, kk);
-        if (ic == 0 || ic == P) atomicAdd(a.y + g, v);
-        else a.y[g] = v;
+        if (ic == 0 || ic == P) {
+          const long long gi = (c == 0) ? (long long)ex * P + ii : (c == 1) ? (long long)ey * P + jj
+                                                                           : (long long)ez * P + kk;
+          if (!(a.ess && face_masked(a.ess, c, gi, a.n[c]))) atomicAdd(a.y + g, v);
+        } else {
+          a.y[g] = v;
+        }
       }
       __syncthreads();
     }
@@ -334,6 +346,7 @@ cudaError_t launch_g(const hdiv_ctx* h, const double* x, double* y, const int* s
   for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
   a.nrt = h->nrt;
   a.has_z = h->has_z ? 1 : 0;
+  a.ess = (MODE == GMODE_MASS || MODE == GMODE_BLOCK) ? h->ess : 0;
   a.skip = skip;
   general_kernel<DIM, P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();

@@ -18,6 +18,7 @@ namespace {
 struct Grid {
   long long NL[3], n[3], off[3];
   int p, dim;
+  int ess;                        // eliminated essential sides (NEXT-3), local bitmask
   long long ghost_lo, ghost_hi;   // first ghost column below / above the slab, -1 if none
   __device__ __forceinline__ long long l2(long long X, long long Y, long long Z) const {
     long long e = (X / p) + NL[0] * ((Y / p) + NL[1] * (Z / p));
@@ -49,7 +50,7 @@ struct Grid {
 Grid make_grid(const hdiv_ctx* h) {
   Grid g;
   for (int d = 0; d < 3; ++d) { g.NL[d] = h->NL[d]; g.n[d] = h->n[d]; g.off[d] = h->off[d]; }
-  g.p = h->p; g.dim = h->dim;
+  g.p = h->p; g.dim = h->dim; g.ess = h->ess;
   const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
   g.ghost_lo = (h->rank > 0) ? h->nl2 : -1;
   g.ghost_hi = (h->rank < h->nranks - 1) ? h->nl2 + lplane : -1;
@@ -65,9 +66,14 @@ __global__ void div_kernel(Grid g, const double* __restrict__ u, double* __restr
   if (i >= nl2) return;
   long long X, Y, Z;
   g.cell_of_l2(i, &X, &Y, &Z);
-  double s = u[g.rt(0, X + 1, Y, Z)] - u[g.rt(0, X, Y, Z)];
-  s += u[g.rt(1, X, Y + 1, Z)] - u[g.rt(1, X, Y, Z)];
-  if (g.dim == 3) s += u[g.rt(2, X, Y, Z + 1)] - u[g.rt(2, X, Y, Z)];
+  // eliminated essential faces act as zero (NEXT-3: the (2,1) block is D F)
+  auto uu = [&](int c, long long I, long long J, long long K) {
+    const long long idx = (c == 0) ? I : (c == 1) ? J : K;
+    return face_masked(g.ess, c, idx, g.n[c]) ? 0.0 : u[g.rt(c, I, J, K)];
+  };
+  double s = uu(0, X + 1, Y, Z) - uu(0, X, Y, Z);
+  s += uu(1, X, Y + 1, Z) - uu(1, X, Y, Z);
+  if (g.dim == 3) s += uu(2, X, Y, Z + 1) - uu(2, X, Y, Z);
   yq[i] = s;
 }
 
@@ -82,6 +88,7 @@ __global__ void divT_kernel(Grid g, const double* __restrict__ q, double* __rest
   long long I = r % e0, J = (r / e0) % e1, K = (g.dim == 3) ? r / (e0 * e1) : 0;
   long long idx[3] = {I, J, K};
   long long nn = g.n[c];
+  if (face_masked(g.ess, c, idx[c], nn)) { yu[f] = 0.0; return; }   // F D^T (NEXT-3)
   double s = 0.0;
   if (idx[c] > 0) {
     long long m[3] = {I, J, K};
@@ -159,6 +166,8 @@ __global__ void schur_fill_kernel(Grid g, const double* __restrict__ mdiag,
   int m = 0;
   double d = ctil[i];
   for (int k = 0; k < nd; ++k) {
+    // an eliminated boundary face (k = 2 axis + side, the ess bit layout) is not in F(i)
+    if (nb[k] < 0 && ((g.ess >> k) & 1)) continue;
     double w = 1.0 / mdiag[face[k]];
     d += w;
     if (nb[k] >= 0) { cc[m] = nb[k]; vv[m] = -w; ++m; }
@@ -187,6 +196,26 @@ __global__ void sell_kernel(const int64_t* __restrict__ rp, const int32_t* __res
     ec[base + 32 * k] = (t < r1) ? c[t] : (int32_t)i;
     ev[base + 32 * k] = (t < r1) ? v[t] : 0.0;
   }
+}
+
+// NEXT-3: y_b = x_b (x != nullptr) or cval on the faces of the eliminated sides; blockIdx.y =
+// 2 c + side, one thread per face of that side's plane
+__global__ void ess_fixup_kernel(Grid g, const double* __restrict__ x, double* __restrict__ y,
+                                 double cval, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int k = blockIdx.y, c = k >> 1, side = k & 1;
+  if (c >= g.dim || !((g.ess >> k) & 1)) return;
+  // the two tangential axes (2D: one) of component c
+  const int t0 = (c == 0) ? 1 : 0, t1 = (c == 2) ? 1 : 2;
+  const long long n0 = g.n[t0], n1 = (g.dim == 3) ? g.n[t1] : 1;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n0 * n1) return;
+  long long idx[3] = {0, 0, 0};
+  idx[c] = side ? g.n[c] : 0;
+  idx[t0] = i % n0;
+  if (g.dim == 3) idx[t1] = i / n0;
+  const long long f = g.rt(c, idx[0], idx[1], idx[2]);
+  y[f] = x ? x[f] : cval;
 }
 
 __global__ void recip_kernel(const double* __restrict__ a, double* __restrict__ r, long long n) {
@@ -269,6 +298,21 @@ __global__ void geom_check_kernel(const double* __restrict__ vert, Tab1D tab, lo
 
 }  // namespace
 
+cudaError_t launch_ess_fixup(const hdiv_ctx* h, const double* x, double* y, double cval,
+                             const int* skip, cudaStream_t s) {
+  if (!h->ess) return cudaSuccess;
+  long long mx = 0;
+  for (int c = 0; c < h->dim; ++c) {
+    long long pl = 1;
+    for (int a = 0; a < h->dim; ++a)
+      if (a != c) pl *= h->n[a];
+    if (pl > mx) mx = pl;
+  }
+  dim3 grid(nblocks(mx, 256), 2 * h->dim);
+  ess_fixup_kernel<<<grid, 256, 0, s>>>(make_grid(h), x, y, cval, skip);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_div(const hdiv_ctx* h, const double* u, double* yq, cudaStream_t s) {
   div_kernel<<<nblocks(h->nl2, 256), 256, 0, s>>>(make_grid(h), u, yq, h->nl2);
   return cudaGetLastError();
@@ -331,6 +375,7 @@ hdiv_status build_schur(hdiv_ctx* h, cudaStream_t s) {
     HDIV_CUDA_TRY(cudaMalloc(&h->d_minv, sizeof(double) * (h->nrt > 0 ? h->nrt : 1)));
     recip_kernel<<<nblocks(h->nrt, 256), 256, 0, s>>>(h->d_mdiag, h->d_minv, h->nrt);
     HDIV_CUDA_TRY(cudaGetLastError());
+    if (h->ess) HDIV_CUDA_TRY(launch_ess_fixup(h, nullptr, h->d_minv, 0.0, nullptr, s));
     return HDIV_OK;
   }
   // sliced-ELL copy used by the SpMV inside S^-1 (coalesced slot loads)

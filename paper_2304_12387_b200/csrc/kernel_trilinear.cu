@@ -31,6 +31,7 @@ struct TriArgs {
   long long off[3];
   long long nrt;
   int has_z;
+  int ess;              // eliminated essential sides (NEXT-3): zero inputs, outputs skipped
   const int* skip;
 };
 
@@ -157,17 +158,21 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     const long long gx = a.off[0] + (long long)ex * P + (nx + 1) * ((long long)ey * P + ny * (long long)ez * P);
     const long long gy = a.off[1] + (long long)ex * P + nx * ((long long)ey * P + (ny + 1) * (long long)ez * P);
     const long long gz = a.off[2] + (long long)ex * P + nx * ((long long)ey * P + ny * (long long)ez * P);
+    // eliminated essential faces (NEXT-3) act as zero inputs
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % (P + 1), lj = (l / (P + 1)) % P, lk = l / ((P + 1) * P);
-      su(0)[li + T::U0::S1 * lj + T::U0::S2 * lk] = a.x[gx + li + (nx + 1) * (lj + ny * lk)];
+      const bool m = a.ess && face_masked(a.ess, 0, (long long)ex * P + li, nx);
+      su(0)[li + T::U0::S1 * lj + T::U0::S2 * lk] = m ? 0.0 : a.x[gx + li + (nx + 1) * (lj + ny * lk)];
     }
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % P, lj = (l / P) % (P + 1), lk = l / (P * (P + 1));
-      su(1)[li + T::U1::S1 * lj + T::U1::S2 * lk] = a.x[gy + li + nx * (lj + (ny + 1) * lk)];
+      const bool m = a.ess && face_masked(a.ess, 1, (long long)ey * P + lj, ny);
+      su(1)[li + T::U1::S1 * lj + T::U1::S2 * lk] = m ? 0.0 : a.x[gy + li + nx * (lj + (ny + 1) * lk)];
     }
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % P, lj = (l / P) % P, lk = l / (P * P);
-      su(2)[li + T::U2::S1 * lj + T::U2::S2 * lk] = a.x[gz + li + nx * (lj + ny * lk)];
+      const bool m = a.ess && face_masked(a.ess, 2, (long long)ez * P + lk, a.n[2]);
+      su(2)[li + T::U2::S1 * lj + T::U2::S2 * lk] = m ? 0.0 : a.x[gz + li + nx * (lj + ny * lk)];
     }
   }
   if constexpr (HASQ) {
@@ -257,9 +262,14 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     const long long gx = a.off[0] + (long long)ex * P + (nx + 1) * ((long long)ey * P + ny * (long long)ez * P);
     const long long gy = a.off[1] + (long long)ex * P + nx * ((long long)ey * P + (ny + 1) * (long long)ez * P);
     const long long gz = a.off[2] + (long long)ex * P + nx * ((long long)ey * P + ny * (long long)ez * P);
-    auto put = [&](double* g, double v, int ic) {
-      if (ic == 0 || ic == P) atomicAdd(g, v);
-      else *g = v;
+    // element-boundary faces by atomics onto the zeroed output; eliminated essential faces
+    // are skipped (their identity rows are written by the fixup kernel)
+    auto put = [&](double* g, double v, int ic, int c, long long gi) {
+      if (ic == 0 || ic == P) {
+        if (!(a.ess && face_masked(a.ess, c, gi, a.n[c]))) atomicAdd(g, v);
+      } else {
+        *g = v;
+      }
     };
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % (P + 1), lj = (l / (P + 1)) % P, lk = l / ((P + 1) * P);
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
         if (li > 0) v += sq[cell - 1];
         if (li < P) v -= sq[cell];
       }
-      put(a.y + gx + li + (nx + 1) * (lj + ny * lk), v, li);
+      put(a.y + gx + li + (nx + 1) * (lj + ny * lk), v, li, 0, (long long)ex * P + li);
     }
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % P, lj = (l / P) % (P + 1), lk = l / (P * (P + 1));
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
         if (lj > 0) v += sq[cell - T::L2::S1];
         if (lj < P) v -= sq[cell];
       }
-      put(a.y + gy + li + nx * (lj + (ny + 1) * lk), v, lj);
+      put(a.y + gy + li + nx * (lj + (ny + 1) * lk), v, lj, 1, (long long)ey * P + lj);
     }
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % P, lj = (l / P) % P, lk = l / (P * P);
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
         if (lk > 0) v += sq[cell - T::L2::S2];
         if (lk < P) v -= sq[cell];
       }
-      put(a.y + gz + li + nx * (lj + ny * lk), v, lk);
+      put(a.y + gz + li + nx * (lj + ny * lk), v, lk, 2, (long long)ez * P + lk);
     }
   }
   }  // !ZONLY
@@ -519,6 +529,7 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
   a.nrt = h->nrt;
   a.has_z = h->has_z ? 1 : 0;
+  a.ess = (MODE == 2) ? 0 : h->ess;
   a.skip = skip;
   if constexpr (MODE == 2 && P <= 2) {
     tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);

@@ -337,6 +337,39 @@ __global__ void latch_kernel(MState* st) {
   if (threadIdx.x == 0 && st->done == 2) st->done = 1;
 }
 
+// NEXT-3 orthogonalization after S^-1 (reading A21): partial sums of y, then
+// y -= mean (the rank-ordered global sum / n) fused with the partial <y, v> MINRES needs
+__global__ void __launch_bounds__(RED_NT)
+sum_kernel(const double* __restrict__ y, long long n, double* __restrict__ part,
+           const int* __restrict__ done) {
+  if (done && *done) return;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT)
+    s += y[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(RED_NT)
+mean_sub_kernel(double* __restrict__ y, long long n, const double* __restrict__ glob, int P,
+                double inv_n, const double* __restrict__ v, double* __restrict__ part,
+                const int* __restrict__ done) {
+  if (done && *done) return;
+  const double mean = rank_sum(glob, P) * inv_n;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    const double t = y[i] - mean;
+    y[i] = t;
+    if (part) s = fma(t, v[i], s);
+  }
+  if (part) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
 inline unsigned nb(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -446,9 +479,12 @@ static cudaError_t launch_cheb_stencil(const hdiv_ctx* h, const double* rin, dou
   return cudaErrorInvalidValue;
 }
 
+static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
+                                 cudaStream_t s);
+
 // Chebyshev-Jacobi S^-1 applied to vq -> y (uses mw->r, mw->d); partial <y, vq> if part
-static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
-                              const int* done, cudaStream_t s) {
+static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, double* part,
+                                  const int* done, cudaStream_t s) {
   MinresWork* mw = h->mw;
   if (h->opts.schur_solver == HDIV_SCHUR_AMG) {   // NEXT-1: one V-cycle
     hdiv_status st = amg_vcycle(h, vq, y, done, s);
@@ -488,6 +524,23 @@ static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* 
     HDIV_CUDA_TRY(cudaGetLastError());
     rin = mw->r;
   }
+  return HDIV_OK;
+}
+
+// S^-1 (Chebyshev or AMG) followed, with options.project_mean, by the orthogonalization step
+// of P:1038-1040; the partial <y, vq> is taken after the projection
+static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
+                              const int* done, cudaStream_t s) {
+  if (!h->opts.project_mean) return cheb_apply_raw(h, vq, y, part, done, s);
+  MinresWork* mw = h->mw;
+  hdiv_status st = cheb_apply_raw(h, vq, y, nullptr, done, s);
+  if (st != HDIV_OK) return st;
+  sum_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(y, h->nl2, mw->part_b, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  if ((st = reduce_scalar(h, mw->part_b, nullptr, done, s)) != HDIV_OK) return st;
+  mean_sub_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(y, h->nl2, mw->glob, h->nranks,
+                                                1.0 / (double)h->nl2_g, vq, part, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
   return HDIV_OK;
 }
 

@@ -1,0 +1,3 @@
+#!/bin/bash
+timeout 1200 python -m pytest tests/test_gpu_essential.py -x -q 2>&1 | tail -25
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -3
