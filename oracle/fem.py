@@ -172,8 +172,9 @@ def element_rt_mass(X, beta: float, ref: RefTables) -> np.ndarray:
     return Aw @ Am.T
 
 
-def element_l2_mass(X, c: float, ref: RefTables) -> np.ndarray:
-    """W^e_ab = sum_q w_q c psi_a psi_b det J_q, psi = psi_hat / det J."""
+def element_l2_mass(X, c, ref: RefTables) -> np.ndarray:
+    """W^e_ab = sum_q w_q c psi_a psi_b det J_q, psi = psi_hat / det J.
+    c: a constant, or its values at the quadrature points (variable coefficient, NEXT-3)."""
     J, det = jacobian(X, ref.pts)
     check_geometry(det)
     wt = ref.w * c / det

@@ -5,6 +5,9 @@ P:517-520 eq.(transformed-system-darcy): A' = [[M_{1/eps}, D^T], [D, -W^-1 W_gam
 P:451-456 eq.(approx-schur): M~ = diag(M_beta), W~ = diag(W_alpha), S~ = W~^-1 + D M~^-1 D^T
 P:466-471 eq.(approx-schur-entries) entry formula of S~
 P:555  Darcy: W^-1 W_gamma W^-1 approximated by the product of the (reciprocal) diagonals
+P:552, P:761 (NEXT-3): general (not piecewise-constant) gamma keeps the full (2,2) block
+       W^-1 W_gamma W^-1 (two W^-1 per apply); reading A22: gamma is the trilinear (Q_1)
+       field of per-vertex values, evaluated at the quadrature points
 P:886  S~ via the sparse triple product D M~^-1 D^T
 NEXT-3 (reading A21): essential flux conditions on whole domain sides by
 elimination — identity rows/columns for the prescribed RT DOFs (u_b), which are dropped from
@@ -38,6 +41,9 @@ def _check_coeffs(prob):
     else:
         if np.any(prob.eps <= 0) or np.any(prob.gamma < 0):
             raise ValueError("coefficient error: eps > 0, gamma >= 0 required")
+        gv = getattr(prob, "gamma_vertex", None)
+        if gv is not None and np.any(gv < 0):
+            raise ValueError("coefficient error: gamma >= 0 required")
 
 
 class Assembled:
@@ -73,7 +79,13 @@ class Assembled:
                 self.Wdiag[sl] = np.diag(We)
             else:
                 We = fem.element_l2_mass(X, 1.0, ref)
-                Wg = fem.element_l2_mass(X, float(prob.gamma[e]), ref)
+                Gv = getattr(prob, "gamma_vertex", None)
+                if Gv is not None:   # general gamma (NEXT-3, reading A22): trilinear vertex
+                    Ge = fem.element_vertices(Gv[..., None], dim, space.element_index(dim, N, e))
+                    gq = fem.physical_points(Ge, ref.pts)[:, 0]    # field at the quadrature points
+                    Wg = fem.element_l2_mass(X, gq, ref)
+                else:
+                    Wg = fem.element_l2_mass(X, float(prob.gamma[e]), ref)
                 cf = sla.cho_factor(We)
                 Ze = sla.cho_solve(cf, Wg @ sla.cho_solve(cf, np.eye(nl)))  # W^-1 W_g W^-1
                 self.Wdiag[sl] = np.diag(We)

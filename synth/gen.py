@@ -147,6 +147,8 @@ class Problem:
     beta: Optional[np.ndarray] = None    # grad-div  M_beta weight,  per element
     eps: Optional[np.ndarray] = None     # Darcy     M_{1/eps},       per element
     gamma: Optional[np.ndarray] = None   # Darcy     W_gamma,         per element
+    gamma_vertex: Optional[np.ndarray] = None   # Darcy general gamma: per-vertex values of a
+                                         # trilinear field (shape vertices.shape[:-1]), NEXT-3
     affine: bool = True                  # axis-aligned boxes (generator knows it)
     Q: int = 0                           # 0 -> p+2 (A3)
     essential: int = 0                   # essential-flux sides bitmask (bit 2a: x_a = min,
