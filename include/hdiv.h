@@ -66,6 +66,13 @@ typedef struct {
 typedef struct {              /* HOST per-element arrays of the slab [E_local], or NULL       */
   const double *alpha, *beta, *gamma, *eps;
   double alpha0, beta0, gamma0, eps0;   /* constants used where an array is NULL              */
+  /* NEXT-3 (reading A22): Darcy with a general (not piecewise-constant) gamma —
+   * HOST per-vertex values of the slab's vertex layers (layout of hdiv_mesh_desc.vertices
+   * without the coordinate axis), gamma(x) = their trilinear interpolant, >= 0.  When set,
+   * `gamma`/`gamma0` are ignored and the (2,2) block is the full W^-1 W_gamma W^-1 (two
+   * element-local W^-1 solves per apply); 3D only (HDIV_ERR_UNSUPPORTED in 2D), always on the
+   * quadrature kernel. */
+  const double* gamma_vertex;
 } hdiv_coeffs;
 
 typedef struct {

@@ -35,7 +35,7 @@ class Coeffs(C.Structure):
     _fields_ = [("alpha", C.POINTER(C.c_double)), ("beta", C.POINTER(C.c_double)),
                 ("gamma", C.POINTER(C.c_double)), ("eps", C.POINTER(C.c_double)),
                 ("alpha0", C.c_double), ("beta0", C.c_double), ("gamma0", C.c_double),
-                ("eps0", C.c_double)]
+                ("eps0", C.c_double), ("gamma_vertex", C.POINTER(C.c_double))]
 
 
 class Options(C.Structure):
@@ -166,7 +166,7 @@ class HdivOperator:
     tensors in the canonical numbering."""
 
     def __init__(self, dim, N, p, kind, vertices=None, alpha=None, beta=None, gamma=None,
-                 eps=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
+                 eps=None, gamma_vertex=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
                  schur="chebyshev", amg_sweeps=2, amg_max_coarse=512, essential=0,
                  project_mean=False, slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
         import torch
@@ -187,7 +187,8 @@ class HdivOperator:
         V = arr(vertices)
         md = MeshDesc(dim, N[0], N[1], N[2] if dim == 3 else 1, z0, z1, _dptr(V))
         a_, b_, g_, e_ = arr(alpha), arr(beta), arr(gamma), arr(eps)
-        co = Coeffs(_dptr(a_), _dptr(b_), _dptr(g_), _dptr(e_), 1.0, 1.0, 0.0, 1.0)
+        gv_ = arr(gamma_vertex)
+        co = Coeffs(_dptr(a_), _dptr(b_), _dptr(g_), _dptr(e_), 1.0, 1.0, 0.0, 1.0, _dptr(gv_))
         op = Options(tau, cheb_degree, cheb_ratio, kernel, SCHUR_SOLVERS[schur], amg_sweeps,
                      amg_max_coarse, int(essential), int(bool(project_mean)))
         h = C.c_void_p()
@@ -391,6 +392,7 @@ class HdivOperator:
 def from_problem(prob, **kw) -> HdivOperator:
     """Build an operator from a synth.Problem (inputs only)."""
     kw.setdefault("essential", getattr(prob, "essential", 0))
+    kw.setdefault("gamma_vertex", getattr(prob, "gamma_vertex", None))
     kw.setdefault("project_mean", getattr(prob, "project_mean", False))
     return HdivOperator(prob.dim, prob.N, prob.p, prob.kind, vertices=prob.vertices,
                         alpha=prob.alpha, beta=prob.beta, gamma=prob.gamma, eps=prob.eps, **kw)

@@ -95,6 +95,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_ecol);
   cudaFree(h->d_minv);
   cudaFree(h->d_zcoef);
+  cudaFree(h->d_gvert);
   amg_free(h);
   gmres_free(h);
   cudaFree(h->d_eval);
@@ -206,6 +207,26 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   const int64_t E = h->E;
   std::vector<double> mw(E), c2(E);
   bool any_gamma = false;
+  // NEXT-3: general gamma as a trilinear vertex field (reading A22)
+  const bool gvert = (kind == HDIV_DARCY && co->gamma_vertex != nullptr);
+  if (gvert) {
+    if (dim != 3) {
+      delete h;
+      return fail(HDIV_ERR_UNSUPPORTED, "general (vertex-field) gamma is 3D only");
+    }
+    if (opts && opts->kernel == 2) {
+      delete h;
+      return fail(HDIV_ERR_UNSUPPORTED, "general gamma needs the quadrature kernel");
+    }
+    const int64_t nvg = (h->NL[0] + 1) * (h->NL[1] + 1) * (h->NL[2] + 1);
+    for (int64_t v = 0; v < nvg; ++v) {
+      if (!(co->gamma_vertex[v] >= 0)) {
+        delete h;
+        return fail(HDIV_ERR_COEFFICIENT, "gamma_vertex must be >= 0");
+      }
+      if (co->gamma_vertex[v] > 0) any_gamma = true;
+    }
+  }
   for (int64_t e = 0; e < E; ++e) {
     if (kind == HDIV_GRAD_DIV) {
       double al = co->alpha ? co->alpha[e] : co->alpha0;
@@ -217,13 +238,13 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
       mw[e] = be; c2[e] = al;
     } else {
       double ep = co->eps ? co->eps[e] : co->eps0;
-      double ga = co->gamma ? co->gamma[e] : co->gamma0;
+      double ga = gvert ? 1.0 : (co->gamma ? co->gamma[e] : co->gamma0);   // gvert: s_e = 1
       if (!(ep > 0) || !(ga >= 0)) {
         delete h;
         return fail(HDIV_ERR_COEFFICIENT, "eps > 0 and gamma >= 0 required");
       }
       mw[e] = 1.0 / ep; c2[e] = ga;
-      if (ga > 0) any_gamma = true;
+      if (ga > 0 && !gvert) any_gamma = true;
     }
   }
   h->has_z = (kind == HDIV_GRAD_DIV) || any_gamma;
@@ -274,7 +295,7 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     delete h;
     return fail(HDIV_ERR_UNSUPPORTED, "affine tile kernel needs 3D axis-aligned boxes");
   }
-  h->kernel = (want == 1) ? 1 : ((dim == 3 && all_box) ? 2 : 1);
+  h->kernel = (want == 1 || gvert) ? 1 : ((dim == 3 && all_box) ? 2 : 1);
   for (int64_t e = 0; e < E; ++e) {
     int64_t ex = e % h->NL[0], ey = (e / h->NL[0]) % h->NL[1], ez = (dim == 3) ? e / (h->NL[0] * h->NL[1]) : 0;
     double X[8][3];
@@ -358,6 +379,12 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   SETUP_TRY(cudaMalloc(&h->d_ctil, sizeof(double) * h->nl2));
   SETUP_TRY(cudaMemcpyAsync(h->d_vert, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, s));
   SETUP_TRY(cudaMemcpyAsync(h->d_c2, c2.data(), sizeof(double) * E, cudaMemcpyHostToDevice, s));
+  if (gvert) {
+    const size_t nvg = (size_t)((h->NL[0] + 1) * (h->NL[1] + 1) * (h->NL[2] + 1));
+    SETUP_TRY(cudaMalloc(&h->d_gvert, sizeof(double) * nvg));
+    SETUP_TRY(cudaMemcpyAsync(h->d_gvert, co->gamma_vertex, sizeof(double) * nvg,
+                              cudaMemcpyHostToDevice, s));
+  }
   // the diagonal kernel reads {mass weight} from d_coef: upload general layout first
   SETUP_TRY(cudaMemcpyAsync(h->d_coef, gcoef.data(), sizeof(double) * 4 * E, cudaMemcpyHostToDevice, s));
   if (h->geom == GEOM_TRILINEAR) {

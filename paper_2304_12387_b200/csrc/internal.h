@@ -73,6 +73,7 @@ struct hdiv_ctx {
   double* d_ctil = nullptr;       // C~
   double* d_c2 = nullptr;         // per element alpha (grad-div) | gamma (Darcy)
   double* d_zcoef = nullptr;      // 3D: per element {mass weight, s_e = 1/alpha | gamma, 0, 0}
+  double* d_gvert = nullptr;      // NEXT-3 general gamma: per local vertex (nullptr: per element)
   double* d_sdinv = nullptr;      // 1 / diag(S~)
   int64_t* d_srow = nullptr;      // S~ CSR (local rows; ghost columns >= nl2 for multi-GPU)
   int32_t* d_scol = nullptr;

@@ -33,6 +33,7 @@ struct GenArgs {
   long long nrt;
   int has_z;
   int ess;              // eliminated essential sides (NEXT-3): zero inputs, outputs skipped
+  const double* gvert;  // DIAGW: weight by the trilinear gamma field (NEXT-3), else nullptr
   const int* skip;
 };
 
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
   __shared__ double sq[BLOCK ? NL2 : 1], sy[BLOCK || MODE == GMODE_DIAGW ? NL2 : 1];
   __shared__ double sMhi[P * P];
   __shared__ double scoef[2];
+  __shared__ double sG[8];   // vertex gamma values (DIAGW with a.gvert)
 
   const int tid = threadIdx.x;
   const long long e = blockIdx.x;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
                       ? (((long long)(ez + cc) * (NLy + 1) + (ey + cb)) * (NLx + 1) + (ex + ca))
                       : ((long long)(ey + cb) * (NLx + 1) + (ex + ca));
     sX[v * DIM + d] = a.vert[g * DIM + d];
+    if (DIM == 3 && MODE == GMODE_DIAGW && a.gvert && d == 0) sG[v] = a.gvert[g];
   }
   const long long nx = a.n[0], ny = a.n[1];
   // global index of local DOF (component c, local tensor index (i,j,k))
@@ -232,7 +235,13 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
     }
     double wq = sw[qx] * sw[qy] * (DIM == 3 ? sw[qz] : 1.0);
     if (MODE == GMODE_DIAGW) {
-      sT1[qi] = wq / det;
+      double gw = 1.0;
+      if (DIM == 3 && a.gvert) {   // gamma(x_hat_q), trilinear in the vertex values
+        gw = 0.0;
+        for (int v = 0; v < 8; ++v)
+          gw += sG[v] * ((v & 1) ? xh : 1 - xh) * ((v & 2) ? yh : 1 - yh) * ((v & 4) ? zh : 1 - zh);
+      }
+      sT1[qi] = gw * wq / det;
       continue;
     }
     double s = wq * scoef[0] / det;
@@ -347,6 +356,7 @@ cudaError_t launch_g(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.nrt = h->nrt;
   a.has_z = h->has_z ? 1 : 0;
   a.ess = (MODE == GMODE_MASS || MODE == GMODE_BLOCK) ? h->ess : 0;
+  a.gvert = nullptr;
   a.skip = skip;
   general_kernel<DIM, P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
@@ -396,6 +406,33 @@ cudaError_t launch_mass_diag(const hdiv_ctx* h, double* diag, cudaStream_t s) {
 // diag(W_1) per L2 DOF into `w1` (sum_q w_q psi_hat_a^2 / det J)
 cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s) {
   return dispatch<GMODE_DIAGW>(h, nullptr, w1, nullptr, s);
+}
+
+// diag(W_gamma) per L2 DOF for the general (vertex-field) gamma, 3D (NEXT-3)
+template <int P>
+static cudaError_t launch_wg(const hdiv_ctx* h, double* wg, cudaStream_t s) {
+  GenArgs a;
+  a.x = nullptr; a.y = wg; a.vert = h->d_vert; a.coef = h->d_coef;
+  for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
+  a.nrt = h->nrt;
+  a.has_z = 0;
+  a.ess = 0;
+  a.gvert = h->d_gvert;
+  a.skip = nullptr;
+  general_kernel<3, P, 128, GMODE_DIAGW><<<(unsigned)h->E, 128, 0, s>>>(a, h->tab);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l2_diag_gamma(const hdiv_ctx* h, double* wg, cudaStream_t s) {
+  switch (h->p) {
+    case 1: return launch_wg<1>(h, wg, s);
+    case 2: return launch_wg<2>(h, wg, s);
+    case 3: return launch_wg<3>(h, wg, s);
+    case 4: return launch_wg<4>(h, wg, s);
+    case 5: return launch_wg<5>(h, wg, s);
+    case 6: return launch_wg<6>(h, wg, s);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace hdiv

@@ -336,10 +336,28 @@ cudaError_t launch_geometry_check(const hdiv_ctx* h, int* bad, cudaStream_t s) {
 }
 
 cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s);   // kernel_general.cu
+cudaError_t launch_l2_diag_gamma(const hdiv_ctx* h, double* wg, cudaStream_t s);
+
+// general gamma (NEXT-3): C~ = diag(W_gamma) / diag(W)^2
+__global__ void ctil_g_kernel(const double* __restrict__ w1, const double* __restrict__ wg,
+                              double* ctil, long long nl2) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= nl2) return;
+  const double w = w1[i];
+  ctil[i] = wg[i] / (w * w);
+}
 
 cudaError_t launch_ctil(const hdiv_ctx* h, const double* d_c2, double* ctil, cudaStream_t s) {
   cudaError_t e = launch_l2_diag(h, ctil, s);   // w1 into ctil, then transform in place
   if (e != cudaSuccess) return e;
+  if (h->d_gvert) {
+    double* wg = nullptr;
+    if ((e = cudaMallocAsync(&wg, sizeof(double) * h->nl2, s)) != cudaSuccess) return e;
+    if ((e = launch_l2_diag_gamma(h, wg, s)) != cudaSuccess) return e;
+    ctil_g_kernel<<<nblocks(h->nl2, 256), 256, 0, s>>>(ctil, wg, ctil, h->nl2);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaFreeAsync(wg, s);
+  }
   long long pd = (h->dim == 2) ? (long long)h->p * h->p : (long long)h->p * h->p * h->p;
   ctil_kernel<<<nblocks(h->nl2, 256), 256, 0, s>>>(ctil, d_c2, ctil, h->nl2, pd,
                                                   h->kind == HDIV_DARCY);

@@ -32,6 +32,7 @@ struct TriArgs {
   long long nrt;
   int has_z;
   int ess;              // eliminated essential sides (NEXT-3): zero inputs, outputs skipped
+  const double* gvert;  // general gamma (NEXT-3): per-vertex field; Z = W^-1 W_gamma W^-1
   const int* skip;
 };
 
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   __shared__ double sq[HASQ ? T::SL : 1], sy[BLOCK ? P3 : 1], sz1[HASQ ? T::SL : 1],
       sz2[HASQ ? T::SL : 1];
   __shared__ double scoef[2];
+  __shared__ double sG[8];   // vertex gamma values (general gamma)
 
   const int tid = threadIdx.x;
   const long long e = blockIdx.x;
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     const long long g = ((long long)(ez + (v >> 2)) * (NLy + 1) + (ey + ((v >> 1) & 1))) * (NLx + 1) +
                         (ex + (v & 1));
     sX[i] = a.vert[g * 3 + d];
+    if (HASQ && a.gvert && d == 0) sG[v] = a.gvert[g];
   }
   // gather u per component (compile-time extents, i fastest; padded smem layouts)
   if constexpr (!ZONLY) {
@@ -345,6 +348,47 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       __syncthreads();
       lines<NT, Q, P, P, 0, P, TB_G2, false, GA, L2>(ta, vd, tab);
       __syncthreads();
+      // general gamma: Z = W^-1 W_gamma W^-1 — two passes of the local CG
+      // with t = W_gamma (W^-1 q~) in between; piecewise-constant gamma: one pass, Z = s_e W^-1
+      const int npass = a.gvert ? 2 : 1;
+      for (int pass = 0; pass < npass; ++pass) {
+      if (pass == 1) {
+        // t = W_gamma y in the histopolation basis: B_h^T diag(w_q gamma_q / det J_q) B_h,
+        // y = W^-1 q~ (sz1) -> sq (free: D^T q~ was scattered before)
+        lines<NT, P, P, P, 0, Q, TB_H, true, L2, GA>(sz1, ta, tab);
+        __syncthreads();
+        lines<NT, Q, P, P, 1, Q, TB_H, true, GA, GB>(ta, tb, tab);
+        __syncthreads();
+        lines<NT, Q, Q, P, 2, Q, TB_H, true, GB, GV>(tb, tv, tab);
+        __syncthreads();
+        for (int qi = tid; qi < NQ; qi += NT) {
+          const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
+          const double xh = tab.xq[qx], yh = tab.xq[qy], zh = tab.xq[qz];
+          double g = 0.0;
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            g += sG[v] * ((v & 1) ? xh : 1 - xh) * ((v & 2) ? yh : 1 - yh) * ((v & 4) ? zh : 1 - zh);
+          const int o = qx + GV::S1 * qy + GV::S2 * qz;
+          tv[o] *= g * gq[o];
+        }
+        __syncthreads();
+        lines<NT, Q, Q, Q, 2, P, TB_H, false, GV, GB>(tv, tb, tab);
+        __syncthreads();
+        lines<NT, Q, Q, P, 1, P, TB_H, false, GB, GA>(tb, ta, tab);
+        __syncthreads();
+        lines<NT, Q, P, P, 0, P, TB_H, false, GA, L2>(ta, sq, tab);
+        __syncthreads();
+        // r = H^T t for the second solve; diag(W_g) again into vd (= sz1, which held y)
+        lines<NT, P, P, P, 0, P, TB_HGT, true, L2, L2>(sq, vz, tab);
+        lines<NT, Q, Q, Q, 2, P, TB_G2, false, GV, GB>(gq, tb, tab);
+        __syncthreads();
+        lines<NT, P, P, P, 1, P, TB_HGT, true, L2, L2>(vz, vap, tab);
+        lines<NT, Q, Q, P, 1, P, TB_G2, false, GB, GA>(tb, ta, tab);
+        __syncthreads();
+        lines<NT, P, P, P, 2, P, TB_HGT, true, L2, L2>(vap, vr, tab);
+        lines<NT, Q, P, P, 0, P, TB_G2, false, GA, L2>(ta, vd, tab);
+        __syncthreads();
+      }
       // z = 0, p = D^-1 r
       double rs = 0.0;
       for (int i = tid; i < P3; i += NT) {
@@ -406,6 +450,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       __syncthreads();
       lines<NT, P, P, P, 2, P, TB_HG, true, L2, L2>(vp, sz1, tab);
       __syncthreads();
+      }   // pass
     }
     const double z = scoef[1];
     if constexpr (ZONLY) {
@@ -530,10 +575,13 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.nrt = h->nrt;
   a.has_z = h->has_z ? 1 : 0;
   a.ess = (MODE == 2) ? 0 : h->ess;
+  a.gvert = h->d_gvert;
   a.skip = skip;
   if constexpr (MODE == 2 && P <= 2) {
-    tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
-    return cudaGetLastError();
+    if (!h->d_gvert) {
+      tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
+      return cudaGetLastError();
+    }
   }
   tri_kernel<P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
