@@ -435,6 +435,34 @@ def main():
                 del b4, xs4
                 torch.cuda.empty_cache()
 
+    # NEXT-3: the SPE10-shaped pure-Neumann Darcy solve: config 3's jittered
+    # 64^3 p=4 mesh and eps = 10^U(-2,2), u.n prescribed on every side (eliminated), gamma = 0,
+    # singular S~ with the projection after every S^-1 (one AMG V-cycle); b = A x*
+    if not args.no_minres and ws == 1:
+        from synth import make_config, random_vector
+        from paper_2304_12387_b200 import from_problem
+        prs = make_config("c3s")
+        t0s = time.time()
+        ops = from_problem(prs, schur="amg")
+        t_setup_s = time.time() - t0s
+        xs = torch.rand(ops.sizes.n, dtype=torch.float64, device="cuda") * 2 - 1
+        bs = ops.apply_block(xs)
+        ops.minres(bs, rtol=1e-12, maxit=6)   # warm-up (graph build)
+        xo, rs = ops.minres(bs, rtol=1e-12, maxit=5000)
+        nrt = ops.sizes.n_rt
+        dq = xo[nrt:] - xs[nrt:]
+        result["spe10_like"] = {
+            "workload": "config 3 mesh/coefficients (64^3 jittered hexes, p=4, eps=10^U(-2,2)), "
+                        "u.n prescribed on all six sides, gamma=0: singular S~, projection "
+                        "after every S^-1 (P:1035-1040); S^-1 = AMG V-cycle; rtol 1e-12",
+            "dofs": ops.sizes.n, "iters": rs.iters, "converged": bool(rs.converged),
+            "time_to_solve_s": rs.t_solve_ms / 1e3, "setup_s": round(t_setup_s, 2),
+            "u_err": ((xo[:nrt] - xs[:nrt]).abs().max() / xs[:nrt].abs().max()).item(),
+            "q_err_mod_const": ((dq - dq.mean()).abs().max() / xs[nrt:].abs().max()).item()}
+        ops.close()
+        del xs, bs, xo, dq
+        torch.cuda.empty_cache()
+
     # W^-1 benchmark of Table dg-mass-inv (NEXT-2): ~1.7e6 L2 DOFs on a jittered
     # hex mesh, 100 applications of the (2,2)-block inverse by the fused element-local CG
     if not args.no_minres and ws == 1:
