@@ -145,8 +145,12 @@ hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* st
  * the Gauss-Legendre nodal basis (exact Kronecker case converges in one
  * step).  q, y_q: DEVICE [n_l2].  3D only (HDIV_ERR_UNSUPPORTED in 2D). */
 hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y_q, void* stream);
-/* Same as hdiv_apply_block with HOST x, y (pinned or pageable): H2D copy, apply, D2H copy on
- * `stream`; blocks until y is on the host (end-to-end path). */
+/* Same as hdiv_apply_block with HOST x, y (pinned or pageable): H2D copy, apply, D2H copy,
+ * ordered after `stream`; blocks until y is on the host (end-to-end path).  On box meshes (one
+ * rank) the copies and the fused apply are pipelined over ~16 chunks of element layers along z
+ * on three library streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the apply of chunk c;
+ * the result is bitwise the device apply's; HDIV_HOST_PIPELINE=0 disables it).  Device staging
+ * buffers (2 vectors) are allocated on first use. */
 hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* x_host, double* y_host,
                                   void* stream);
 /* Number of kernels one hdiv_apply_block launches (for launch accounting). */

@@ -2,6 +2,7 @@
 // dispatch only; every step of the hot path runs in the kernels of this directory.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -102,6 +103,11 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_scratch);
   cudaFree(h->d_xbuf);
   cudaFree(h->d_ybuf);
+  for (int i = 0; i < 3; ++i)
+    if (h->hs[i]) cudaStreamDestroy(h->hs[i]);
+  for (int k = 0; k < 2; ++k)
+    for (int c = 0; c < hdiv_ctx::kMaxChunks; ++c)
+      if (h->hev[k][c]) cudaEventDestroy(h->hev[k][c]);
   delete h;
 }
 
@@ -502,12 +508,83 @@ hdiv_status hdiv_apply_launches(hdiv_handle h, int* n) {
   return HDIV_OK;
 }
 
+// End-to-end host apply on box meshes (one rank): the mesh is cut into chunks of element
+// layers along z (whole halo tiles) and the chunks are pipelined over three streams —
+// H2D of chunk c+1 and D2H of chunk c-1 overlap the fused apply of chunk c (PCIe is full
+// duplex).  Chunk c needs x for its own layers plus the - halo layer and the top z-face plane
+// (already sent with chunks <= c); it owns the outputs of its layers except the top z-face
+// plane, which belongs to chunk c+1 (the + tile owns a shared plane).
+static hdiv_status apply_block_host_pipelined(hdiv_ctx* h, const double* xh, double* yh,
+                                              cudaStream_t caller) {
+  int TZ = 0;
+  HDIV_CUDA_TRY(launch_affine_apply_range(h, nullptr, nullptr, 0, 0, &TZ, caller));
+  const int64_t NLz = h->NL[2], P = h->p;
+  int64_t cz = (NLz + 15) / 16;   // ~16 chunks: fill + drain cost ~2/16 of a transfer
+  cz = ((cz + TZ - 1) / TZ) * TZ;
+  const int nch = (int)((NLz + cz - 1) / cz);
+  if (nch > hdiv_ctx::kMaxChunks) return HDIV_ERR_UNSUPPORTED;
+  for (int i = 0; i < 3; ++i)
+    if (!h->hs[i]) HDIV_CUDA_TRY(cudaStreamCreateWithFlags(&h->hs[i], cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k)
+    for (int c = 0; c < nch; ++c)
+      if (!h->hev[k][c]) HDIV_CUDA_TRY(cudaEventCreateWithFlags(&h->hev[k][c], cudaEventDisableTiming));
+  cudaEvent_t start;
+  HDIV_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  HDIV_CUDA_TRY(cudaEventRecord(start, caller));
+  for (int i = 0; i < 3; ++i) HDIV_CUDA_TRY(cudaStreamWaitEvent(h->hs[i], start, 0));
+  cudaEventDestroy(start);
+  const int64_t n0 = h->n[0], n1 = h->n[1];
+  const int64_t sx = (n0 + 1) * n1, sy = n0 * (n1 + 1), sz = n0 * n1;   // doubles per K plane
+  const int64_t sq = h->NL[0] * h->NL[1] * P * P * P;                   // per element layer
+  double* dx = h->d_xbuf;
+  double* dy = h->d_ybuf;
+  auto cpy = [&](double* dst, const double* src, int64_t off, int64_t cnt, cudaMemcpyKind kd,
+                 cudaStream_t st) -> cudaError_t {
+    if (cnt <= 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst + off, src + off, sizeof(double) * cnt, kd, st);
+  };
+  for (int c = 0; c < nch; ++c) {
+    const int64_t z0 = c * cz, z1 = std::min<int64_t>(NLz, z0 + cz);
+    const bool last = (z1 == NLz);
+    const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+    // H2D: x/y faces of planes [z0 P, z1 P), z faces (previous top, z1 P], q layers [z0, z1)
+    const int64_t Ka = (c == 0) ? 0 : z0 * P + 1, Kb = z1 * P + 1;
+    HDIV_CUDA_TRY(cpy(dx, xh, h->off[0] + sx * z0 * P, sx * (z1 - z0) * P, H2D, h->hs[0]));
+    HDIV_CUDA_TRY(cpy(dx, xh, h->off[1] + sy * z0 * P, sy * (z1 - z0) * P, H2D, h->hs[0]));
+    HDIV_CUDA_TRY(cpy(dx, xh, h->off[2] + sz * Ka, sz * (Kb - Ka), H2D, h->hs[0]));
+    HDIV_CUDA_TRY(cpy(dx, xh, h->nrt + sq * z0, sq * (z1 - z0), H2D, h->hs[0]));
+    HDIV_CUDA_TRY(cudaEventRecord(h->hev[0][c], h->hs[0]));
+    // fused apply of the chunk's tiles
+    HDIV_CUDA_TRY(cudaStreamWaitEvent(h->hs[1], h->hev[0][c], 0));
+    HDIV_CUDA_TRY(launch_affine_apply_range(h, dx, dy, (int)(z0 / TZ), (int)((z1 + TZ - 1) / TZ),
+                                            nullptr, h->hs[1]));
+    HDIV_CUDA_TRY(cudaEventRecord(h->hev[1][c], h->hs[1]));
+    // D2H of the owned outputs
+    HDIV_CUDA_TRY(cudaStreamWaitEvent(h->hs[2], h->hev[1][c], 0));
+    const int64_t Ke = last ? z1 * P + 1 : z1 * P;
+    HDIV_CUDA_TRY(cpy(yh, dy, h->off[0] + sx * z0 * P, sx * (z1 - z0) * P, D2H, h->hs[2]));
+    HDIV_CUDA_TRY(cpy(yh, dy, h->off[1] + sy * z0 * P, sy * (z1 - z0) * P, D2H, h->hs[2]));
+    HDIV_CUDA_TRY(cpy(yh, dy, h->off[2] + sz * z0 * P, sz * (Ke - z0 * P), D2H, h->hs[2]));
+    HDIV_CUDA_TRY(cpy(yh, dy, h->nrt + sq * z0, sq * (z1 - z0), D2H, h->hs[2]));
+  }
+  HDIV_CUDA_TRY(cudaStreamSynchronize(h->hs[2]));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(h->hs[1]));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(h->hs[0]));
+  return HDIV_OK;
+}
+
 hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* xh, double* yh, void* stream) {
   if (!h || !xh || !yh) return fail(HDIV_ERR_NULL, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = sizeof(double) * (h->nrt + h->nl2);
   if (!h->d_xbuf) HDIV_CUDA_TRY(cudaMalloc(&h->d_xbuf, bytes));
   if (!h->d_ybuf) HDIV_CUDA_TRY(cudaMalloc(&h->d_ybuf, bytes));
+  const char* ep = getenv("HDIV_HOST_PIPELINE");
+  const bool pipe = !(ep && atoi(ep) == 0);
+  if (pipe && h->kernel == 2 && h->dim == 3 && h->nranks == 1 && h->NL[2] >= 2) {
+    hdiv_status st = apply_block_host_pipelined(h, xh, yh, s);
+    if (st != HDIV_ERR_UNSUPPORTED) return st;
+  }
   HDIV_CUDA_TRY(cudaMemcpyAsync(h->d_xbuf, xh, bytes, cudaMemcpyHostToDevice, s));
   HDIV_CUDA_TRY(apply_block_dev(h, h->d_xbuf, h->d_ybuf, nullptr, s));
   HDIV_CUDA_TRY(cudaMemcpyAsync(yh, h->d_ybuf, bytes, cudaMemcpyDeviceToHost, s));

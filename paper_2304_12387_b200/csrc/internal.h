@@ -86,6 +86,9 @@ struct hdiv_ctx {
   double* d_scratch = nullptr;    // reduction partials etc.
   double* d_xbuf = nullptr;       // host-API staging (lazily allocated)
   double* d_ybuf = nullptr;
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host pipeline: H2D, compute, D2H
+  static constexpr int kMaxChunks = 32;
+  cudaEvent_t hev[2][kMaxChunks] = {};                // H2D done / compute done per chunk
   // NEXT-3: essential (eliminated) RT sides of THIS rank's slab, bit 2a = side x_a = min of
   // the local grid, bit 2a+1 = max (the last-axis bits only where the slab touches the domain
   // boundary); 0 = natural everywhere
@@ -112,6 +115,8 @@ void set_error(const std::string& s);
 
 namespace hdiv {
 // kernel launchers (return cudaGetLastError())
+cudaError_t launch_affine_apply_range(const hdiv_ctx* h, const double* x, double* y, int tz0,
+                                      int tz1, int* tz_out, cudaStream_t s);
 cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                 const int* skip, cudaStream_t s);
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,

@@ -117,8 +117,17 @@ struct AffArgs {
   int ntile[3];
   int has_z;
   int ess;             // eliminated essential sides (NEXT-3), local bitmask (0: none)
+  int tz0;             // first z tile of this launch (z-chunked host pipeline; else 0)
   const int* skip;     // MINRES done flag (nullptr: never skip)
 };
+
+// z-tile range of the next halo-tile launch (host side, set by launch_affine_apply_range):
+// tz1 < 0 = all tiles; tz_out != nullptr = only report the variant's TZ, launch nothing
+struct TileRange {
+  int tz0 = 0, tz1 = -1;
+  int* tz_out = nullptr;
+};
+static thread_local TileRange g_range;
 
 struct TileInfo {
   int e0[3];    // first element of the tile
@@ -445,7 +454,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     const int tx = t % a.ntile[0];
     t /= a.ntile[0];
     const int ty = t % a.ntile[1];
-    const int tz = t / a.ntile[1];
+    const int tz = t / a.ntile[1] + a.tz0;
     const int T3[3] = {TX, TY, TZ};
     const int tt[3] = {tx, ty, tz};
 #pragma unroll
@@ -629,6 +638,13 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.has_z = h->has_z ? 1 : 0;
   a.ess = h->ess;
   a.skip = skip;
+  if (g_range.tz_out) {   // query: the variant's tile depth along z
+    *g_range.tz_out = TZ;
+    return cudaSuccess;
+  }
+  const int tz1 = (g_range.tz1 < 0) ? a.ntile[2] : min(g_range.tz1, a.ntile[2]);
+  a.tz0 = g_range.tz0;
+  if (tz1 <= a.tz0) return cudaSuccess;
   const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
   auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD>;
   static bool attr_done = false;   // per instantiation
@@ -638,7 +654,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const long long nblk = (long long)a.ntile[0] * a.ntile[1] * a.ntile[2];
+  const long long nblk = (long long)a.ntile[0] * a.ntile[1] * (tz1 - a.tz0);
   kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff);
   return cudaGetLastError();
 }
@@ -1005,6 +1021,7 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ntile[2] = (int)((h->NL[2] + zc - 1) / zc);
   a.has_z = h->has_z ? 1 : 0;
   a.ess = 0;   // the marching kernel is not dispatched with eliminated sides
+  a.tz0 = 0;
   a.skip = skip;
   const size_t smem = M::smem_doubles(BLOCK) * sizeof(double);
   auto kern = affine_march_kernel<P, TX, TY, NT, BLOCK>;
@@ -1045,7 +1062,8 @@ template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
                      cudaStream_t s) {
   const int mv = march_variant(h->p);
-  if (mv >= 0 && !h->ess) {
+  const bool ranged = g_range.tz_out != nullptr || g_range.tz1 >= 0 || g_range.tz0 != 0;
+  if (mv >= 0 && !h->ess && !ranged) {
     switch (h->p) {
       case 1: return launch_m<1, 8, 8, 128, BLOCK>(h, x, y, k, s);
       case 2:
@@ -1130,6 +1148,18 @@ cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, i
                                 const int* skip, cudaStream_t s) {
   if (mode == MODE_BLOCK) return dispatch<true>(h, x, y, skip, s);
   return dispatch<false>(h, x, y, skip, s);
+}
+
+// the block apply restricted to the halo tiles with z-tile index in [tz0, tz1) (the z-chunked
+// host pipeline of hdiv_apply_block_host); tz_out != nullptr: report the tile depth only
+cudaError_t launch_affine_apply_range(const hdiv_ctx* h, const double* x, double* y, int tz0,
+                                      int tz1, int* tz_out, cudaStream_t s) {
+  g_range.tz0 = tz0;
+  g_range.tz1 = tz1;
+  g_range.tz_out = tz_out;
+  cudaError_t e = dispatch<true>(h, x, y, nullptr, s);
+  g_range = TileRange();
+  return e;
 }
 
 }  // namespace hdiv

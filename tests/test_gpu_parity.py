@@ -346,3 +346,27 @@ def test_gmres_triangular_parity(name, N, p, schur):
     assert conv_o and rep.converged
     assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
     assert _rel(_host(x), xo) < 1e-7
+
+
+# ---- end-to-end host apply: z-chunked H2D / apply / D2H pipeline (box meshes) ----
+@pytest.mark.parametrize("name,N,p,ess", [("c2", (5, 3, 19), 4, 0), ("c2", (4, 3, 17), 3, 63),
+                                          ("c5", (5, 5, 9), 2, 0), ("c2", (3, 2, 33), 6, 48),
+                                          ("c3", (3, 2, 9), 2, 0)])
+def test_host_apply_pipeline_matches_device_apply(name, N, p, ess, monkeypatch):
+    """hdiv_apply_block_host (pinned host buffers) returns exactly the device apply's bytes,
+    for chunk boundaries inside the mesh, every tile depth, eliminated sides, and (c3) the
+    unpipelined quadrature path."""
+    import torch
+    pr = _problem(name, N, p)
+    pr.essential = ess
+    op = _gpu(pr)
+    n = op.sizes.n
+    x = random_vector(n, 23)
+    y = _host(op.apply_block(_dev(x)))
+    xh = torch.from_numpy(x).pin_memory()
+    for pipe in ("1", "0"):
+        monkeypatch.setenv("HDIV_HOST_PIPELINE", pipe)
+        yh = torch.full((n,), np.nan, dtype=torch.float64).pin_memory()
+        op.apply_block_host(xh, yh)
+        assert np.array_equal(yh.numpy(), y), pipe
+    op.close()
