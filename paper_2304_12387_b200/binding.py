@@ -121,6 +121,13 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def loopback_id(key: int) -> bytes:
+    """Communicator id of a LOOPBACK slab group (single-GPU tests of the multi-rank path): the P
+    ranks live in one process, one host thread each, and exchange by device-to-device copies
+    (libhdiv comm.cu); `key` names the group."""
+    return b"HDIVLOOP" + int(key).to_bytes(8, "little") + bytes(112)
+
+
 def debug_tables(p: int, Q: int = 0) -> dict:
     """Host-only: the library's 1D tables (no GPU needed)."""
     lib = load_library()

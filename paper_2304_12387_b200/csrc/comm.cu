@@ -17,7 +17,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
 
 #include "internal.h"
 
@@ -95,10 +100,42 @@ __global__ void pack_l2_layers_kernel(const double* __restrict__ x, double* lo, 
     if (hi) hi[i] = x[(ex + NLx * (NLy - 1)) * pd + a + p * (p - 1)];
   }
 }
+
+// Loopback communicator for single-GPU tests of the slab path: the P ranks live in ONE process,
+// each driven by its own host thread on its own stream; the id passed to hdiv_setup is
+// "HDIVLOOP" + a 64-bit group key.  Every exchange posts the rank's send pointers, records an
+// event, meets the others at a host barrier, then copies device-to-device from the peers'
+// buffers after their events (and a second barrier + event wait keeps the senders' buffers
+// untouched until the peers' copies are done).  Same data movement as the NCCL path.
+struct LoopGroup {
+  int P = 0, members = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+  std::vector<const double*> send_lo, send_hi;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+std::mutex g_loop_m;
+std::map<unsigned long long, std::shared_ptr<LoopGroup>> g_loops;
+const char kLoopMagic[8] = {'H', 'D', 'I', 'V', 'L', 'O', 'O', 'P'};
 }  // namespace
 
 struct Comm {
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LoopGroup> loop;   // loopback group (tests), else NCCL
+  unsigned long long loop_key = 0;
   int rank = 0, P = 1;
   long long plane = 0;      // RT interface plane size (faces)
   long long lplane = 0;     // L2 ghost layer size (cells)
@@ -111,20 +148,73 @@ static hdiv_status nccl_fail(ncclResult_t r, const char* what) {
   return HDIV_ERR_NCCL;
 }
 
+// exchange with the two slab neighbours through the loopback group: send_lo -> rank-1 (its
+// recv_hi), send_hi -> rank+1 (its recv_lo); n doubles each
+static hdiv_status loop_exchange(hdiv_ctx* h, const double* send_lo, const double* send_hi,
+                                 double* recv_lo, double* recv_hi, long long n, cudaStream_t s) {
+  Comm* c = h->comm;
+  LoopGroup& g = *c->loop;
+  const int r = c->rank;
+  g.send_lo[r] = send_lo;
+  g.send_hi[r] = send_hi;
+  HDIV_CUDA_TRY(cudaEventRecord(g.ev_ready[r], s));
+  g.barrier();
+  if (recv_lo && r > 0) {
+    HDIV_CUDA_TRY(cudaStreamWaitEvent(s, g.ev_ready[r - 1], 0));
+    HDIV_CUDA_TRY(cudaMemcpyAsync(recv_lo, g.send_hi[r - 1], sizeof(double) * n,
+                                  cudaMemcpyDeviceToDevice, s));
+  }
+  if (recv_hi && r < c->P - 1) {
+    HDIV_CUDA_TRY(cudaStreamWaitEvent(s, g.ev_ready[r + 1], 0));
+    HDIV_CUDA_TRY(cudaMemcpyAsync(recv_hi, g.send_lo[r + 1], sizeof(double) * n,
+                                  cudaMemcpyDeviceToDevice, s));
+  }
+  HDIV_CUDA_TRY(cudaEventRecord(g.ev_done[r], s));
+  g.barrier();
+  if (r > 0) HDIV_CUDA_TRY(cudaStreamWaitEvent(s, g.ev_done[r - 1], 0));
+  if (r < c->P - 1) HDIV_CUDA_TRY(cudaStreamWaitEvent(s, g.ev_done[r + 1], 0));
+  g.barrier();   // the event slots may be re-recorded by the next exchange only after this
+  return HDIV_OK;
+}
+
+bool comm_is_loopback(const hdiv_ctx* h) { return h->comm && h->comm->loop; }
+
 hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s) {
   (void)s;
-  std::string err;
-  if (!load_nccl(&err)) { set_error(err); return HDIV_ERR_NCCL; }
   auto* c = new Comm();
   h->comm = c;
   c->rank = h->rank;
   c->P = h->nranks;
   c->plane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
   c->lplane = c->plane;
+  if (std::memcmp(id, kLoopMagic, 8) == 0) {   // loopback group (single-GPU tests)
+    std::memcpy(&c->loop_key, (const char*)id + 8, sizeof(c->loop_key));
+    {
+      std::lock_guard<std::mutex> lk(g_loop_m);
+      auto& gp = g_loops[c->loop_key];
+      if (!gp) {
+        gp = std::make_shared<LoopGroup>();
+        gp->P = c->P;
+        gp->ev_ready.assign(c->P, nullptr);
+        gp->ev_done.assign(c->P, nullptr);
+        gp->send_lo.assign(c->P, nullptr);
+        gp->send_hi.assign(c->P, nullptr);
+      }
+      if (gp->P != c->P) { set_error("loopback group size mismatch"); return HDIV_ERR_SHAPE; }
+      c->loop = gp;
+      ++gp->members;
+    }
+    HDIV_CUDA_TRY(cudaEventCreateWithFlags(&c->loop->ev_ready[c->rank], cudaEventDisableTiming));
+    HDIV_CUDA_TRY(cudaEventCreateWithFlags(&c->loop->ev_done[c->rank], cudaEventDisableTiming));
+    c->loop->barrier();   // every rank registered
+  } else {
+  std::string err;
+  if (!load_nccl(&err)) { set_error(err); return HDIV_ERR_NCCL; }
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
   ncclResult_t r = g_nccl.CommInitRank(&c->comm, c->P, uid, c->rank);
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+  }
   HDIV_CUDA_TRY(cudaMalloc(&c->buf, sizeof(double) * 4 * c->plane));
   c->rlo = c->buf;
   c->rhi = c->buf + c->plane;
@@ -135,6 +225,16 @@ hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s) {
 
 void comm_free(hdiv_ctx* h) {
   if (!h->comm) return;
+  if (h->comm->loop) {
+    std::lock_guard<std::mutex> lk(g_loop_m);
+    auto& gp = h->comm->loop;
+    if (--gp->members == 0) {
+      for (auto e : gp->ev_ready) if (e) cudaEventDestroy(e);
+      for (auto e : gp->ev_done) if (e) cudaEventDestroy(e);
+      g_loops.erase(h->comm->loop_key);
+    }
+    h->comm->loop.reset();
+  }
   if (h->comm->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm->comm);
   cudaFree(h->comm->buf);
   delete h->comm;
@@ -154,6 +254,15 @@ hdiv_status comm_reverse_add(hdiv_ctx* h, double* y, cudaStream_t s) {
   if (!c) return HDIV_OK;
   double *lo, *hi;
   planes(h, y, &lo, &hi);
+  if (c->loop) {
+    hdiv_status st = loop_exchange(h, lo, hi, lo ? c->rlo : nullptr, hi ? c->rhi : nullptr,
+                                   c->plane, s);
+    if (st != HDIV_OK) return st;
+    add_planes_kernel<<<(unsigned)((c->plane + 255) / 256), 256, 0, s>>>(lo, c->rlo, hi, c->rhi,
+                                                                         c->plane);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    return HDIV_OK;
+  }
   ncclResult_t r = g_nccl.GroupStart();
   if (lo) {
     g_nccl.Send(lo, c->plane, ncclDouble, c->rank - 1, c->comm, s);
@@ -182,6 +291,9 @@ hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s) {
   HDIV_CUDA_TRY(cudaGetLastError());
   double* glo = x + h->nl2;
   double* ghi = x + h->nl2 + c->lplane;
+  if (c->loop)
+    return loop_exchange(h, down ? c->slo : nullptr, up ? c->shi : nullptr,
+                         down ? glo : nullptr, up ? ghi : nullptr, c->lplane, s);
   ncclResult_t r = g_nccl.GroupStart();
   if (down) {
     g_nccl.Send(c->slo, c->lplane, ncclDouble, c->rank - 1, c->comm, s);
@@ -199,6 +311,24 @@ hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s) {
 // all-gather of k local scalars into glob[P][k] (rank-ordered)
 hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, cudaStream_t s) {
   Comm* c = h->comm;
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    const int rk = c->rank;
+    g.send_lo[rk] = loc;
+    HDIV_CUDA_TRY(cudaEventRecord(g.ev_ready[rk], s));
+    g.barrier();
+    for (int q = 0; q < c->P; ++q) {
+      if (q != rk) HDIV_CUDA_TRY(cudaStreamWaitEvent(s, g.ev_ready[q], 0));
+      HDIV_CUDA_TRY(cudaMemcpyAsync(glob + (size_t)q * k, g.send_lo[q], sizeof(double) * k,
+                                    cudaMemcpyDeviceToDevice, s));
+    }
+    HDIV_CUDA_TRY(cudaEventRecord(g.ev_done[rk], s));
+    g.barrier();
+    for (int q = 0; q < c->P; ++q)
+      if (q != rk) HDIV_CUDA_TRY(cudaStreamWaitEvent(s, g.ev_done[q], 0));
+    g.barrier();
+    return HDIV_OK;
+  }
   ncclResult_t r = g_nccl.AllGather(loc, glob, k, ncclDouble, c->comm, s);
   if (r != ncclSuccess) return nccl_fail(r, "allgather");
   return HDIV_OK;

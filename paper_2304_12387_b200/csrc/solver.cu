@@ -28,6 +28,7 @@ namespace hdiv {
 
 hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s);
 hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, cudaStream_t s);
+bool comm_is_loopback(const hdiv_ctx* h);
 
 namespace {
 
@@ -633,8 +634,9 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
   // capture 6 iterations (the buffer pattern repeats with period 6)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  bool use_graph = true;
-  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+  // (the loopback test communicator meets its peers at host barriers: no graph capture)
+  bool use_graph = !comm_is_loopback(h);
+  if (!use_graph || cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     use_graph = false;
     cudaGetLastError();
   } else {

@@ -1,0 +1,137 @@
+"""GPU parity of the multi-rank slab path on ONE GPU: P ranks of one
+process (one host thread and stream each) joined by libhdiv's loopback communicator, which moves
+the same interface planes, L2 ghost layers and all-gathered scalars as the NCCL path by
+device-to-device copies.  Every rank's slab result must match the single-rank result on the same
+global problem: block applies (reverse-added interface planes), M~, S~ with ghost columns inside
+S^-1, and MINRES (masked dots, rank-ordered sums: iteration counts +-1, solutions 1e-9)."""
+import threading
+
+import numpy as np
+import pytest
+
+from synth import make_config, random_vector
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    d = np.abs(np.asarray(a) - np.asarray(b)).max()
+    s = np.abs(np.asarray(b)).max()
+    return d / s if s > 0 else d
+
+
+def _run_slabs(pr, P, fn, key, **kw):
+    """fn(rank, op, rt_map, l2_map) on every rank (threads); returns the per-rank results."""
+    import torch
+    from paper_2304_12387_b200 import HdivOperator, slabs
+    from paper_2304_12387_b200.binding import loopback_id
+    uid = loopback_id(key)
+    out, errs = [None] * P, []
+    last = pr.dim - 1
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                z0, z1 = slabs.slab_bounds(pr.N[last], P, r)
+                V, a, b, g, e = slabs.slab_inputs(pr, z0, z1)
+                op = HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b,
+                                  gamma=g, eps=e, essential=pr.essential,
+                                  project_mean=pr.project_mean, slab=(z0, z1), nccl_id=uid,
+                                  rank=r, nranks=P, **kw)
+                rt = slabs.local_to_global_rt(pr.dim, pr.N, pr.p, z0, z1)
+                l2 = slabs.local_to_global_l2(pr.dim, pr.N, pr.p, z0, z1)
+                out[r] = fn(r, op, rt, l2)
+                torch.cuda.current_stream().synchronize()
+                op.close()
+        except Exception as ex:   # pragma: no cover - surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
+
+
+def _problem(name, N, p, ess=0, project=False):
+    pr = make_config(name, N=N, p=p)
+    if name == "c2":
+        pr.alpha = 10.0 ** random_vector(pr.E, 31)
+        pr.beta = 10.0 ** random_vector(pr.E, 32)
+    pr.essential, pr.project_mean = ess, project
+    return pr
+
+
+CASES = [("c2", (4, 3, 6), 3, 2, 0), ("c2", (3, 4, 7), 2, 3, 0), ("c3", (3, 3, 4), 2, 2, 0),
+         ("c1", (4, 6), 2, 3, 0), ("c2", (4, 3, 5), 4, 2, 63), ("c5", (5, 5, 6), 2, 2, 0)]
+
+
+@pytest.mark.parametrize("name,N,p,P,ess", CASES)
+def test_slab_apply_and_diag(name, N, p, P, ess):
+    import torch
+    from paper_2304_12387_b200 import from_problem
+    pr = _problem(name, N, p, ess)
+    ref = from_problem(pr)
+    n_rt = ref.sizes.n_rt
+    x = random_vector(ref.sizes.n, 11)
+    y = ref.apply_block(torch.from_numpy(x).cuda()).cpu().numpy()
+    md = ref.mass_diag().cpu().numpy()
+    ref.close()
+
+    def fn(r, op, rt, l2):
+        xl = np.concatenate([x[:n_rt][rt], x[n_rt:][l2]])
+        yl = op.apply_block(torch.from_numpy(xl).cuda()).cpu().numpy()
+        return yl, op.mass_diag().cpu().numpy(), rt, l2
+
+    res = _run_slabs(pr, P, fn, key=1000 + hash((name, N, p, P, ess)) % 1000)
+    planes = {}
+    for yl, mdl, rt, l2 in res:
+        nrl = len(rt)
+        assert _rel(yl[:nrl], y[:n_rt][rt]) < 1e-12
+        assert _rel(yl[nrl:], y[n_rt:][l2]) < 1e-12
+        assert _rel(mdl, md[rt]) < 1e-12
+        for i, g in enumerate(rt):   # replicated interface faces: bitwise equal on both ranks
+            if g in planes:
+                assert planes[g] == yl[i]
+            planes[g] = yl[i]
+
+
+@pytest.mark.parametrize("name,N,p,P,ess,project", [("c2", (4, 3, 6), 3, 2, 0, False),
+                                                    ("c3", (3, 3, 4), 2, 2, 0, False),
+                                                    ("c1", (4, 6), 2, 3, 0, False),
+                                                    ("c3", (3, 3, 4), 2, 2, 63, True)])
+def test_slab_minres(name, N, p, P, ess, project):
+    import torch
+    from paper_2304_12387_b200 import from_problem
+    pr = _problem(name, N, p, ess, project)
+    if project:
+        pr.gamma = np.zeros(pr.E)
+    ref = from_problem(pr)
+    n_rt = ref.sizes.n_rt
+    xs = random_vector(ref.sizes.n, 3)
+    b = ref.apply_block(torch.from_numpy(xs).cuda())
+    x1, rep1 = ref.minres(b, rtol=1e-12, maxit=3000)
+    b = b.cpu().numpy()
+    x1 = x1.cpu().numpy()
+    ref.close()
+
+    def fn(r, op, rt, l2):
+        bl = np.concatenate([b[:n_rt][rt], b[n_rt:][l2]])
+        xl, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
+        return xl.cpu().numpy(), rep.iters, rep.converged, rt, l2
+
+    res = _run_slabs(pr, P, fn, key=2000 + hash((name, N, p, P, ess)) % 1000)
+    its = {r[1] for r in res}
+    assert len(its) == 1, its                     # every rank takes the same decisions
+    assert all(r[2] for r in res) and abs(res[0][1] - rep1.iters) <= 1, (res[0][1], rep1.iters)
+    dqs = []
+    for xl, _, _, rt, l2 in res:
+        nrl = len(rt)
+        assert _rel(xl[:nrl], x1[:n_rt][rt]) < 1e-9
+        dqs.append(xl[nrl:] - x1[n_rt:][l2])
+    c = np.concatenate(dqs).mean() if project else 0.0   # p~ unique up to ONE global constant
+    for dq in dqs:
+        assert np.abs(dq - c).max() < 1e-9 * np.abs(x1[n_rt:]).max()
