@@ -313,18 +313,26 @@ struct StA {
   long long d[3], n;
   int dim;
   const double* st;
+  int id[3];   // 32-bit extents: coarse levels have < 2^31 rows (row coordinates in 32-bit)
+  // sum_k st[k][i] f(j_k, x_k, y_k, z_k) over the in-range 3^d neighbours (x_k, y_k, z_k) of row i
   template <class F>
-  __device__ __forceinline__ double dot(long long i, F f) const {
-    const long long X = i % d[0], Y = (i / d[0]) % d[1], Z = i / (d[0] * d[1]);
+  __device__ __forceinline__ double dot_xyz(long long i, F f) const {
+    const int ii = (int)i;
+    const int X = ii % id[0], r = ii / id[0], Y = r % id[1], Z = r / id[1];
     const int NS = (dim == 3) ? 27 : 9;
     double s = 0.0;
+#pragma unroll 9
     for (int k = 0; k < NS; ++k) {
       const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = (dim == 3) ? k / 9 - 1 : 0;
-      const long long x = X + dx, y = Y + dy, z = Z + dz;
-      if (x < 0 || y < 0 || z < 0 || x >= d[0] || y >= d[1] || z >= d[2]) continue;
-      s = fma(st[k * n + i], f(x + d[0] * (y + d[1] * z)), s);
+      const int x = X + dx, y = Y + dy, z = Z + dz;
+      if (x < 0 || y < 0 || z < 0 || x >= id[0] || y >= id[1] || z >= id[2]) continue;
+      s = fma(st[k * n + i], f(ii + dx + id[0] * (dy + id[1] * dz), x, y, z), s);
     }
     return s;
+  }
+  template <class F>
+  __device__ __forceinline__ double dot(long long i, F f) const {
+    return dot_xyz(i, [&](int j, int, int, int) { return f((long long)j); });
   }
   __device__ __forceinline__ long long agg(long long j, long long cd0, long long cd1) const {
     const long long X = j % d[0], Y = (j / d[0]) % d[1], Z = j / (d[0] * d[1]);
@@ -365,23 +373,31 @@ __global__ void __launch_bounds__(ANT) scale_kernel(long long n, const double* _
 }
 
 // s = r - omega A D^-1 r with r = b - A x  (computed in two passes: r then s)
+// r = b - A x and t = D^-1 r (so the next pass gathers one vector, not two)
 template <class Acc>
 __global__ void __launch_bounds__(ANT) resid_kernel(Acc A, long long n, const double* __restrict__ b,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ r,
+                                                    const double* __restrict__ dinv,
+                                                    double* __restrict__ t,
                                                     const int* __restrict__ done) {
   if (done && *done) return;
-  AMG_LOOP(n) r[i] = b[i] - A.dot(i, [&](long long j) { return x[j]; });
+  AMG_LOOP(n) {
+    const double ri = b[i] - A.dot(i, [&](long long j) { return x[j]; });
+    r[i] = ri;
+    t[i] = dinv[i] * ri;
+  }
 }
 
+// s = r - omega A t, t = D^-1 r
 template <class Acc>
 __global__ void __launch_bounds__(ANT) smooth_r_kernel(Acc A, long long n,
                                                        const double* __restrict__ r,
-                                                       const double* __restrict__ dinv, double omega,
+                                                       const double* __restrict__ t, double omega,
                                                        double* __restrict__ s,
                                                        const int* __restrict__ done) {
   if (done && *done) return;
-  AMG_LOOP(n) s[i] = r[i] - omega * A.dot(i, [&](long long j) { return dinv[j] * r[j]; });
+  AMG_LOOP(n) s[i] = r[i] - omega * A.dot(i, [&](long long j) { return t[j]; });
 }
 
 // b_c[I] = sum over aggregate I of s (level 0: element-major fine rows)
@@ -437,16 +453,28 @@ __global__ void __launch_bounds__(ANT) prolong_kernel(Acc A, Agg agg, long long 
   }
 }
 
+// stencil levels: the aggregate of a neighbour from its coordinates (no index division)
+__global__ void __launch_bounds__(ANT) prolong_st_kernel(StA A, long long cd0, long long cd1,
+                                                         long long n, const double* __restrict__ x,
+                                                         const double* __restrict__ ec,
+                                                         const double* __restrict__ dinv,
+                                                         double omega, double* __restrict__ xout,
+                                                         const int* __restrict__ done) {
+  if (done && *done) return;
+  const int c0 = (int)cd0, c1 = (int)cd1;
+  AMG_LOOP(n) {
+    const double ae = A.dot_xyz(i, [&](int, int x, int y, int z) {
+      return ec[x / 3 + c0 * (y / 3 + c1 * (z / 3))];
+    });
+    const int ii = (int)i;
+    const int X = ii % A.id[0], r = ii / A.id[0], Y = r % A.id[1], Z = r / A.id[1];
+    xout[i] = x[i] + ec[X / 3 + c0 * (Y / 3 + c1 * (Z / 3))] - omega * dinv[i] * ae;
+  }
+}
+
 struct Agg0 {
   const int32_t* a;
   __device__ __forceinline__ long long operator()(long long j) const { return a[j]; }
-};
-struct AggS {
-  long long d0, d1, cd0, cd1;
-  __device__ __forceinline__ long long operator()(long long j) const {
-    const long long X = j % d0, Y = (j / d0) % d1, Z = j / (d0 * d1);
-    return X / 3 + cd0 * (Y / 3 + cd1 * (Z / 3));
-  }
 };
 
 // coarsest: x = A^-1 b (dense, one CTA)
@@ -490,6 +518,7 @@ OpS make_ops(const AmgLevel& L) {
 
 StA make_sta(const AmgLevel& L) {
   StA o;
+  for (int a = 0; a < 3; ++a) o.id[a] = (int)L.d[a];
   for (int a = 0; a < 3; ++a) o.d[a] = L.d[a];
   o.n = L.n;
   o.dim = L.dim;
@@ -700,12 +729,12 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   }
   // r = b - A x ; s = r - omega A D^-1 r ; b_c = aggregate sums of s
   if (lev0) {
-    resid_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, b, cur, L.r, done);
-    smooth_r_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, L.r, L.dinv, L.omega, L.sv, done);
+    resid_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, b, cur, L.r, L.dinv, nxt, done);
+    smooth_r_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, L.r, nxt, L.omega, L.sv, done);
     aggsum0_kernel<<<nbk(C.n), ANT, 0, s>>>(make_op0(h), C.d[0], C.d[1], C.n, L.sv, C.b, done);
   } else {
-    resid_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, cur, L.r, done);
-    smooth_r_kernel<StA><<<g, ANT, 0, s>>>(sta, n, L.r, L.dinv, L.omega, L.sv, done);
+    resid_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, cur, L.r, L.dinv, nxt, done);
+    smooth_r_kernel<StA><<<g, ANT, 0, s>>>(sta, n, L.r, nxt, L.omega, L.sv, done);
     aggsumS_kernel<<<nbk(C.n), ANT, 0, s>>>(L.d[0], L.d[1], L.d[2], C.d[0], C.d[1], C.n, L.dim,
                                             L.sv, C.b, done);
   }
@@ -718,8 +747,8 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   if (lev0)
     prolong_kernel<SellA, Agg0><<<g, ANT, 0, s>>>(sa, Agg0{H->agg0}, n, cur, ecv, L.dinv, L.omega, nxt, done);
   else
-    prolong_kernel<StA, AggS><<<g, ANT, 0, s>>>(sta, AggS{L.d[0], L.d[1], C.d[0], C.d[1]}, n, cur,
-                                                ecv, L.dinv, L.omega, nxt, done);
+    prolong_st_kernel<<<g, ANT, 0, s>>>(sta, C.d[0], C.d[1], n, cur, ecv, L.dinv, L.omega, nxt,
+                                        done);
   HDIV_CUDA_TRY(cudaGetLastError());
   std::swap(cur, nxt);
   // post-smoothing; the last sweep writes x
