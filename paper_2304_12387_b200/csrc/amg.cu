@@ -477,17 +477,21 @@ struct Agg0 {
   __device__ __forceinline__ long long operator()(long long j) const { return a[j]; }
 };
 
-// coarsest: x = A^-1 b (dense, one CTA)
+// coarsest: x = A^-1 b (dense): one warp per row, lanes over the columns (coalesced row reads,
+// fixed-order lane sums -> deterministic); many CTAs so the inverse streams from all SMs
 __global__ void __launch_bounds__(ANT) coarse_kernel(const double* __restrict__ cinv, long long nc,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ x,
                                                      const int* __restrict__ done) {
   if (done && *done) return;
-  for (long long i = threadIdx.x; i < nc; i += ANT) {
-    double s = 0.0;
-    for (long long j = 0; j < nc; ++j) s = fma(cinv[i * nc + j], b[j], s);
-    x[i] = s;
-  }
+  const long long w = blockIdx.x * (long long)(ANT / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (w >= nc) return;
+  const double* row = cinv + w * nc;
+  double s = 0.0;
+  for (long long j = lane; j < nc; j += 32) s = fma(row[j], b[j], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[w] = s;
 }
 
 inline unsigned nbk(long long n) {
@@ -704,7 +708,8 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   AmgHier* H = h->amg;
   AmgLevel& L = H->L[l];
   if (l + 1 == H->L.size()) {
-    coarse_kernel<<<1, ANT, 0, s>>>(H->cinv, L.n, b, x, done);
+    coarse_kernel<<<(unsigned)((L.n + ANT / 32 - 1) / (ANT / 32)), ANT, 0, s>>>(H->cinv, L.n, b, x,
+                                                                               done);
     return cudaGetLastError() == cudaSuccess ? HDIV_OK : HDIV_ERR_CUDA;
   }
   AmgLevel& C = H->L[l + 1];

@@ -19,6 +19,7 @@
 // Every kernel reads the device `done` flag and returns early once converged.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -70,19 +71,19 @@ dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__device__ __forceinline__ double sum_partials(const double* part) {
+__device__ __forceinline__ double sum_partials(const double* part, int nb) {
   double s = 0.0;
-  for (int i = threadIdx.x; i < RED_BLOCKS; i += RED_NT) s += part[i];
+  for (int i = threadIdx.x; i < nb; i += RED_NT) s += part[i];
   return block_sum(s);
 }
 
-// loc[0] = sum(part_a) (+ sum(part_b))
+// loc[0] = sum(part_a) (+ sum(part_b)); nb = the reduction grid of the partials
 __global__ void __launch_bounds__(RED_NT)
 local_reduce_kernel(const double* part_a, const double* part_b, double* loc,
-                    const int* __restrict__ done) {
+                    const int* __restrict__ done, int nb) {
   if (done && *done) return;
-  double s = sum_partials(part_a);
-  double t = part_b ? sum_partials(part_b) : 0.0;
+  double s = sum_partials(part_a, nb);
+  double t = part_b ? sum_partials(part_b, nb) : 0.0;
   if (threadIdx.x == 0) loc[0] = s + t;
 }
 
@@ -92,21 +93,19 @@ __device__ __forceinline__ double rank_sum(const double* glob, int P) {
   return s;
 }
 
-__global__ void fin_delta_kernel(const double* glob, int P, MState* st) {
-  if (threadIdx.x != 0 || st->done) return;
-  st->delta = rank_sum(glob, P) / (st->gamma * st->gamma);
-}
 
+// delta = <Az, z>/gamma^2 from the all-gathered partial (fused: no separate scalar launch);
 // v_new = Az/g - (delta/g) v - (g/g_old) v_old ; z_new_u = v_new_u / (tau M~)
 __global__ void __launch_bounds__(RED_NT)
 vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
             const double* __restrict__ v_old, double* __restrict__ v_new,
             double* __restrict__ z_new, const double* __restrict__ mdiag, double tau,
             long long nrt, long long n, long long ex_lo, long long ex_hi,
-            const MState* __restrict__ st, double* part) {
+            MState* __restrict__ st, const double* __restrict__ glob, int P, double* part) {
   if (st->done) return;
   const double g = st->gamma, ig = 1.0 / g;
-  const double cd = st->delta * ig, co = g / st->gamma_old;
+  const double delta = rank_sum(glob, P) / (g * g);
+  const double cd = delta * ig, co = g / st->gamma_old;
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
        i += (long long)gridDim.x * RED_NT) {
@@ -119,7 +118,10 @@ vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
     }
   }
   s = block_sum(s);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    if (blockIdx.x == 0) st->delta = delta;   // for scalar_kernel (a later launch)
+  }
 }
 
 // Chebyshev semi-iteration (reading A10).  first: y = d = Dinv r / theta.
@@ -377,6 +379,7 @@ inline unsigned nb(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); 
 
 struct MinresWork {
   long long n = 0;
+  int nb = 0;                      // reduction grid: min(RED_BLOCKS, ceil(n / RED_NT))
   double* buf = nullptr;           // all vectors
   double *v[3], *w[3], *z[2], *Az, *r, *d[2];
   double *part_a, *part_b, *loc, *glob;
@@ -396,6 +399,7 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
   const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
   const long long nqg = nq + (h->nranks > 1 ? 2 * lplane : 0);   // + ghost layers
   mw->n = n;
+  mw->nb = (int)std::max(1LL, std::min<long long>(RED_BLOCKS, (n + RED_NT - 1) / RED_NT));
   size_t tot = 9 * (size_t)n + (size_t)nq + 2 * (size_t)nqg + 2 * RED_BLOCKS + 2 + 2 * h->nranks;
   HDIV_CUDA_TRY(cudaMalloc(&mw->buf, tot * sizeof(double)));
   HDIV_CUDA_TRY(cudaMemset(mw->buf, 0, tot * sizeof(double)));
@@ -449,7 +453,7 @@ static cudaError_t stencil_p(const hdiv_ctx* h, const StencilGeo& g, const doubl
                              double* rout, const double* d, double* dn, double* y, double c1,
                              double c2, int last, const double* vin, double* part, const int* done,
                              cudaStream_t s) {
-  cheb_stencil_kernel<DIM, P><<<RED_BLOCKS, RED_NT, 0, s>>>(g, h->d_minv, h->d_ctil, rin, rout, d,
+  cheb_stencil_kernel<DIM, P><<<h->mw->nb, RED_NT, 0, s>>>(g, h->d_minv, h->d_ctil, rin, rout, d,
                                                             dn, y, c1, c2, last, vin, part, done);
   return cudaGetLastError();
 }
@@ -491,14 +495,14 @@ static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, doub
     hdiv_status st = amg_vcycle(h, vq, y, done, s);
     if (st != HDIV_OK) return st;
     if (part) {
-      dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(y, vq, h->nl2, 0, 0, part, done);
+      dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(y, vq, h->nl2, 0, 0, part, done);
       HDIV_CUDA_TRY(cudaGetLastError());
     }
     return HDIV_OK;
   }
   const long long n = h->nl2;
   const int k = h->opts.cheb_degree;
-  cheb_first_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0], y, n,
+  cheb_first_kernel<<<h->mw->nb, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0], y, n,
                                                   k == 1, part, done);
   HDIV_CUDA_TRY(cudaGetLastError());
   const double* rin = vq;
@@ -513,12 +517,12 @@ static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, doub
                                           mw->c2[i - 1], i == k - 1, vq, part, done, s);
       HDIV_CUDA_TRY(e);
     } else if (h->dim == 3)
-      cheb_step_kernel<7><<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
+      cheb_step_kernel<7><<<h->mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
                                                         mw->d[i & 1], h->d_sdinv, y,
                                                         mw->c1[i - 1], mw->c2[i - 1], n,
                                                         i == k - 1, vq, part, done);
     else
-      cheb_step_kernel<5><<<RED_BLOCKS, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
+      cheb_step_kernel<5><<<h->mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
                                                         mw->d[i & 1], h->d_sdinv, y,
                                                         mw->c1[i - 1], mw->c2[i - 1], n,
                                                         i == k - 1, vq, part, done);
@@ -536,10 +540,10 @@ static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* 
   MinresWork* mw = h->mw;
   hdiv_status st = cheb_apply_raw(h, vq, y, nullptr, done, s);
   if (st != HDIV_OK) return st;
-  sum_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(y, h->nl2, mw->part_b, done);
+  sum_kernel<<<h->mw->nb, RED_NT, 0, s>>>(y, h->nl2, mw->part_b, done);
   HDIV_CUDA_TRY(cudaGetLastError());
   if ((st = reduce_scalar(h, mw->part_b, nullptr, done, s)) != HDIV_OK) return st;
-  mean_sub_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(y, h->nl2, mw->glob, h->nranks,
+  mean_sub_kernel<<<h->mw->nb, RED_NT, 0, s>>>(y, h->nl2, mw->glob, h->nranks,
                                                 1.0 / (double)h->nl2_g, vq, part, done);
   HDIV_CUDA_TRY(cudaGetLastError());
   return HDIV_OK;
@@ -564,7 +568,7 @@ hdiv_status schur_inv_apply(hdiv_ctx* h, const double* vq, double* y, cudaStream
 static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
                                  cudaStream_t s) {
   MinresWork* mw = h->mw;
-  local_reduce_kernel<<<1, RED_NT, 0, s>>>(pa, pb, mw->loc, done);
+  local_reduce_kernel<<<1, RED_NT, 0, s>>>(pa, pb, mw->loc, done, mw->nb);
   HDIV_CUDA_TRY(cudaGetLastError());
   if (h->nranks > 1) return comm_allgather(h, mw->loc, mw->glob, 1, s);
   return HDIV_OK;
@@ -593,7 +597,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
   HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[1], 0, n * sizeof(double), s));
   HDIV_CUDA_TRY(cudaMemcpyAsync(mw->v[1], b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   diag_scale_kernel<<<nb(nrt, 256), 256, 0, s>>>(mw->v[1], h->d_mdiag, h->opts.tau, mw->z[0], nrt);
-  dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->z[0], mw->v[1], nrt, mw->ex_lo, mw->ex_hi,
+  dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->z[0], mw->v[1], nrt, mw->ex_lo, mw->ex_hi,
                                            mw->part_a, nullptr);
   HDIV_CUDA_TRY(cudaGetLastError());
   if ((stt = cheb_apply(h, mw->v[1] + nrt, mw->z[0] + nrt, mw->part_b, nullptr, s)) != HDIV_OK)
@@ -614,19 +618,19 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     double* zc = mw->z[(j + 1) % 2];
     double* zn = mw->z[j % 2];
     HDIV_CUDA_TRY(apply_block_dev(h, zc, mw->Az, done, s));
-    dot_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_a,
+    dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_a,
                                              done);
     HDIV_CUDA_TRY(cudaGetLastError());
     hdiv_status st = reduce_scalar(h, mw->part_a, nullptr, done, s);
     if (st != HDIV_OK) return st;
-    fin_delta_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st);
-    vupd_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
-                                              nrt, n, mw->ex_lo, mw->ex_hi, mw->st, mw->part_a);
+    vupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
+                                              nrt, n, mw->ex_lo, mw->ex_hi, mw->st, mw->glob, P,
+                                              mw->part_a);
     HDIV_CUDA_TRY(cudaGetLastError());
     if ((st = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s)) != HDIV_OK) return st;
     if ((st = reduce_scalar(h, mw->part_a, mw->part_b, done, s)) != HDIV_OK) return st;
     scalar_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st);
-    wupd_kernel<<<RED_BLOCKS, RED_NT, 0, s>>>(zc, wo, wc, wn, x, n, mw->st);
+    wupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(zc, wo, wc, wn, x, n, mw->st);
     latch_kernel<<<1, 32, 0, s>>>(mw->st);
     HDIV_CUDA_TRY(cudaGetLastError());
     return HDIV_OK;
