@@ -437,6 +437,34 @@ def main():
                 del b4, xs4
                 torch.cuda.empty_cache()
 
+    # Crooked-pipe-shaped p sweep (config 5a, paper scale: 24x24x25 graded two-material hexes,
+    # grad-div with the P:915 coefficients), MINRES + one AMG V-cycle for S^-1, rtol 1e-12, next
+    # to the paper's own saddle-point solver on 4 V100 (Table crooked-pipe-gpu) as
+    # context: same method and problem shape, different hardware, mesh and right-hand side
+    if not args.no_minres and ws == 1:
+        from synth import make_config, random_vector
+        from paper_2304_12387_b200 import from_problem
+        paper = {2: (193, 0.85, 356500), 3: (251, 1.52, 1190115), 4: (298, 2.19, 2805520),
+                 5: (335, 3.49, 5461375), 6: (360, 4.01, 9416340)}
+        cp = {"workload": "config 5a: 24x24x25 graded two-material box mesh (crooked-pipe analogue, "
+                          "alpha/beta of P:915), grad-div, b = A x* (x* = U(-1,1), seed 5), x0 = 0, "
+                          "rtol 1e-12, S^-1 = AMG V-cycle; paper: 4x V100, 14,370 hexes of the real "
+                          "crooked pipe, constant forcing (context, not the target)"}
+        for p in (2, 3, 4, 5, 6):
+            prc = make_config("c5", p=p)
+            opc = from_problem(prc, schur="amg")
+            bc = opc.apply_block(torch.from_numpy(random_vector(opc.sizes.n, 5)).cuda())
+            opc.minres(bc, rtol=1e-12, maxit=6)   # warm-up (graph build)
+            _, rc = opc.minres(bc, rtol=1e-12, maxit=5000)
+            cp[f"p{p}"] = {"rt_dofs": opc.sizes.n_rt, "dofs": opc.sizes.n, "iters": rc.iters,
+                           "converged": bool(rc.converged), "time_s": rc.t_solve_ms / 1e3,
+                           "paper_4xV100": {"iters": paper[p][0], "time_s": paper[p][1],
+                                            "rt_dofs": paper[p][2]}}
+            opc.close()
+            del bc
+            torch.cuda.empty_cache()
+        result["crooked_pipe_like"] = cp
+
     # NEXT-3: the SPE10-shaped pure-Neumann Darcy solve: config 3's jittered
     # 64^3 p=4 mesh and eps = 10^U(-2,2), u.n prescribed on every side (eliminated), gamma = 0,
     # singular S~ with the projection after every S^-1 (one AMG V-cycle); b = A x*

@@ -115,10 +115,15 @@ struct AffArgs {
   long long off[3];    // RT component offsets
   long long nrt;
   int ntile[3];
-  int has_z;
-  int ess;             // eliminated essential sides (NEXT-3), local bitmask (0: none)
-  int tz0;             // first z tile of this launch (z-chunked host pipeline; else 0)
+  // packed (the argument block keeps its round-1 size: ptxas allocated registers differently,
+  // and the p=3/4 kernels ran 4-8 % slower, when two ints were added here):
+  // bit 0 = (2,2) block nonzero, bits 1..6 = eliminated essential sides (NEXT-3),
+  // bits 8.. = first z tile of this launch (z-chunked host pipeline)
+  int flags;
   const int* skip;     // MINRES done flag (nullptr: never skip)
+  __device__ __forceinline__ int has_z() const { return flags & 1; }
+  __device__ __forceinline__ int ess() const { return (flags >> 1) & 63; }
+  __device__ __forceinline__ int tz0() const { return flags >> 8; }
 };
 
 // z-tile range of the next halo-tile launch (host side, set by launch_affine_apply_range):
@@ -237,7 +242,8 @@ __device__ __forceinline__ void load_component(const AffArgs& a, const TileInfo&
 }
 
 // -------- one component phase (AX), data already in `su` ------------------------------------
-template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK, bool XD = kXDirect>
+template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK, bool XD = kXDirect,
+          bool ESS = false>
 __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
                                           const TabAffine& tab, double* su, const double* sq,
                                           const double* hq, const double* sco, double* acc) {
@@ -252,9 +258,10 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
 
   // ---- NEXT-3: eliminated essential planes act as zero inputs (the tile's first plane when
   //      it starts at the domain's - side, its last when it ends at the + side) ----
-  const bool ess_lo = ((a.ess >> (2 * AX)) & 1) && ti.e0[AX] == 0;
-  const bool ess_hi = ((a.ess >> (2 * AX + 1)) & 1) && ti.last[AX];
-  if (ess_lo || ess_hi) {   // block-uniform
+  // (ESS instantiations only: the common path compiles exactly as without eliminated sides)
+  const bool ess_lo = ESS && ((a.ess() >> (2 * AX)) & 1) && ti.e0[AX] == 0;
+  const bool ess_hi = ESS && ((a.ess() >> (2 * AX + 1)) & 1) && ti.last[AX];
+  if (ESS && (ess_lo || ess_hi)) {   // block-uniform
     for (int it = tid; it < EL1 * EL2; it += NT) {
       double* line = su + (it % EL1) * C::SA1 + (it / EL1) * C::SA2;
       if (ess_lo) line[P * C::SA] = 0.0;
@@ -399,7 +406,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
             o += qprev - qc;
             qprev = qc;
           }
-          if (i == 0 && et == 0 && ess_lo)   // identity row of the eliminated plane
+          if (ESS && i == 0 && et == 0 && ess_lo)   // identity row of the eliminated plane
             o = a.x[gtile + (l1 * gs1 + l2 * gs2) + P * gsa];
           if (AX == 0 && !XD) eb[i * C::SA] = o;
           else __stcs(gl + ((et + 1) * P + i) * gsa, o);
@@ -411,7 +418,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
       }
     }
     if (ti.last[AX]) {
-      const double o = ess_hi ? a.x[gtile + (l1 * gs1 + l2 * gs2) + (m_a + 1) * P * gsa]
+      const double o = (ESS && ess_hi) ? a.x[gtile + (l1 * gs1 + l2 * gs2) + (m_a + 1) * P * gsa]
                               : carry + (BLOCK ? qprev : 0.0);
       if (AX == 0 && !XD) line[(m_a + 1) * P * C::SA] = o;
       else __stcs(gl + (m_a + 1) * P * gsa, o);
@@ -431,7 +438,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
 }
 
-template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB, int MINB, bool XD>
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB, int MINB, bool XD,
+          bool ESS = false>
 __global__ void __launch_bounds__(NT, MINB)
 affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   using G = Geo<P, TX, TY, TZ>;
@@ -454,7 +462,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     const int tx = t % a.ntile[0];
     t /= a.ntile[0];
     const int ty = t % a.ntile[1];
-    const int tz = t / a.ntile[1] + a.tz0;
+    const int tz = t / a.ntile[1] + a.tz0();
     const int T3[3] = {TX, TY, TZ};
     const int tt[3] = {tx, ty, tz};
 #pragma unroll
@@ -541,7 +549,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   else cp_async_wait_group<0>();
   __syncthreads();
   if constexpr (BLOCK) {
-    if (a.has_z) {
+    if (a.has_z()) {
       // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in B (subcell-major like sq):
       // X-lines (lanes over Y, odd stride Q1; sq -> B), then Y- and Z-lines (lanes over X)
       hpass<P, NT>(sq, bufB, tab.Mhinv, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
@@ -580,28 +588,28 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK, XD>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq0, sco, acc);
     // ---- group 3: z component -> A ; compute y from B ----
     load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK, XD>(a, ti, tab, bufB, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS>(a, ti, tab, bufB, sq, hq1, sco, acc);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK, XD>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq2, sco, acc);
   } else {
     load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK, XD>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq0, sco, acc);
     load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK, XD>(a, ti, tab, bufA, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq1, sco, acc);
     load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK, XD>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq2, sco, acc);
   }
 
   if constexpr (BLOCK) {
@@ -624,7 +632,8 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   }
 }
 
-template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true, int MINB = 0, bool XD = kXDirect>
+template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true, int MINB = 0, bool XD = kXDirect,
+          bool ESS = false>
 cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
   using G = Geo<P, TX, TY, TZ>;
@@ -635,18 +644,18 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ntile[0] = (int)((h->NL[0] + TX - 1) / TX);
   a.ntile[1] = (int)((h->NL[1] + TY - 1) / TY);
   a.ntile[2] = (int)((h->NL[2] + TZ - 1) / TZ);
-  a.has_z = h->has_z ? 1 : 0;
-  a.ess = h->ess;
+  a.flags = (h->has_z ? 1 : 0) | (h->ess << 1);
   a.skip = skip;
   if (g_range.tz_out) {   // query: the variant's tile depth along z
     *g_range.tz_out = TZ;
     return cudaSuccess;
   }
   const int tz1 = (g_range.tz1 < 0) ? a.ntile[2] : min(g_range.tz1, a.ntile[2]);
-  a.tz0 = g_range.tz0;
-  if (tz1 <= a.tz0) return cudaSuccess;
+  const int tz0 = g_range.tz0;
+  a.flags |= tz0 << 8;
+  if (tz1 <= tz0) return cudaSuccess;
   const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
-  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD>;
+  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, ESS>;
   static bool attr_done = false;   // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -654,7 +663,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const long long nblk = (long long)a.ntile[0] * a.ntile[1] * (tz1 - a.tz0);
+  const long long nblk = (long long)a.ntile[0] * a.ntile[1] * (tz1 - tz0);
   kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff);
   return cudaGetLastError();
 }
@@ -962,7 +971,7 @@ affine_march_kernel(const AffArgs a, const __grid_constant__ TabAffine tab, int 
       }
     }
     if constexpr (BLOCK) {
-      if (a.has_z) {   // -Z q~ of this layer: M_h^-1 along I, J (planes) and K (cells)
+      if (a.has_z()) {   // -Z q~ of this layer: M_h^-1 along I, J (planes) and K (cells)
         hpass<P, NT>(sq, zs, tab.Mhinv, CY, ZS1, P, ZS2, TX, P, 1);
         __syncthreads();
         hpass<P, NT>(zs, zs, tab.Mhinv, CX, 1, P, ZS2, TY, P * ZS1, ZS1);
@@ -1019,9 +1028,7 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
   if (e) zc = atoi(e);
   if (zc > h->NL[2]) zc = (int)h->NL[2];
   a.ntile[2] = (int)((h->NL[2] + zc - 1) / zc);
-  a.has_z = h->has_z ? 1 : 0;
-  a.ess = 0;   // the marching kernel is not dispatched with eliminated sides
-  a.tz0 = 0;
+  a.flags = h->has_z ? 1 : 0;   // the marching kernel: no eliminated sides, no z-chunking
   a.skip = skip;
   const size_t smem = M::smem_doubles(BLOCK) * sizeof(double);
   auto kern = affine_march_kernel<P, TX, TY, NT, BLOCK>;
@@ -1086,6 +1093,17 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
   }
   // halo-tile variants: 0..3 double-buffered shapes, 4/5 single-buffered (more CTAs per SM),
   // 6/7 other CTA sizes, 8/9 register caps (__launch_bounds__ min blocks), 10 x copy-out
+  if (h->ess) {   // eliminated essential sides: one instantiation per order (default tiles)
+    switch (h->p) {
+      case 1: return launch_t<1, 8, 8, 4, 128, BLOCK, true, 0, kXDirect, true>(h, x, y, k, s);
+      case 2: return launch_t<2, 8, 4, 4, 128, BLOCK, true, 0, kXDirect, true>(h, x, y, k, s);
+      case 3: return launch_t<3, 4, 4, 2, 160, BLOCK, false, 0, kXDirect, true>(h, x, y, k, s);
+      case 4: return launch_t<4, 4, 2, 2, 128, BLOCK, false, 0, kXDirect, true>(h, x, y, k, s);
+      case 5: return launch_t<5, 2, 2, 2, 128, BLOCK, false, 0, false, true>(h, x, y, k, s);
+      case 6: return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3, false, true>(h, x, y, k, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   const int v = tile_variant(h->p);
   switch (h->p) {
     case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
