@@ -101,10 +101,19 @@ vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
             const double* __restrict__ v_old, double* __restrict__ v_new,
             double* __restrict__ z_new, const double* __restrict__ mdiag, double tau,
             long long nrt, long long n, long long ex_lo, long long ex_hi,
-            MState* __restrict__ st, const double* __restrict__ glob, int P, double* part) {
+            MState* __restrict__ st, const double* __restrict__ glob, int P,
+            const double* __restrict__ dpart, int nb, double* part) {
   if (st->done) return;
   const double g = st->gamma, ig = 1.0 / g;
-  const double delta = rank_sum(glob, P) / (g * g);
+  // single rank: every block sums the <Az, z> partials itself (same order as the reduction
+  // kernel it replaces, so bitwise the same delta); multi-rank: the all-gathered scalars
+  __shared__ double sdel;
+  if (dpart) {
+    const double t = sum_partials(dpart, nb);
+    if (threadIdx.x == 0) sdel = t;
+    __syncthreads();
+  }
+  const double delta = (dpart ? sdel : rank_sum(glob, P)) / (g * g);
   const double cd = delta * ig, co = g / st->gamma_old;
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
@@ -293,10 +302,20 @@ __global__ void init_kernel(const double* glob, int P, MState* st, double rtol, 
   *st = m;
 }
 
-__global__ void scalar_kernel(const double* glob, int P, MState* st) {
-  if (threadIdx.x != 0 || st->done) return;
+// single rank (pa != nullptr): gamma^2 = sum(pa) + sum(pb) summed here (as the reduction
+// kernel it replaces did); multi-rank: from the all-gathered scalars
+__global__ void scalar_kernel(const double* glob, int P, MState* st, const double* pa,
+                              const double* pb, int nb) {
+  if (st->done) return;
+  double red = 0.0;
+  if (pa) {
+    const double a = sum_partials(pa, nb);
+    const double b = sum_partials(pb, nb);
+    red = a + b;
+  }
+  if (threadIdx.x != 0) return;
   MState m = *st;
-  double g2 = rank_sum(glob, P);
+  double g2 = pa ? red : rank_sum(glob, P);
   if (g2 < 0.0) { m.breakdown = 1; m.done = 1; *st = m; return; }
   const double gn = std::sqrt(g2);
   const double delta = m.delta, g = m.gamma;
@@ -382,7 +401,7 @@ struct MinresWork {
   int nb = 0;                      // reduction grid: min(RED_BLOCKS, ceil(n / RED_NT))
   double* buf = nullptr;           // all vectors
   double *v[3], *w[3], *z[2], *Az, *r, *d[2];
-  double *part_a, *part_b, *loc, *glob;
+  double *part_a, *part_b, *part_c, *loc, *glob;
   MState* st = nullptr;
   MState* st_host = nullptr;       // pinned
   cudaStream_t stream = nullptr;   // own non-blocking stream (graph capture needs one)
@@ -400,7 +419,7 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
   const long long nqg = nq + (h->nranks > 1 ? 2 * lplane : 0);   // + ghost layers
   mw->n = n;
   mw->nb = (int)std::max(1LL, std::min<long long>(RED_BLOCKS, (n + RED_NT - 1) / RED_NT));
-  size_t tot = 9 * (size_t)n + (size_t)nq + 2 * (size_t)nqg + 2 * RED_BLOCKS + 2 + 2 * h->nranks;
+  size_t tot = 9 * (size_t)n + (size_t)nq + 2 * (size_t)nqg + 3 * RED_BLOCKS + 2 + 2 * h->nranks;
   HDIV_CUDA_TRY(cudaMalloc(&mw->buf, tot * sizeof(double)));
   HDIV_CUDA_TRY(cudaMemset(mw->buf, 0, tot * sizeof(double)));
   double* p = mw->buf;
@@ -412,6 +431,7 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
   for (int i = 0; i < 2; ++i) { mw->d[i] = p; p += nqg; }
   mw->part_a = p; p += RED_BLOCKS;
   mw->part_b = p; p += RED_BLOCKS;
+  mw->part_c = p; p += RED_BLOCKS;
   mw->loc = p; p += 2;
   mw->glob = (h->nranks > 1) ? p : mw->loc;
   p += 2 * h->nranks;
@@ -618,18 +638,22 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     double* zc = mw->z[(j + 1) % 2];
     double* zn = mw->z[j % 2];
     HDIV_CUDA_TRY(apply_block_dev(h, zc, mw->Az, done, s));
-    dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_a,
+    // single rank: the consumers (vupd, scalar) sum the partials themselves — two launches
+    // fewer per iteration; multi-rank: local reduction + all-gather as before
+    const bool one = (P == 1);
+    dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_c,
                                              done);
     HDIV_CUDA_TRY(cudaGetLastError());
-    hdiv_status st = reduce_scalar(h, mw->part_a, nullptr, done, s);
-    if (st != HDIV_OK) return st;
+    hdiv_status st = HDIV_OK;
+    if (!one && (st = reduce_scalar(h, mw->part_c, nullptr, done, s)) != HDIV_OK) return st;
     vupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
                                               nrt, n, mw->ex_lo, mw->ex_hi, mw->st, mw->glob, P,
-                                              mw->part_a);
+                                              one ? mw->part_c : nullptr, mw->nb, mw->part_a);
     HDIV_CUDA_TRY(cudaGetLastError());
     if ((st = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s)) != HDIV_OK) return st;
-    if ((st = reduce_scalar(h, mw->part_a, mw->part_b, done, s)) != HDIV_OK) return st;
-    scalar_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st);
+    if (!one && (st = reduce_scalar(h, mw->part_a, mw->part_b, done, s)) != HDIV_OK) return st;
+    scalar_kernel<<<1, RED_NT, 0, s>>>(mw->glob, P, mw->st, one ? mw->part_a : nullptr,
+                                       mw->part_b, mw->nb);
     wupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(zc, wo, wc, wn, x, n, mw->st);
     latch_kernel<<<1, 32, 0, s>>>(mw->st);
     HDIV_CUDA_TRY(cudaGetLastError());
