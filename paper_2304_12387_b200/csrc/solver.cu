@@ -302,21 +302,10 @@ __global__ void init_kernel(const double* glob, int P, MState* st, double rtol, 
   *st = m;
 }
 
-// single rank (pa != nullptr): gamma^2 = sum(pa) + sum(pb) summed here (as the reduction
-// kernel it replaces did); multi-rank: from the all-gathered scalars
-__global__ void scalar_kernel(const double* glob, int P, MState* st, const double* pa,
-                              const double* pb, int nb) {
-  if (st->done) return;
-  double red = 0.0;
-  if (pa) {
-    const double a = sum_partials(pa, nb);
-    const double b = sum_partials(pb, nb);
-    red = a + b;
-  }
-  if (threadIdx.x != 0) return;
-  MState m = *st;
-  double g2 = pa ? red : rank_sum(glob, P);
-  if (g2 < 0.0) { m.breakdown = 1; m.done = 1; *st = m; return; }
+// one MINRES scalar step: Givens rotation from (delta, gamma_new),
+// the w/x update coefficients, eta and the stopping test (done = 2: converged this iteration)
+__device__ __forceinline__ MState scalar_step(MState m, double g2) {
+  if (g2 < 0.0) { m.breakdown = 1; m.done = 1; return m; }
   const double gn = std::sqrt(g2);
   const double delta = m.delta, g = m.gamma;
   const double a0 = m.c * delta - m.c_old * m.s * g;
@@ -336,27 +325,49 @@ __global__ void scalar_kernel(const double* glob, int P, MState* st, const doubl
   m.rel = fabs(m.eta) / m.gamma1;
   if (fabs(m.eta) <= m.rtol * m.gamma1 || gn == 0.0) { m.conv = 1; m.done = 2; }
   else if (m.iters >= m.maxit) m.done = 2;
-  *st = m;
+  return m;
 }
 
-// w_new = wz z - wa3 w_old - wa2 w ;  x += xc w_new.  Runs in the iteration that set done=2
-// (its final update) and is skipped once latch_kernel turned done into 1.
+// Fused end of an iteration: every block derives the new scalars from the old state S and
+// gamma^2 (single rank: sum(pa) + sum(pb), summed here in the reduction kernel's order;
+// multi-rank: the all-gathered scalars) — identical in every block — then
+// w_new = wz z - wa3 w_old - wa2 w, x += xc w_new; block 0 publishes the new state in the
+// OTHER state slot (double-buffered: no block can see a half-updated state), with done = 2
+// (converged in this iteration, whose update still runs) latched to 1.
 __global__ void __launch_bounds__(RED_NT)
-wupd_kernel(const double* __restrict__ z, const double* __restrict__ w_old,
-            const double* __restrict__ w, double* __restrict__ w_new, double* __restrict__ x,
-            long long n, const MState* __restrict__ st) {
-  if (st->done == 1) return;
-  const double wz = st->wz, wa3 = st->wa3, wa2 = st->wa2, xc = st->xc;
-  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * RED_NT) {
-    double wn = wz * z[i] - wa3 * w_old[i] - wa2 * w[i];
-    w_new[i] = wn;
-    x[i] = fma(xc, wn, x[i]);
+wstep_kernel(const double* __restrict__ glob, int P, const MState* __restrict__ S,
+             MState* __restrict__ Snext, const double* __restrict__ pa,
+             const double* __restrict__ pb, int nb, const double* __restrict__ z,
+             const double* __restrict__ w_old, const double* __restrict__ w,
+             double* __restrict__ w_new, double* __restrict__ x, long long n) {
+  __shared__ MState sm;
+  if (S->done) {   // (done is 0 or 1 here) propagate the finished state
+    if (blockIdx.x == 0 && threadIdx.x == 0) *Snext = *S;
+    return;
   }
-}
-
-__global__ void latch_kernel(MState* st) {
-  if (threadIdx.x == 0 && st->done == 2) st->done = 1;
+  double red = 0.0;
+  if (pa) {
+    const double a = sum_partials(pa, nb);
+    const double b = sum_partials(pb, nb);
+    red = a + b;
+  }
+  if (threadIdx.x == 0) sm = scalar_step(*S, pa ? red : rank_sum(glob, P));
+  __syncthreads();
+  const MState m = sm;
+  if (!m.breakdown) {
+    const double wz = m.wz, wa3 = m.wa3, wa2 = m.wa2, xc = m.xc;
+    for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+         i += (long long)gridDim.x * RED_NT) {
+      const double wn = wz * z[i] - wa3 * w_old[i] - wa2 * w[i];
+      w_new[i] = wn;
+      x[i] = fma(xc, wn, x[i]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    MState o = m;
+    if (o.done == 2) o.done = 1;
+    *Snext = o;
+  }
 }
 
 // NEXT-3 orthogonalization after S^-1 (reading A21): partial sums of y, then
@@ -402,7 +413,7 @@ struct MinresWork {
   double* buf = nullptr;           // all vectors
   double *v[3], *w[3], *z[2], *Az, *r, *d[2];
   double *part_a, *part_b, *part_c, *loc, *glob;
-  MState* st = nullptr;
+  MState* st = nullptr;            // [2]: iteration j reads st[j & 1], publishes st[(j + 1) & 1]
   MState* st_host = nullptr;       // pinned
   cudaStream_t stream = nullptr;   // own non-blocking stream (graph capture needs one)
   std::vector<double> c1, c2;      // Chebyshev step constants
@@ -440,7 +451,7 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
     mw->ex_lo = h->off[last];
     mw->ex_hi = h->off[last] + lplane;
   }
-  HDIV_CUDA_TRY(cudaMalloc(&mw->st, sizeof(MState)));
+  HDIV_CUDA_TRY(cudaMalloc(&mw->st, 2 * sizeof(MState)));   // double-buffered (wstep_kernel)
   HDIV_CUDA_TRY(cudaMallocHost(&mw->st_host, sizeof(MState)));
   HDIV_CUDA_TRY(cudaStreamCreateWithFlags(&mw->stream, cudaStreamNonBlocking));
   // Chebyshev constants on [lmax/ratio, lmax], lmax = 2 (reading A10)
@@ -600,7 +611,9 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
   if (stt != HDIV_OK) return stt;
   MinresWork* mw = h->mw;
   const long long n = mw->n, nrt = h->nrt;
-  const int* done = &mw->st->done;
+  // state slots: init writes st[1]; iteration j (1..6 per graph launch) reads st[j & 1] and
+  // publishes st[(j + 1) & 1], so after every 6 iterations the latest state is in st[1]
+  MState* const st_last = mw->st + 1;
   const int P = h->nranks;
   // the solve runs on the handle's own (capturable) stream, ordered after `caller`
   cudaStream_t s = mw->stream;
@@ -623,7 +636,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
   if ((stt = cheb_apply(h, mw->v[1] + nrt, mw->z[0] + nrt, mw->part_b, nullptr, s)) != HDIV_OK)
     return stt;
   if ((stt = reduce_scalar(h, mw->part_a, mw->part_b, nullptr, s)) != HDIV_OK) return stt;
-  init_kernel<<<1, 32, 0, s>>>(mw->glob, P, mw->st, rtol, maxit);
+  init_kernel<<<1, 32, 0, s>>>(mw->glob, P, st_last, rtol, maxit);
   HDIV_CUDA_TRY(cudaGetLastError());
 
   // iteration j: (v_old, v, v_new) = v[(j-1)%3], v[j%3], v[(j+1)%3]; same for w;
@@ -637,6 +650,9 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     double* wn = mw->w[(j + 1) % 3];
     double* zc = mw->z[(j + 1) % 2];
     double* zn = mw->z[j % 2];
+    MState* stc = mw->st + (j & 1);
+    MState* stn = mw->st + ((j + 1) & 1);
+    const int* done = &stc->done;
     HDIV_CUDA_TRY(apply_block_dev(h, zc, mw->Az, done, s));
     // single rank: the consumers (vupd, scalar) sum the partials themselves — two launches
     // fewer per iteration; multi-rank: local reduction + all-gather as before
@@ -647,15 +663,13 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     hdiv_status st = HDIV_OK;
     if (!one && (st = reduce_scalar(h, mw->part_c, nullptr, done, s)) != HDIV_OK) return st;
     vupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
-                                              nrt, n, mw->ex_lo, mw->ex_hi, mw->st, mw->glob, P,
+                                              nrt, n, mw->ex_lo, mw->ex_hi, stc, mw->glob, P,
                                               one ? mw->part_c : nullptr, mw->nb, mw->part_a);
     HDIV_CUDA_TRY(cudaGetLastError());
     if ((st = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s)) != HDIV_OK) return st;
     if (!one && (st = reduce_scalar(h, mw->part_a, mw->part_b, done, s)) != HDIV_OK) return st;
-    scalar_kernel<<<1, RED_NT, 0, s>>>(mw->glob, P, mw->st, one ? mw->part_a : nullptr,
-                                       mw->part_b, mw->nb);
-    wupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(zc, wo, wc, wn, x, n, mw->st);
-    latch_kernel<<<1, 32, 0, s>>>(mw->st);
+    wstep_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->glob, P, stc, stn, one ? mw->part_a : nullptr,
+                                              mw->part_b, mw->nb, zc, wo, wc, wn, x, n);
     HDIV_CUDA_TRY(cudaGetLastError());
     return HDIV_OK;
   };
@@ -690,7 +704,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
       }
     }
     launched += 6;
-    HDIV_CUDA_TRY(cudaMemcpyAsync(mw->st_host, mw->st, sizeof(MState), cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaMemcpyAsync(mw->st_host, st_last, sizeof(MState), cudaMemcpyDeviceToHost, s));
     HDIV_CUDA_TRY(cudaStreamSynchronize(s));
     if (mw->st_host->done || launched >= maxit + 6) break;
   }
