@@ -81,7 +81,8 @@ typedef struct {
   double cheb_ratio;   /* interval [2/ratio, 2]; <= 0 => 30                                  */
   int kernel;          /* 0 auto, 1 force the general quadrature kernel, 2 force affine tile */
   int schur_solver;    /* S^-1: HDIV_SCHUR_CHEBYSHEV (0, reading A10) or HDIV_SCHUR_AMG (1):  */
-                       /* one smoothed-aggregation V-cycle (reading A9b; 1 rank)  */
+                       /* one smoothed-aggregation V-cycle (reading A9b); with     */
+                       /* slabs the block-Jacobi of per-slab V-cycles (reading A9c)          */
   int amg_sweeps;      /* l1-Jacobi sweeps before and after the coarse correction; <= 0 => 2 */
   int amg_max_coarse;  /* dense solve once a level has <= this many rows; <= 0 => 512        */
   /* NEXT-3 (reading A21).  essential_sides: bitmask of domain sides whose RT

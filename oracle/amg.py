@@ -123,13 +123,35 @@ def vcycle(levels, b, nu=1, l=0):
 
 
 class AMGSchur:
-    """S^-1 = one V-cycle on S~ (drop-in for the Chebyshev polynomial in BlockDiagPrecond)."""
+    """S^-1 = one V-cycle on S~ (drop-in for the Chebyshev polynomial in BlockDiagPrecond).
 
-    def __init__(self, asm, nu=2, max_coarse=512, pin=False):
+    slabs = [(z0, z1), ...] element-layer ranges along the last axis (reading A9c, the
+    multi-rank build): S^-1 = block-Jacobi of one V-cycle per diagonal block S~[slab, slab]
+    (slab-local aggregation of the block's own subcell grid; couplings between slabs dropped).
+    In the element-contiguous L2 numbering every slab is one contiguous index range."""
+
+    def __init__(self, asm, nu=2, max_coarse=512, pin=False, slabs=None):
         coords = l2_cell_coords(asm.dim, asm.N, asm.p)
-        dims = tuple(int(asm.N[a]) * asm.p for a in range(asm.dim))
-        self.levels = build_hierarchy(asm.S, coords, dims, max_coarse=max_coarse, pin=pin)
+        dims = [int(asm.N[a]) * asm.p for a in range(asm.dim)]
         self.nu = nu
+        last = asm.dim - 1
+        per_layer = int(np.prod(asm.N[:last])) * asm.p ** asm.dim
+        if not slabs:
+            slabs = [(0, int(asm.N[last]))]
+        self.blocks = []
+        S = asm.S.tocsr()
+        for z0, z1 in slabs:
+            a, b = z0 * per_layer, z1 * per_layer
+            c = coords[a:b].copy()
+            c[:, last] -= z0 * asm.p
+            d = list(dims)
+            d[last] = (z1 - z0) * asm.p
+            lv = build_hierarchy(S[a:b, a:b], c, tuple(d), max_coarse=max_coarse, pin=pin)
+            self.blocks.append((a, b, lv))
+        self.levels = self.blocks[0][2] if len(self.blocks) == 1 else None
 
     def __call__(self, r):
-        return vcycle(self.levels, r, self.nu)
+        out = np.empty_like(r)
+        for a, b, lv in self.blocks:
+            out[a:b] = vcycle(lv, r[a:b], self.nu)
+        return out

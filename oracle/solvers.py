@@ -38,7 +38,8 @@ class BlockDiagPrecond:
     """P^-1 = diag((tau M~)^-1, S^-1)."""
 
     def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, exact_schur=False, exact_blocks=False,
-                 schur="chebyshev", amg_nu=2, amg_max_coarse=512, project_mean=None):
+                 schur="chebyshev", amg_nu=2, amg_max_coarse=512, project_mean=None,
+                 amg_slabs=None):
         self.asm, self.tau, self.degree, self.ratio = asm, tau, degree, ratio
         # NEXT-3 (P:1038-1040): with pure-Neumann (all-essential flux) Darcy and gamma = 0 the
         # Schur complement is singular with the constants as nullspace, so every application of
@@ -50,7 +51,8 @@ class BlockDiagPrecond:
         self.amg = None
         if schur == "amg":   # NEXT-1: one AMG V-cycle on S~ (reading A9b)
             from .amg import AMGSchur
-            self.amg = AMGSchur(asm, nu=amg_nu, max_coarse=amg_max_coarse, pin=project_mean)
+            self.amg = AMGSchur(asm, nu=amg_nu, max_coarse=amg_max_coarse, pin=project_mean,
+                                slabs=amg_slabs)
         self.n_rt = asm.n_rt
         self.exact_schur = exact_schur
         self.exact_blocks = exact_blocks

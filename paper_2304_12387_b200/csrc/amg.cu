@@ -11,7 +11,10 @@
 //
 // B200 layout: level 0 is S~ itself (SELL-32 copy for the SpMVs, its 7-point face form for the
 // setup); levels >= 1 are structured stencils stored as [3^d][n] (SoA: coalesced per offset),
-// lexicographic x-fastest numbering.  P and P^T are never stored: P e = inject(e) - omega D^-1 A
+// lexicographic x-fastest numbering.  Multi-rank (slabs): every rank builds the hierarchy of its
+// own diagonal block of S~ (slab-local aggregates, ghost couplings dropped: the face terms of the
+// interface stay on the diagonal) and the V-cycles act independently — S^-1 is the block-Jacobi
+// of the per-slab V-cycles (reading A9c), no communication inside S^-1.  P and P^T are never stored: P e = inject(e) - omega D^-1 A
 // inject(e) and P^T r = aggregate-sum(r - omega A D^-1 r) reuse the level's SpMV.  The Galerkin
 // product is formed matrix-free per coarse row (one CTA: phi_I on the 5^d box, A phi_I on 7^d,
 // (I - omega A D^-1) A phi_I on 9^d, summed per neighbouring aggregate), no SpGEMM.
@@ -300,11 +303,16 @@ struct SellA {
   const int32_t* col;
   const double* val;
   int W;
+  int nloc;   // local rows: slab ghost columns (>= nloc) are dropped — multi-rank AMG is the
+              // block-Jacobi of the per-slab V-cycles (reading A9c)
   template <class F>
   __device__ __forceinline__ double dot(long long i, F f) const {
     const long long base = (i >> 5) * (32LL * W) + (i & 31);
     double s = 0.0;
-    for (int k = 0; k < W; ++k) s = fma(val[base + 32 * k], f(col[base + 32 * k]), s);
+    for (int k = 0; k < W; ++k) {
+      const int c = col[base + 32 * k];
+      if (c < nloc) s = fma(val[base + 32 * k], f(c), s);
+    }
     return s;
   }
 };
@@ -573,10 +581,6 @@ void amg_free(hdiv_ctx* h) {
 }
 
 hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
-  if (h->nranks > 1) {
-    set_error("AMG Schur preconditioner: single-rank only in this build");
-    return HDIV_ERR_UNSUPPORTED;
-  }
   auto* H = new AmgHier();
   h->amg = H;
   H->nu = h->opts.amg_sweeps;
@@ -669,7 +673,8 @@ hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
     HDIV_CUDA_TRY(cudaMemcpyAsync(val.data(), h->d_sval, sizeof(double) * rp[nc], cudaMemcpyDeviceToHost, s));
     HDIV_CUDA_TRY(cudaStreamSynchronize(s));
     for (long long i = 0; i < nc; ++i)
-      for (int64_t t = rp[i]; t < rp[i + 1]; ++t) Ad[i * nc + col[t]] = val[t];
+      for (int64_t t = rp[i]; t < rp[i + 1]; ++t)
+        if (col[t] < nc) Ad[i * nc + col[t]] = val[t];   // slab ghost columns dropped (A9c)
   } else {
     std::vector<double> st(NS * nc);
     HDIV_CUDA_TRY(cudaMemcpyAsync(st.data(), Lc.st, sizeof(double) * NS * nc, cudaMemcpyDeviceToHost, s));
@@ -716,7 +721,7 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   const int nu = H->nu;
   const long long n = L.n;
   const unsigned g = nbk(n);
-  SellA sa{h->d_ecol, h->d_eval, 2 * h->dim + 1};
+  SellA sa{h->d_ecol, h->d_eval, 2 * h->dim + 1, (int)h->nl2};
   StA sta = make_sta(L);
   const bool lev0 = (l == 0);
   // buffers: pre-smoothing ping-pong in xa/xb, final post-smoothing output in x

@@ -153,10 +153,6 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     delete h;
     return fail(HDIV_ERR_SHAPE, "schur_solver must be HDIV_SCHUR_CHEBYSHEV or HDIV_SCHUR_AMG");
   }
-  if (h->opts.schur_solver == HDIV_SCHUR_AMG && nranks > 1) {
-    delete h;
-    return fail(HDIV_ERR_UNSUPPORTED, "AMG Schur preconditioner is single-rank in this build");
-  }
   for (int d = 0; d < 3; ++d) { h->N[d] = N[d]; h->NL[d] = N[d]; }
   h->ez0 = mesh->ez_begin; h->ez1 = mesh->ez_end;
   h->NL[last] = h->ez1 - h->ez0;

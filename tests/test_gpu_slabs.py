@@ -135,3 +135,50 @@ def test_slab_minres(name, N, p, P, ess, project):
     c = np.concatenate(dqs).mean() if project else 0.0   # p~ unique up to ONE global constant
     for dq in dqs:
         assert np.abs(dq - c).max() < 1e-9 * np.abs(x1[n_rt:]).max()
+
+
+@pytest.mark.parametrize("name,N,p,P,ess,project", [("c2", (4, 3, 7), 3, 2, 0, False),
+                                                    ("c3", (3, 3, 6), 2, 3, 0, False),
+                                                    ("c5", (5, 5, 6), 2, 2, 0, False),
+                                                    ("c3", (3, 3, 4), 2, 2, 63, True)])
+def test_slab_minres_amg(name, N, p, P, ess, project):
+    """Multi-rank S^-1 = block-Jacobi of per-slab AMG V-cycles (reading A9c): each rank's
+    preconditioner output and the MINRES iteration counts (+-1) against the oracle's
+    block-Jacobi AMG on the same slabs."""
+    import torch
+    from oracle import operators, solvers
+    from paper_2304_12387_b200 import slabs as sl
+    pr = _problem(name, N, p, ess, project)
+    if project:
+        pr.gamma = np.zeros(pr.E)
+    A = operators.Assembled(pr)
+    last = pr.dim - 1
+    bounds = [sl.slab_bounds(pr.N[last], P, r) for r in range(P)]
+    Po = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds)
+    n_rt = A.n_rt
+    v = random_vector(A.n_rt + A.n_l2, 8)
+    if project:
+        v[n_rt:] -= v[n_rt:].mean()
+    zo = Po.apply(v)
+    xs = random_vector(A.n_rt + A.n_l2, 3)
+    b = A.apply_block(xs)
+    xo, it_o, conv_o, _ = solvers.minres(A.apply_block, Po.apply, b, rtol=1e-12, maxit=3000)
+
+    def fn(r, op, rt, l2):
+        vl = np.concatenate([v[:n_rt][rt], v[n_rt:][l2]])
+        zl = op.apply_precond(torch.from_numpy(vl).cuda()).cpu().numpy()
+        bl = np.concatenate([b[:n_rt][rt], b[n_rt:][l2]])
+        xl, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
+        return zl, xl.cpu().numpy(), rep.iters, rep.converged, rt, l2
+
+    res = _run_slabs(pr, P, fn, key=3000 + hash((name, N, p, P, ess)) % 1000,
+                     schur="amg", amg_max_coarse=16)
+    assert conv_o
+    its = {r[2] for r in res}
+    assert len(its) == 1 and all(r[3] for r in res), its
+    assert abs(res[0][2] - it_o) <= 1, (res[0][2], it_o)
+    for zl, xl, _, _, rt, l2 in res:
+        nrl = len(rt)
+        assert _rel(zl[:nrl], zo[:n_rt][rt]) < 1e-12
+        assert _rel(zl[nrl:], zo[n_rt:][l2]) < 1e-10   # (projection: the global mean)
+        assert _rel(xl[:nrl], xo[:n_rt][rt]) < 1e-8

@@ -124,3 +124,30 @@ def test_minres_with_amg_beats_chebyshev_on_config2():
         assert conv
         its[schur] = it
     assert its["amg"] < its["chebyshev"], its
+
+
+def test_block_jacobi_amg_of_slabs():
+    """Reading A9c (multi-rank S^-1): the block-Jacobi of per-slab V-cycles.  With a one-level
+    hierarchy per block (max_coarse >= block size) every block solve is exact, so it must equal
+    the independent block-diagonal solve S~[slab, slab]^-1 v; with deeper hierarchies it stays
+    symmetric positive definite."""
+    import scipy.sparse.linalg as spla
+    from oracle import amg as amgmod, operators
+    from synth import make_config, random_vector
+    pr = make_config("c2", N=(3, 3, 5), p=2)
+    A = operators.Assembled(pr)
+    slabs = [(0, 2), (2, 3), (3, 5)]
+    per = 3 * 3 * 8
+    v = random_vector(A.n_l2, 3)
+    exact = amgmod.AMGSchur(A, max_coarse=10 ** 6, slabs=slabs)
+    z = exact(v)
+    S = A.S.tocsc()
+    for z0, z1 in slabs:
+        a, b = z0 * per, z1 * per
+        zb = spla.spsolve(S[a:b, a:b], v[a:b])
+        assert np.abs(z[a:b] - zb).max() < 1e-11 * np.abs(zb).max()
+    deep = amgmod.AMGSchur(A, max_coarse=8, slabs=slabs)
+    n = A.n_l2
+    Bm = np.column_stack([deep(e) for e in np.eye(n)])
+    assert np.abs(Bm - Bm.T).max() < 1e-12 * np.abs(Bm).max()
+    assert np.linalg.eigvalsh(0.5 * (Bm + Bm.T)).min() > 0
