@@ -1,6 +1,8 @@
 import csv, sys, collections, subprocess
 rep = sys.argv[1]
-raw = subprocess.run(["ncu","-i",rep,"--page","raw","--csv"],capture_output=True,text=True).stdout
+# argument: an .ncu-rep (read through `ncu -i`) or the `--page raw --csv` export of one
+raw = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu","-i",rep,"--page","raw","--csv"],capture_output=True,text=True).stdout)
 rows = list(csv.reader(raw.splitlines()))
 hdr, units, vals = rows[0], rows[1], rows[2]
 d = dict(zip(hdr, vals)); u = dict(zip(hdr, units))
