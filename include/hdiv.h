@@ -185,14 +185,16 @@ hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double 
 
 /* NEXT-4 (P:423-438 Remark): z = B^-1 v with the block upper-triangular preconditioner
  * B = [tau M~, D^T; 0, -S^] (S^-1 per options.schur_solver):  z_q = -S^-1 v_q,
- * z_u = (tau M~)^-1 (v_u - D^T z_q).  v, z: DEVICE [n_rt + n_l2].  Single rank. */
+ * z_u = (tau M~)^-1 (v_u - D^T z_q).  v, z: DEVICE [n_rt + n_l2].  Slabs: D^T reverse-added. */
 hdiv_status hdiv_apply_precond_tri(hdiv_handle h, const double* v, double* z, void* stream);
 
 /* NEXT-4: right-preconditioned restarted GMRES(restart) with B above, x0 = 0;
  * Arnoldi with classical Gram-Schmidt applied twice, Givens rotations; stops when the
  * least-squares residual (the true residual norm, right preconditioning) <= rtol ||b||.
  * restart <= 64; the (restart+1) basis vectors are allocated on first use (8 (restart+1) n
- * bytes).  Synchronous (host-driven Hessenberg algebra).  Single rank. */
+ * bytes).  Synchronous (host-driven Hessenberg algebra).  Slabs: every projection is
+ * all-gathered and summed in rank order (the interface plane counted once), so all ranks build
+ * the same Hessenberg matrix and take the same decisions. */
 hdiv_status hdiv_gmres_solve(hdiv_handle h, const double* b, double* x, double rtol, int maxit,
                              int restart, hdiv_report* report, void* stream);
 

@@ -21,6 +21,9 @@
 
 namespace hdiv {
 
+hdiv_status comm_reverse_add(hdiv_ctx* h, double* y_rt, cudaStream_t s);   // comm.cu
+hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, cudaStream_t s);
+
 constexpr int GMAX = 64;   // maximum restart length
 
 struct GmresWork {
@@ -33,7 +36,10 @@ struct GmresWork {
   double* tu = nullptr;
   double* part = nullptr;   // [GMAX+1][GBLK] partial sums
   double* hd = nullptr;     // device copy of the projection coefficients
+  double* glob = nullptr;   // multi-rank: all-gathered per-rank projections [P][GMAX+1]
+  long long ex_lo = 0, ex_hi = 0;   // RT range excluded from dots (replicated interface plane)
   std::vector<double> hh;   // host
+  std::vector<double> hg;   // host copy of glob
 };
 
 namespace {
@@ -56,17 +62,19 @@ __device__ __forceinline__ double gblock_sum(double v, double* red) {
   return r;
 }
 
-// part[k][blk] = partial <V_{k0+k}, w> for k < nk (<= KB)
+// part[k][blk] = partial <V_{k0+k}, w> for k < nk (<= KB), entries [ex_lo, ex_hi) excluded
+// (multi-rank: the interface plane replicated on the upper rank counts once)
 __global__ void __launch_bounds__(GNT) proj_kernel(const double* __restrict__ V, long long n,
                                                    int k0, int nk, const double* __restrict__ w,
-                                                   double* __restrict__ part) {
+                                                   double* __restrict__ part, long long ex_lo,
+                                                   long long ex_hi) {
   __shared__ double red[GNT / 32];
   double s[KB];
 #pragma unroll
   for (int k = 0; k < KB; ++k) s[k] = 0.0;
   for (long long i = blockIdx.x * (long long)GNT + threadIdx.x; i < n;
        i += (long long)gridDim.x * GNT) {
-    const double wi = w[i];
+    const double wi = (i >= ex_lo && i < ex_hi) ? 0.0 : w[i];
 #pragma unroll
     for (int k = 0; k < KB; ++k)
       if (k < nk) s[k] = fma(V[(long long)(k0 + k) * n + i], wi, s[k]);
@@ -143,7 +151,7 @@ __global__ void neg_kernel(const double* __restrict__ y, double* __restrict__ z,
 void gmres_free(hdiv_ctx* h) {
   if (!h->gw) return;
   cudaFree(h->gw->V); cudaFree(h->gw->w); cudaFree(h->gw->t); cudaFree(h->gw->tq);
-  cudaFree(h->gw->tu); cudaFree(h->gw->part); cudaFree(h->gw->hd);
+  cudaFree(h->gw->tu); cudaFree(h->gw->part); cudaFree(h->gw->hd); cudaFree(h->gw->glob);
   delete h->gw;
   h->gw = nullptr;
 }
@@ -162,15 +170,19 @@ static hdiv_status ensure_gw(hdiv_ctx* h, int m) {
   HDIV_CUDA_TRY(cudaMalloc(&g->tu, sizeof(double) * (h->nrt > 0 ? h->nrt : 1)));
   HDIV_CUDA_TRY(cudaMalloc(&g->part, sizeof(double) * (GMAX + 1) * GBLK));
   HDIV_CUDA_TRY(cudaMalloc(&g->hd, sizeof(double) * (GMAX + 1)));
+  HDIV_CUDA_TRY(cudaMalloc(&g->glob, sizeof(double) * (GMAX + 1) * h->nranks));
   g->hh.resize(GMAX + 1);
+  g->hg.resize((size_t)(GMAX + 1) * h->nranks);
+  if (h->rank > 0) {   // the lower rank owns the shared interface plane
+    const int last = h->dim - 1;
+    const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
+    g->ex_lo = h->off[last];
+    g->ex_hi = h->off[last] + lplane;
+  }
   return HDIV_OK;
 }
 
 hdiv_status apply_precond_tri(hdiv_ctx* h, const double* v, double* z, cudaStream_t s) {
-  if (h->nranks > 1) {
-    set_error("block-triangular preconditioner / GMRES: single-rank in this build");
-    return HDIV_ERR_UNSUPPORTED;
-  }
   hdiv_status st = ensure_gw(h, h->gw ? h->gw->m : 1);
   if (st != HDIV_OK) return st;
   GmresWork* g = h->gw;
@@ -178,29 +190,47 @@ hdiv_status apply_precond_tri(hdiv_ctx* h, const double* v, double* z, cudaStrea
   st = schur_inv_apply(h, v + h->nrt, g->tq, s);
   if (st != HDIV_OK) return st;
   HDIV_CUDA_TRY(launch_divT(h, g->tq, g->tu, s));
+  if (h->nranks > 1 && (st = comm_reverse_add(h, g->tu, s)) != HDIV_OK) return st;
   tri_u_kernel<<<GBLK, GNT, 0, s>>>(v, g->tu, h->d_mdiag, h->opts.tau, z, h->nrt);
   neg_kernel<<<GBLK, GNT, 0, s>>>(g->tq, z + h->nrt, h->nl2);
   HDIV_CUDA_TRY(cudaGetLastError());
   return HDIV_OK;
 }
 
-// <a,b> over the whole vector (deterministic), via the projection kernels with V = a
-static hdiv_status dot_host(GmresWork* g, const double* a, const double* b, long long n,
+// the nk projections in g->hd (this rank's) -> global values on the host: multi-rank, the P
+// per-rank vectors are all-gathered and summed in rank order (identical on every rank)
+static hdiv_status global_proj(hdiv_ctx* h, int nk, double* out, cudaStream_t s) {
+  GmresWork* g = h->gw;
+  if (h->nranks == 1) {
+    HDIV_CUDA_TRY(cudaMemcpyAsync(out, g->hd, sizeof(double) * nk, cudaMemcpyDeviceToHost, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    return HDIV_OK;
+  }
+  hdiv_status st = comm_allgather(h, g->hd, g->glob, nk, s);
+  if (st != HDIV_OK) return st;
+  HDIV_CUDA_TRY(cudaMemcpyAsync(g->hg.data(), g->glob, sizeof(double) * nk * h->nranks,
+                                cudaMemcpyDeviceToHost, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int k = 0; k < nk; ++k) {
+    double v = 0.0;
+    for (int r = 0; r < h->nranks; ++r) v += g->hg[(size_t)r * nk + k];
+    out[k] = v;
+  }
+  return HDIV_OK;
+}
+
+// <a,b> over the whole (global) vector (deterministic), via the projection kernels with V = a
+static hdiv_status dot_host(hdiv_ctx* h, const double* a, const double* b, long long n,
                             double* out, cudaStream_t s) {
-  proj_kernel<<<GBLK, GNT, 0, s>>>(a, n, 0, 1, b, g->part);
+  GmresWork* g = h->gw;
+  proj_kernel<<<GBLK, GNT, 0, s>>>(a, n, 0, 1, b, g->part, g->ex_lo, g->ex_hi);
   proj_final_kernel<<<1, GNT, 0, s>>>(g->part, 1, g->hd);
   HDIV_CUDA_TRY(cudaGetLastError());
-  HDIV_CUDA_TRY(cudaMemcpyAsync(out, g->hd, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
-  return HDIV_OK;
+  return global_proj(h, 1, out, s);
 }
 
 hdiv_status gmres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxit, int restart,
                   hdiv_report* rep, cudaStream_t s) {
-  if (h->nranks > 1) {
-    set_error("GMRES: single-rank in this build");
-    return HDIV_ERR_UNSUPPORTED;
-  }
   const int m = std::max(1, std::min(restart, GMAX));
   hdiv_status st = ensure_gw(h, m);
   if (st != HDIV_OK) return st;
@@ -212,7 +242,7 @@ hdiv_status gmres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxi
   HDIV_CUDA_TRY(cudaEventRecord(e0, s));
   HDIV_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
   double bb = 0.0;
-  if ((st = dot_host(g, b, b, n, &bb, s)) != HDIV_OK) return st;
+  if ((st = dot_host(h, b, b, n, &bb, s)) != HDIV_OK) return st;
   const double bnorm = std::sqrt(bb);
   int it = 0;
   bool conv = (bnorm == 0.0);
@@ -224,7 +254,7 @@ hdiv_status gmres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxi
     HDIV_CUDA_TRY(apply_block_dev(h, x, g->w, nullptr, s));
     sub_kernel<<<GBLK, GNT, 0, s>>>(b, g->w, g->w, n);
     double rr = 0.0;
-    if ((st = dot_host(g, g->w, g->w, n, &rr, s)) != HDIV_OK) return st;
+    if ((st = dot_host(h, g->w, g->w, n, &rr, s)) != HDIV_OK) return st;
     const double beta = std::sqrt(rr);
     rel = beta / bnorm;
     if (beta <= rtol * bnorm) { conv = true; break; }
@@ -239,17 +269,20 @@ hdiv_status gmres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxi
       HDIV_CUDA_TRY(apply_block_dev(h, g->t, g->w, nullptr, s));
       for (int pass = 0; pass < 2; ++pass) {   // classical Gram-Schmidt, twice
         for (int k0 = 0; k0 <= j; k0 += KB)
-          proj_kernel<<<GBLK, GNT, 0, s>>>(g->V, n, k0, std::min(KB, j + 1 - k0), g->w, g->part);
+          proj_kernel<<<GBLK, GNT, 0, s>>>(g->V, n, k0, std::min(KB, j + 1 - k0), g->w, g->part,
+                                           g->ex_lo, g->ex_hi);
         proj_final_kernel<<<1, GNT, 0, s>>>(g->part, j + 1, g->hd);
+        HDIV_CUDA_TRY(cudaGetLastError());
+        if ((st = global_proj(h, j + 1, g->hh.data(), s)) != HDIV_OK) return st;
+        if (h->nranks > 1)   // the global projections back to the device for the update
+          HDIV_CUDA_TRY(cudaMemcpyAsync(g->hd, g->hh.data(), sizeof(double) * (j + 1),
+                                        cudaMemcpyHostToDevice, s));
         combo_kernel<<<GBLK, GNT, 0, s>>>(g->V, n, j + 1, g->hd, g->w, 0);
         HDIV_CUDA_TRY(cudaGetLastError());
-        HDIV_CUDA_TRY(cudaMemcpyAsync(g->hh.data(), g->hd, sizeof(double) * (j + 1),
-                                      cudaMemcpyDeviceToHost, s));
-        HDIV_CUDA_TRY(cudaStreamSynchronize(s));
         for (int i = 0; i <= j; ++i) Hij(i, j) += g->hh[i];
       }
       double ww = 0.0;
-      if ((st = dot_host(g, g->w, g->w, n, &ww, s)) != HDIV_OK) return st;
+      if ((st = dot_host(h, g->w, g->w, n, &ww, s)) != HDIV_OK) return st;
       Hij(j + 1, j) = std::sqrt(ww);
       if (Hij(j + 1, j) > 0.0)
         scale_copy_kernel<<<GBLK, GNT, 0, s>>>(g->w, 1.0 / Hij(j + 1, j), g->V + (size_t)(j + 1) * n, n);

@@ -182,3 +182,50 @@ def test_slab_minres_amg(name, N, p, P, ess, project):
         assert _rel(zl[:nrl], zo[:n_rt][rt]) < 1e-12
         assert _rel(zl[nrl:], zo[n_rt:][l2]) < 1e-10   # (projection: the global mean)
         assert _rel(xl[:nrl], xo[:n_rt][rt]) < 1e-8
+
+
+@pytest.mark.parametrize("name,N,p,P,schur", [("c2", (4, 3, 6), 3, 2, "chebyshev"),
+                                              ("c3", (3, 3, 6), 2, 3, "chebyshev"),
+                                              ("c5", (5, 5, 6), 2, 2, "amg")])
+def test_slab_gmres(name, N, p, P, schur):
+    """NEXT-4 on slabs: block-triangular preconditioner (D^T reverse-added) + GMRES with
+    all-gathered projections — every rank takes the same decisions; iteration counts +-1 and
+    solutions vs the single-rank GPU solve (Chebyshev S^-1) or vs the oracle's GMRES with the
+    block-Jacobi AMG S^-1 (reading A9c)."""
+    import torch
+    from oracle import operators, solvers
+    from paper_2304_12387_b200 import from_problem, slabs as sl
+    pr = _problem(name, N, p)
+    kw = {"schur": schur, "amg_max_coarse": 16}
+    ref = from_problem(pr, **kw)
+    n_rt = ref.sizes.n_rt
+    xs = random_vector(ref.sizes.n, 3)
+    b = ref.apply_block(torch.from_numpy(xs).cuda())
+    if schur == "chebyshev":
+        x1, r1 = ref.gmres(b, rtol=1e-10, restart=20, maxit=2000)
+        x1, it1 = x1.cpu().numpy(), r1.iters
+    b = b.cpu().numpy()
+    ref.close()
+    if schur == "amg":
+        A = operators.Assembled(pr)
+        last = pr.dim - 1
+        bounds = [sl.slab_bounds(pr.N[last], P, r) for r in range(P)]
+        B = solvers.BlockTriPrecond(A, schur="amg", amg_max_coarse=16)
+        B.diag = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds,
+                                          project_mean=False)
+        x1, it1, conv, _ = solvers.gmres(A.apply_block, B.apply, b, rtol=1e-10, restart=20)
+        assert conv
+
+    def fn(r, op, rt, l2):
+        bl = np.concatenate([b[:n_rt][rt], b[n_rt:][l2]])
+        xl, rep = op.gmres(torch.from_numpy(bl).cuda(), rtol=1e-10, restart=20, maxit=2000)
+        return xl.cpu().numpy(), rep.iters, rep.converged, rt, l2
+
+    res = _run_slabs(pr, P, fn, key=4000 + hash((name, N, p, P, schur)) % 1000, **kw)
+    its = {r[1] for r in res}
+    assert len(its) == 1 and all(r[2] for r in res), its
+    assert abs(res[0][1] - it1) <= 1, (res[0][1], it1)
+    for xl, _, _, rt, l2 in res:
+        nrl = len(rt)
+        assert _rel(xl[:nrl], x1[:n_rt][rt]) < 1e-8
+        assert _rel(xl[nrl:], x1[n_rt:][l2]) < 1e-7
