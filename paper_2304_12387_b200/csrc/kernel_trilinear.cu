@@ -101,6 +101,38 @@ __device__ __forceinline__ void lines(const double* in, double* out, const Tab1D
   }
 }
 
+// the same line pass with every output multiplied by scale[] (laid out like `out`): the
+// pointwise quadrature weights folded into the last forward contraction
+template <int NT, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI, class LO>
+__device__ __forceinline__ void lines_scaled(const double* in, double* out,
+                                             const double* __restrict__ scale, const Tab1D& tab) {
+  constexpr int NIN = (AX == 0) ? N0 : (AX == 1) ? N1 : N2;
+  constexpr int B0 = (AX == 0) ? N1 : N0;
+  constexpr int B1 = (AX == 2) ? N1 : N2;
+  constexpr int SI_A = (AX == 0) ? 1 : (AX == 1) ? LI::S1 : LI::S2;
+  constexpr int SI_0 = (AX == 0) ? LI::S1 : 1;
+  constexpr int SI_1 = (AX == 2) ? LI::S1 : LI::S2;
+  constexpr int SO_A = (AX == 0) ? 1 : (AX == 1) ? LO::S1 : LO::S2;
+  constexpr int SO_0 = (AX == 0) ? LO::S1 : 1;
+  constexpr int SO_1 = (AX == 2) ? LO::S1 : LO::S2;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < B0 * B1; it += NT) {
+    const int b0 = it % B0, b1 = it / B0;
+    const double* pi = in + b0 * SI_0 + b1 * SI_1;
+    const int oo = b0 * SO_0 + b1 * SO_1;
+    double v[NIN];
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) v[t] = pi[t * SI_A];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < NIN; ++t) s = fma(tcoef<KIND, FWD>(tab, o, t), v[t], s);
+      out[oo + o * SO_A] = s * scale[oo + o * SO_A];
+    }
+  }
+}
+
 template <int P>
 struct TG {   // per-component layouts at every stage
   static constexpr int Q = P + 2;
@@ -389,29 +421,35 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
         lines<NT, Q, P, P, 0, P, TB_G2, false, GA, L2>(ta, vd, tab);
         __syncthreads();
       }
-      // z = 0, p = D^-1 r
+      // PCG with the iterate, residual, direction and diagonal in registers (KP entries per
+      // thread); only the direction goes through shared memory for the W_g apply
+      constexpr int KP = (P3 + NT - 1) / NT;
+      auto off = [&](int i) { return i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P)); };
+      double rz[KP], rr[KP], rp[KP], rd[KP], ra[KP];
       double rs = 0.0;
-      for (int i = tid; i < P3; i += NT) {
-        const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
-        vz[o] = 0.0;
-        const double s = vr[o] / vd[o];
-        vp[o] = s;
-        rs += vr[o] * s;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {   // z = 0, p = D^-1 r
+        const int i = tid + k * NT;
+        rz[k] = 0.0;
+        rr[k] = 0.0; rd[k] = 1.0; rp[k] = 0.0;
+        if (i < P3) {
+          const int o = off(i);
+          rr[k] = vr[o];
+          rd[k] = vd[o];
+          rp[k] = rr[k] / rd[k];
+          vp[o] = rp[k];
+          rs += rr[k] * rp[k];
+        }
       }
       rs = cta_sum<NT>(rs, red);
       const double rs0 = rs;
       for (int it = 0; it < 40 && rs > 1e-30 * rs0 && rs > 0.0; ++it) {
-        // ap = W_g p
+        // ap = W_g p (the pointwise w_q / det J_q folded into the last forward pass)
         lines<NT, P, P, P, 0, Q, TB_G, true, L2, GA>(vp, ta, tab);
         __syncthreads();
         lines<NT, Q, P, P, 1, Q, TB_G, true, GA, GB>(ta, tb, tab);
         __syncthreads();
-        lines<NT, Q, Q, P, 2, Q, TB_G, true, GB, GV>(tb, tv, tab);
-        __syncthreads();
-        for (int qi = tid; qi < NQ; qi += NT) {
-          const int o = qi % Q + GV::S1 * ((qi / Q) % Q) + GV::S2 * (qi / (Q * Q));
-          tv[o] *= gq[o];
-        }
+        lines_scaled<NT, Q, Q, P, 2, Q, TB_G, true, GB, GV>(tb, tv, gq, tab);
         __syncthreads();
         lines<NT, Q, Q, Q, 2, P, TB_G, false, GV, GB>(tv, tb, tab);
         __syncthreads();
@@ -420,29 +458,38 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
         lines<NT, Q, P, P, 0, P, TB_G, false, GA, L2>(ta, vap, tab);
         __syncthreads();
         double pap = 0.0;
-        for (int i = tid; i < P3; i += NT) {
-          const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
-          pap += vp[o] * vap[o];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int i = tid + k * NT;
+          ra[k] = (i < P3) ? vap[off(i)] : 0.0;
+          pap += rp[k] * ra[k];
         }
         pap = cta_sum<NT>(pap, red);
         const double al = rs / pap;
         double rsn = 0.0;
-        for (int i = tid; i < P3; i += NT) {
-          const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
-          vz[o] += al * vp[o];
-          const double r = vr[o] - al * vap[o];
-          vr[o] = r;
-          rsn += r * (r / vd[o]);
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          rz[k] += al * rp[k];
+          rr[k] -= al * ra[k];
+          rsn += rr[k] * (rr[k] / rd[k]);
         }
         rsn = cta_sum<NT>(rsn, red);
         const double be = rsn / rs;
-        for (int i = tid; i < P3; i += NT) {
-          const int o = i % P + L2::S1 * ((i / P) % P) + L2::S2 * (i / (P * P));
-          vp[o] = vr[o] / vd[o] + be * vp[o];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int i = tid + k * NT;
+          rp[k] = rr[k] / rd[k] + be * rp[k];
+          if (i < P3) vp[off(i)] = rp[k];
         }
         rs = rsn;
         __syncthreads();
       }
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int i = tid + k * NT;
+        if (i < P3) vz[off(i)] = rz[k];
+      }
+      __syncthreads();
       // y = H z (histopolation basis) -> sz1
       lines<NT, P, P, P, 0, P, TB_HG, true, L2, L2>(vz, vap, tab);
       __syncthreads();
@@ -566,7 +613,8 @@ __global__ void __launch_bounds__(128) tri_z_direct_kernel(const TriArgs a,
 template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
-  constexpr int NT = 64;
+  // W^-1 alone at p = 3 (27 cells): one warp per element — its barriers are warp-synchronous
+  constexpr int NT = (MODE == 2 && P == 3) ? 32 : 64;
   TriArgs a;
   a.x = x; a.y = y;
   a.vert = h->d_vert;
