@@ -14,6 +14,8 @@
 // faces stored.  Z (constant-J elements only) and D u are element-local.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace hdiv {
@@ -72,7 +74,8 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
 
 // line contraction along AX: in (N0,N1,N2) layout LI -> out (.. NO at AX ..) layout LO
 template <int NT, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI, class LO>
-__device__ __forceinline__ void lines(const double* in, double* out, const Tab1D& tab) {
+__device__ __forceinline__ void lines(const double* in, double* out, const Tab1D& tab,
+                                      int start = -1, int stride = NT) {
   constexpr int NIN = (AX == 0) ? N0 : (AX == 1) ? N1 : N2;
   // the two other axes (lanes over the first: odd stride)
   constexpr int B0 = (AX == 0) ? N1 : N0;
@@ -84,7 +87,7 @@ __device__ __forceinline__ void lines(const double* in, double* out, const Tab1D
   constexpr int SO_0 = (AX == 0) ? LO::S1 : 1;
   constexpr int SO_1 = (AX == 2) ? LO::S1 : LO::S2;
 #pragma unroll 1
-  for (int it = threadIdx.x; it < B0 * B1; it += NT) {
+  for (int it = (start < 0 ? (int)threadIdx.x : start); it < B0 * B1; it += stride) {
     const int b0 = it % B0, b1 = it / B0;
     const double* pi = in + b0 * SI_0 + b1 * SI_1;
     double* po = out + b0 * SO_0 + b1 * SO_1;
@@ -130,6 +133,19 @@ __device__ __forceinline__ void lines_scaled(const double* in, double* out,
       for (int t = 0; t < NIN; ++t) s = fma(tcoef<KIND, FWD>(tab, o, t), v[t], s);
       out[oo + o * SO_A] = s * scale[oo + o * SO_A];
     }
+  }
+}
+
+// one component's line pass of a stage: with 96-thread CTAs warp COMP takes component COMP's
+// lines (the three components run side by side, no divergence), else all threads take them
+template <int NT, int COMP, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI,
+          class LO>
+__device__ __forceinline__ void lines_c(const double* in, double* out, const Tab1D& tab) {
+  if constexpr (NT == 96) {
+    if ((int)(threadIdx.x >> 5) == COMP)
+      lines<NT, N0, N1, N2, AX, NO, KIND, FWD, LI, LO>(in, out, tab, threadIdx.x & 31, 32);
+  } else {
+    lines<NT, N0, N1, N2, AX, NO, KIND, FWD, LI, LO>(in, out, tab);
   }
 }
 
@@ -238,9 +254,9 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   }
   if constexpr (!ZONLY) {
   // ---- forward: axis 0, 1, 2 (3 components per stage), + D u and Z q~ ----
-  lines<NT, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0>(su(0), sA(0), tab);
-  lines<NT, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1>(su(1), sA(1), tab);
-  lines<NT, P, P, P + 1, 0, Q, TB_H, true, typename T::U2, typename T::A2>(su(2), sA(2), tab);
+  lines_c<NT, 0, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0>(su(0), sA(0), tab);
+  lines_c<NT, 1, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1>(su(1), sA(1), tab);
+  lines_c<NT, 2, P, P, P + 1, 0, Q, TB_H, true, typename T::U2, typename T::A2>(su(2), sA(2), tab);
   if constexpr (BLOCK) {
     for (int i = tid; i < P3; i += NT) {
       const int A = i % P, B = (i / P) % P, C = i / (P * P);
@@ -251,13 +267,13 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     }
   }
   __syncthreads();
-  lines<NT, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0>(sA(0), sB(0), tab);
-  lines<NT, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1>(sA(1), sB(1), tab);
-  lines<NT, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2>(sA(2), sB(2), tab);
+  lines_c<NT, 0, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0>(sA(0), sB(0), tab);
+  lines_c<NT, 1, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1>(sA(1), sB(1), tab);
+  lines_c<NT, 2, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2>(sA(2), sB(2), tab);
   __syncthreads();
-  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V>(sB(0), sV(0), tab);
-  lines<NT, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V>(sB(1), sV(1), tab);
-  lines<NT, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V>(sB(2), sV(2), tab);
+  lines_c<NT, 0, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V>(sB(0), sV(0), tab);
+  lines_c<NT, 1, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V>(sB(1), sV(1), tab);
+  lines_c<NT, 2, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V>(sB(2), sV(2), tab);
   __syncthreads();
   // ---- pointwise G_q = w_q mw / det J  J^T J ----
   const double mw = scoef[0];
@@ -280,17 +296,17 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   }
   __syncthreads();
   // ---- backward: axis 2, 1, 0 ----
-  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B0>(sV(0), sB(0), tab);
-  lines<NT, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B1>(sV(1), sB(1), tab);
-  lines<NT, Q, Q, Q, 2, P + 1, TB_L, false, typename T::V, typename T::B2>(sV(2), sB(2), tab);
+  lines_c<NT, 0, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B0>(sV(0), sB(0), tab);
+  lines_c<NT, 1, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B1>(sV(1), sB(1), tab);
+  lines_c<NT, 2, Q, Q, Q, 2, P + 1, TB_L, false, typename T::V, typename T::B2>(sV(2), sB(2), tab);
   __syncthreads();
-  lines<NT, Q, Q, P, 1, P, TB_H, false, typename T::B0, typename T::A0>(sB(0), sA(0), tab);
-  lines<NT, Q, Q, P, 1, P + 1, TB_L, false, typename T::B1, typename T::A1>(sB(1), sA(1), tab);
-  lines<NT, Q, Q, P + 1, 1, P, TB_H, false, typename T::B2, typename T::A2>(sB(2), sA(2), tab);
+  lines_c<NT, 0, Q, Q, P, 1, P, TB_H, false, typename T::B0, typename T::A0>(sB(0), sA(0), tab);
+  lines_c<NT, 1, Q, Q, P, 1, P + 1, TB_L, false, typename T::B1, typename T::A1>(sB(1), sA(1), tab);
+  lines_c<NT, 2, Q, Q, P + 1, 1, P, TB_H, false, typename T::B2, typename T::A2>(sB(2), sA(2), tab);
   __syncthreads();
-  lines<NT, Q, P, P, 0, P + 1, TB_L, false, typename T::A0, typename T::U0>(sA(0), su(0), tab);
-  lines<NT, Q, P + 1, P, 0, P, TB_H, false, typename T::A1, typename T::U1>(sA(1), su(1), tab);
-  lines<NT, Q, P, P + 1, 0, P, TB_H, false, typename T::A2, typename T::U2>(sA(2), su(2), tab);
+  lines_c<NT, 0, Q, P, P, 0, P + 1, TB_L, false, typename T::A0, typename T::U0>(sA(0), su(0), tab);
+  lines_c<NT, 1, Q, P + 1, P, 0, P, TB_H, false, typename T::A1, typename T::U1>(sA(1), su(1), tab);
+  lines_c<NT, 2, Q, P, P + 1, 0, P, TB_H, false, typename T::A2, typename T::U2>(sA(2), su(2), tab);
   __syncthreads();
   // ---- D^T q~ and scatter (per component; boundary faces by atomics) ----
   {
@@ -613,8 +629,11 @@ __global__ void __launch_bounds__(128) tri_z_direct_kernel(const TriArgs a,
 template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
-  // W^-1 alone at p = 3 (27 cells): one warp per element — its barriers are warp-synchronous
-  constexpr int NT = (MODE == 2 && P == 3) ? 32 : 64;
+  // CTA size (r01 A/B, scripts/tri_nt.sh): W^-1 alone at p = 3 — one warp per element (its
+  // barriers are warp-synchronous); mass-only / gamma = 0 applies at p = 4, 5 — three warps,
+  // one per RT component in every line-pass stage; otherwise 64 threads (the local CG prefers it)
+  constexpr int NT = (MODE == 2) ? (P == 3 ? 32 : 64) : 64;
+  const bool wide = (MODE != 2) && (P == 4 || P == 5) && !(MODE == 1 && h->has_z);
   TriArgs a;
   a.x = x; a.y = y;
   a.vert = h->d_vert;
@@ -628,6 +647,12 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   if constexpr (MODE == 2 && P <= 2) {
     if (!h->d_gvert) {
       tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (MODE != 2 && (P == 4 || P == 5)) {
+    if (wide) {
+      tri_kernel<P, 96, MODE><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab);
       return cudaGetLastError();
     }
   }
