@@ -493,6 +493,36 @@ def main():
         del xs, bs, xo, dq
         torch.cuda.empty_cache()
 
+    # Config 3's own apply (trilinear hexes: quadrature kernel, FP64-ALU-class):
+    # GDOF/s and the fraction of the measured FP64 FMA peak (profiles/r01_fp64_peak.txt) for the
+    # analytic flop count of the sum-factorised kernel
+    if not args.no_minres and ws == 1:
+        from synth import make_config
+        from paper_2304_12387_b200 import from_problem
+        pr3 = make_config("c3")
+        op3 = from_problem(pr3)
+        x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
+        y3 = torch.empty_like(x3)
+        ms3 = time_applies(op3, x3, y3, 20, 5, None, torch) / 20
+        P3_, Q3_ = pr3.p, pr3.p + 2
+        fma = 0
+        for c in range(3):   # forward interpolation of component c + its transpose
+            E3 = [P3_ + 1 if a == c else P3_ for a in range(3)]
+            fma += E3[1] * E3[2] * E3[0] * Q3_ + Q3_ * E3[2] * E3[1] * Q3_ + Q3_ * Q3_ * E3[2] * Q3_
+        flops_el = 2 * 2 * fma + 60 * Q3_ ** 3 + 6 * P3_ ** 3 + 2 * 3 * P3_ ** 2 * (P3_ + 1)
+        fp64_peak = 34.116   # measured, profiles/r01_fp64_peak.txt
+        tf = flops_el * pr3.E / (ms3 * 1e-3) / 1e12
+        result["config3_apply"] = {
+            "workload": WORKLOADS["c3"] + " (block apply; gamma = 0: no W^-1)",
+            "dofs": op3.sizes.n, "ms": ms3, "GDOF_s": op3.sizes.n / ms3 / 1e6,
+            "roofline": {"bound": "alu", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": tf / fp64_peak, "flops_per_element": flops_el,
+                         "peak_source": "measured FP64 FMA microbenchmark (scripts/fp64_peak.cu)"},
+            "hbm_frac": 16 * op3.sizes.n / (ms3 * 1e-3) / 1e9 / peak}
+        op3.close()
+        del x3, y3
+        torch.cuda.empty_cache()
+
     # W^-1 benchmark of Table dg-mass-inv (NEXT-2): ~1.7e6 L2 DOFs on a jittered
     # hex mesh, 100 applications of the (2,2)-block inverse by the fused element-local CG
     if not args.no_minres and ws == 1:
