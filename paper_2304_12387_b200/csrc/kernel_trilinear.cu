@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "tri_layouts.h"
 
 namespace hdiv {
 namespace {
@@ -38,10 +39,16 @@ struct TriArgs {
   const int* skip;
 };
 
-// padded layout of a (D0, D1, D2) array
-template <int D0, int D1, int D2>
+// padded layout of a (D0, D1, D2) array of the order-PP kernel: the strides with the fewest
+// modelled bank-conflict wavefronts over every pass that touches arrays of this shape
+// (tri_layouts.h, scripts/tri_layout_model.py), else odd-padded extents
+template <int D0, int D1, int D2, int PP = 0>
 struct Lay {
-  static constexpr int S1 = odd_up(D0), S2 = S1 * odd_up(D1), SIZE = S2 * D2;
+  static constexpr int LI = find_tri_layout(PP, 64, D0, D1, D2);
+  static constexpr int S1 = LI >= 0 ? kTriLayouts[LI].S1 : odd_up(D0);
+  static constexpr int S2 = LI >= 0 ? kTriLayouts[LI].S2 : S1 * odd_up(D1);
+  static constexpr int SIZE = S2 * D2;
+  static_assert(S1 >= D0 && S2 >= S1 * D1, "overlapping layout");
 };
 
 // 1D tables: B_l, B_h, M_h^-1, GL-nodal basis at the quadrature points (BG), its square
@@ -152,11 +159,11 @@ __device__ __forceinline__ void lines_c(const double* in, double* out, const Tab
 template <int P>
 struct TG {   // per-component layouts at every stage
   static constexpr int Q = P + 2;
-  using U0 = Lay<P + 1, P, P>;  using U1 = Lay<P, P + 1, P>;  using U2 = Lay<P, P, P + 1>;
-  using A0 = Lay<Q, P, P>;      using A1 = Lay<Q, P + 1, P>;  using A2 = Lay<Q, P, P + 1>;
-  using B0 = Lay<Q, Q, P>;      using B1 = Lay<Q, Q, P>;      using B2 = Lay<Q, Q, P + 1>;
-  using V = Lay<Q, Q, Q>;
-  using L2 = Lay<P, P, P>;
+  using U0 = Lay<P + 1, P, P, P>;  using U1 = Lay<P, P + 1, P, P>;  using U2 = Lay<P, P, P + 1, P>;
+  using A0 = Lay<Q, P, P, P>;      using A1 = Lay<Q, P + 1, P, P>;  using A2 = Lay<Q, P, P + 1, P>;
+  using B0 = Lay<Q, Q, P, P>;      using B1 = Lay<Q, Q, P, P>;      using B2 = Lay<Q, Q, P + 1, P>;
+  using V = Lay<Q, Q, Q, P>;
+  using L2 = Lay<P, P, P, P>;
   static constexpr int SU = (U0::SIZE > U1::SIZE ? (U0::SIZE > U2::SIZE ? U0::SIZE : U2::SIZE)
                                                   : (U1::SIZE > U2::SIZE ? U1::SIZE : U2::SIZE));
   static constexpr int SA = A2::SIZE > A1::SIZE ? A2::SIZE : A1::SIZE;
@@ -360,9 +367,9 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
       //      element-local PCG in the Gauss-Legendre nodal basis with Jacobi preconditioning
       //      (P:606-609): W_h^-1 = H W_g^-1 H^T, W_g = H^T W_h H, H = HG^{(x)3}.
       //      W_g v = B_G^T diag(w_q / det J_q) B_G v by sum factorisation (Q = p+2 points).
-      using GA = Lay<Q, P, P>;
-      using GB = Lay<Q, Q, P>;
-      using GV = Lay<Q, Q, Q>;
+      using GA = Lay<Q, P, P, P>;
+      using GB = Lay<Q, Q, P, P>;
+      using GV = Lay<Q, Q, Q, P>;
       using L2 = typename T::L2;
       __syncthreads();   // sreg is free: the mass part is done
       double* ta = sreg;
