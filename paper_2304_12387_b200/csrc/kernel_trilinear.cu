@@ -242,22 +242,29 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   }
   __syncthreads();
 
-  // trilinear Jacobian column factors on the Q x Q point pairs
-  for (int i = tid; i < 3 * Q * Q * 3; i += NT) {
-    const int c = i / (Q * Q * 3), r = i % (Q * Q * 3), pr = r / 3, d = r % 3;
+  // trilinear Jacobian column factors on the Q x Q point pairs: dT/dx_hat_c is bilinear in the
+  // other two reference coordinates (s, t) with the four edge vectors along c as coefficients
+  // E[c][k] (k = corner (s, t) in {0,1}^2); first the 36 edge-vector entries, then one item per
+  // (c, point pair) evaluating the three coordinates
+  __shared__ double sE[3][4][3];
+  for (int i = tid; i < 36; i += NT) {   // (NT may be 32)
+    const int c = i / 12, k = (i / 3) % 4, d = i % 3;
+    const int s1 = k & 1, t1 = k >> 1;   // corner along the (first, second) other axis
+    int lo[3], hi[3];
+    const int o0 = (c == 0) ? 1 : 0, o1 = (c == 2) ? 1 : 2;
+    lo[c] = 0; hi[c] = 1;
+    lo[o0] = hi[o0] = s1;
+    lo[o1] = hi[o1] = t1;
+    sE[c][k][d] = sX[(hi[0] + 2 * hi[1] + 4 * hi[2]) * 3 + d] - sX[(lo[0] + 2 * lo[1] + 4 * lo[2]) * 3 + d];
+  }
+  __syncthreads();
+  for (int i = tid; i < 3 * Q * Q; i += NT) {
+    const int c = i / (Q * Q), pr = i % (Q * Q);
     const double s = tab.xq[pr % Q], t = tab.xq[pr / Q];
-    auto X = [&](int va, int vb, int vc) { return sX[(va + 2 * vb + 4 * vc) * 3 + d]; };
-    double v;
-    if (c == 0)        // (s,t) = (y,z)
-      v = (1 - s) * (1 - t) * (X(1, 0, 0) - X(0, 0, 0)) + s * (1 - t) * (X(1, 1, 0) - X(0, 1, 0)) +
-          (1 - s) * t * (X(1, 0, 1) - X(0, 0, 1)) + s * t * (X(1, 1, 1) - X(0, 1, 1));
-    else if (c == 1)   // (s,t) = (x,z)
-      v = (1 - s) * (1 - t) * (X(0, 1, 0) - X(0, 0, 0)) + s * (1 - t) * (X(1, 1, 0) - X(1, 0, 0)) +
-          (1 - s) * t * (X(0, 1, 1) - X(0, 0, 1)) + s * t * (X(1, 1, 1) - X(1, 0, 1));
-    else               // (s,t) = (x,y)
-      v = (1 - s) * (1 - t) * (X(0, 0, 1) - X(0, 0, 0)) + s * (1 - t) * (X(1, 0, 1) - X(1, 0, 0)) +
-          (1 - s) * t * (X(0, 1, 1) - X(0, 1, 0)) + s * t * (X(1, 1, 1) - X(1, 1, 0));
-    sJ[c][pr][d] = v;
+    const double w00 = (1 - s) * (1 - t), w10 = s * (1 - t), w01 = (1 - s) * t, w11 = s * t;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      sJ[c][pr][d] = w00 * sE[c][0][d] + w10 * sE[c][1][d] + w01 * sE[c][2][d] + w11 * sE[c][3][d];
   }
   if constexpr (!ZONLY) {
   // ---- forward: axis 0, 1, 2 (3 components per stage), + D u and Z q~ ----
