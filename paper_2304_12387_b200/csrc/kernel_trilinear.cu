@@ -200,7 +200,10 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   const int tid = threadIdx.x;
   const long long e = blockIdx.x;
   const long long NLx = a.NL[0], NLy = a.NL[1];
-  const int ex = (int)(e % NLx), ey = (int)((e / NLx) % NLy), ez = (int)(e / (NLx * NLy));
+  // element coordinates in 32-bit (the grid is < 2^31 CTAs)
+  const unsigned eu = blockIdx.x, nlx = (unsigned)NLx, nly = (unsigned)NLy;
+  const unsigned eyz = eu / nlx;
+  const int ex = (int)(eu - eyz * nlx), ey = (int)(eyz % nly), ez = (int)(eyz / nly);
   const long long nx = a.n[0], ny = a.n[1];
 
   if (tid < 2) scoef[tid] = a.coef[4 * e + tid];
