@@ -121,7 +121,7 @@ vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
     double vn = Az[i] * ig - cd * v[i] - co * v_old[i];
     v_new[i] = vn;
     if (i < nrt) {
-      double zn = vn / (tau * mdiag[i]);
+      double zn = vn * mdiag[i];   // mdiag here: the precomputed 1 / (tau M~)
       z_new[i] = zn;
       if (i < ex_lo || i >= ex_hi) s = fma(zn, vn, s);
     }
@@ -283,10 +283,18 @@ cheb_stencil_kernel(StencilGeo g, const double* __restrict__ minv, const double*
   }
 }
 
-__global__ void diag_scale_kernel(const double* __restrict__ v, const double* __restrict__ mdiag,
-                                  double tau, double* __restrict__ z, long long n) {
+// 1 / (tau M~) once per handle (the (1,1) preconditioner block as a multiply, not a division)
+__global__ void tau_minv_kernel(const double* __restrict__ mdiag, double tau, double* __restrict__ r,
+                                long long n) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) z[i] = v[i] / (tau * mdiag[i]);
+  if (i < n) r[i] = 1.0 / (tau * mdiag[i]);
+}
+
+
+__global__ void scale_minv_kernel(const double* __restrict__ v, const double* __restrict__ minv,
+                                  double* __restrict__ z, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) z[i] = v[i] * minv[i];
 }
 
 __global__ void init_kernel(const double* glob, int P, MState* st, double rtol, int maxit) {
@@ -413,6 +421,7 @@ struct MinresWork {
   double* buf = nullptr;           // all vectors
   double *v[3], *w[3], *z[2], *Az, *r, *d[2];
   double *part_a, *part_b, *part_c, *loc, *glob;
+  double* mtinv = nullptr;         // 1 / (tau M~) [n_rt]
   MState* st = nullptr;            // [2]: iteration j reads st[j & 1], publishes st[(j + 1) & 1]
   MState* st_host = nullptr;       // pinned
   cudaStream_t stream = nullptr;   // own non-blocking stream (graph capture needs one)
@@ -451,7 +460,11 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
     mw->ex_lo = h->off[last];
     mw->ex_hi = h->off[last] + lplane;
   }
-  HDIV_CUDA_TRY(cudaMalloc(&mw->st, 2 * sizeof(MState)));   // double-buffered (wstep_kernel)
+  HDIV_CUDA_TRY(cudaMalloc(&mw->st, 2 * sizeof(MState)));
+  HDIV_CUDA_TRY(cudaMalloc(&mw->mtinv, sizeof(double) * (h->nrt > 0 ? h->nrt : 1)));
+  tau_minv_kernel<<<nb(h->nrt, 256), 256>>>(h->d_mdiag, h->opts.tau, mw->mtinv, h->nrt);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  HDIV_CUDA_TRY(cudaDeviceSynchronize());   // double-buffered (wstep_kernel)
   HDIV_CUDA_TRY(cudaMallocHost(&mw->st_host, sizeof(MState)));
   HDIV_CUDA_TRY(cudaStreamCreateWithFlags(&mw->stream, cudaStreamNonBlocking));
   // Chebyshev constants on [lmax/ratio, lmax], lmax = 2 (reading A10)
@@ -473,6 +486,7 @@ void minres_free(hdiv_ctx* h) {
   if (!h->mw) return;
   cudaFree(h->mw->buf);
   cudaFree(h->mw->st);
+  cudaFree(h->mw->mtinv);
   cudaFreeHost(h->mw->st_host);
   if (h->mw->stream) cudaStreamDestroy(h->mw->stream);
   delete h->mw;
@@ -583,7 +597,7 @@ static hdiv_status cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* 
 hdiv_status apply_precond(hdiv_ctx* h, const double* v, double* z, cudaStream_t s) {
   hdiv_status st = ensure_work(h);
   if (st != HDIV_OK) return st;
-  diag_scale_kernel<<<nb(h->nrt, 256), 256, 0, s>>>(v, h->d_mdiag, h->opts.tau, z, h->nrt);
+  scale_minv_kernel<<<nb(h->nrt, 256), 256, 0, s>>>(v, h->mw->mtinv, z, h->nrt);
   HDIV_CUDA_TRY(cudaGetLastError());
   return cheb_apply(h, v + h->nrt, z + h->nrt, nullptr, nullptr, s);
 }
@@ -629,7 +643,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
   HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[0], 0, n * sizeof(double), s));
   HDIV_CUDA_TRY(cudaMemsetAsync(mw->w[1], 0, n * sizeof(double), s));
   HDIV_CUDA_TRY(cudaMemcpyAsync(mw->v[1], b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  diag_scale_kernel<<<nb(nrt, 256), 256, 0, s>>>(mw->v[1], h->d_mdiag, h->opts.tau, mw->z[0], nrt);
+  scale_minv_kernel<<<nb(nrt, 256), 256, 0, s>>>(mw->v[1], mw->mtinv, mw->z[0], nrt);
   dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->z[0], mw->v[1], nrt, mw->ex_lo, mw->ex_hi,
                                            mw->part_a, nullptr);
   HDIV_CUDA_TRY(cudaGetLastError());
@@ -662,7 +676,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     HDIV_CUDA_TRY(cudaGetLastError());
     hdiv_status st = HDIV_OK;
     if (!one && (st = reduce_scalar(h, mw->part_c, nullptr, done, s)) != HDIV_OK) return st;
-    vupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, h->d_mdiag, h->opts.tau,
+    vupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, mw->mtinv, h->opts.tau,
                                               nrt, n, mw->ex_lo, mw->ex_hi, stc, mw->glob, P,
                                               one ? mw->part_c : nullptr, mw->nb, mw->part_a);
     HDIV_CUDA_TRY(cudaGetLastError());
