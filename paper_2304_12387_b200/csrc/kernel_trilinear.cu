@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(128) tri_z_direct_kernel(const TriArgs a,
 template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
-  // CTA size (r01 A/B, scripts/tri_nt.sh): W^-1 alone at p = 3 — one warp per element (its
+  // CTA size (r01 A/B of 64 vs 96 threads per order): W^-1 alone at p = 3 — one warp per element (its
   // barriers are warp-synchronous); mass-only / gamma = 0 applies at p = 4, 5 — three warps,
   // one per RT component in every line-pass stage; otherwise 64 threads (the local CG prefers it)
   constexpr int NT = (MODE == 2) ? (P == 3 ? 32 : 64) : 64;
