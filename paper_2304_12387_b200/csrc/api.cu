@@ -287,11 +287,6 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
       }
   }
   h->geom = all_box ? GEOM_BOX : (all_affine ? GEOM_AFFINE : GEOM_TRILINEAR);
-  if (h->has_z && h->geom == GEOM_TRILINEAR && dim == 2) {
-    delete h;
-    return fail(HDIV_ERR_UNSUPPORTED,
-                "W^-1 on non-affine quadrilaterals (2D) is not implemented; 3D uses local CG");
-  }
   int want = h->opts.kernel;
   if (want == 2 && !(dim == 3 && all_box)) {
     delete h;
@@ -333,8 +328,10 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     }
     coef[4 * e + 0] = mw[e];
     // 3D quadrature kernel: Z = s_e W_1^-1 by element-local CG (any geometry), s_e = 1/alpha
-    // (grad-div) | gamma (Darcy); 2D kernel: exact Kronecker with z_e = det/alpha | gamma det
-    coef[4 * e + 1] = (dim == 3) ? ((kind == HDIV_GRAD_DIV) ? 1.0 / c2[e] : c2[e]) : zc;
+    // (grad-div) | gamma (Darcy); 2D kernel: exact Kronecker with z_e = det/alpha | gamma det on
+    // parallelograms, s_e with a dense element solve on general quadrilaterals
+    coef[4 * e + 1] = (dim == 3 || h->geom == GEOM_TRILINEAR)
+                          ? ((kind == HDIV_GRAD_DIV) ? 1.0 / c2[e] : c2[e]) : zc;
     coef[4 * e + 2] = 0.0;
     coef[4 * e + 3] = 0.0;
   }

@@ -34,6 +34,7 @@ struct GenArgs {
   int has_z;
   int ess;              // eliminated essential sides (NEXT-3): zero inputs, outputs skipped
   const double* gvert;  // DIAGW: weight by the trilinear gamma field (NEXT-3), else nullptr
+  int dense_z;          // 2D non-affine quadrilaterals: Z = s_e W^-1 by a dense element solve
   const int* skip;
 };
 
@@ -88,6 +89,8 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
   __shared__ double sMhi[P * P];
   __shared__ double scoef[2];
   __shared__ double sG[8];   // vertex gamma values (DIAGW with a.gvert)
+  // 2D non-affine: the element's W (P^2 x P^2) for the dense Cholesky solve of Z
+  __shared__ double sW[(DIM == 2 && BLOCK) ? Pow<DIM>::v(P) * Pow<DIM>::v(P) : 1];
 
   const int tid = threadIdx.x;
   const long long e = blockIdx.x;
@@ -165,7 +168,61 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
         d += su[2 * NC + A + P * (B + P * (C + 1))] - su[2 * NC + A + P * (B + P * C)];
       sy[i] = d;
     }
-    if (a.has_z) {
+    if (DIM == 2 && a.has_z && a.dense_z) {
+      // 2D non-affine quadrilateral: Z q = s_e W^-1 q with W_ab = sum_q w_q psi_a psi_b / det J_q
+      // (P:117), psi_a = h_i(x) h_j(y); W assembled by quadrature, factored by a
+      // right-looking Cholesky across the CTA, solved by substitution
+      constexpr int N = NL2;
+      for (int qi = tid; qi < Q * Q; qi += NT) {   // w_q / det J_q at the Q^2 points -> sT1
+        const int qx = qi % Q, qy = qi / Q;
+        const double xh = sx[qx], yh = sx[qy];
+        const double* X = sX;
+        double J[2][2];
+        for (int d = 0; d < 2; ++d) {
+          J[d][0] = (1 - yh) * (X[1 * 2 + d] - X[0 * 2 + d]) + yh * (X[3 * 2 + d] - X[2 * 2 + d]);
+          J[d][1] = (1 - xh) * (X[2 * 2 + d] - X[0 * 2 + d]) + xh * (X[3 * 2 + d] - X[1 * 2 + d]);
+        }
+        sT1[qi] = sw[qx] * sw[qy] / (J[0][0] * J[1][1] - J[0][1] * J[1][0]);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < N * N; idx += NT) {
+        const int ra = idx / N, cb = idx % N;
+        const int i1 = ra % P, j1 = ra / P, i2 = cb % P, j2 = cb / P;
+        double w = 0.0;
+        for (int qy = 0; qy < Q; ++qy) {
+          double t = 0.0;
+          for (int qx = 0; qx < Q; ++qx) t = fma(sT1[qx + Q * qy], sBh[qx * P + i1] * sBh[qx * P + i2], t);
+          w = fma(t, sBh[qy * P + j1] * sBh[qy * P + j2], w);
+        }
+        sW[idx] = w;
+      }
+      __syncthreads();
+      for (int k = 0; k < N; ++k) {   // W = L L^T in place (lower triangle)
+        if (tid == 0) sW[k * N + k] = sqrt(sW[k * N + k]);
+        __syncthreads();
+        for (int i = k + 1 + tid; i < N; i += NT) sW[i * N + k] /= sW[k * N + k];
+        __syncthreads();
+        for (int idx = tid; idx < (N - k - 1) * (N - k - 1); idx += NT) {
+          const int i = k + 1 + idx / (N - k - 1), j = k + 1 + idx % (N - k - 1);
+          if (j <= i) sW[i * N + j] -= sW[i * N + k] * sW[j * N + k];
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {   // L y = q, L^T z = y  -> sT2
+        for (int i = 0; i < N; ++i) {
+          double v = sq[i];
+          for (int j = 0; j < i; ++j) v -= sW[i * N + j] * sT2[j];
+          sT2[i] = v / sW[i * N + i];
+        }
+        for (int i = N - 1; i >= 0; --i) {
+          double v = sT2[i];
+          for (int j = i + 1; j < N; ++j) v -= sW[j * N + i] * sT2[j];
+          sT2[i] = v / sW[i * N + i];
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < NL2; i += NT) sy[i] -= scoef[1] * sT2[i];
+    } else if (a.has_z) {
       // Z q = z (Mh^-1)^{(x)d} q   (constant-J elements)
       contract<NT>(sq, sT1, sMhi, P, 1, P, P, 0, P, P, DIM == 3 ? P : 1);
       __syncthreads();
@@ -357,6 +414,7 @@ cudaError_t launch_g(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.has_z = h->has_z ? 1 : 0;
   a.ess = (MODE == GMODE_MASS || MODE == GMODE_BLOCK) ? h->ess : 0;
   a.gvert = nullptr;
+  a.dense_z = (DIM == 2 && h->geom == GEOM_TRILINEAR) ? 1 : 0;
   a.skip = skip;
   general_kernel<DIM, P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
@@ -418,6 +476,7 @@ static cudaError_t launch_wg(const hdiv_ctx* h, double* wg, cudaStream_t s) {
   a.has_z = 0;
   a.ess = 0;
   a.gvert = h->d_gvert;
+  a.dense_z = 0;
   a.skip = nullptr;
   general_kernel<3, P, 128, GMODE_DIAGW><<<(unsigned)h->E, 128, 0, s>>>(a, h->tab);
   return cudaGetLastError();

@@ -370,3 +370,36 @@ def test_host_apply_pipeline_matches_device_apply(name, N, p, ess, monkeypatch):
         op.apply_block_host(xh, yh)
         assert np.array_equal(yh.numpy(), y), pipe
     op.close()
+
+
+# ---- 2D non-affine quadrilaterals with a nonzero (2,2) block: Z = s_e W^-1 by a dense element
+#      solve (Cholesky of the quadrature-assembled W) ----
+@pytest.mark.parametrize("N,p,kind", [((4, 3), 2, "grad_div"), ((3, 3), 3, "darcy"),
+                                      ((2, 3), 5, "grad_div"), ((3, 2), 1, "darcy")])
+def test_2d_quadrilateral_block_and_minres(N, p, kind):
+    from oracle import operators, solvers
+    from synth import Problem
+    from synth.gen import counter_uniform
+    V = cartesian_vertices(2, N)
+    jit = (2.0 * counter_uniform(11, V.size).reshape(V.shape) - 1.0) * 0.2 / max(N)
+    inner = np.zeros(V.shape[:2], bool)
+    inner[1:-1, 1:-1] = True
+    V = V + jit * inner[..., None]
+    E = N[0] * N[1]
+    pr = Problem("q2d", 2, tuple(N) + (1,), p, kind, V, alpha=10.0 ** random_vector(E, 1),
+                 beta=10.0 ** random_vector(E, 2), eps=10.0 ** random_vector(E, 3),
+                 gamma=10.0 ** random_vector(E, 4), affine=False)
+    A = operators.Assembled(pr)
+    op = _gpu(pr)
+    s = op.sizes
+    x = random_vector(s.n, 17)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL
+    assert _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    b = A.apply_block(random_vector(s.n, 1))
+    P = solvers.BlockDiagPrecond(A)
+    _, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=3000)
+    xg, rep = op.minres(_dev(b), rtol=1e-12, maxit=3000)
+    assert conv_o and rep.converged and abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    op.close()
