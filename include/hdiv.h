@@ -42,7 +42,7 @@ typedef enum {
   HDIV_ERR_CUDA = 5,            /* CUDA runtime error (allocation, launch)             */
   HDIV_ERR_NCCL = 6,            /* NCCL error                                          */
   HDIV_ERR_BREAKDOWN = 7,       /* MINRES gamma^2 < 0: preconditioner not SPD          */
-  HDIV_ERR_UNSUPPORTED = 8,     /* e.g. W^-1 on a non-affine element (NEXT-2)          */
+  HDIV_ERR_UNSUPPORTED = 8,     /* a combination this build does not provide, e.g. hdiv_apply_z in 2D */
   HDIV_ERR_NULL = 9             /* NULL handle or required pointer                      */
 } hdiv_status;
 
