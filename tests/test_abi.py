@@ -41,7 +41,7 @@ def test_status_strings(lib):
 
 
 def _setup(lib, dim=3, N=(2, 2, 2), p=2, kind=0, alpha=None, beta=None, eps=None, gamma=None,
-           slab=None, nranks=1, rank=0, verts=None):
+           slab=None, nranks=1, rank=0, verts=None, gvert=None, essential=0, kernel=0):
     from paper_2304_12387_b200 import binding as b
     z0, z1 = slab or (0, N[min(dim, 3) - 1])
     md = b.MeshDesc(dim, N[0], N[1], N[2] if dim == 3 else 1, z0, z1,
@@ -54,8 +54,8 @@ def _setup(lib, dim=3, N=(2, 2, 2), p=2, kind=0, alpha=None, beta=None, eps=None
         a = np.ascontiguousarray(a, float)
         keep.append(a)
         return a.ctypes.data_as(C.POINTER(C.c_double))
-    co = b.Coeffs(ptr(alpha), ptr(beta), ptr(gamma), ptr(eps), 1.0, 1.0, 0.0, 1.0)
-    op = b.Options(1.0, 4, 30.0, 0)
+    co = b.Coeffs(ptr(alpha), ptr(beta), ptr(gamma), ptr(eps), 1.0, 1.0, 0.0, 1.0, ptr(gvert))
+    op = b.Options(1.0, 4, 30.0, kernel, 0, 0, 0, essential, 0)
     h = C.c_void_p()
     st = lib.hdiv_setup(C.byref(md), p, C.byref(co), kind, C.byref(op), None, rank, nranks, None,
                         C.byref(h))
@@ -76,11 +76,17 @@ def test_setup_validation_before_device_work(lib):
     from synth import cartesian_vertices
     V = cartesian_vertices(3, (2, 2, 2))[:, :, ::-1, :].copy()
     assert _setup(lib, verts=V)[0] == 2
-    # W^-1 on non-affine quadrilaterals (2D) is not implemented (3D uses the local CG, NEXT-2)
+    # unsupported combinations, rejected before device work: the general (vertex-field) gamma
+    # in 2D (NEXT-3, 3D only), the affine tile kernel forced on a non-box mesh
     from synth import cartesian_vertices as cv
     V2 = cv(2, (2, 2)).copy()
     V2[1, 1] += [0.1, 0.05]
-    assert _setup(lib, dim=2, N=(2, 2, 1), verts=V2, alpha=np.ones(4), beta=np.ones(4))[0] == 8
+    assert _setup(lib, dim=2, N=(2, 2, 1), kind=1, eps=np.ones(4), gvert=np.ones(9))[0] == 8
+    assert _setup(lib, dim=2, N=(2, 2, 1), verts=V2, alpha=np.ones(4), beta=np.ones(4),
+                  kernel=2)[0] == 8
+    # essential_sides beyond the 2 dim side bits -> SHAPE
+    assert _setup(lib, dim=2, N=(2, 2, 1), essential=16)[0] == 4
+    assert _setup(lib, essential=64)[0] == 4
 
 
 @pytest.mark.parametrize("p", range(1, 7))
