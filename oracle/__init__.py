@@ -17,13 +17,23 @@ formula of S~ and the sparse triple product, MINRES step by step):
   fem       - element geometry, RT/L2 reference bases, M^e, W^e, B^e    (eq. matrices)
   space     - canonical numbering, Algorithm 1 index tables, D in CSR   (Alg. 1)
   operators - assembled M, W, Z, block apply, diagonals, S~ two paths
-  solvers   - Chebyshev-Jacobi S^-1, block-diagonal preconditioner, MINRES
+  solvers   - Chebyshev-Jacobi S^-1, block-diagonal preconditioner, MINRES (P:411-421, P:663, P:899);
+              block-triangular preconditioner + GMRES (NEXT-4); the pure-Neumann
+              projection after S^-1 (NEXT-3)
+  amg       - smoothed-aggregation AMG V-cycle for S^-1 (NEXT-1, reading A9b), per-slab
+              block-Jacobi (reading A9c)
+  mms       - manufactured-solution loads (convergence-rate pins)
   sample    - element-local evaluation of sampled output rows (full-size parity)
+Essential-flux sides by elimination (NEXT-3) and the general (vertex-field) gamma with
+the full W^-1 W_gamma W^-1 block (NEXT-3) live in operators / space / fem.
 
 Parity pins (tests/test_oracle_*.py, `-m "not gpu"`): closed-form 1D tables,
 SPD / exactness of M, B = W D, D's incidence structure,
 M-matrix S~, Prop. 2.1/2.2 spectra, dense-solve MINRES,
-manufactured-solution convergence rates, closed-form traces.
+manufactured-solution convergence rates, closed-form traces; eliminated sides: the incidence
+boundary, the one-dimensional pure-Neumann nullspace, S~ 1 = 0, exact uniform flow; general
+gamma: the constant-field reduction, an exact weighted Kronecker product, the p = 1
+mean-value closed form; block-Jacobi AMG: exact block solves.
 Parity unpinned: trilinear-element values of M^e beyond the invariants above
 (no closed form exists).
 """
