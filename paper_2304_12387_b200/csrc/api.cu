@@ -512,7 +512,9 @@ static hdiv_status apply_block_host_pipelined(hdiv_ctx* h, const double* xh, dou
   int TZ = 0;
   HDIV_CUDA_TRY(launch_affine_apply_range(h, nullptr, nullptr, 0, 0, &TZ, caller));
   const int64_t NLz = h->NL[2], P = h->p;
-  int64_t cz = (NLz + 15) / 16;   // ~16 chunks: fill + drain cost ~2/16 of a transfer
+  const char* ec = getenv("HDIV_HOST_CHUNKS");
+  const int64_t want = ec ? std::max(1, atoi(ec)) : 32;   // fill + drain cost ~2/want of a transfer
+  int64_t cz = (NLz + want - 1) / want;
   cz = ((cz + TZ - 1) / TZ) * TZ;
   const int nch = (int)((NLz + cz - 1) / cz);
   if (nch > hdiv_ctx::kMaxChunks) return HDIV_ERR_UNSUPPORTED;

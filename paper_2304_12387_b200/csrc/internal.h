@@ -87,7 +87,7 @@ struct hdiv_ctx {
   double* d_xbuf = nullptr;       // host-API staging (lazily allocated)
   double* d_ybuf = nullptr;
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host pipeline: H2D, compute, D2H
-  static constexpr int kMaxChunks = 32;
+  static constexpr int kMaxChunks = 64;
   cudaEvent_t hev[2][kMaxChunks] = {};                // H2D done / compute done per chunk
   // NEXT-3: essential (eliminated) RT sides of THIS rank's slab, bit 2a = side x_a = min of
   // the local grid, bit 2a+1 = max (the last-axis bits only where the slab touches the domain
