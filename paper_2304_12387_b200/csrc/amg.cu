@@ -351,6 +351,37 @@ struct StA {
 #define AMG_LOOP(n) \
   for (long long i = blockIdx.x * (long long)ANT + threadIdx.x; i < (n); i += (long long)gridDim.x * ANT)
 
+// the last level-0 post-smoothing sweep with the MINRES partial <x_out, b> (b = the V-cycle's
+// right-hand side = v_q): saves the separate dot pass; part has gridDim.x entries
+template <class Acc>
+__global__ void __launch_bounds__(ANT) jacobi_dot_kernel(Acc A, long long n,
+                                                         const double* __restrict__ b,
+                                                         const double* __restrict__ xin,
+                                                         double* __restrict__ xout,
+                                                         const double* __restrict__ dl1inv,
+                                                         double* __restrict__ part,
+                                                         const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double red[ANT / 32];
+  double sdot = 0.0;
+  AMG_LOOP(n) {
+    const double ax = A.dot(i, [&](long long j) { return xin[j]; });
+    const double bi = b[i];
+    const double xo = xin[i] + dl1inv[i] * (bi - ax);
+    xout[i] = xo;
+    sdot = fma(xo, bi, sdot);
+  }
+  for (int o = 16; o > 0; o >>= 1) sdot += __shfl_down_sync(0xffffffffu, sdot, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) red[w] = sdot;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double r = (l < ANT / 32) ? red[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+    if (l == 0) part[blockIdx.x] = r;
+  }
+}
+
 // x_out = x_in + Dl1^-1 (b - A x_in); x_in = nullptr means x_in = Dl1^-1 b (first sweep from 0)
 template <class Acc>
 __global__ void __launch_bounds__(ANT) jacobi_kernel(Acc A, long long n, const double* __restrict__ b,
@@ -408,21 +439,39 @@ __global__ void __launch_bounds__(ANT) smooth_r_kernel(Acc A, long long n,
   AMG_LOOP(n) s[i] = r[i] - omega * A.dot(i, [&](long long j) { return t[j]; });
 }
 
-// b_c[I] = sum over aggregate I of s (level 0: element-major fine rows)
+// b_c[I] = sum over aggregate I of s (level 0: element-major fine rows); the 3 x 3 (x 3)
+// subcells' element / local coordinates per axis once, 32-bit (level 0 has < 2^31 rows), then
+// the 27 (9) row indices by adds; summation order x fastest as before
 __global__ void __launch_bounds__(ANT) aggsum0_kernel(Op0 A, long long cd0, long long cd1,
                                                       long long nc, const double* __restrict__ s,
                                                       double* __restrict__ bc,
                                                       const int* __restrict__ done) {
   if (done && *done) return;
+  const int p = A.p;
+  const int pd = (A.dim == 2) ? p * p : p * p * p;
   AMG_LOOP(nc) {
     const long long IX = i % cd0, IY = (i / cd0) % cd1, IZ = (A.dim == 3) ? i / (cd0 * cd1) : 0;
+    int ox[3], oy[3], oz[3];   // element offset * pd + local offset per coordinate
+    bool vx[3], vy[3], vz[3];
+    for (int k = 0; k < 3; ++k) {
+      const int X = (int)(3 * IX) + k, Y = (int)(3 * IY) + k, Z = (int)(3 * IZ) + k;
+      vx[k] = X < A.n[0];
+      vy[k] = Y < A.n[1];
+      vz[k] = (A.dim == 3) ? (Z < A.n[2]) : (k == 0);
+      const int ex = X / p, ey = Y / p, ez = (A.dim == 3) ? Z / p : 0;
+      ox[k] = ex * pd + (X - ex * p);
+      oy[k] = ey * (int)A.NL[0] * pd + p * (Y - ey * p);
+      oz[k] = (A.dim == 3) ? ez * (int)(A.NL[0] * A.NL[1]) * pd + p * p * (Z - ez * p) : 0;
+    }
     double v = 0.0;
-    for (int cz = 0; cz < (A.dim == 3 ? 3 : 1); ++cz)
-      for (int cy = 0; cy < 3; ++cy)
-        for (int cx = 0; cx < 3; ++cx) {
-          const long long X = 3 * IX + cx, Y = 3 * IY + cy, Z = 3 * IZ + cz;
-          if (A.in(X, Y, Z)) v += s[A.idx(X, Y, Z)];
-        }
+    for (int cz = 0; cz < (A.dim == 3 ? 3 : 1); ++cz) {
+      if (!vz[cz]) continue;
+      for (int cy = 0; cy < 3; ++cy) {
+        if (!vy[cy]) continue;
+        for (int cx = 0; cx < 3; ++cx)
+          if (vx[cx]) v += s[(long long)ox[cx] + oy[cy] + oz[cz]];
+      }
+    }
     bc[i] = v;
   }
 }
@@ -709,7 +758,7 @@ hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
 
 // one V-cycle at level l: x = B_l b (x written, b read)
 static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, const int* done,
-                          cudaStream_t s) {
+                          cudaStream_t s, double* part = nullptr, int nbpart = 0) {
   AmgHier* H = h->amg;
   AmgLevel& L = H->L[l];
   if (l + 1 == H->L.size()) {
@@ -767,19 +816,24 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   }
   for (int k = 0; k < nu; ++k) {
     double* out = (k == nu - 1) ? x : nxt;
-    jac(cur, out);
+    if (k == nu - 1 && part && lev0)
+      jacobi_dot_kernel<SellA><<<nbpart, ANT, 0, s>>>(sa, n, b, cur, out, L.dl1inv, part, done);
+    else
+      jac(cur, out);
     if (k < nu - 1) std::swap(cur, nxt);
   }
   HDIV_CUDA_TRY(cudaGetLastError());
   return HDIV_OK;
 }
 
-hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s) {
+hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s,
+                       double* part, int nbpart) {
   if (!h->amg) {
     set_error("AMG hierarchy missing");
     return HDIV_ERR_UNSUPPORTED;
   }
-  return vcycle(h, 0, b, x, done, s);
+  if (part && (h->amg->nu < 1 || h->amg->L.size() < 2)) return HDIV_ERR_UNSUPPORTED;
+  return vcycle(h, 0, b, x, done, s, part, nbpart);
 }
 
 int amg_num_levels(const hdiv_ctx* h) { return h->amg ? (int)h->amg->L.size() : 0; }

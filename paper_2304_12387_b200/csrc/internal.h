@@ -148,7 +148,10 @@ hdiv_status gmres(hdiv_ctx* h, const double* b, double* x, double rtol, int maxi
 void gmres_free(hdiv_ctx* h);
 hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s);
 void amg_free(hdiv_ctx* h);
-hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s);
+// part != nullptr: the last level-0 sweep also writes the partial <x, b> into part[0..nbpart)
+// (HDIV_ERR_UNSUPPORTED, nothing launched, when the hierarchy has no such sweep)
+hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s,
+                       double* part = nullptr, int nbpart = 0);
 int amg_num_levels(const hdiv_ctx* h);
 hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, double* omega,
                            const double** st);

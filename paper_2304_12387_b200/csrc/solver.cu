@@ -537,6 +537,11 @@ static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, doub
                                   const int* done, cudaStream_t s) {
   MinresWork* mw = h->mw;
   if (h->opts.schur_solver == HDIV_SCHUR_AMG) {   // NEXT-1: one V-cycle
+    if (part) {   // the partial <y, vq> fused into the last level-0 smoothing sweep
+      hdiv_status st = amg_vcycle(h, vq, y, done, s, part, h->mw->nb);
+      if (st == HDIV_OK) return HDIV_OK;
+      if (st != HDIV_ERR_UNSUPPORTED) return st;
+    }
     hdiv_status st = amg_vcycle(h, vq, y, done, s);
     if (st != HDIV_OK) return st;
     if (part) {
