@@ -403,3 +403,26 @@ def test_2d_quadrilateral_block_and_minres(N, p, kind):
     xg, rep = op.minres(_dev(b), rtol=1e-12, maxit=3000)
     assert conv_o and rep.converged and abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
     op.close()
+
+
+# ---- degenerate sizes: single elements and one-element-thick meshes, every order ----
+@pytest.mark.parametrize("N,p", [((1, 1, 1), 1), ((1, 1, 1), 4), ((1, 1, 1), 6), ((1, 2, 1), 3),
+                                 ((2, 1, 1), 5), ((1, 1, 3), 2), ((7, 1, 1), 4)])
+def test_tiny_meshes(N, p):
+    from oracle import operators, solvers
+    pr = _problem("c2", N, p)
+    A = operators.Assembled(pr)
+    op = _gpu(pr)
+    s = op.sizes
+    x = random_vector(s.n, 5)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL and _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    rp, col, val = [_host(t) for t in op.schur_csr()]
+    assert np.array_equal(rp, A.S.indptr) and np.array_equal(col, A.S.indices)
+    b = A.apply_block(random_vector(s.n, 6))
+    P = solvers.BlockDiagPrecond(A)
+    _, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=2000)
+    _, rep = op.minres(_dev(b), rtol=1e-12, maxit=2000)
+    assert conv_o and rep.converged and abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    op.close()
