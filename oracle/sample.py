@@ -26,7 +26,12 @@ def element_blocks(prob, e):
         Ze = sla.cho_solve(sla.cho_factor(We), np.eye(nl))
     else:
         We = fem.element_l2_mass(X, 1.0, ref)
-        Wg = fem.element_l2_mass(X, float(prob.gamma[e]), ref)
+        Gv = getattr(prob, "gamma_vertex", None)
+        if Gv is not None:   # general gamma (NEXT-3, reading A22), as in operators.Assembled
+            Ge = fem.element_vertices(Gv[..., None], dim, space.element_index(dim, N, e))
+            Wg = fem.element_l2_mass(X, fem.physical_points(Ge, ref.pts)[:, 0], ref)
+        else:
+            Wg = fem.element_l2_mass(X, float(prob.gamma[e]), ref)
         cf = sla.cho_factor(We)
         Ze = sla.cho_solve(cf, Wg @ sla.cho_solve(cf, np.eye(nl)))
     return Me, Ze

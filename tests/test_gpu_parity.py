@@ -206,13 +206,17 @@ def test_config2_minres_full():
     assert _rel(_host(x), xs) < 1e-7
 
 
-@pytest.mark.parametrize("name,p", [("c4", 4), ("c3", 4)])
+@pytest.mark.parametrize("name,p", [("c4", 4), ("c3", 4), ("c3gv", 4)])
 def test_full_size_sampled_parity(name, p):
-    """BASELINE full sizes (config 4: 128^3 p=4 grad-div; config 3: 64^3 p=4 perturbed Darcy) in
-    the launch configuration bench.py times; sampled outputs computed one by one by the oracle
-    from the element matrices of the touching elements."""
+    """BASELINE full sizes (config 4: 128^3 p=4 grad-div; config 3: 64^3 p=4 perturbed Darcy;
+    config 3b with a general vertex-field gamma, NEXT-3) in the launch configuration bench.py
+    times; sampled outputs computed one by one by the oracle from the element matrices of the
+    touching elements."""
     from oracle import sample
-    pr = make_config(name)
+    pr = make_config("c3" if name == "c3gv" else name)
+    if name == "c3gv":
+        pr.gamma_vertex = (10.0 ** random_vector(pr.vertices[..., 0].size, 42)).reshape(
+            pr.vertices.shape[:-1])
     if name == "c4":
         pr.alpha = 10.0 ** random_vector(pr.E, 41)   # heterogeneous, exercises per-element c_e
         pr.beta = 10.0 ** random_vector(pr.E, 42)
