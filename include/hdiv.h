@@ -42,7 +42,7 @@ typedef enum {
   HDIV_ERR_CUDA = 5,            /* CUDA runtime error (allocation, launch)             */
   HDIV_ERR_NCCL = 6,            /* NCCL error                                          */
   HDIV_ERR_BREAKDOWN = 7,       /* MINRES gamma^2 < 0: preconditioner not SPD          */
-  HDIV_ERR_UNSUPPORTED = 8,     /* a combination this build does not provide, e.g. hdiv_apply_z in 2D */
+  HDIV_ERR_UNSUPPORTED = 8,     /* a combination this build does not provide              */
   HDIV_ERR_NULL = 9             /* NULL handle or required pointer                      */
 } hdiv_status;
 
@@ -144,7 +144,8 @@ hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* st
 /* y_q = Z q: the (2,2) block alone, Z = W_alpha^-1 (grad-div) or gamma_e W^-1 (Darcy, piecewise-
  * constant gamma), P:235-238, P:535-553 — on every 3D geometry through the element-local CG in
  * the Gauss-Legendre nodal basis (exact Kronecker case converges in one
- * step).  q, y_q: DEVICE [n_l2].  3D only (HDIV_ERR_UNSUPPORTED in 2D). */
+ * step); 2D: the quadrature kernel (exact Kronecker inverse on parallelograms, Cholesky of the
+ * quadrature-assembled W on general quadrilaterals); Z = 0 gives y_q = 0.  q, y_q: DEVICE [n_l2]. */
 hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y_q, void* stream);
 /* Same as hdiv_apply_block with HOST x, y (pinned or pageable): H2D copy, apply, D2H copy,
  * ordered after `stream`; blocks until y is on the host (end-to-end path).  On box meshes (one

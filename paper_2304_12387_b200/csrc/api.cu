@@ -475,7 +475,14 @@ hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* st
 
 hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y, void* stream) {
   if (!h || !q || !y) return fail(HDIV_ERR_NULL, "NULL argument");
-  if (h->dim != 3) return fail(HDIV_ERR_UNSUPPORTED, "apply_z is 3D only");
+  if (h->dim == 2) {
+    if (!h->has_z) {   // Darcy gamma = 0: Z = 0
+      HDIV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * h->nl2, (cudaStream_t)stream));
+      return HDIV_OK;
+    }
+    HDIV_CUDA_TRY(launch_general_z(h, q, y, (cudaStream_t)stream));
+    return HDIV_OK;
+  }
   HDIV_CUDA_TRY(launch_trilinear_apply(h, q, y, MODE_ZONLY, nullptr, (cudaStream_t)stream));
   return HDIV_OK;
 }

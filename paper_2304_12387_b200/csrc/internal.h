@@ -122,6 +122,7 @@ cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, i
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                  const int* skip, cudaStream_t s);
 cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s);
+cudaError_t launch_general_z(const hdiv_ctx* h, const double* q, double* y, cudaStream_t s);
 cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                    const int* skip, cudaStream_t s);
 cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,

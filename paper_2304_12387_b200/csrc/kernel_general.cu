@@ -20,7 +20,7 @@
 namespace hdiv {
 namespace {
 
-enum { GMODE_MASS = 1, GMODE_BLOCK = 2, GMODE_DIAGM = 3, GMODE_DIAGW = 4 };
+enum { GMODE_MASS = 1, GMODE_BLOCK = 2, GMODE_DIAGM = 3, GMODE_DIAGW = 4, GMODE_ZONLY = 5 };
 
 struct GenArgs {
   const double* x;      // [u ; q]  (MASS: u)
@@ -79,18 +79,19 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
   constexpr int NC = (P + 1) * Pow<DIM>::v(P) / P;     // DOFs per component
   constexpr int NL2 = Pow<DIM>::v(P);
   constexpr bool BLOCK = (MODE == GMODE_BLOCK);
+  constexpr bool ZO = (MODE == GMODE_ZONLY);   // y = Z q alone (hdiv_apply_z, 2D)
   if (a.skip && *a.skip) return;
   __shared__ double sBl[Q * (P + 1)], sBh[Q * P], sw[Q], sx[Q];
   __shared__ double sX[8 * 3];
   __shared__ double su[DIM * NC];      // inputs u^c (local tensor order, i fastest)
   __shared__ double sV[DIM * NQ];      // quadrature values per component
   __shared__ double sT1[NQ], sT2[NQ];  // contraction scratch
-  __shared__ double sq[BLOCK ? NL2 : 1], sy[BLOCK || MODE == GMODE_DIAGW ? NL2 : 1];
+  __shared__ double sq[BLOCK || ZO ? NL2 : 1], sy[BLOCK || ZO || MODE == GMODE_DIAGW ? NL2 : 1];
   __shared__ double sMhi[P * P];
   __shared__ double scoef[2];
   __shared__ double sG[8];   // vertex gamma values (DIAGW with a.gvert)
   // 2D non-affine: the element's W (P^2 x P^2) for the dense Cholesky solve of Z
-  __shared__ double sW[(DIM == 2 && BLOCK) ? Pow<DIM>::v(P) * Pow<DIM>::v(P) : 1];
+  __shared__ double sW[(DIM == 2 && (BLOCK || ZO)) ? Pow<DIM>::v(P) * Pow<DIM>::v(P) : 1];
 
   const int tid = threadIdx.x;
   const long long e = blockIdx.x;
@@ -149,15 +150,16 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
       su[i] = v;
     }
   }
-  if constexpr (BLOCK) {
-    const double* q = a.x + a.nrt;
+  if constexpr (BLOCK || ZO) {
+    const double* q = ZO ? a.x : a.x + a.nrt;
     for (int i = tid; i < NL2; i += NT) sq[i] = q[e * NL2 + i];
   }
   __syncthreads();
 
   // ---- D u - Z q (element-local) ----
-  if constexpr (BLOCK) {
+  if constexpr (BLOCK || ZO) {
     for (int i = tid; i < NL2; i += NT) {
+      if constexpr (ZO) { sy[i] = 0.0; continue; }
       int A = i % P, B = (i / P) % P, C = (DIM == 3) ? i / (P * P) : 0;
       double d = 0.0;
       // x faces: component 0 index A + (P+1)(B + P C)
@@ -236,6 +238,10 @@ __global__ void __launch_bounds__(NT) general_kernel(const GenArgs a,
       for (int i = tid; i < NL2; i += NT) sy[i] -= scoef[1] * zq[i];
     }
     __syncthreads();
+    if constexpr (ZO) {   // y = Z q = -(0 - Z q)
+      for (int i = tid; i < NL2; i += NT) a.y[e * NL2 + i] = -sy[i];
+      return;
+    }
   }
 
   // ---- forward: component values at quadrature points ----
@@ -415,6 +421,7 @@ cudaError_t launch_g(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ess = (MODE == GMODE_MASS || MODE == GMODE_BLOCK) ? h->ess : 0;
   a.gvert = nullptr;
   a.dense_z = (DIM == 2 && h->geom == GEOM_TRILINEAR) ? 1 : 0;
+  if (MODE == GMODE_ZONLY) a.has_z = 1;
   a.skip = skip;
   general_kernel<DIM, P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
@@ -453,6 +460,11 @@ cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, 
   if (e != cudaSuccess) return e;
   if (mode == MODE_BLOCK) return dispatch<GMODE_BLOCK>(h, x, y, skip, s);
   return dispatch<GMODE_MASS>(h, x, y, skip, s);
+}
+
+// y = Z q, the (2,2) block alone, 2D (3D: the trilinear kernel's W^-1 path)
+cudaError_t launch_general_z(const hdiv_ctx* h, const double* q, double* y, cudaStream_t s) {
+  return dispatch<GMODE_ZONLY>(h, q, y, nullptr, s);
 }
 
 cudaError_t launch_mass_diag(const hdiv_ctx* h, double* diag, cudaStream_t s) {

@@ -315,9 +315,11 @@ def test_amg_precond_and_minres_parity(name, N, p, mc):
 
 
 @pytest.mark.parametrize("name,N,p", [("c3gd", (3, 2, 2), 2), ("c3gd", (2, 2, 3), 5), ("c3g", (2, 3, 2), 4),
-                                      ("c2", (3, 2, 2), 3), ("c5", (5, 5, 3), 1)])
+                                      ("c2", (3, 2, 2), 3), ("c5", (5, 5, 3), 1), ("c1", None, None),
+                                      ("c1", (5, 3), 4)])
 def test_apply_z_parity(name, N, p):
-    """Z q alone (W^-1 through the local CG on any 3D geometry) against the oracle's Cholesky."""
+    """Z q alone (W^-1 through the local CG on any 3D geometry; 2D: the quadrature kernel's
+    Kronecker / dense element solve) against the oracle's Cholesky."""
     from oracle import operators
     pr = _problem(name, N, p)
     A = operators.Assembled(pr, with_schur=False)
@@ -401,6 +403,8 @@ def test_2d_quadrilateral_block_and_minres(N, p, kind):
     yo = A.apply_block(x)
     assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL
     assert _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    q = random_vector(s.n_l2, 29)
+    assert _rel(_host(op.apply_z(_dev(q))), A.apply_Z(q)) < TOL     # the (2,2) block alone
     b = A.apply_block(random_vector(s.n, 1))
     P = solvers.BlockDiagPrecond(A)
     _, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=3000)
