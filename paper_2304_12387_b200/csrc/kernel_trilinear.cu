@@ -80,7 +80,9 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
 }
 
 // line contraction along AX: in (N0,N1,N2) layout LI -> out (.. NO at AX ..) layout LO
-template <int NT, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI, class LO>
+// EPC > 1: the lines of EPC elements whose arrays sit ES doubles apart form one item space
+template <int NT, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI, class LO,
+          int EPC = 1, int ES = 0>
 __device__ __forceinline__ void lines(const double* in, double* out, const Tab1D& tab,
                                       int start = -1, int stride = NT) {
   constexpr int NIN = (AX == 0) ? N0 : (AX == 1) ? N1 : N2;
@@ -93,11 +95,14 @@ __device__ __forceinline__ void lines(const double* in, double* out, const Tab1D
   constexpr int SO_A = (AX == 0) ? 1 : (AX == 1) ? LO::S1 : LO::S2;
   constexpr int SO_0 = (AX == 0) ? LO::S1 : 1;
   constexpr int SO_1 = (AX == 2) ? LO::S1 : LO::S2;
+  constexpr int NB = B0 * B1;
 #pragma unroll 1
-  for (int it = (start < 0 ? (int)threadIdx.x : start); it < B0 * B1; it += stride) {
-    const int b0 = it % B0, b1 = it / B0;
-    const double* pi = in + b0 * SI_0 + b1 * SI_1;
-    double* po = out + b0 * SO_0 + b1 * SO_1;
+  for (int it = (start < 0 ? (int)threadIdx.x : start); it < EPC * NB; it += stride) {
+    const int el = (EPC > 1) ? it / NB : 0;
+    const int r = (EPC > 1) ? it - el * NB : it;
+    const int b0 = r % B0, b1 = r / B0;
+    const double* pi = in + el * ES + b0 * SI_0 + b1 * SI_1;
+    double* po = out + el * ES + b0 * SO_0 + b1 * SO_1;
     double v[NIN];
 #pragma unroll
     for (int t = 0; t < NIN; ++t) v[t] = pi[t * SI_A];
@@ -146,13 +151,13 @@ __device__ __forceinline__ void lines_scaled(const double* in, double* out,
 // one component's line pass of a stage: with 96-thread CTAs warp COMP takes component COMP's
 // lines (the three components run side by side, no divergence), else all threads take them
 template <int NT, int COMP, int N0, int N1, int N2, int AX, int NO, int KIND, bool FWD, class LI,
-          class LO>
+          class LO, int EPC = 1, int ES = 0>
 __device__ __forceinline__ void lines_c(const double* in, double* out, const Tab1D& tab) {
   if constexpr (NT == 96) {
     if ((int)(threadIdx.x >> 5) == COMP)
-      lines<NT, N0, N1, N2, AX, NO, KIND, FWD, LI, LO>(in, out, tab, threadIdx.x & 31, 32);
+      lines<NT, N0, N1, N2, AX, NO, KIND, FWD, LI, LO, EPC, ES>(in, out, tab, threadIdx.x & 31, 32);
   } else {
-    lines<NT, N0, N1, N2, AX, NO, KIND, FWD, LI, LO>(in, out, tab);
+    lines<NT, N0, N1, N2, AX, NO, KIND, FWD, LI, LO, EPC, ES>(in, out, tab);
   }
 }
 
@@ -548,6 +553,224 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   }
 }
 
+// Mass apply / gamma = 0 block apply with EPC elements per 96-thread CTA: warp c takes the line
+// passes of RT component c for all EPC elements, so a stage's lines fill the lanes (one element
+// leaves 37 % of them idle at p = 4: 16-24 lines per component and stage) — same arithmetic,
+// same order per output as tri_kernel<P, 96, MODE>.
+template <int P, int EPC, bool BLOCK>
+__global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
+                                                       const __grid_constant__ Tab1D tab,
+                                                       long long E) {
+  constexpr int NT = 96;
+  using T = TG<P>;
+  constexpr int Q = P + 2;
+  constexpr int NQ = Q * Q * Q;
+  constexpr int P3 = P * P * P;
+  constexpr int NU = (P + 1) * P * P;
+  if (a.skip && *a.skip) return;
+  constexpr int R1 = (3 * T::SU > 3 * T::SB) ? 3 * T::SU : 3 * T::SB;
+  constexpr int R2 = (3 * T::SA > 3 * T::SV) ? 3 * T::SA : 3 * T::SV;
+  constexpr int ES = R1 + R2;   // per-element stride of the stage arrays
+  __shared__ double sreg[EPC * ES];
+  __shared__ double sX[EPC][24];
+  __shared__ double sE[EPC][3][4][3];
+  __shared__ double sJ[EPC][3][Q * Q][3];
+  __shared__ double sq[BLOCK ? EPC * T::SL : 1], sy[BLOCK ? EPC * P3 : 1];
+  __shared__ double smw[EPC];
+  __shared__ int sEc[EPC][4];   // ex, ey, ez, valid
+  const int tid = threadIdx.x;
+  const long long e0 = (long long)blockIdx.x * EPC;
+  const long long NLx = a.NL[0], NLy = a.NL[1];
+  const long long nx = a.n[0], ny = a.n[1];
+  if (tid < EPC) {
+    const long long e = e0 + tid;
+    const bool ok = e < E;
+    const unsigned eu = ok ? (unsigned)e : 0u, nlx = (unsigned)NLx, nly = (unsigned)NLy;
+    const unsigned eyz = eu / nlx;
+    sEc[tid][0] = (int)(eu - eyz * nlx);
+    sEc[tid][1] = (int)(eyz % nly);
+    sEc[tid][2] = (int)(eyz / nly);
+    sEc[tid][3] = ok ? 1 : 0;
+    smw[tid] = ok ? a.coef[4 * e] : 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < EPC * 24; i += NT) {
+    const int el = i / 24, v = (i % 24) / 3, d = i % 3;
+    double xv = 0.0;
+    if (sEc[el][3]) {
+      const long long g = ((long long)(sEc[el][2] + (v >> 2)) * (NLy + 1) + (sEc[el][1] + ((v >> 1) & 1))) *
+                              (NLx + 1) + (sEc[el][0] + (v & 1));
+      xv = a.vert[g * 3 + d];
+    }
+    sX[el][v * 3 + d] = xv;
+  }
+  // gather u (eliminated essential faces act as zero inputs; absent elements as zeros)
+  for (int l = tid; l < EPC * NU; l += NT) {
+    const int el = l / NU, r = l - (l / NU) * NU;
+    const int ex = sEc[el][0], ey = sEc[el][1], ez = sEc[el][2];
+    double* sr = sreg + el * ES;
+    {
+      const int li = r % (P + 1), lj = (r / (P + 1)) % P, lk = r / ((P + 1) * P);
+      const long long g = a.off[0] + (long long)ex * P + li + (nx + 1) * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
+      const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 0, (long long)ex * P + li, nx));
+      sr[0 * T::SU + li + T::U0::S1 * lj + T::U0::S2 * lk] = m ? 0.0 : a.x[g];
+    }
+    {
+      const int li = r % P, lj = (r / P) % (P + 1), lk = r / (P * (P + 1));
+      const long long g = a.off[1] + (long long)ex * P + li + nx * ((long long)ey * P + lj + (ny + 1) * ((long long)ez * P + lk));
+      const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 1, (long long)ey * P + lj, ny));
+      sr[1 * T::SU + li + T::U1::S1 * lj + T::U1::S2 * lk] = m ? 0.0 : a.x[g];
+    }
+    {
+      const int li = r % P, lj = (r / P) % P, lk = r / (P * P);
+      const long long g = a.off[2] + (long long)ex * P + li + nx * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
+      const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 2, (long long)ez * P + lk, a.n[2]));
+      sr[2 * T::SU + li + T::U2::S1 * lj + T::U2::S2 * lk] = m ? 0.0 : a.x[g];
+    }
+  }
+  if constexpr (BLOCK) {
+    const double* q = a.x + a.nrt;
+    for (int i = tid; i < EPC * P3; i += NT) {
+      const int el = i / P3, r = i - (i / P3) * P3;
+      const int A = r % P, B = (r / P) % P, C = r / (P * P);
+      sq[el * T::SL + A + T::L2::S1 * B + T::L2::S2 * C] = sEc[el][3] ? q[(e0 + el) * P3 + r] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < EPC * 36; i += NT) {
+    const int el = i / 36, j = i % 36;
+    const int c = j / 12, k = (j / 3) % 4, d = j % 3;
+    const int s1 = k & 1, t1 = k >> 1;
+    int lo[3], hi[3];
+    const int o0 = (c == 0) ? 1 : 0, o1 = (c == 2) ? 1 : 2;
+    lo[c] = 0; hi[c] = 1;
+    lo[o0] = hi[o0] = s1;
+    lo[o1] = hi[o1] = t1;
+    sE[el][c][k][d] = sX[el][(hi[0] + 2 * hi[1] + 4 * hi[2]) * 3 + d] - sX[el][(lo[0] + 2 * lo[1] + 4 * lo[2]) * 3 + d];
+  }
+  __syncthreads();
+  for (int i = tid; i < EPC * 3 * Q * Q; i += NT) {
+    const int el = i / (3 * Q * Q), j = i % (3 * Q * Q);
+    const int c = j / (Q * Q), pr = j % (Q * Q);
+    const double s = tab.xq[pr % Q], t = tab.xq[pr / Q];
+    const double w00 = (1 - s) * (1 - t), w10 = s * (1 - t), w01 = (1 - s) * t, w11 = s * t;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      sJ[el][c][pr][d] = w00 * sE[el][c][0][d] + w10 * sE[el][c][1][d] + w01 * sE[el][c][2][d] + w11 * sE[el][c][3][d];
+  }
+  // ---- forward: axis 0, 1, 2 (warp c: component c of every element), + D u ----
+  lines_c<NT, 0, P + 1, P, P, 0, Q, TB_L, true, typename T::U0, typename T::A0, EPC, ES>(su(0), sA(0), tab);
+  lines_c<NT, 1, P, P + 1, P, 0, Q, TB_H, true, typename T::U1, typename T::A1, EPC, ES>(su(1), sA(1), tab);
+  lines_c<NT, 2, P, P, P + 1, 0, Q, TB_H, true, typename T::U2, typename T::A2, EPC, ES>(su(2), sA(2), tab);
+  if constexpr (BLOCK) {
+    for (int i = tid; i < EPC * P3; i += NT) {
+      const int el = i / P3, r = i - (i / P3) * P3;
+      const int A = r % P, B = (r / P) % P, C = r / (P * P);
+      const double* u0 = su(0) + el * ES + A + T::U0::S1 * B + T::U0::S2 * C;
+      const double* u1 = su(1) + el * ES + A + T::U1::S1 * B + T::U1::S2 * C;
+      const double* u2 = su(2) + el * ES + A + T::U2::S1 * B + T::U2::S2 * C;
+      sy[i] = (u0[1] - u0[0]) + (u1[T::U1::S1] - u1[0]) + (u2[T::U2::S2] - u2[0]);
+    }
+  }
+  __syncthreads();
+  lines_c<NT, 0, Q, P, P, 1, Q, TB_H, true, typename T::A0, typename T::B0, EPC, ES>(sA(0), sB(0), tab);
+  lines_c<NT, 1, Q, P + 1, P, 1, Q, TB_L, true, typename T::A1, typename T::B1, EPC, ES>(sA(1), sB(1), tab);
+  lines_c<NT, 2, Q, P, P + 1, 1, Q, TB_H, true, typename T::A2, typename T::B2, EPC, ES>(sA(2), sB(2), tab);
+  __syncthreads();
+  lines_c<NT, 0, Q, Q, P, 2, Q, TB_H, true, typename T::B0, typename T::V, EPC, ES>(sB(0), sV(0), tab);
+  lines_c<NT, 1, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V, EPC, ES>(sB(1), sV(1), tab);
+  lines_c<NT, 2, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V, EPC, ES>(sB(2), sV(2), tab);
+  __syncthreads();
+  // ---- pointwise G_q = w_q mw / det J  J^T J ----
+  for (int i = tid; i < EPC * NQ; i += NT) {
+    const int el = i / NQ, qi = i - (i / NQ) * NQ;
+    const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
+    const double* c0 = sJ[el][0][qy + Q * qz];
+    const double* c1 = sJ[el][1][qx + Q * qz];
+    const double* c2 = sJ[el][2][qx + Q * qy];
+    const double det = c0[0] * (c1[1] * c2[2] - c1[2] * c2[1]) - c1[0] * (c0[1] * c2[2] - c0[2] * c2[1]) +
+                       c2[0] * (c0[1] * c1[2] - c0[2] * c1[1]);
+    const double s = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] * smw[el] / det;
+    const int o = el * ES + qx + T::V::S1 * qy + T::V::S2 * qz;
+    const double u0 = sV(0)[o], u1 = sV(1)[o], u2 = sV(2)[o];
+    double Ju[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) Ju[d] = c0[d] * u0 + c1[d] * u1 + c2[d] * u2;
+    sV(0)[o] = s * (c0[0] * Ju[0] + c0[1] * Ju[1] + c0[2] * Ju[2]);
+    sV(1)[o] = s * (c1[0] * Ju[0] + c1[1] * Ju[1] + c1[2] * Ju[2]);
+    sV(2)[o] = s * (c2[0] * Ju[0] + c2[1] * Ju[1] + c2[2] * Ju[2]);
+  }
+  __syncthreads();
+  // ---- backward: axis 2, 1, 0 ----
+  lines_c<NT, 0, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B0, EPC, ES>(sV(0), sB(0), tab);
+  lines_c<NT, 1, Q, Q, Q, 2, P, TB_H, false, typename T::V, typename T::B1, EPC, ES>(sV(1), sB(1), tab);
+  lines_c<NT, 2, Q, Q, Q, 2, P + 1, TB_L, false, typename T::V, typename T::B2, EPC, ES>(sV(2), sB(2), tab);
+  __syncthreads();
+  lines_c<NT, 0, Q, Q, P, 1, P, TB_H, false, typename T::B0, typename T::A0, EPC, ES>(sB(0), sA(0), tab);
+  lines_c<NT, 1, Q, Q, P, 1, P + 1, TB_L, false, typename T::B1, typename T::A1, EPC, ES>(sB(1), sA(1), tab);
+  lines_c<NT, 2, Q, Q, P + 1, 1, P, TB_H, false, typename T::B2, typename T::A2, EPC, ES>(sB(2), sA(2), tab);
+  __syncthreads();
+  lines_c<NT, 0, Q, P, P, 0, P + 1, TB_L, false, typename T::A0, typename T::U0, EPC, ES>(sA(0), su(0), tab);
+  lines_c<NT, 1, Q, P + 1, P, 0, P, TB_H, false, typename T::A1, typename T::U1, EPC, ES>(sA(1), su(1), tab);
+  lines_c<NT, 2, Q, P, P + 1, 0, P, TB_H, false, typename T::A2, typename T::U2, EPC, ES>(sA(2), su(2), tab);
+  __syncthreads();
+  // ---- D^T q~ and scatter (boundary faces by atomics onto the zeroed y, eliminated faces skipped) ----
+  auto put = [&](double* g, double v, int ic, int c, long long gi) {
+    if (ic == 0 || ic == P) {
+      if (!(a.ess && face_masked(a.ess, c, gi, a.n[c]))) atomicAdd(g, v);
+    } else {
+      *g = v;
+    }
+  };
+  for (int l = tid; l < EPC * NU; l += NT) {
+    const int el = l / NU, r = l - (l / NU) * NU;
+    if (!sEc[el][3]) continue;
+    const int ex = sEc[el][0], ey = sEc[el][1], ez = sEc[el][2];
+    const double* sr = sreg + el * ES;
+    const double* sqe = sq + (BLOCK ? el * T::SL : 0);
+    {
+      const int li = r % (P + 1), lj = (r / (P + 1)) % P, lk = r / ((P + 1) * P);
+      double v = sr[0 * T::SU + li + T::U0::S1 * lj + T::U0::S2 * lk];
+      if constexpr (BLOCK) {
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;
+        if (li > 0) v += sqe[cell - 1];
+        if (li < P) v -= sqe[cell];
+      }
+      const long long g = a.off[0] + (long long)ex * P + li + (nx + 1) * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
+      put(a.y + g, v, li, 0, (long long)ex * P + li);
+    }
+    {
+      const int li = r % P, lj = (r / P) % (P + 1), lk = r / (P * (P + 1));
+      double v = sr[1 * T::SU + li + T::U1::S1 * lj + T::U1::S2 * lk];
+      if constexpr (BLOCK) {
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;
+        if (lj > 0) v += sqe[cell - T::L2::S1];
+        if (lj < P) v -= sqe[cell];
+      }
+      const long long g = a.off[1] + (long long)ex * P + li + nx * ((long long)ey * P + lj + (ny + 1) * ((long long)ez * P + lk));
+      put(a.y + g, v, lj, 1, (long long)ey * P + lj);
+    }
+    {
+      const int li = r % P, lj = (r / P) % P, lk = r / (P * P);
+      double v = sr[2 * T::SU + li + T::U2::S1 * lj + T::U2::S2 * lk];
+      if constexpr (BLOCK) {
+        const int cell = li + T::L2::S1 * lj + T::L2::S2 * lk;
+        if (lk > 0) v += sqe[cell - T::L2::S2];
+        if (lk < P) v -= sqe[cell];
+      }
+      const long long g = a.off[2] + (long long)ex * P + li + nx * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
+      put(a.y + g, v, lk, 2, (long long)ez * P + lk);
+    }
+  }
+  if constexpr (BLOCK) {
+    double* yq = a.y + a.nrt;
+    for (int i = tid; i < EPC * P3; i += NT) {
+      const int el = i / P3;
+      if (sEc[el][3]) yq[e0 * P3 + i] = sy[i];
+    }
+  }
+}
+
 // Z q for p <= 2: one thread per element assembles W^e = sum_q (w_q / det J_q) psi psi^T
 // (P^3 x P^3, P:117/P:135 with the histopolation tensor basis) and solves it by Cholesky in
 // registers — the paper's "explicit inverse for p <= 2" regime, where a
@@ -643,6 +866,16 @@ __global__ void __launch_bounds__(128) tri_z_direct_kernel(const TriArgs a,
   for (int i = 0; i < N; ++i) a.y[e * N + i] = z * y[i];
 }
 
+// elements per CTA of the mass / gamma = 0 applies (r01 A/B, scripts/tri_epc.py on config 3)
+static int tri_epc(int p, int mode) {
+  const char* e = getenv("HDIV_TRI_EPC");
+  if (e) return atoi(e);
+  if (p == 2) return 4;   // 0.76 -> 0.37 ms per config-3-mesh apply (6 and 8: slower)
+  if (p == 3) return 2;   // 1.09 -> 0.80 ms (3, 4: slower)
+  if (p == 4) return (mode == 1) ? 2 : 1;   // block 1.55 -> 1.49 ms; mass-only and p = 5 slower
+  return 1;
+}
+
 template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
@@ -664,6 +897,28 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   if constexpr (MODE == 2 && P <= 2) {
     if (!h->d_gvert) {
       tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (MODE != 2 && P >= 2 && P <= 5) {
+    // EPC elements per 96-thread CTA (mass / gamma = 0 applies); env HDIV_TRI_EPC = 1 selects
+    // the one-element kernels for A/B
+    const int epc = tri_epc(P, MODE);
+    if (!(MODE == 1 && h->has_z) && epc >= 2) {
+      const unsigned nb2 = (unsigned)((h->E + epc - 1) / epc);
+      if constexpr (P <= 3) {
+        if (epc >= 4) {
+          tri_multi_kernel<P, 4, MODE == 1><<<(unsigned)((h->E + 3) / 4), 96, 0, s>>>(a, h->tab, h->E);
+          return cudaGetLastError();
+        }
+      }
+      if constexpr (P <= 4) {   // three elements fit the 48 KB of static shared memory
+        if (epc == 3) {
+          tri_multi_kernel<P, 3, MODE == 1><<<nb2, 96, 0, s>>>(a, h->tab, h->E);
+          return cudaGetLastError();
+        }
+      }
+      tri_multi_kernel<P, 2, MODE == 1><<<(unsigned)((h->E + 1) / 2), 96, 0, s>>>(a, h->tab, h->E);
       return cudaGetLastError();
     }
   }

@@ -434,3 +434,25 @@ def test_tiny_meshes(N, p):
     _, rep = op.minres(_dev(b), rtol=1e-12, maxit=2000)
     assert conv_o and rep.converged and abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
     op.close()
+
+
+# ---- trilinear mass / gamma = 0 applies with several elements per CTA (tri_multi_kernel):
+#      element counts not divisible by EPC, eliminated sides, both the 1-element and batched kernels
+@pytest.mark.parametrize("epc", ["1", "2", "3", "4", "8"])
+@pytest.mark.parametrize("N,p,ess", [((3, 3, 1), 3, 0), ((5, 3, 1), 2, 2 | 16), ((5, 2, 1), 4, 1 | 32), ((3, 1, 3), 5, 0),
+                                     ((7, 1, 1), 4, 63), ((1, 1, 1), 3, 0)])
+def test_trilinear_multi_element_ctas(monkeypatch, epc, N, p, ess):
+    from oracle import operators
+    monkeypatch.setenv("HDIV_TRI_EPC", epc)
+    pr = _problem("c3", N, p)
+    pr.essential = ess
+    A = operators.Assembled(pr, with_schur=False)
+    op = _gpu(pr)
+    s = op.sizes
+    x = random_vector(s.n, 41)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL and _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    u = x[:s.n_rt]
+    assert _rel(_host(op.apply_mass(_dev(u))), A.M @ u) < TOL
+    op.close()
