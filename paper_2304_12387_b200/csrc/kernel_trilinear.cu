@@ -24,6 +24,13 @@ namespace {
 
 constexpr int odd_up(int v) { return (v % 2) ? v : v + 1; }
 
+// 8-byte global -> shared copy, asynchronous; !ok writes 0 (src-size 0: nothing is read)
+__device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(ok ? 8 : 0) : "memory");
+}
+
 struct TriArgs {
   const double* x;      // [u ; q]  (MASS: u)
   double* y;            // zeroed RT part on entry
@@ -212,12 +219,20 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
   const long long nx = a.n[0], ny = a.n[1];
 
   if (tid < 2) scoef[tid] = a.coef[4 * e + tid];
+  // inputs land by cp.async at p <= 4 and for Z alone (all loads of the element in flight at
+  // once: the register-path gather was the top long-scoreboard stall); the p = 5, 6 block apply
+  // with the local CG ran 4-7 % slower that way (r01 A/B, scripts/tri_z_time.py)
+  constexpr bool ASYNC = (P <= 4) || ZONLY;
+  auto ld = [&](double* dst, const double* src, bool ok) {
+    if constexpr (ASYNC) cp_async8z(dst, ok ? src : a.x, ok);
+    else *dst = ok ? *src : 0.0;
+  };
   for (int i = tid; i < 24; i += NT) {
     const int v = i / 3, d = i % 3;
     const long long g = ((long long)(ez + (v >> 2)) * (NLy + 1) + (ey + ((v >> 1) & 1))) * (NLx + 1) +
                         (ex + (v & 1));
-    sX[i] = a.vert[g * 3 + d];
-    if (HASQ && a.gvert && d == 0) sG[v] = a.gvert[g];
+    ld(&sX[i], a.vert + g * 3 + d, true);
+    if (HASQ && a.gvert && d == 0) ld(&sG[v], a.gvert + g, true);
   }
   // gather u per component (compile-time extents, i fastest; padded smem layouts)
   if constexpr (!ZONLY) {
@@ -228,26 +243,27 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % (P + 1), lj = (l / (P + 1)) % P, lk = l / ((P + 1) * P);
       const bool m = a.ess && face_masked(a.ess, 0, (long long)ex * P + li, nx);
-      su(0)[li + T::U0::S1 * lj + T::U0::S2 * lk] = m ? 0.0 : a.x[gx + li + (nx + 1) * (lj + ny * lk)];
+      ld(su(0) + li + T::U0::S1 * lj + T::U0::S2 * lk, a.x + gx + li + (nx + 1) * (lj + ny * lk), !m);
     }
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % P, lj = (l / P) % (P + 1), lk = l / (P * (P + 1));
       const bool m = a.ess && face_masked(a.ess, 1, (long long)ey * P + lj, ny);
-      su(1)[li + T::U1::S1 * lj + T::U1::S2 * lk] = m ? 0.0 : a.x[gy + li + nx * (lj + (ny + 1) * lk)];
+      ld(su(1) + li + T::U1::S1 * lj + T::U1::S2 * lk, a.x + gy + li + nx * (lj + (ny + 1) * lk), !m);
     }
     for (int l = tid; l < (P + 1) * P * P; l += NT) {
       const int li = l % P, lj = (l / P) % P, lk = l / (P * P);
       const bool m = a.ess && face_masked(a.ess, 2, (long long)ez * P + lk, a.n[2]);
-      su(2)[li + T::U2::S1 * lj + T::U2::S2 * lk] = m ? 0.0 : a.x[gz + li + nx * (lj + ny * lk)];
+      ld(su(2) + li + T::U2::S1 * lj + T::U2::S2 * lk, a.x + gz + li + nx * (lj + ny * lk), !m);
     }
   }
   if constexpr (HASQ) {
     const double* q = ZONLY ? a.x : a.x + a.nrt;
     for (int i = tid; i < P3; i += NT) {
       const int A = i % P, B = (i / P) % P, C = i / (P * P);
-      sq[A + T::L2::S1 * B + T::L2::S2 * C] = q[e * P3 + i];
+      ld(sq + A + T::L2::S1 * B + T::L2::S2 * C, q + e * P3 + i, true);
     }
   }
+  if constexpr (ASYNC) asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 
   // trilinear Jacobian column factors on the Q x Q point pairs: dT/dx_hat_c is bilinear in the
@@ -594,15 +610,13 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
     smw[tid] = ok ? a.coef[4 * e] : 0.0;
   }
   __syncthreads();
+  // every input lands by cp.async (all loads in flight at once; masked / absent -> 0)
   for (int i = tid; i < EPC * 24; i += NT) {
     const int el = i / 24, v = (i % 24) / 3, d = i % 3;
-    double xv = 0.0;
-    if (sEc[el][3]) {
-      const long long g = ((long long)(sEc[el][2] + (v >> 2)) * (NLy + 1) + (sEc[el][1] + ((v >> 1) & 1))) *
-                              (NLx + 1) + (sEc[el][0] + (v & 1));
-      xv = a.vert[g * 3 + d];
-    }
-    sX[el][v * 3 + d] = xv;
+    const bool ok = sEc[el][3];
+    const long long g = ((long long)(sEc[el][2] + (v >> 2)) * (NLy + 1) + (sEc[el][1] + ((v >> 1) & 1))) *
+                            (NLx + 1) + (sEc[el][0] + (v & 1));
+    cp_async8z(&sX[el][v * 3 + d], a.vert + (ok ? g * 3 + d : 0), ok);
   }
   // gather u (eliminated essential faces act as zero inputs; absent elements as zeros)
   for (int l = tid; l < EPC * NU; l += NT) {
@@ -613,19 +627,19 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
       const int li = r % (P + 1), lj = (r / (P + 1)) % P, lk = r / ((P + 1) * P);
       const long long g = a.off[0] + (long long)ex * P + li + (nx + 1) * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
       const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 0, (long long)ex * P + li, nx));
-      sr[0 * T::SU + li + T::U0::S1 * lj + T::U0::S2 * lk] = m ? 0.0 : a.x[g];
+      cp_async8z(sr + 0 * T::SU + li + T::U0::S1 * lj + T::U0::S2 * lk, a.x + (m ? 0 : g), !m);
     }
     {
       const int li = r % P, lj = (r / P) % (P + 1), lk = r / (P * (P + 1));
       const long long g = a.off[1] + (long long)ex * P + li + nx * ((long long)ey * P + lj + (ny + 1) * ((long long)ez * P + lk));
       const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 1, (long long)ey * P + lj, ny));
-      sr[1 * T::SU + li + T::U1::S1 * lj + T::U1::S2 * lk] = m ? 0.0 : a.x[g];
+      cp_async8z(sr + 1 * T::SU + li + T::U1::S1 * lj + T::U1::S2 * lk, a.x + (m ? 0 : g), !m);
     }
     {
       const int li = r % P, lj = (r / P) % P, lk = r / (P * P);
       const long long g = a.off[2] + (long long)ex * P + li + nx * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
       const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 2, (long long)ez * P + lk, a.n[2]));
-      sr[2 * T::SU + li + T::U2::S1 * lj + T::U2::S2 * lk] = m ? 0.0 : a.x[g];
+      cp_async8z(sr + 2 * T::SU + li + T::U2::S1 * lj + T::U2::S2 * lk, a.x + (m ? 0 : g), !m);
     }
   }
   if constexpr (BLOCK) {
@@ -633,9 +647,11 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
     for (int i = tid; i < EPC * P3; i += NT) {
       const int el = i / P3, r = i - (i / P3) * P3;
       const int A = r % P, B = (r / P) % P, C = r / (P * P);
-      sq[el * T::SL + A + T::L2::S1 * B + T::L2::S2 * C] = sEc[el][3] ? q[(e0 + el) * P3 + r] : 0.0;
+      const bool ok = sEc[el][3];
+      cp_async8z(sq + el * T::SL + A + T::L2::S1 * B + T::L2::S2 * C, q + (ok ? (e0 + el) * P3 + r : 0), ok);
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   for (int i = tid; i < EPC * 36; i += NT) {
     const int el = i / 36, j = i % 36;
@@ -866,14 +882,18 @@ __global__ void __launch_bounds__(128) tri_z_direct_kernel(const TriArgs a,
   for (int i = 0; i < N; ++i) a.y[e * N + i] = z * y[i];
 }
 
-// elements per CTA of the mass / gamma = 0 applies (r01 A/B, scripts/tri_epc.py on config 3)
+// elements per CTA of the mass / gamma = 0 applies (r01 A/B, scripts/tri_epc.py on config 3's
+// mesh); 0 = the one-element tri_kernel.  Env HDIV_TRI_EPC overrides (clamped to what fits).
 static int tri_epc(int p, int mode) {
   const char* e = getenv("HDIV_TRI_EPC");
   if (e) return atoi(e);
-  if (p == 2) return 4;   // 0.76 -> 0.37 ms per config-3-mesh apply (6 and 8: slower)
-  if (p == 3) return 2;   // 1.09 -> 0.80 ms (3, 4: slower)
-  if (p == 4) return (mode == 1) ? 2 : 1;   // block 1.55 -> 1.49 ms; mass-only and p = 5 slower
-  return 1;
+  (void)mode;
+  // block apply (mass-only) per apply, one-element tri_kernel -> chosen EPC:
+  if (p <= 2) return 4;                      // p1 0.50 -> 0.21, p2 0.76 -> 0.34 ms
+  if (p == 3) return 2;                      // 1.09 -> 0.78 (0.95 -> 0.71)
+  if (p == 4) return (mode == 1) ? 1 : 2;    // 1.55 -> 1.32 (1.25 -> 1.18)
+  if (p == 5) return 1;                      // 3.20 -> 2.76 (2.58 -> 2.43)
+  return (mode == 1) ? 1 : 0;                // p6 2.52 -> 2.12 (mass: 1.77 stays, 1.91 with EPC 1)
 }
 
 template <int P, int MODE>
@@ -900,12 +920,10 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
       return cudaGetLastError();
     }
   }
-  if constexpr (MODE != 2 && P >= 2 && P <= 5) {
-    // EPC elements per 96-thread CTA (mass / gamma = 0 applies); env HDIV_TRI_EPC = 1 selects
-    // the one-element kernels for A/B
+  if constexpr (MODE != 2) {
+    // EPC elements per 96-thread CTA (mass / gamma = 0 applies), inputs landed by cp.async
     const int epc = tri_epc(P, MODE);
-    if (!(MODE == 1 && h->has_z) && epc >= 2) {
-      const unsigned nb2 = (unsigned)((h->E + epc - 1) / epc);
+    if (!(MODE == 1 && h->has_z) && epc >= 1) {
       if constexpr (P <= 3) {
         if (epc >= 4) {
           tri_multi_kernel<P, 4, MODE == 1><<<(unsigned)((h->E + 3) / 4), 96, 0, s>>>(a, h->tab, h->E);
@@ -913,12 +931,18 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
         }
       }
       if constexpr (P <= 4) {   // three elements fit the 48 KB of static shared memory
-        if (epc == 3) {
-          tri_multi_kernel<P, 3, MODE == 1><<<nb2, 96, 0, s>>>(a, h->tab, h->E);
+        if (epc >= 3) {
+          tri_multi_kernel<P, 3, MODE == 1><<<(unsigned)((h->E + 2) / 3), 96, 0, s>>>(a, h->tab, h->E);
           return cudaGetLastError();
         }
       }
-      tri_multi_kernel<P, 2, MODE == 1><<<(unsigned)((h->E + 1) / 2), 96, 0, s>>>(a, h->tab, h->E);
+      if constexpr (P <= 5) {
+        if (epc >= 2) {
+          tri_multi_kernel<P, 2, MODE == 1><<<(unsigned)((h->E + 1) / 2), 96, 0, s>>>(a, h->tab, h->E);
+          return cudaGetLastError();
+        }
+      }
+      tri_multi_kernel<P, 1, MODE == 1><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab, h->E);
       return cudaGetLastError();
     }
   }

@@ -438,8 +438,9 @@ def test_tiny_meshes(N, p):
 
 # ---- trilinear mass / gamma = 0 applies with several elements per CTA (tri_multi_kernel):
 #      element counts not divisible by EPC, eliminated sides, both the 1-element and batched kernels
-@pytest.mark.parametrize("epc", ["1", "2", "3", "4", "8"])
-@pytest.mark.parametrize("N,p,ess", [((3, 3, 1), 3, 0), ((5, 3, 1), 2, 2 | 16), ((5, 2, 1), 4, 1 | 32), ((3, 1, 3), 5, 0),
+@pytest.mark.parametrize("epc", ["0", "1", "2", "3", "4", "8"])
+@pytest.mark.parametrize("N,p,ess", [((3, 3, 1), 3, 0), ((5, 3, 1), 2, 2 | 16), ((3, 2, 1), 6, 4),
+                                     ((7, 1, 1), 1, 1 | 2), ((5, 2, 1), 4, 1 | 32), ((3, 1, 3), 5, 0),
                                      ((7, 1, 1), 4, 63), ((1, 1, 1), 3, 0)])
 def test_trilinear_multi_element_ctas(monkeypatch, epc, N, p, ess):
     from oracle import operators
