@@ -20,6 +20,25 @@ hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s);      // comm
 void comm_free(hdiv_ctx* h);
 hdiv_status comm_reverse_add(hdiv_ctx* h, double* y_rt, cudaStream_t s);  // interface planes
 hdiv_status comm_setup_schur_ghosts(hdiv_ctx* h, cudaStream_t s);
+void comm_overlap_handles(const hdiv_ctx* h, cudaStream_t* cs, cudaEvent_t* fork, cudaEvent_t* join);
+
+// Slab apply with the interface exchange overlapped: the first and last z-tile
+// layers, which alone write the two interface planes, run first; the reverse-add exchange and
+// its add kernel run on the comm stream while the interior tile layers compute, joined before
+// return.  Box meshes with >= 3 tile layers per slab (HDIV_SLAB_OVERLAP=0 disables).
+static bool slab_overlap(const hdiv_ctx* h, int* ntz) {
+  if (h->nranks < 2 || h->kernel != 2) return false;
+  static const bool on = [] {
+    const char* e = getenv("HDIV_SLAB_OVERLAP");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!on) return false;
+  int TZ = 0;
+  if (launch_affine_apply_range(h, nullptr, nullptr, 0, 0, &TZ, nullptr) != cudaSuccess || TZ <= 0)
+    return false;
+  *ntz = (int)((h->NL[2] + TZ - 1) / TZ);
+  return *ntz >= 3;
+}
 
 static hdiv_status fail(hdiv_status st, const std::string& msg) {
   set_error(msg);
@@ -39,6 +58,22 @@ static void corners(const std::vector<double>& V, int dim, int64_t NLx, int64_t 
 
 cudaError_t apply_block_dev(hdiv_ctx* h, const double* x, double* y, const int* skip,
                             cudaStream_t s) {
+  int ntz = 0;
+  if (slab_overlap(h, &ntz)) {
+    cudaStream_t cs;
+    cudaEvent_t fork, join;
+    comm_overlap_handles(h, &cs, &fork, &join);
+    cudaError_t e = launch_affine_apply_range(h, x, y, 0, 1, nullptr, s, skip);
+    if (e == cudaSuccess) e = launch_affine_apply_range(h, x, y, ntz - 1, ntz, nullptr, s, skip);
+    if (e == cudaSuccess) e = cudaEventRecord(fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, fork, 0);
+    if (e != cudaSuccess) return e;
+    if (comm_reverse_add(h, y, cs) != HDIV_OK) return cudaErrorUnknown;
+    e = cudaEventRecord(join, cs);
+    if (e == cudaSuccess) e = launch_affine_apply_range(h, x, y, 1, ntz - 1, nullptr, s, skip);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, join, 0);
+    return e;
+  }
   cudaError_t e = (h->kernel == 2)  ? launch_affine_apply(h, x, y, MODE_BLOCK, skip, s)
                    : (h->dim == 3) ? launch_trilinear_apply(h, x, y, MODE_BLOCK, skip, s)
                                    : launch_general_apply(h, x, y, MODE_BLOCK, skip, s);

@@ -141,6 +141,8 @@ struct Comm {
   long long lplane = 0;     // L2 ghost layer size (cells)
   double* buf = nullptr;    // recv_lo, recv_hi (RT) ; send_lo, send_hi (L2)
   double *rlo, *rhi, *slo, *shi;
+  cudaStream_t cs = nullptr;               // exchange stream of the overlapped slab apply
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static hdiv_status nccl_fail(ncclResult_t r, const char* what) {
@@ -179,6 +181,13 @@ static hdiv_status loop_exchange(hdiv_ctx* h, const double* send_lo, const doubl
 
 bool comm_is_loopback(const hdiv_ctx* h) { return h->comm && h->comm->loop; }
 
+// exchange stream + fork/join events of the overlapped slab apply (created with the comm)
+void comm_overlap_handles(const hdiv_ctx* h, cudaStream_t* cs, cudaEvent_t* fork, cudaEvent_t* join) {
+  *cs = h->comm->cs;
+  *fork = h->comm->ev_fork;
+  *join = h->comm->ev_join;
+}
+
 hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s) {
   (void)s;
   auto* c = new Comm();
@@ -216,6 +225,9 @@ hdiv_status comm_init(hdiv_ctx* h, const void* id, cudaStream_t s) {
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
   }
   HDIV_CUDA_TRY(cudaMalloc(&c->buf, sizeof(double) * 4 * c->plane));
+  HDIV_CUDA_TRY(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  HDIV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  HDIV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   c->rlo = c->buf;
   c->rhi = c->buf + c->plane;
   c->slo = c->buf + 2 * c->plane;
@@ -237,6 +249,9 @@ void comm_free(hdiv_ctx* h) {
   }
   if (h->comm->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm->comm);
   cudaFree(h->comm->buf);
+  if (h->comm->cs) cudaStreamDestroy(h->comm->cs);
+  if (h->comm->ev_fork) cudaEventDestroy(h->comm->ev_fork);
+  if (h->comm->ev_join) cudaEventDestroy(h->comm->ev_join);
   delete h->comm;
   h->comm = nullptr;
 }

@@ -116,7 +116,8 @@ void set_error(const std::string& s);
 namespace hdiv {
 // kernel launchers (return cudaGetLastError())
 cudaError_t launch_affine_apply_range(const hdiv_ctx* h, const double* x, double* y, int tz0,
-                                      int tz1, int* tz_out, cudaStream_t s);
+                                      int tz1, int* tz_out, cudaStream_t s,
+                                      const int* skip = nullptr);
 cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                 const int* skip, cudaStream_t s);
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,

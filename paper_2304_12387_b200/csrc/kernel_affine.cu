@@ -1171,11 +1171,11 @@ cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, i
 // the block apply restricted to the halo tiles with z-tile index in [tz0, tz1) (the z-chunked
 // host pipeline of hdiv_apply_block_host); tz_out != nullptr: report the tile depth only
 cudaError_t launch_affine_apply_range(const hdiv_ctx* h, const double* x, double* y, int tz0,
-                                      int tz1, int* tz_out, cudaStream_t s) {
+                                      int tz1, int* tz_out, cudaStream_t s, const int* skip) {
   g_range.tz0 = tz0;
   g_range.tz1 = tz1;
   g_range.tz_out = tz_out;
-  cudaError_t e = dispatch<true>(h, x, y, nullptr, s);
+  cudaError_t e = dispatch<true>(h, x, y, skip, s);
   g_range = TileRange();
   return e;
 }

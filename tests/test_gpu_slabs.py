@@ -65,8 +65,11 @@ def _problem(name, N, p, ess=0, project=False):
     return pr
 
 
+# the last three have >= 3 z-tile layers per slab: the interface exchange runs on the comm
+# stream while the interior tile layers compute (apply_block_dev's overlapped path)
 CASES = [("c2", (4, 3, 6), 3, 2, 0), ("c2", (3, 4, 7), 2, 3, 0), ("c3", (3, 3, 4), 2, 2, 0),
-         ("c1", (4, 6), 2, 3, 0), ("c2", (4, 3, 5), 4, 2, 63), ("c5", (5, 5, 6), 2, 2, 0)]
+         ("c1", (4, 6), 2, 3, 0), ("c2", (4, 3, 5), 4, 2, 63), ("c5", (5, 5, 6), 2, 2, 0),
+         ("c2", (4, 3, 12), 3, 2, 0), ("c2", (4, 3, 10), 4, 2, 63), ("c2", (5, 3, 27), 2, 3, 0)]
 
 
 @pytest.mark.parametrize("name,N,p,P,ess", CASES)
@@ -100,6 +103,8 @@ def test_slab_apply_and_diag(name, N, p, P, ess):
 
 
 @pytest.mark.parametrize("name,N,p,P,ess,project", [("c2", (4, 3, 6), 3, 2, 0, False),
+                                                    ("c2", (4, 3, 12), 3, 2, 0, False),
+                                                    ("c2", (4, 3, 10), 4, 2, 63, False),
                                                     ("c3", (3, 3, 4), 2, 2, 0, False),
                                                     ("c1", (4, 6), 2, 3, 0, False),
                                                     ("c3", (3, 3, 4), 2, 2, 63, True)])
@@ -185,6 +190,7 @@ def test_slab_minres_amg(name, N, p, P, ess, project):
 
 
 @pytest.mark.parametrize("name,N,p,P,schur", [("c2", (4, 3, 6), 3, 2, "chebyshev"),
+                                              ("c2", (4, 3, 12), 3, 2, "amg"),
                                               ("c3", (3, 3, 6), 2, 3, "chebyshev"),
                                               ("c5", (5, 5, 6), 2, 2, "amg")])
 def test_slab_gmres(name, N, p, P, schur):
