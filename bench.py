@@ -116,17 +116,16 @@ def winv_bench(torch):
     from synth import make_config, random_vector
     from paper_2304_12387_b200 import from_problem
     out = {"workload": "W^-1 q (the (2,2) block) by the fused element-local CG in the GL-nodal "
-                       "basis; config-3 jittered hex mesh sized to ~1.7e6 L2 DOFs, grad-div "
+                       "basis (p >= 3 also by the precomputed explicit element inverses, "
+                       "explicit_*); config-3 jittered hex mesh sized to ~1.7e6 L2 DOFs, grad-div "
                        "alpha = 1 (Z = W^-1); 100 applies (Table dg-mass-inv shape, P:773-822)",
            "paper_v100_context": "P:792-794 local-CG solve x100: " +
                                  ", ".join(f"p{p} {t} s" for p, t in _PAPER_WINV_S.items())}
-    for p in range(1, 7):
-        ne = max(2, int(round((1.7e6 / p ** 3) ** (1.0 / 3.0))))
-        pr = make_config("c3", N=(ne, ne, ne), p=p)
-        pr.kind = "grad_div"
-        pr.alpha = np.ones(pr.E)
-        pr.beta = np.ones(pr.E)
+    def run(pr):
+        t0 = time.perf_counter()
         op = from_problem(pr)
+        torch.cuda.synchronize()
+        setup = time.perf_counter() - t0
         q = torch.from_numpy(random_vector(op.sizes.n_l2, 5)).cuda()
         y = torch.empty_like(q)
         for _ in range(3):
@@ -140,10 +139,25 @@ def winv_bench(torch):
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1e3
         n = op.sizes.n_l2
-        out[f"p{p}"] = {"N": ne, "l2_dofs": n, "solve_x100_s": t, "GDOF_s": 100 * n / t / 1e9}
         op.close()
         del q, y
         torch.cuda.empty_cache()
+        return n, t, setup
+
+    for p in range(1, 7):
+        ne = max(2, int(round((1.7e6 / p ** 3) ** (1.0 / 3.0))))
+        pr = make_config("c3", N=(ne, ne, ne), p=p)
+        pr.kind = "grad_div"
+        pr.alpha = np.ones(pr.E)
+        pr.beta = np.ones(pr.E)
+        os.environ["HDIV_WINV"] = "cg"      # the local CG (explicit inverses not built)
+        n, t, _ = run(pr)
+        os.environ.pop("HDIV_WINV")
+        out[f"p{p}"] = {"N": ne, "l2_dofs": n, "solve_x100_s": t, "GDOF_s": 100 * n / t / 1e9}
+        if p in (3, 4):   # the precomputed explicit inverses, the default at p <= 4
+            n, t, setup = run(pr)
+            out[f"p{p}"].update({"explicit_x100_s": t, "explicit_GDOF_s": 100 * n / t / 1e9,
+                                 "explicit_setup_s": setup})
     return out
 
 

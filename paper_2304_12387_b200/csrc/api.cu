@@ -131,6 +131,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_ecol);
   cudaFree(h->d_minv);
   cudaFree(h->d_zcoef);
+  cudaFree(h->d_winv);
   cudaFree(h->d_gvert);
   amg_free(h);
   gmres_free(h);
@@ -433,6 +434,20 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     if (hb) {
       hdiv_destroy(h);
       return fail(HDIV_ERR_INVALID_MESH, "det J <= 0 at a quadrature point");
+    }
+  }
+  // W^-1 by precomputed explicit element inverses on trilinear meshes at
+  // p <= 4 when they fit (<= 16 GB and a quarter of the free memory; env HDIV_WINV=cg: local CG)
+  if (dim == 3 && h->geom == GEOM_TRILINEAR && h->has_z && !gvert && h->p <= 4) {
+    const char* wm = getenv("HDIV_WINV");
+    const size_t n3 = (size_t)h->p * h->p * h->p;
+    const size_t bytes = sizeof(double) * n3 * n3 * (size_t)E;
+    size_t fr = 0, tot = 0;
+    SETUP_TRY(cudaMemGetInfo(&fr, &tot));
+    const bool want = !(wm && std::string(wm) == "cg");
+    if (want && bytes <= ((size_t)16 << 30) && bytes <= fr / 4) {
+      SETUP_TRY(cudaMalloc(&h->d_winv, bytes));
+      SETUP_TRY(build_winv(h, s));
     }
   }
   SETUP_TRY(launch_mass_diag(h, h->d_mdiag, s));

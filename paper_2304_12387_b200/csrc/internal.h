@@ -73,6 +73,7 @@ struct hdiv_ctx {
   double* d_ctil = nullptr;       // C~
   double* d_c2 = nullptr;         // per element alpha (grad-div) | gamma (Darcy)
   double* d_zcoef = nullptr;      // 3D: per element {mass weight, s_e = 1/alpha | gamma, 0, 0}
+  double* d_winv = nullptr;       // [E][p^3][p^3] explicit W^e inverses (nullptr: local CG)
   double* d_gvert = nullptr;      // NEXT-3 general gamma: per local vertex (nullptr: per element)
   double* d_sdinv = nullptr;      // 1 / diag(S~)
   int64_t* d_srow = nullptr;      // S~ CSR (local rows; ghost columns >= nl2 for multi-GPU)
@@ -133,6 +134,7 @@ cudaError_t launch_divT(const hdiv_ctx* h, const double* q, double* yu, cudaStre
 cudaError_t launch_mass_diag(const hdiv_ctx* h, double* diag, cudaStream_t s);
 cudaError_t launch_ctil(const hdiv_ctx* h, const double* d_c2, double* ctil, cudaStream_t s);
 cudaError_t launch_geometry_check(const hdiv_ctx* h, int* bad, cudaStream_t s);
+cudaError_t build_winv(hdiv_ctx* h, cudaStream_t s);   // explicit W^e inverses (trilinear, p <= 4)
 cudaError_t launch_div_csr(const hdiv_ctx* h, int64_t* rp, int64_t* col, double* val,
                            cudaStream_t s);
 hdiv_status build_schur(hdiv_ctx* h, cudaStream_t s);

@@ -896,21 +896,23 @@ static int tri_epc(int p, int mode) {
   return (mode == 1) ? 1 : 0;                // p6 2.52 -> 2.12 (mass: 1.77 stays, 1.91 with EPC 1)
 }
 
+// noz: the block apply without its Z term (added by the explicit-inverse apply afterwards)
 template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool noz = false) {
+  const bool hz = h->has_z && !noz;
   // CTA size (r01 A/B of 64 vs 96 threads per order): W^-1 alone at p = 3 — one warp per element (its
   // barriers are warp-synchronous); mass-only / gamma = 0 applies at p = 4, 5 — three warps,
   // one per RT component in every line-pass stage; otherwise 64 threads (the local CG prefers it)
   constexpr int NT = (MODE == 2) ? (P == 3 ? 32 : 64) : 64;
-  const bool wide = (MODE != 2) && (P == 4 || P == 5) && !(MODE == 1 && h->has_z);
+  const bool wide = (MODE != 2) && (P == 4 || P == 5) && !(MODE == 1 && hz);
   TriArgs a;
   a.x = x; a.y = y;
   a.vert = h->d_vert;
   a.coef = (MODE == 2) ? h->d_zcoef : h->d_coef;
   for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
   a.nrt = h->nrt;
-  a.has_z = h->has_z ? 1 : 0;
+  a.has_z = hz ? 1 : 0;
   a.ess = (MODE == 2) ? 0 : h->ess;
   a.gvert = h->d_gvert;
   a.skip = skip;
@@ -923,7 +925,7 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   if constexpr (MODE != 2) {
     // EPC elements per 96-thread CTA (mass / gamma = 0 applies), inputs landed by cp.async
     const int epc = tri_epc(P, MODE);
-    if (!(MODE == 1 && h->has_z) && epc >= 1) {
+    if (!(MODE == 1 && hz) && epc >= 1) {
       if constexpr (P <= 3) {
         if (epc >= 4) {
           tri_multi_kernel<P, 4, MODE == 1><<<(unsigned)((h->E + 3) / 4), 96, 0, s>>>(a, h->tab, h->E);
@@ -957,27 +959,207 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
 }
 
 template <int MODE>
-cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k, cudaStream_t s) {
+cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k, cudaStream_t s,
+                     bool noz = false) {
   switch (h->p) {
-    case 1: return launch_p<1, MODE>(h, x, y, k, s);
-    case 2: return launch_p<2, MODE>(h, x, y, k, s);
-    case 3: return launch_p<3, MODE>(h, x, y, k, s);
-    case 4: return launch_p<4, MODE>(h, x, y, k, s);
-    case 5: return launch_p<5, MODE>(h, x, y, k, s);
-    case 6: return launch_p<6, MODE>(h, x, y, k, s);
+    case 1: return launch_p<1, MODE>(h, x, y, k, s, noz);
+    case 2: return launch_p<2, MODE>(h, x, y, k, s, noz);
+    case 3: return launch_p<3, MODE>(h, x, y, k, s, noz);
+    case 4: return launch_p<4, MODE>(h, x, y, k, s, noz);
+    case 5: return launch_p<5, MODE>(h, x, y, k, s, noz);
+    case 6: return launch_p<6, MODE>(h, x, y, k, s, noz);
   }
   return cudaErrorInvalidValue;
 }
 
+
+// ---- explicit element inverses of W (the paper's "precomputed explicit inverse", P:706-715,
+//      P:770; on B200's 180 GB affordable up to p = 4) ----
+// Build: one CTA per element assembles W^e_ab = sum_q (w_q / det J_q) psi_a psi_b in the
+// histopolation basis psi_a = h_i h_j h_k, factors it W = L L^T in shared
+// memory (right-looking, CTA-parallel) and stores (W^e)^-1 column by column: winv[e][c][i] =
+// (W^-1)_{ic}, found by the two triangular solves of L L^T x = e_c (one thread per column).
+template <int P>
+__global__ void __launch_bounds__(128) winv_build_kernel(const double* __restrict__ vert,
+                                                         long long NLx, long long NLy,
+                                                         const __grid_constant__ Tab1D tab,
+                                                         double* __restrict__ winv) {
+  constexpr int N = P * P * P, Q = P + 2, NQ = Q * Q * Q, NT = 128;
+  extern __shared__ double wsm[];
+  double* W = wsm;            // N x N, lower triangle -> L
+  double* Y = W + N * N;      // N x N, columns of the inverse
+  double* g = Y + N * N;      // NQ: w_q / det J_q
+  __shared__ double sX[24];
+  const int tid = threadIdx.x;
+  const long long e = blockIdx.x;
+  const long long ex = e % NLx, ey = (e / NLx) % NLy, ez = e / (NLx * NLy);
+  if (tid < 24) {
+    const int v = tid / 3, d = tid % 3;
+    const long long gv = ((ez + (v >> 2)) * (NLy + 1) + (ey + ((v >> 1) & 1))) * (NLx + 1) + (ex + (v & 1));
+    sX[tid] = vert[gv * 3 + d];
+  }
+  __syncthreads();
+  for (int qi = tid; qi < NQ; qi += NT) {
+    const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
+    const double xh = tab.xq[qx], yh = tab.xq[qy], zh = tab.xq[qz];
+    double J[3][3];
+    for (int d = 0; d < 3; ++d) {
+      auto X = [&](int a, int b, int c) { return sX[(a + 2 * b + 4 * c) * 3 + d]; };
+      J[d][0] = (1 - yh) * (1 - zh) * (X(1, 0, 0) - X(0, 0, 0)) + yh * (1 - zh) * (X(1, 1, 0) - X(0, 1, 0)) +
+                (1 - yh) * zh * (X(1, 0, 1) - X(0, 0, 1)) + yh * zh * (X(1, 1, 1) - X(0, 1, 1));
+      J[d][1] = (1 - xh) * (1 - zh) * (X(0, 1, 0) - X(0, 0, 0)) + xh * (1 - zh) * (X(1, 1, 0) - X(1, 0, 0)) +
+                (1 - xh) * zh * (X(0, 1, 1) - X(0, 0, 1)) + xh * zh * (X(1, 1, 1) - X(1, 0, 1));
+      J[d][2] = (1 - xh) * (1 - yh) * (X(0, 0, 1) - X(0, 0, 0)) + xh * (1 - yh) * (X(1, 0, 1) - X(1, 0, 0)) +
+                (1 - xh) * yh * (X(0, 1, 1) - X(0, 1, 0)) + xh * yh * (X(1, 1, 1) - X(1, 1, 0));
+    }
+    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                       J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                       J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    g[qi] = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] / det;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < N * N; idx += NT) {   // lower triangle (a >= b)
+    const int a = idx / N, b = idx % N;
+    if (b > a) continue;
+    const int ia = a % P, ja = (a / P) % P, ka = a / (P * P);
+    const int ib = b % P, jb = (b / P) % P, kb = b / (P * P);
+    double w = 0.0;
+    for (int qz = 0; qz < Q; ++qz) {
+      double ty = 0.0;
+      for (int qy = 0; qy < Q; ++qy) {
+        double tx = 0.0;
+        const double* gr = g + Q * (qy + Q * qz);
+        for (int qx = 0; qx < Q; ++qx) tx = fma(gr[qx], tab.Bh[qx][ia] * tab.Bh[qx][ib], tx);
+        ty = fma(tx, tab.Bh[qy][ja] * tab.Bh[qy][jb], ty);
+      }
+      w = fma(ty, tab.Bh[qz][ka] * tab.Bh[qz][kb], w);
+    }
+    W[a * N + b] = w;
+  }
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {   // W = L L^T, L in the lower triangle
+    if (tid == 0) W[k * N + k] = sqrt(W[k * N + k]);
+    __syncthreads();
+    const double dk = W[k * N + k];
+    for (int i = k + 1 + tid; i < N; i += NT) W[i * N + k] /= dk;
+    __syncthreads();
+    const int m = N - k - 1;
+    for (int idx = tid; idx < m * m; idx += NT) {
+      const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+      if (j <= i) W[i * N + j] -= W[i * N + k] * W[j * N + k];
+    }
+    __syncthreads();
+  }
+  if (tid < N) {   // column c of W^-1: L y = e_c, L^T x = y (in place in Y's column c)
+    const int c = tid;
+    for (int i = 0; i < N; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) v -= W[i * N + k] * Y[k * N + c];
+      Y[i * N + c] = v / W[i * N + i];
+    }
+    for (int i = N - 1; i >= 0; --i) {
+      double v = Y[i * N + c];
+      for (int k = i + 1; k < N; ++k) v -= W[k * N + i] * Y[k * N + c];
+      Y[i * N + c] = v / W[i * N + i];
+    }
+    double* out = winv + e * (long long)(N * N) + (long long)c * N;
+    for (int i = 0; i < N; ++i) out[i] = Y[i * N + c];
+  }
+}
+
+// y_q = s_e W_e^-1 q_e (ACC: y_q -= s_e W_e^-1 q_e), one warp per element: for every column c
+// the warp streams winv[e][c][0..N) (contiguous) and adds q_c times it into lane rows
+// r = lane, lane + 32 (fixed order: deterministic)
+template <int P, bool ACC>
+__global__ void __launch_bounds__(128) winv_apply_kernel(const double* __restrict__ winv,
+                                                         const double* __restrict__ q,
+                                                         double* __restrict__ y,
+                                                         const double* __restrict__ zcoef,
+                                                         long long E, const int* skip) {
+  constexpr int N = P * P * P;
+  static_assert(N <= 64, "two rows per lane");
+  if (skip && *skip) return;
+  const int lane = threadIdx.x & 31;
+  const long long e = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (e >= E) return;
+  const double* qe = q + e * N;
+  const double q0 = lane < N ? qe[lane] : 0.0;
+  const double q1 = lane + 32 < N ? qe[lane + 32] : 0.0;
+  const double* we = winv + e * (long long)(N * N);
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < N; ++c) {
+    const double qc = __shfl_sync(0xffffffffu, c < 32 ? q0 : q1, c & 31);
+    const double* col = we + c * N;
+    if (lane < N) a0 = fma(col[lane], qc, a0);
+    if (lane + 32 < N) a1 = fma(col[lane + 32], qc, a1);
+  }
+  const double s = zcoef[4 * e + 1];
+  double* ye = y + e * N;
+  if (lane < N) ye[lane] = ACC ? ye[lane] - s * a0 : s * a0;
+  if (lane + 32 < N) ye[lane + 32] = ACC ? ye[lane + 32] - s * a1 : s * a1;
+}
+
+template <int P>
+cudaError_t winv_build_p(hdiv_ctx* h, cudaStream_t s) {
+  constexpr int N = P * P * P, Q = P + 2;
+  const size_t smem = sizeof(double) * (2 * N * N + Q * Q * Q);
+  cudaError_t e = cudaFuncSetAttribute(winv_build_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  winv_build_kernel<P><<<(unsigned)h->E, 128, smem, s>>>(h->d_vert, h->NL[0], h->NL[1], h->tab, h->d_winv);
+  return cudaGetLastError();
+}
+
+template <int P, bool ACC>
+cudaError_t winv_apply_p(const hdiv_ctx* h, const double* q, double* y, const int* skip, cudaStream_t s) {
+  winv_apply_kernel<P, ACC><<<(unsigned)((h->E + 3) / 4), 128, 0, s>>>(h->d_winv, q, y, h->d_zcoef, h->E, skip);
+  return cudaGetLastError();
+}
+
+template <bool ACC>
+cudaError_t winv_apply(const hdiv_ctx* h, const double* q, double* y, const int* skip, cudaStream_t s) {
+  switch (h->p) {
+    case 1: return winv_apply_p<1, ACC>(h, q, y, skip, s);
+    case 2: return winv_apply_p<2, ACC>(h, q, y, skip, s);
+    case 3: return winv_apply_p<3, ACC>(h, q, y, skip, s);
+    case 4: return winv_apply_p<4, ACC>(h, q, y, skip, s);
+  }
+  return cudaErrorInvalidValue;
+}
 }  // namespace
 
-// y (RT part zeroed here) = M u  /  [M u + D^T q ; D u - Z q], 3D, any trilinear geometry
+// the explicit element inverses of W (p <= 4), built at setup when they fit the memory budget
+cudaError_t build_winv(hdiv_ctx* h, cudaStream_t s) {
+  switch (h->p) {
+    case 1: return winv_build_p<1>(h, s);
+    case 2: return winv_build_p<2>(h, s);
+    case 3: return winv_build_p<3>(h, s);
+    case 4: return winv_build_p<4>(h, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// y (RT part zeroed here) = M u  /  [M u + D^T q ; D u - Z q], 3D, any trilinear geometry.
+// With the explicit inverses: Z q by the streaming inverse apply (block: the gamma = 0 kernel
+// writes [M u + D^T q ; D u], then y_q -= s_e W_e^-1 q_e)
 cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                    const int* skip, cudaStream_t s) {
-  if (mode == MODE_ZONLY) return dispatch<2>(h, x, y, skip, s);   // y (L2) fully written
+  if (mode == MODE_ZONLY) {
+    // p <= 2: the thread-per-element register Cholesky (tri_z_direct_kernel) stays faster
+    if (h->d_winv && h->p >= 3) return winv_apply<false>(h, x, y, skip, s);
+    return dispatch<2>(h, x, y, skip, s);   // y (L2) fully written
+  }
   cudaError_t e = cudaMemsetAsync(y, 0, sizeof(double) * h->nrt, s);
   if (e != cudaSuccess) return e;
-  if (mode == MODE_BLOCK) return dispatch<1>(h, x, y, skip, s);
+  if (mode == MODE_BLOCK) {
+    if (h->d_winv) {
+      e = dispatch<1>(h, x, y, skip, s, true);
+      if (e != cudaSuccess) return e;
+      return winv_apply<true>(h, x + h->nrt, y + h->nrt, skip, s);
+    }
+    return dispatch<1>(h, x, y, skip, s);
+  }
   return dispatch<0>(h, x, y, skip, s);
 }
 

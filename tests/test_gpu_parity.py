@@ -457,3 +457,33 @@ def test_trilinear_multi_element_ctas(monkeypatch, epc, N, p, ess):
     u = x[:s.n_rt]
     assert _rel(_host(op.apply_mass(_dev(u))), A.M @ u) < TOL
     op.close()
+
+
+# ---- W^-1 on trilinear hexes: precomputed explicit element inverses (default at p <= 4,
+#      P:796-798) and the local CG (HDIV_WINV=cg) — block apply, Z alone and MINRES ----
+@pytest.mark.parametrize("winv", ["explicit", "cg"])
+@pytest.mark.parametrize("name,N,p", [("c3gd", (3, 2, 2), 1), ("c3gd", (3, 2, 2), 2), ("c3g", (2, 3, 2), 3),
+                                      ("c3gd", (2, 2, 3), 4), ("c3g", (3, 1, 2), 4)])
+def test_trilinear_winv_modes(monkeypatch, winv, name, N, p):
+    from oracle import operators, solvers
+    if winv == "cg":
+        monkeypatch.setenv("HDIV_WINV", "cg")
+    else:
+        monkeypatch.delenv("HDIV_WINV", raising=False)
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    op = _gpu(pr)
+    s = op.sizes
+    x = random_vector(s.n, 43)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL and _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    q = x[s.n_rt:]
+    assert _rel(_host(op.apply_z(_dev(q))), A.apply_Z(q)) < TOL
+    b = A.apply_block(random_vector(s.n, 1))
+    P = solvers.BlockDiagPrecond(A)
+    xo, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=3000)
+    xg, rep = op.minres(_dev(b), rtol=1e-12, maxit=3000)
+    assert conv_o and rep.converged and abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    assert _rel(_host(xg), xo) < 1e-9
+    op.close()
