@@ -116,7 +116,7 @@ def winv_bench(torch):
     from synth import make_config, random_vector
     from paper_2304_12387_b200 import from_problem
     out = {"workload": "W^-1 q (the (2,2) block) by the fused element-local CG in the GL-nodal "
-                       "basis (p >= 3 also by the precomputed explicit element inverses, "
+                       "basis (p <= 4 also by the precomputed explicit element inverses, "
                        "explicit_*); config-3 jittered hex mesh sized to ~1.7e6 L2 DOFs, grad-div "
                        "alpha = 1 (Z = W^-1); 100 applies (Table dg-mass-inv shape, P:773-822)",
            "paper_v100_context": "P:792-794 local-CG solve x100: " +
@@ -154,7 +154,7 @@ def winv_bench(torch):
         n, t, _ = run(pr)
         os.environ.pop("HDIV_WINV")
         out[f"p{p}"] = {"N": ne, "l2_dofs": n, "solve_x100_s": t, "GDOF_s": 100 * n / t / 1e9}
-        if p in (3, 4):   # the precomputed explicit inverses, the default at p <= 4
+        if p <= 4:   # the precomputed explicit inverses, the default at p <= 4
             n, t, setup = run(pr)
             out[f"p{p}"].update({"explicit_x100_s": t, "explicit_GDOF_s": 100 * n / t / 1e9,
                                  "explicit_setup_s": setup})

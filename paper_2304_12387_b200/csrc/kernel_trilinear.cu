@@ -1100,6 +1100,28 @@ __global__ void __launch_bounds__(128) winv_apply_kernel(const double* __restric
   if (lane + 32 < N) ye[lane + 32] = ACC ? ye[lane + 32] - s * a1 : s * a1;
 }
 
+// p <= 2 (p^3 <= 8 rows): one thread per (element, row), columns in order
+template <int P, bool ACC>
+__global__ void __launch_bounds__(256) winv_apply_small_kernel(const double* __restrict__ winv,
+                                                               const double* __restrict__ q,
+                                                               double* __restrict__ y,
+                                                               const double* __restrict__ zcoef,
+                                                               long long E, const int* skip) {
+  constexpr int N = P * P * P;
+  if (skip && *skip) return;
+  const long long t = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (t >= E * N) return;
+  const long long e = t / N;
+  const int r = (int)(t - e * N);
+  const double* we = winv + e * (N * N) + r;
+  const double* qe = q + e * N;
+  double a = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c) a = fma(we[c * N], qe[c], a);
+  const double s = zcoef[4 * e + 1];
+  y[t] = ACC ? y[t] - s * a : s * a;
+}
+
 template <int P>
 cudaError_t winv_build_p(hdiv_ctx* h, cudaStream_t s) {
   constexpr int N = P * P * P, Q = P + 2;
@@ -1113,6 +1135,11 @@ cudaError_t winv_build_p(hdiv_ctx* h, cudaStream_t s) {
 
 template <int P, bool ACC>
 cudaError_t winv_apply_p(const hdiv_ctx* h, const double* q, double* y, const int* skip, cudaStream_t s) {
+  if constexpr (P <= 2) {
+    const long long n = h->E * P * P * P;
+    winv_apply_small_kernel<P, ACC><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h->d_winv, q, y, h->d_zcoef, h->E, skip);
+    return cudaGetLastError();
+  }
   winv_apply_kernel<P, ACC><<<(unsigned)((h->E + 3) / 4), 128, 0, s>>>(h->d_winv, q, y, h->d_zcoef, h->E, skip);
   return cudaGetLastError();
 }
@@ -1146,8 +1173,7 @@ cudaError_t build_winv(hdiv_ctx* h, cudaStream_t s) {
 cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                    const int* skip, cudaStream_t s) {
   if (mode == MODE_ZONLY) {
-    // p <= 2: the thread-per-element register Cholesky (tri_z_direct_kernel) stays faster
-    if (h->d_winv && h->p >= 3) return winv_apply<false>(h, x, y, skip, s);
+    if (h->d_winv) return winv_apply<false>(h, x, y, skip, s);
     return dispatch<2>(h, x, y, skip, s);   // y (L2) fully written
   }
   cudaError_t e = cudaMemsetAsync(y, 0, sizeof(double) * h->nrt, s);
