@@ -1053,7 +1053,10 @@ static int tile_variant(int p) {
   // tiles (more CTAs per SM) win at p = 3..6, double-buffered at p = 1, 2; at p = 5, 6 the x
   // component is written back through shared memory (coalesced copy-out), at p = 3 a
   // 160-thread CTA owns one cell column per thread
-  return (p == 3) ? 7 : (p == 4) ? 4 : (p == 5 || p == 6) ? 10 : 0;
+  // p = 5: a 3x2x2 tile (less halo, modelled 0.706 -> 0.644 wavefronts/DOF), 160 threads:
+  // 2.245 -> 2.160 ms at N = 96 (4x3x2 at p = 4 and 5x4x2 at p = 3 were slower)
+  // p = 6: 3x2x2, 224 threads: 2.556 -> 2.494 ms at N = 80
+  return (p == 3) ? 7 : (p == 4) ? 4 : (p == 5 || p == 6) ? 12 : 0;
 }
 
 // The z-marching kernel is correct at every order but no longer the fastest anywhere (same
@@ -1099,8 +1102,8 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
       case 2: return launch_t<2, 8, 4, 4, 128, BLOCK, true, 0, kXDirect, true>(h, x, y, k, s);
       case 3: return launch_t<3, 4, 4, 2, 160, BLOCK, false, 0, kXDirect, true>(h, x, y, k, s);
       case 4: return launch_t<4, 4, 2, 2, 128, BLOCK, false, 0, kXDirect, true>(h, x, y, k, s);
-      case 5: return launch_t<5, 2, 2, 2, 128, BLOCK, false, 0, false, true>(h, x, y, k, s);
-      case 6: return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3, false, true>(h, x, y, k, s);
+      case 5: return launch_t<5, 3, 2, 2, 160, BLOCK, false, 0, false, true>(h, x, y, k, s);
+      case 6: return launch_t<6, 3, 2, 2, 224, BLOCK, false, 2, false, true>(h, x, y, k, s);
     }
     return cudaErrorInvalidValue;
   }
@@ -1144,6 +1147,8 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
       if (v == 8) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 6>(h, x, y, k, s);
       if (v == 9) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 5>(h, x, y, k, s);
       if (v == 10) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
+      if (v == 11) return launch_t<5, 3, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
+      if (v == 12) return launch_t<5, 3, 2, 2, 160, BLOCK, false, 0, false>(h, x, y, k, s);
       return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
     case 6:
       if (v == 1) return launch_t<6, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
@@ -1154,6 +1159,7 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
       if (v == 7) return launch_t<6, 4, 2, 2, 288, BLOCK, false>(h, x, y, k, s);
       if (v == 8) return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3>(h, x, y, k, s);
       if (v == 10) return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3, false>(h, x, y, k, s);
+      if (v == 12) return launch_t<6, 3, 2, 2, 224, BLOCK, false, 2, false>(h, x, y, k, s);
       if (v == 9) return launch_t<6, 2, 2, 2, 128, BLOCK, false, 4>(h, x, y, k, s);
       return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
   }

@@ -8,7 +8,7 @@ from synth import make_config
 from paper_2304_12387_b200 import from_problem
 
 SIZES = {2: 160, 3: 128, 4: 128, 5: 96, 6: 80}
-VARS = {2: [0], 3: [7], 4: [4], 5: [10], 6: [10]}
+VARS = {2: [0], 3: [7], 4: [4], 5: [12, 10], 6: [12, 10]}
 ps = [int(a) for a in sys.argv[1:]] or [2, 3, 4, 5, 6]
 os.environ["HDIV_MARCH_TILE"] = "-1"
 for p in ps:
