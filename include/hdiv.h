@@ -144,7 +144,8 @@ hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* st
 /* y_q = Z q: the (2,2) block alone, Z = W_alpha^-1 (grad-div) or gamma_e W^-1 (Darcy, piecewise-
  * constant gamma), P:235-238, P:535-553 — on every 3D geometry through the element-local CG in
  * the Gauss-Legendre nodal basis (exact Kronecker case converges in one
- * step); 2D: the quadrature kernel (exact Kronecker inverse on parallelograms, Cholesky of the
+ * step); on trilinear meshes at p <= 4 through precomputed explicit element inverses built at
+ * setup when they fit the memory budget (env HDIV_WINV=cg keeps the CG); 2D: the quadrature kernel (exact Kronecker inverse on parallelograms, Cholesky of the
  * quadrature-assembled W on general quadrilaterals); Z = 0 gives y_q = 0.  q, y_q: DEVICE [n_l2]. */
 hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y_q, void* stream);
 /* Same as hdiv_apply_block with HOST x, y (pinned or pageable): H2D copy, apply, D2H copy,
