@@ -44,6 +44,8 @@ struct TriArgs {
   int ess;              // eliminated essential sides (NEXT-3): zero inputs, outputs skipped
   const double* gvert;  // general gamma (NEXT-3): per-vertex field; Z = W^-1 W_gamma W^-1
   const int* skip;
+  const double* winv;   // explicit W^e inverses fused into tri_multi_kernel's y_q store (or nullptr)
+  const double* zc;     // {., s_e, ., .} per element (with winv)
 };
 
 // padded layout of a (D0, D1, D2) array of the order-PP kernel: the strides with the fewest
@@ -780,9 +782,24 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
   }
   if constexpr (BLOCK) {
     double* yq = a.y + a.nrt;
-    for (int i = tid; i < EPC * P3; i += NT) {
-      const int el = i / P3;
-      if (sEc[el][3]) yq[e0 * P3 + i] = sy[i];
+    if (a.winv) {   // y_q = D u - s_e W_e^-1 q~_e: the stored inverse streamed column by column
+      for (int i = tid; i < EPC * P3; i += NT) {
+        const int el = i / P3, r = i - (i / P3) * P3;
+        if (!sEc[el][3]) continue;
+        const long long e = e0 + el;
+        const double* w = a.winv + e * (long long)(P3 * P3) + r;
+        const double* qe = sq + el * T::SL;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < P3; ++c)
+          acc = fma(w[c * P3], qe[(c % P) + T::L2::S1 * ((c / P) % P) + T::L2::S2 * (c / (P * P))], acc);
+        yq[e0 * P3 + i] = sy[i] - a.zc[4 * e + 1] * acc;
+      }
+    } else {
+      for (int i = tid; i < EPC * P3; i += NT) {
+        const int el = i / P3;
+        if (sEc[el][3]) yq[e0 * P3 + i] = sy[i];
+      }
     }
   }
 }
@@ -899,7 +916,7 @@ static int tri_epc(int p, int mode) {
 // noz: the block apply without its Z term (added by the explicit-inverse apply afterwards)
 template <int P, int MODE>
 cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* skip,
-                     cudaStream_t s, bool noz = false) {
+                     cudaStream_t s, bool noz = false, bool* fused = nullptr) {
   const bool hz = h->has_z && !noz;
   // CTA size (r01 A/B of 64 vs 96 threads per order): W^-1 alone at p = 3 — one warp per element (its
   // barriers are warp-synchronous); mass-only / gamma = 0 applies at p = 4, 5 — three warps,
@@ -916,6 +933,8 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ess = (MODE == 2) ? 0 : h->ess;
   a.gvert = h->d_gvert;
   a.skip = skip;
+  a.winv = nullptr;
+  a.zc = h->d_zcoef;
   if constexpr (MODE == 2 && P <= 2) {
     if (!h->d_gvert) {
       tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
@@ -926,6 +945,10 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
     // EPC elements per 96-thread CTA (mass / gamma = 0 applies), inputs landed by cp.async
     const int epc = tri_epc(P, MODE);
     if (!(MODE == 1 && hz) && epc >= 1) {
+      if (MODE == 1 && noz && fused && h->d_winv) {   // Z by the stored inverses, in the epilogue
+        a.winv = h->d_winv;
+        *fused = true;
+      }
       if constexpr (P <= 3) {
         if (epc >= 4) {
           tri_multi_kernel<P, 4, MODE == 1><<<(unsigned)((h->E + 3) / 4), 96, 0, s>>>(a, h->tab, h->E);
@@ -960,14 +983,14 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
 
 template <int MODE>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k, cudaStream_t s,
-                     bool noz = false) {
+                     bool noz = false, bool* fused = nullptr) {
   switch (h->p) {
-    case 1: return launch_p<1, MODE>(h, x, y, k, s, noz);
-    case 2: return launch_p<2, MODE>(h, x, y, k, s, noz);
-    case 3: return launch_p<3, MODE>(h, x, y, k, s, noz);
-    case 4: return launch_p<4, MODE>(h, x, y, k, s, noz);
-    case 5: return launch_p<5, MODE>(h, x, y, k, s, noz);
-    case 6: return launch_p<6, MODE>(h, x, y, k, s, noz);
+    case 1: return launch_p<1, MODE>(h, x, y, k, s, noz, fused);
+    case 2: return launch_p<2, MODE>(h, x, y, k, s, noz, fused);
+    case 3: return launch_p<3, MODE>(h, x, y, k, s, noz, fused);
+    case 4: return launch_p<4, MODE>(h, x, y, k, s, noz, fused);
+    case 5: return launch_p<5, MODE>(h, x, y, k, s, noz, fused);
+    case 6: return launch_p<6, MODE>(h, x, y, k, s, noz, fused);
   }
   return cudaErrorInvalidValue;
 }
@@ -1180,8 +1203,13 @@ cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y
   if (e != cudaSuccess) return e;
   if (mode == MODE_BLOCK) {
     if (h->d_winv) {
-      e = dispatch<1>(h, x, y, skip, s, true);
-      if (e != cudaSuccess) return e;
+      static const bool fuse = [] {
+        const char* v = getenv("HDIV_WINV_FUSE");
+        return !(v && atoi(v) == 0);
+      }();
+      bool fused = false;
+      e = dispatch<1>(h, x, y, skip, s, true, fuse ? &fused : nullptr);
+      if (e != cudaSuccess || fused) return e;
       return winv_apply<true>(h, x + h->nrt, y + h->nrt, skip, s);
     }
     return dispatch<1>(h, x, y, skip, s);
