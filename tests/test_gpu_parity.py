@@ -461,15 +461,19 @@ def test_trilinear_multi_element_ctas(monkeypatch, epc, N, p, ess):
 
 # ---- W^-1 on trilinear hexes: precomputed explicit element inverses (default at p <= 4,
 #      P:796-798) and the local CG (HDIV_WINV=cg) — block apply, Z alone and MINRES ----
-@pytest.mark.parametrize("winv", ["explicit", "cg"])
+@pytest.mark.parametrize("winv", ["explicit", "explicit-separate", "cg"])
 @pytest.mark.parametrize("name,N,p", [("c3gd", (3, 2, 2), 1), ("c3gd", (3, 2, 2), 2), ("c3g", (2, 3, 2), 3),
                                       ("c3gd", (2, 2, 3), 4), ("c3g", (3, 1, 2), 4)])
 def test_trilinear_winv_modes(monkeypatch, winv, name, N, p):
+    """explicit: the inverses fused into the batched kernel's epilogue; explicit-separate: the
+    one-element kernel (HDIV_TRI_EPC=0) + the separate streaming apply; cg: the local CG."""
     from oracle import operators, solvers
     if winv == "cg":
         monkeypatch.setenv("HDIV_WINV", "cg")
     else:
         monkeypatch.delenv("HDIV_WINV", raising=False)
+    if winv == "explicit-separate":
+        monkeypatch.setenv("HDIV_TRI_EPC", "0")
     pr = _problem(name, N, p)
     A = operators.Assembled(pr)
     op = _gpu(pr)
