@@ -536,6 +536,32 @@ def main():
         op3.close()
         del x3, y3
         torch.cuda.empty_cache()
+        # the same mesh with a nonzero (2,2) block (grad-div, alpha/beta = 10^U(-2,2)): Z by the
+        # precomputed explicit element inverses fused into the batched kernel;
+        # HBM roofline with the inverses' 8 p^3 B per L2 DOF counted as algorithmic bytes
+        try:
+            import numpy as np
+            from synth import random_vector
+            pr3.kind = "grad_div"
+            pr3.alpha = 10.0 ** random_vector(pr3.E, 33)
+            pr3.beta = 10.0 ** random_vector(pr3.E, 34)
+            op3 = from_problem(pr3)
+            x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
+            y3 = torch.empty_like(x3)
+            ms3 = time_applies(op3, x3, y3, 20, 5, None, torch) / 20
+            alg = 16 * op3.sizes.n + 8 * P3_ ** 3 * op3.sizes.n_l2
+            result["config3_graddiv_apply"] = {
+                "workload": "config 3 mesh, grad-div alpha, beta = 10^U(-2,2) (block apply with "
+                            "Z = W_alpha^-1 by the explicit element inverses)",
+                "dofs": op3.sizes.n, "ms": ms3, "GDOF_s": op3.sizes.n / ms3 / 1e6,
+                "roofline": {"bound": "hbm", "achieved": alg / (ms3 * 1e-3) / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": alg / (ms3 * 1e-3) / 1e9 / peak,
+                             "alg_bytes_per_launch": alg}}
+            op3.close()
+            del x3, y3
+        except Exception as ex:   # reported, never fatal to the bench line
+            result["config3_graddiv_apply"] = {"error": str(ex)[:200]}
+        torch.cuda.empty_cache()
 
     # W^-1 benchmark of Table dg-mass-inv (NEXT-2): ~1.7e6 L2 DOFs on a jittered
     # hex mesh, 100 applications of the (2,2)-block inverse by the fused element-local CG
