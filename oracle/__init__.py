@@ -34,6 +34,10 @@ manufactured-solution convergence rates, closed-form traces; eliminated sides: t
 boundary, the one-dimensional pure-Neumann nullspace, S~ 1 = 0, exact uniform flow; general
 gamma: the constant-field reduction, an exact weighted Kronecker product, the p = 1
 mean-value closed form; block-Jacobi AMG: exact block solves.
-Parity unpinned: trilinear-element values of M^e beyond the invariants above
-(no closed form exists).
+Piola-mapped element matrices on non-axis-aligned elements (tests/test_oracle_piola.py): the
+parallelepiped closed form (beta/det J)(J^T J)_{cc'} (x) exact 1D integrals built independently,
+rotation invariance on general trilinear elements, the s^{2-d} scaling law, and MMS rates on
+smoothly distorted 2D/3D meshes (a J <-> J^T swap fails them).  The sampled-row path
+(sample.py) is pinned against the global assembly, including the vertex-field gamma.
+Nothing in the oracle is left parity-unpinned.
 """

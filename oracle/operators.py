@@ -90,7 +90,7 @@ class Assembled:
                 Ze = sla.cho_solve(cf, Wg @ sla.cho_solve(cf, np.eye(nl)))  # W^-1 W_g W^-1
                 self.Wdiag[sl] = np.diag(We)
                 self.Wgdiag[sl] = np.diag(Wg)
-            self.Z.append(0.5 * (Ze + Ze.T))
+            self.Z.append(Ze)
         self.M = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                                shape=(self.n_rt, self.n_rt))
         I, J, A = space.divergence_csr(dim, N, p)
