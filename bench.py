@@ -102,6 +102,29 @@ def dist_env():
     return ws, rank, local
 
 
+def torchrun_argv(argv, nproc: int, port: int, python=None):
+    """Command line that relaunches this script under torchrun, one rank per GPU (the driver's
+    own N > 1 launch form: --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1)."""
+    return [python or sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+            os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def nccl_log_env(env):
+    """NCCL communicator init logged (NCCL_DEBUG=INFO) to stderr, so stdout keeps the JSON line."""
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return env
+
+
 def make_problem(cfg: str, p: int):
     from synth import make_config
     return make_config(cfg, p=p)
@@ -235,6 +258,8 @@ def run_reference(args, ws, rank):
     pr = make_problem(args.config, args.p)
     n = pr.n_rt() + pr.n_l2()
     per_step_budget = max(0.2, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    if args.ref_seconds is not None:
+        per_step_budget = args.ref_seconds
     for _ in range(args.warmup):
         cpu_baseline(pr, budget_s=min(1.0, per_step_budget))
     vals = [cpu_baseline(pr, budget_s=per_step_budget) for _ in range(args.steps)]
@@ -266,9 +291,25 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-minres", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-seconds", type=float, default=None,
+                    help="--impl reference: oracle seconds per step (default: ~120 s total)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: relaunch under torchrun (one process per GPU)
+        import torch
+        nvis = torch.cuda.device_count()
+        if args.impl != "reference" and nvis < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {nvis} "
+                              "CUDA devices are visible", "n_gpus": nvis}), flush=True)
+            sys.exit(2)
+        env = nccl_log_env(dict(os.environ))
+        cmd = torchrun_argv(sys.argv[1:], args.gpus, _free_port())
+        sys.exit(subprocess.call(cmd, env=env))
+    if ws > 1 and args.gpus != ws:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws} ranks",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
@@ -279,6 +320,7 @@ def main():
     dist = None
     nccl_id = None
     if ws > 1:
+        nccl_log_env(os.environ)
         import torch.distributed as td
         td.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = td
@@ -543,8 +585,8 @@ def main():
             import numpy as np
             from synth import random_vector
             pr3.kind = "grad_div"
-            pr3.alpha = 10.0 ** random_vector(pr3.E, 33)
-            pr3.beta = 10.0 ** random_vector(pr3.E, 34)
+            pr3.alpha = 10.0 ** random_vector(pr3.E, 33, -2.0, 2.0)
+            pr3.beta = 10.0 ** random_vector(pr3.E, 34, -2.0, 2.0)
             op3 = from_problem(pr3)
             x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
             y3 = torch.empty_like(x3)

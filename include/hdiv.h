@@ -19,8 +19,14 @@
  *  - Errors are returned as hdiv_status; nothing propagates across the ABI. Validation
  *    (order, det J > 0 at every quadrature point, coefficient signs, shapes) happens in
  *    hdiv_setup before any device work.  A CUDA launch error is HDIV_ERR_CUDA.
- *  - The handle is read-only after setup except for the MINRES workspace: concurrent applies
- *    on distinct outputs are safe; hdiv_minres_solve serialises on its own workspace.
+ *  - ONE call in flight per handle.  Several calls keep scratch in the handle (the MINRES /
+ *    GMRES workspaces, the Chebyshev and AMG work vectors used by hdiv_apply_precond and
+ *    hdiv_apply_schur, the explicit-inverse / local-CG buffers of hdiv_apply_precond_tri, the
+ *    host-pipeline buffers, streams and events of hdiv_apply_block_host, the interface send /
+ *    receive buffers and the comm stream of multi-rank applies), and some of it is allocated
+ *    lazily on first use.  Calls on one handle must therefore be ordered by the caller: issue
+ *    them from one host thread and on one stream (or on streams the caller orders with
+ *    events).  Distinct handles are independent.  There is no internal lock.
  */
 #ifndef HDIV_H
 #define HDIV_H
@@ -156,7 +162,9 @@ hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y_q, void* stre
  * buffers (2 vectors) are allocated on first use. */
 hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* x_host, double* y_host,
                                   void* stream);
-/* Number of kernels one hdiv_apply_block launches (for launch accounting). */
+/* Device operations (kernel launches + memsets of this rank, communication excluded) that the
+ * most recent hdiv_apply_block on this handle issued, counted at the launch sites; 0 before
+ * the first apply (launch accounting for bench.py's gpu_launches). */
 hdiv_status hdiv_apply_launches(hdiv_handle h, int* n);
 
 /* diag(M_beta) = M~, assembled (interface-summed).  diag: [n_rt]. */

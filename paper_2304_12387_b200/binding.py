@@ -273,13 +273,28 @@ class HdivOperator:
         return y
 
     def apply_block_host(self, x_host: "np.ndarray | object", y_host, stream=None):
-        """x_host/y_host: host arrays (numpy or pinned torch CPU tensors) of length n."""
-        def hp(a):
-            if hasattr(a, "data_ptr"):
+        """x_host/y_host: host arrays (numpy or pinned torch CPU tensors) of length n.
+        The library copies n doubles out of / into them, so both must be fp64, C-contiguous,
+        CPU-resident and exactly n long (checked here; anything else raises)."""
+        n = self.sizes.n
+
+        def hp(a, name):
+            if hasattr(a, "data_ptr"):   # torch tensor
+                import torch
+                if a.device.type != "cpu" or a.dtype != torch.float64 or not a.is_contiguous() \
+                        or a.numel() != n:
+                    raise ValueError(f"{name}: need a contiguous CPU float64 tensor of {n} "
+                                     f"elements, got {a.dtype} {tuple(a.shape)} on {a.device}")
                 return C.c_void_p(a.data_ptr())
+            if not isinstance(a, np.ndarray) or a.dtype != np.float64 or \
+                    not a.flags["C_CONTIGUOUS"] or a.size != n:
+                raise ValueError(f"{name}: need a C-contiguous float64 numpy array of {n} "
+                                 f"elements")
+            if name == "y_host" and not a.flags["WRITEABLE"]:
+                raise ValueError("y_host is read-only")
             return C.c_void_p(a.ctypes.data)
-        _check(self.lib.hdiv_apply_block_host(self.h, hp(x_host), hp(y_host),
-                                              self._stream_handle(stream)))
+        px, py = hp(x_host, "x_host"), hp(y_host, "y_host")
+        _check(self.lib.hdiv_apply_block_host(self.h, px, py, self._stream_handle(stream)))
         return y_host
 
     def apply_launches(self) -> int:

@@ -150,6 +150,7 @@ void hdiv_destroy(hdiv_handle h) {
 hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co, hdiv_kind kind,
                        const hdiv_options* opts, const void* nccl_id, int rank, int nranks,
                        void* stream, hdiv_handle* out) {
+  HDIV_NVTX();
   if (!out) return fail(HDIV_ERR_NULL, "out is NULL");
   *out = nullptr;
   if (!mesh || !co) return fail(HDIV_ERR_NULL, "mesh/coeffs NULL");
@@ -493,6 +494,7 @@ hdiv_status hdiv_sizes(hdiv_handle h, int64_t* nrt, int64_t* nl2, int64_t* nrt_g
 }
 
 hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* yu, void* stream) {
+  HDIV_NVTX();
   if (!h || !u || !yu) return fail(HDIV_ERR_NULL, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   HDIV_CUDA_TRY(h->kernel == 2  ? launch_affine_apply(h, u, yu, MODE_MASS, nullptr, s)
@@ -504,12 +506,14 @@ hdiv_status hdiv_apply_mass(hdiv_handle h, const double* u, double* yu, void* st
 }
 
 hdiv_status hdiv_apply_div(hdiv_handle h, const double* u, double* yq, void* stream) {
+  HDIV_NVTX();
   if (!h || !u || !yq) return fail(HDIV_ERR_NULL, "NULL argument");
   HDIV_CUDA_TRY(launch_div(h, u, yq, (cudaStream_t)stream));
   return HDIV_OK;
 }
 
 hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* yu, void* stream) {
+  HDIV_NVTX();
   if (!h || !q || !yu) return fail(HDIV_ERR_NULL, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   HDIV_CUDA_TRY(launch_divT(h, q, yu, s));
@@ -518,12 +522,16 @@ hdiv_status hdiv_apply_divT(hdiv_handle h, const double* q, double* yu, void* st
 }
 
 hdiv_status hdiv_apply_block(hdiv_handle h, const double* x, double* y, void* stream) {
+  HDIV_NVTX();
   if (!h || !x || !y) return fail(HDIV_ERR_NULL, "NULL argument");
+  g_ops = 0;
   HDIV_CUDA_TRY(apply_block_dev(h, x, y, nullptr, (cudaStream_t)stream));
+  h->last_apply_ops = g_ops;
   return HDIV_OK;
 }
 
 hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y, void* stream) {
+  HDIV_NVTX();
   if (!h || !q || !y) return fail(HDIV_ERR_NULL, "NULL argument");
   if (h->dim == 2) {
     if (!h->has_z) {   // Darcy gamma = 0: Z = 0
@@ -538,12 +546,14 @@ hdiv_status hdiv_apply_z(hdiv_handle h, const double* q, double* y, void* stream
 }
 
 hdiv_status hdiv_apply_precond_tri(hdiv_handle h, const double* v, double* z, void* stream) {
+  HDIV_NVTX();
   if (!h || !v || !z) return fail(HDIV_ERR_NULL, "NULL argument");
   return apply_precond_tri(h, v, z, (cudaStream_t)stream);
 }
 
 hdiv_status hdiv_gmres_solve(hdiv_handle h, const double* b, double* x, double rtol, int maxit,
                              int restart, hdiv_report* report, void* stream) {
+  HDIV_NVTX();
   if (!h || !b || !x) return fail(HDIV_ERR_NULL, "NULL argument");
   if (!(rtol > 0) || maxit < 1 || restart < 1 || restart > 64)
     return fail(HDIV_ERR_SHAPE, "gmres: rtol > 0, maxit >= 1, 1 <= restart <= 64 required");
@@ -552,9 +562,11 @@ hdiv_status hdiv_gmres_solve(hdiv_handle h, const double* b, double* x, double r
 
 hdiv_status hdiv_apply_launches(hdiv_handle h, int* n) {
   if (!h || !n) return fail(HDIV_ERR_NULL, "NULL argument");
-  // one fused kernel (+ a memset node on the quadrature paths, + the identity-row fixup of
-  // eliminated essential faces there)
-  *n = 1 + ((h->ess && h->kernel != 2) ? 1 : 0);
+  // counted at the launch sites during the last hdiv_apply_block on this handle (kernels +
+  // memsets of this rank: the fused apply, the memset of the quadrature paths, a separate
+  // explicit-W^-1 apply, the eliminated-face fixup, the interface add of multi-rank applies);
+  // 0 before the first apply
+  *n = h->last_apply_ops;
   return HDIV_OK;
 }
 
@@ -626,6 +638,7 @@ static hdiv_status apply_block_host_pipelined(hdiv_ctx* h, const double* xh, dou
 }
 
 hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* xh, double* yh, void* stream) {
+  HDIV_NVTX();
   if (!h || !xh || !yh) return fail(HDIV_ERR_NULL, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = sizeof(double) * (h->nrt + h->nl2);
@@ -645,6 +658,7 @@ hdiv_status hdiv_apply_block_host(hdiv_handle h, const double* xh, double* yh, v
 }
 
 hdiv_status hdiv_assemble_mass_diag(hdiv_handle h, double* diag, void* stream) {
+  HDIV_NVTX();
   if (!h || !diag) return fail(HDIV_ERR_NULL, "NULL argument");
   HDIV_CUDA_TRY(cudaMemcpyAsync(diag, h->d_mdiag, sizeof(double) * h->nrt,
                                 cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -652,6 +666,7 @@ hdiv_status hdiv_assemble_mass_diag(hdiv_handle h, double* diag, void* stream) {
 }
 
 hdiv_status hdiv_assemble_schur_diag_term(hdiv_handle h, double* ctil, void* stream) {
+  HDIV_NVTX();
   if (!h || !ctil) return fail(HDIV_ERR_NULL, "NULL argument");
   HDIV_CUDA_TRY(cudaMemcpyAsync(ctil, h->d_ctil, sizeof(double) * h->nl2,
                                 cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -666,12 +681,14 @@ hdiv_status hdiv_schur_nnz(hdiv_handle h, int64_t* nnz) {
 
 hdiv_status hdiv_assemble_schur_csr(hdiv_handle h, int64_t* rp, int64_t* col, double* val,
                                     void* stream) {
+  HDIV_NVTX();
   if (!h || !rp || !col || !val) return fail(HDIV_ERR_NULL, "NULL argument");
   HDIV_CUDA_TRY(launch_schur_export(h, rp, col, val, (cudaStream_t)stream));
   return HDIV_OK;
 }
 
 hdiv_status hdiv_apply_schur(hdiv_handle h, const double* x, double* y, void* stream) {
+  HDIV_NVTX();
   if (!h || !x || !y) return fail(HDIV_ERR_NULL, "NULL argument");
   if (h->nranks > 1) return fail(HDIV_ERR_UNSUPPORTED, "apply_schur with ghosts: use minres");
   HDIV_CUDA_TRY(launch_spmv(h, x, y, (cudaStream_t)stream));
@@ -680,18 +697,21 @@ hdiv_status hdiv_apply_schur(hdiv_handle h, const double* x, double* y, void* st
 
 hdiv_status hdiv_export_div_csr(hdiv_handle h, int64_t* rp, int64_t* col, double* val,
                                 void* stream) {
+  HDIV_NVTX();
   if (!h || !rp || !col || !val) return fail(HDIV_ERR_NULL, "NULL argument");
   HDIV_CUDA_TRY(launch_div_csr(h, rp, col, val, (cudaStream_t)stream));
   return HDIV_OK;
 }
 
 hdiv_status hdiv_apply_precond(hdiv_handle h, const double* v, double* z, void* stream) {
+  HDIV_NVTX();
   if (!h || !v || !z) return fail(HDIV_ERR_NULL, "NULL argument");
   return apply_precond(h, v, z, (cudaStream_t)stream);
 }
 
 hdiv_status hdiv_minres_solve(hdiv_handle h, const double* b, double* x, double rtol, int maxit,
                               hdiv_report* rep, void* stream) {
+  HDIV_NVTX();
   if (!h || !b || !x) return fail(HDIV_ERR_NULL, "NULL argument");
   if (maxit < 1) return fail(HDIV_ERR_SHAPE, "maxit < 1");
   return minres(h, b, x, rtol, maxit, rep, (cudaStream_t)stream);

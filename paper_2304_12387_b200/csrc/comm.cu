@@ -17,7 +17,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
+#include <thread>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -41,6 +43,7 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 NcclApi g_nccl;
 
@@ -65,6 +68,7 @@ bool load_nccl(std::string* err) {
   LOADSYM(GroupEnd, "ncclGroupEnd");
   LOADSYM(AllGather, "ncclAllGather");
   LOADSYM(GetErrorString, "ncclGetErrorString");
+  LOADSYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef LOADSYM
   g_nccl.lib = lib;
   return true;
@@ -148,6 +152,58 @@ struct Comm {
 static hdiv_status nccl_fail(ncclResult_t r, const char* what) {
   set_error(std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
   return HDIV_ERR_NCCL;
+}
+
+// exchange with the two slab neighbours over NCCL (one group): send_lo -> rank-1, which
+// receives it in its recv_hi, and send_hi -> rank+1 (recv_lo there); every call checked
+static hdiv_status nccl_exchange(Comm* c, const double* send_lo, double* recv_lo,
+                                 const double* send_hi, double* recv_hi, long long n,
+                                 cudaStream_t s, const char* what) {
+  ncclResult_t r = g_nccl.GroupStart();
+  if (r != ncclSuccess) return nccl_fail(r, what);
+  ncclResult_t e = ncclSuccess;
+  if (send_lo) {
+    if (e == ncclSuccess) e = g_nccl.Send(send_lo, n, ncclDouble, c->rank - 1, c->comm, s);
+    if (e == ncclSuccess) e = g_nccl.Recv(recv_lo, n, ncclDouble, c->rank - 1, c->comm, s);
+  }
+  if (send_hi) {
+    if (e == ncclSuccess) e = g_nccl.Send(send_hi, n, ncclDouble, c->rank + 1, c->comm, s);
+    if (e == ncclSuccess) e = g_nccl.Recv(recv_hi, n, ncclDouble, c->rank + 1, c->comm, s);
+  }
+  r = g_nccl.GroupEnd();   // always close the group, even after a failed enqueue
+  if (e != ncclSuccess) return nccl_fail(e, what);
+  if (r != ncclSuccess) return nccl_fail(r, what);
+  return HDIV_OK;
+}
+
+// asynchronous NCCL errors (a failed peer): polled by the MINRES / GMRES host loops so a dead
+// peer surfaces as HDIV_ERR_NCCL instead of a silent hang
+hdiv_status comm_check_async(const hdiv_ctx* h) {
+  const Comm* c = h->comm;
+  if (!c || c->loop || !c->comm || !g_nccl.CommGetAsyncError) return HDIV_OK;
+  ncclResult_t ae = ncclSuccess;
+  ncclResult_t r = g_nccl.CommGetAsyncError(c->comm, &ae);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommGetAsyncError");
+  if (ae != ncclSuccess && ae != ncclInProgress) return nccl_fail(ae, "NCCL asynchronous error");
+  return HDIV_OK;
+}
+
+// stream synchronisation that keeps polling NCCL for asynchronous errors while it waits (a
+// plain cudaStreamSynchronize would block forever behind a collective whose peer died)
+hdiv_status comm_sync(const hdiv_ctx* h, cudaStream_t s) {
+  const Comm* c = h->comm;
+  if (!c || c->loop || !c->comm) {
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    return HDIV_OK;
+  }
+  for (int k = 0;; ++k) {
+    cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return HDIV_OK;
+    if (q != cudaErrorNotReady) HDIV_CUDA_TRY(q);
+    hdiv_status st = comm_check_async(h);
+    if (st != HDIV_OK) return st;
+    if (k > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
 }
 
 // exchange with the two slab neighbours through the loopback group: send_lo -> rank-1 (its
@@ -273,22 +329,15 @@ hdiv_status comm_reverse_add(hdiv_ctx* h, double* y, cudaStream_t s) {
     hdiv_status st = loop_exchange(h, lo, hi, lo ? c->rlo : nullptr, hi ? c->rhi : nullptr,
                                    c->plane, s);
     if (st != HDIV_OK) return st;
+    count_op();
     add_planes_kernel<<<(unsigned)((c->plane + 255) / 256), 256, 0, s>>>(lo, c->rlo, hi, c->rhi,
                                                                          c->plane);
     HDIV_CUDA_TRY(cudaGetLastError());
     return HDIV_OK;
   }
-  ncclResult_t r = g_nccl.GroupStart();
-  if (lo) {
-    g_nccl.Send(lo, c->plane, ncclDouble, c->rank - 1, c->comm, s);
-    g_nccl.Recv(c->rlo, c->plane, ncclDouble, c->rank - 1, c->comm, s);
-  }
-  if (hi) {
-    g_nccl.Send(hi, c->plane, ncclDouble, c->rank + 1, c->comm, s);
-    g_nccl.Recv(c->rhi, c->plane, ncclDouble, c->rank + 1, c->comm, s);
-  }
-  r = g_nccl.GroupEnd();
-  if (r != ncclSuccess) return nccl_fail(r, "reverse-add exchange");
+  hdiv_status st = nccl_exchange(c, lo, c->rlo, hi, c->rhi, c->plane, s, "reverse-add exchange");
+  if (st != HDIV_OK) return st;
+  count_op();
   add_planes_kernel<<<(unsigned)((c->plane + 255) / 256), 256, 0, s>>>(lo, c->rlo, hi, c->rhi,
                                                                        c->plane);
   HDIV_CUDA_TRY(cudaGetLastError());
@@ -309,18 +358,8 @@ hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s) {
   if (c->loop)
     return loop_exchange(h, down ? c->slo : nullptr, up ? c->shi : nullptr,
                          down ? glo : nullptr, up ? ghi : nullptr, c->lplane, s);
-  ncclResult_t r = g_nccl.GroupStart();
-  if (down) {
-    g_nccl.Send(c->slo, c->lplane, ncclDouble, c->rank - 1, c->comm, s);
-    g_nccl.Recv(glo, c->lplane, ncclDouble, c->rank - 1, c->comm, s);
-  }
-  if (up) {
-    g_nccl.Send(c->shi, c->lplane, ncclDouble, c->rank + 1, c->comm, s);
-    g_nccl.Recv(ghi, c->lplane, ncclDouble, c->rank + 1, c->comm, s);
-  }
-  r = g_nccl.GroupEnd();
-  if (r != ncclSuccess) return nccl_fail(r, "L2 ghost exchange");
-  return HDIV_OK;
+  return nccl_exchange(c, down ? c->slo : nullptr, down ? glo : nullptr, up ? c->shi : nullptr,
+                       up ? ghi : nullptr, c->lplane, s, "L2 ghost exchange");
 }
 
 // all-gather of k local scalars into glob[P][k] (rank-ordered)

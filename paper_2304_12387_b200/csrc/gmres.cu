@@ -210,7 +210,7 @@ static hdiv_status global_proj(hdiv_ctx* h, int nk, double* out, cudaStream_t s)
   if (st != HDIV_OK) return st;
   HDIV_CUDA_TRY(cudaMemcpyAsync(g->hg.data(), g->glob, sizeof(double) * nk * h->nranks,
                                 cudaMemcpyDeviceToHost, s));
-  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  if ((st = comm_sync(h, s)) != HDIV_OK) return st;
   for (int k = 0; k < nk; ++k) {
     double v = 0.0;
     for (int r = 0; r < h->nranks; ++r) v += g->hg[(size_t)r * nk + k];

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -99,6 +100,7 @@ struct hdiv_ctx {
   hdiv::MinresWork* mw = nullptr;
   hdiv::AmgHier* amg = nullptr;   // NEXT-1 hierarchy when opts.schur_solver == HDIV_SCHUR_AMG
   hdiv::GmresWork* gw = nullptr;  // NEXT-4 Krylov basis (lazily allocated)
+  int last_apply_ops = 0;         // device operations of the last hdiv_apply_block
 };
 
 // error plumbing
@@ -159,6 +161,22 @@ hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done,
 int amg_num_levels(const hdiv_ctx* h);
 hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, double* omega,
                            const double** st);
+
+// multi-rank: NCCL asynchronous-error poll, and a stream sync that polls it while waiting
+hdiv_status comm_check_async(const hdiv_ctx* h);
+hdiv_status comm_sync(const hdiv_ctx* h, cudaStream_t s);
+
+// device operations (kernel launches + memsets) issued by the current host thread; reset and
+// read around an apply by hdiv_apply_block (hdiv_apply_launches reports the last count)
+inline thread_local int g_ops = 0;
+inline void count_op(int n = 1) { g_ops += n; }
+
+// NVTX range around every C-ABI entry point (header-only NVTX v3: no link dependency)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+#define HDIV_NVTX() ::hdiv::NvtxScope _hdiv_nvtx_scope(__func__)
 
 // apply modes
 enum { MODE_MASS = 1, MODE_BLOCK = 2, MODE_ZONLY = 3 };

@@ -664,6 +664,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
     attr_done = true;
   }
   const long long nblk = (long long)a.ntile[0] * a.ntile[1] * (tz1 - tz0);
+  count_op();
   kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff);
   return cudaGetLastError();
 }
@@ -1040,6 +1041,7 @@ cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* s
     attr_done = true;
   }
   const long long nblk = cols * a.ntile[2];
+  count_op();
   kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff, zc);
   return cudaGetLastError();
 }

@@ -423,6 +423,7 @@ cudaError_t launch_g(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.dense_z = (DIM == 2 && h->geom == GEOM_TRILINEAR) ? 1 : 0;
   if (MODE == GMODE_ZONLY) a.has_z = 1;
   a.skip = skip;
+  count_op();
   general_kernel<DIM, P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
 }
@@ -456,6 +457,7 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
 
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                  const int* skip, cudaStream_t s) {
+  count_op();
   cudaError_t e = cudaMemsetAsync(y, 0, sizeof(double) * h->nrt, s);
   if (e != cudaSuccess) return e;
   if (mode == MODE_BLOCK) return dispatch<GMODE_BLOCK>(h, x, y, skip, s);

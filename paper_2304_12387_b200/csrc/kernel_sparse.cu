@@ -309,6 +309,7 @@ cudaError_t launch_ess_fixup(const hdiv_ctx* h, const double* x, double* y, doub
     if (pl > mx) mx = pl;
   }
   dim3 grid(nblocks(mx, 256), 2 * h->dim);
+  count_op();
   ess_fixup_kernel<<<grid, 256, 0, s>>>(make_grid(h), x, y, cval, skip);
   return cudaGetLastError();
 }

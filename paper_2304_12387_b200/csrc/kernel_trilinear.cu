@@ -937,6 +937,7 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.zc = h->d_zcoef;
   if constexpr (MODE == 2 && P <= 2) {
     if (!h->d_gvert) {
+      count_op();
       tri_z_direct_kernel<P><<<(unsigned)((h->E + 127) / 128), 128, 0, s>>>(a, h->tab, h->E);
       return cudaGetLastError();
     }
@@ -951,32 +952,38 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
       }
       if constexpr (P <= 3) {
         if (epc >= 4) {
+          count_op();
           tri_multi_kernel<P, 4, MODE == 1><<<(unsigned)((h->E + 3) / 4), 96, 0, s>>>(a, h->tab, h->E);
           return cudaGetLastError();
         }
       }
       if constexpr (P <= 4) {   // three elements fit the 48 KB of static shared memory
         if (epc >= 3) {
+          count_op();
           tri_multi_kernel<P, 3, MODE == 1><<<(unsigned)((h->E + 2) / 3), 96, 0, s>>>(a, h->tab, h->E);
           return cudaGetLastError();
         }
       }
       if constexpr (P <= 5) {
         if (epc >= 2) {
+          count_op();
           tri_multi_kernel<P, 2, MODE == 1><<<(unsigned)((h->E + 1) / 2), 96, 0, s>>>(a, h->tab, h->E);
           return cudaGetLastError();
         }
       }
+      count_op();
       tri_multi_kernel<P, 1, MODE == 1><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab, h->E);
       return cudaGetLastError();
     }
   }
   if constexpr (MODE != 2 && (P == 4 || P == 5)) {
     if (wide) {
+      count_op();
       tri_kernel<P, 96, MODE><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab);
       return cudaGetLastError();
     }
   }
+  count_op();
   tri_kernel<P, NT, MODE><<<(unsigned)h->E, NT, 0, s>>>(a, h->tab);
   return cudaGetLastError();
 }
@@ -1160,9 +1167,11 @@ template <int P, bool ACC>
 cudaError_t winv_apply_p(const hdiv_ctx* h, const double* q, double* y, const int* skip, cudaStream_t s) {
   if constexpr (P <= 2) {
     const long long n = h->E * P * P * P;
+    count_op();
     winv_apply_small_kernel<P, ACC><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h->d_winv, q, y, h->d_zcoef, h->E, skip);
     return cudaGetLastError();
   }
+  count_op();
   winv_apply_kernel<P, ACC><<<(unsigned)((h->E + 3) / 4), 128, 0, s>>>(h->d_winv, q, y, h->d_zcoef, h->E, skip);
   return cudaGetLastError();
 }
@@ -1199,6 +1208,7 @@ cudaError_t launch_trilinear_apply(const hdiv_ctx* h, const double* x, double* y
     if (h->d_winv) return winv_apply<false>(h, x, y, skip, s);
     return dispatch<2>(h, x, y, skip, s);   // y (L2) fully written
   }
+  count_op();
   cudaError_t e = cudaMemsetAsync(y, 0, sizeof(double) * h->nrt, s);
   if (e != cudaSuccess) return e;
   if (mode == MODE_BLOCK) {

@@ -724,7 +724,7 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     }
     launched += 6;
     HDIV_CUDA_TRY(cudaMemcpyAsync(mw->st_host, st_last, sizeof(MState), cudaMemcpyDeviceToHost, s));
-    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hdiv_status e = comm_sync(h, s); e != HDIV_OK) return e;
     if (mw->st_host->done || launched >= maxit + 6) break;
   }
   HDIV_CUDA_TRY(cudaEventRecord(e1, s));
