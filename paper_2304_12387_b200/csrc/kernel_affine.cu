@@ -669,501 +669,28 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   return cudaGetLastError();
 }
 
-// ============================================================================================
-// z-marching variant: a CTA owns a TX x TY column of elements and walks up a chunk of element
-// layers.  The x/y components of each layer are processed exactly as above (TZ = 1 tiles with
-// one-element x/y halos); the z component needs no halo: the transformed shared z plane, its
-// raw values (for D u), the running plane sum (carry) and the last q~ cell of every (I,J)
-// line stay on chip from one layer to the next.  Loads of the next layer (q~ tile, x, y, z
-// planes) are issued as cp.async groups as soon as their buffers free up, so they stream in
-// while the current layer computes.  Group order per layer s: Q_{s+1}, X_{s+1}, Y_{s+1},
-// Z_{s+1}; every wait is wait_group<3>.
-template <int P, int TX, int TY>
-struct MG {
-  using G = Geo<P, TX, TY, 1>;
-  static constexpr int CX = TX * P, CY = TY * P;
-  static constexpr int ZS1 = G::Q1, ZS2 = G::Q2;             // plane layout [K][J][I] (odd)
-  static constexpr int SX = CG<P, TX, TY, 1, 0>::SIZE, SY = CG<P, TX, TY, 1, 1>::SIZE;
-  static constexpr int SZL = ZS2 * P, SZW = ZS2 * (P + 1);
-  static constexpr int SQ = G::SQSIZE;                       // q~ of one layer (= ZS2 * P)
-  static constexpr int HQ = CY * P + CX * P;                 // x / y halo q~ of one layer
-  static constexpr int NCO2 = 2 * (TX + 1) * (TY + 1);       // coefficient slots: below, cur
-  static constexpr int QB = SQ + HQ + 4 * NCO2;              // one Q buffer
-  static constexpr size_t smem_doubles(bool block) {
-    return (size_t)SX + SY + SZL + SZW + ZS2 + (block ? 2 * (size_t)QB + SQ : 8 * NCO2);
-  }
-};
-
-template <int P, int TX, int TY, int NT, bool BLOCK>
-__global__ void __launch_bounds__(NT)
-affine_march_kernel(const AffArgs a, const __grid_constant__ TabAffine tab, int zchunk) {
-  using M = MG<P, TX, TY>;
-  using G = typename M::G;
-  using O = Own<P, TX, TY, 1, NT>;
-  constexpr int CX = M::CX, CY = M::CY, ZS1 = M::ZS1, ZS2 = M::ZS2;
-  constexpr int P3 = P * P * P;
-  constexpr int NLINE = CX * CY;
-  constexpr int JL = (NLINE + NT - 1) / NT;
-  if (a.skip && *a.skip) return;
-  extern __shared__ double smem[];
-  double* bufX = smem;
-  double* bufY = bufX + M::SX;
-  double* zl = bufY + M::SY;        // raw planes 1..P of the current layer
-  double* zw = zl + M::SZL;         // transformed planes 0..P
-  double* zr = zw + M::SZW;         // raw plane 0 (shared with the layer below)
-  double* qb0 = zr + ZS2;           // two Q buffers {sq, hq0, hq1, sco}
-  double* qb1 = qb0 + (BLOCK ? M::QB : 4 * M::NCO2);
-  double* zs = qb1 + (BLOCK ? M::QB : 4 * M::NCO2);   // Z scratch (BLOCK)
-  auto QSQ = [&](int b) { return (b ? qb1 : qb0); };
-  auto QH0 = [&](int b) { return QSQ(b) + (BLOCK ? M::SQ : 0); };
-  auto QH1 = [&](int b) { return QH0(b) + (BLOCK ? CY * P : 0); };
-  auto QCO = [&](int b) { return QH1(b) + (BLOCK ? CX * P : 0); };
-
-  const int tid = threadIdx.x;
-  int t = blockIdx.x;
-  const int tx = t % a.ntile[0];
-  t /= a.ntile[0];
-  const int ty = t % a.ntile[1];
-  const int tc = t / a.ntile[1];
-  const long long NLx = a.NL[0], NLy = a.NL[1], NLz = a.NL[2];
-  const int z_begin = tc * zchunk;
-  const int z_end = (int)min((long long)z_begin + zchunk, NLz);
-  TileInfo ti;
-  ti.e0[0] = tx * TX; ti.e0[1] = ty * TY;
-  ti.m[0] = (int)min((long long)TX, NLx - ti.e0[0]);
-  ti.m[1] = (int)min((long long)TY, NLy - ti.e0[1]);
-  ti.m[2] = 1;
-  ti.h[0] = ti.e0[0] > 0; ti.h[1] = ti.e0[1] > 0;
-  ti.last[0] = (ti.e0[0] + ti.m[0] == NLx);
-  ti.last[1] = (ti.e0[1] + ti.m[1] == NLy);
-  const int hiX = ti.m[0] * P, hiY = ti.m[1] * P;
-  const double* q = a.x + a.nrt;
-  const long long nx = a.n[0], ny = a.n[1];
-  const long long nxy = nx * ny;
-  // z-face plane K of the tile origin
-  const long long zorg = a.off[2] + (long long)ti.e0[0] * P + nx * ((long long)ti.e0[1] * P);
-  auto gel = [&](int ex, int ey, long long ez) -> long long {
-    return (ez * NLy + (ti.e0[1] + ey)) * NLx + (ti.e0[0] + ex);
-  };
-  auto set_layer = [&](int ez) {
-    ti.e0[2] = ez;
-    ti.h[2] = ez > 0;
-    ti.last[2] = (ez + 1 == NLz);
-  };
-  // load raw z planes [K0, K0 + np) into dst (plane stride ZS2)
-  auto load_planes = [&](double* dst, long long K0, int np) {
-    rows<NT, CX, CY, P + 1, ZS1, ZS2>(
-        a.x + zorg + K0 * nxy, nx, nxy, dst, [&](int i) { return i < hiX; },
-        [&](int j) { return j < hiY; }, [&](int k) { return k < np; },
-        [&](const double* g, double* s) { cp_async8(s, g); });
-  };
-  // Q group of layer ez into buffer b: q~ tile, x/y halo q~, coefficients (cur slot)
-  auto load_q = [&](int b, int ez) {
-    double* sco = QCO(b);
-    for (int i = tid; i < (TX + 1) * (TY + 1); i += NT) {
-      const int ix = i % (TX + 1), iy = i / (TX + 1);
-      const int ex = ti.e0[0] - 1 + ix, ey = ti.e0[1] - 1 + iy;
-      if (ex >= 0 && ey >= 0 && ix <= ti.m[0] && iy <= ti.m[1]) {
-        const double* c = a.coef + 4 * (((long long)ez * NLy + ey) * NLx + ex);
-        double* d = sco + 4 * ((TY + 1) * (TX + 1) + i);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) cp_async8(d + k, c + k);
-      }
-    }
-    if constexpr (BLOCK) {
-      double* sq = QSQ(b);
-#pragma unroll
-      for (int j = 0; j < O::JC; ++j) {
-        const int col = tid + j * NT;
-        if (col < O::NCOL) {
-          const int X = col % CX, Y = col / CX;
-          if (X < hiX && Y < hiY) {
-            const double* qc = q + gel(X / P, Y / P, ez) * P3 + (X % P) + P * (Y % P);
-#pragma unroll
-            for (int c = 0; c < P; ++c) cp_async8(sq + X + ZS1 * Y + ZS2 * c, qc + P * P * c);
-          }
-        }
-      }
-      double* h0 = QH0(b);
-      double* h1 = QH1(b);
-      if (ti.h[0])
-        for (int i = tid; i < CY * P; i += NT) {
-          const int J = i % CY, K = i / CY;
-          if (J < hiY)
-            cp_async8(h0 + i, q + ((ez * NLy + ti.e0[1] + J / P) * NLx + ti.e0[0] - 1) * P3 +
-                                  (P - 1) + P * ((J % P) + P * K));
-        }
-      if (ti.h[1])
-        for (int i = tid; i < CX * P; i += NT) {
-          const int I = i % CX, K = i / CX;
-          if (I < hiX)
-            cp_async8(h1 + i, q + ((ez * NLy + ti.e0[1] - 1) * NLx + ti.e0[0] + I / P) * P3 +
-                                  (I % P) + P * ((P - 1) + P * K));
-        }
-    }
-  };
-
-  // ---------------- prologue ----------------
-  // P0: the layer below (full element: P+1 planes, its coefficients, its top q~ cells) or,
-  //     at the domain bottom, the raw plane K = 0
-  const bool below = z_begin > 0;
-  if (below) {
-    load_planes(zw, (long long)(z_begin - 1) * P, P + 1);
-    double* sco = QCO(0);
-    for (int i = tid; i < TX * TY; i += NT) {
-      const int ex = i % TX, ey = i / TX;
-      if (ex < ti.m[0] && ey < ti.m[1]) {
-        const double* c = a.coef + 4 * gel(ex, ey, z_begin - 1);
-        double* d = sco + 4 * ((ey + 1) * (TX + 1) + ex + 1);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) cp_async8(d + k, c + k);
-      }
-    }
-    if constexpr (BLOCK) {
-      for (int i = tid; i < NLINE; i += NT) {
-        const int X = i % CX, Y = i / CX;
-        if (X < hiX && Y < hiY)
-          cp_async8(zs + X + ZS1 * Y,
-                    q + gel(X / P, Y / P, z_begin - 1) * P3 + (X % P) + P * ((Y % P) + P * (P - 1)));
-      }
-    }
-  } else {
-    load_planes(zw, 0, 1);
-  }
-  cp_async_commit();
-  set_layer(z_begin);
-  load_q(0, z_begin);
-  cp_async_commit();
-  load_component<P, TX, TY, 1, NT, 0>(a, ti, bufX);
-  load_component<P, TX, TY, 1, NT, 1>(a, ti, bufY);
-  load_planes(zl, (long long)z_begin * P + 1, P);
-  cp_async_commit();
-  cp_async_wait_group<3>();
-  __syncthreads();
-  // carry-in of the shared bottom plane of the chunk
-  double carry[JL], qprev[JL];
-  {
-    const int np = below ? P + 1 : 1;
-    // raw bottom plane of the chunk (for D u of its first cell layer)
-    const double* rawbot = zw + (below ? P : 0) * ZS2;
-    for (int i = tid; i < ZS2; i += NT) zr[i] = rawbot[i];
-    __syncthreads();
-    // M_h (x) M_h on the loaded planes: I-lines (lanes over J rows), then J-lines
-    hpass<P, NT>(zw, zw, tab.Mh, CY, ZS1, np, ZS2, TX, P, 1);
-    __syncthreads();
-    hpass<P, NT>(zw, zw, tab.Mh, CX, 1, np, ZS2, TY, P * ZS1, ZS1);
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < JL; ++j) {
-      carry[j] = 0.0;
-      qprev[j] = 0.0;
-      const int ln = tid + j * NT;
-      if (ln < NLINE && below) {
-        const int I = ln % CX, J = ln / CX;
-        double* col = zw + I + ZS1 * J;
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k <= P; ++k) s = fma(tab.Ml[P][k], col[k * ZS2], s);
-        const double cz = QCO(0)[4 * ((J / P + 1) * (TX + 1) + I / P + 1) + 2];
-        carry[j] = cz * s;
-        col[0] = col[P * ZS2];                 // transformed shared plane -> plane 0
-        if (BLOCK) qprev[j] = zs[I + ZS1 * J];
-      }
-    }
-  }
-  __syncthreads();
-
-  double acc[O::NACC];
-  // ---------------- layers ----------------
-  for (int ez = z_begin; ez < z_end; ++ez) {
-    const int cb = (ez - z_begin) & 1;
-    const bool more = ez + 1 < z_end;
-    set_layer(ez);
-#pragma unroll
-    for (int k = 0; k < O::NACC; ++k) acc[k] = 0.0;
-    // prefetch Q of the next layer into the other buffer
-    if (more) load_q(cb ^ 1, ez + 1);
-    cp_async_commit();
-    cp_async_wait_group<3>();
-    __syncthreads();
-    double* sq = QSQ(cb);
-    double* sco = QCO(cb);
-    // x component; then prefetch x of the next layer
-    component<P, TX, TY, 1, NT, 0, BLOCK>(a, ti, tab, bufX, sq, QH0(cb), sco, acc);
-    if (more) {
-      set_layer(ez + 1);
-      load_component<P, TX, TY, 1, NT, 0>(a, ti, bufX);
-      set_layer(ez);
-    } else {
-      cp_async_commit();
-    }
-    cp_async_wait_group<3>();
-    __syncthreads();
-    component<P, TX, TY, 1, NT, 1, BLOCK>(a, ti, tab, bufY, sq, QH1(cb), sco, acc);
-    if (more) {
-      set_layer(ez + 1);
-      load_component<P, TX, TY, 1, NT, 1>(a, ti, bufY);
-      set_layer(ez);
-    } else {
-      cp_async_commit();
-    }
-    cp_async_wait_group<3>();
-    __syncthreads();
-    // ---- z component of this layer ----
-    if constexpr (BLOCK) {   // D u, z faces: planes 0 (zr) .. P (zl[P-1])
-#pragma unroll
-      for (int j = 0; j < O::JC; ++j) {
-        const int col = tid + j * NT;
-        if (col < O::NCOL) {
-          const int o = (col % CX) + ZS1 * (col / CX);
-          double lo = zr[o];
-#pragma unroll
-          for (int c = 0; c < P; ++c) {
-            const double hi = zl[o + c * ZS2];
-            acc[j * P + c] += hi - lo;
-            lo = hi;
-          }
-        }
-      }
-    }
-    // M_h along I: zl -> zw planes 1..P (lanes over J rows, odd stride)
-    hpass<P, NT>(zl, zw + ZS2, tab.Mh, CY, ZS1, P, ZS2, TX, P, 1);
-    __syncthreads();
-    for (int i = tid; i < ZS2; i += NT) zr[i] = zl[(P - 1) * ZS2 + i];   // raw top plane
-    hpass<P, NT>(zw + ZS2, zw + ZS2, tab.Mh, CX, 1, P, ZS2, TY, P * ZS1, ZS1);
-    __syncthreads();
-    if (more) load_planes(zl, (long long)(ez + 1) * P + 1, P);
-    cp_async_commit();
-    // c_z M_l along K with the carried plane sum, + D^T q~, stores; plane P -> plane 0
-    {
-      const bool top = (ez + 1 == NLz);
-      const long long K0 = (long long)ez * P;
-#pragma unroll
-      for (int j = 0; j < JL; ++j) {
-        const int ln = tid + j * NT;
-        if (ln >= NLINE) continue;
-        const int I = ln % CX, J = ln / CX;
-        double* col = zw + I + ZS1 * J;
-        double v[P + 1];
-#pragma unroll
-        for (int k = 0; k <= P; ++k) v[k] = col[k * ZS2];
-        const double cz = sco[4 * ((TY + 1) * (TX + 1) + (J / P + 1) * (TX + 1) + I / P + 1) + 2];
-        const bool ok = I < hiX && J < hiY;
-        double* g = a.y + zorg + I + nx * J + K0 * nxy;
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k <= P; ++k) s = fma(tab.Ml[i][k], v[k], s);
-          double o = (i == 0) ? fma(cz, s, carry[j]) : cz * s;
-          if constexpr (BLOCK) {
-            const double qc = sq[I + ZS1 * J + ZS2 * i];
-            o += qprev[j] - qc;
-            qprev[j] = qc;
-          }
-          if (ok) __stcs(g + i * nxy, o);
-        }
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k <= P; ++k) s = fma(tab.Ml[P][k], v[k], s);
-        carry[j] = cz * s;
-        col[0] = v[P];
-        if (top && ok) __stcs(g + P * nxy, carry[j] + (BLOCK ? qprev[j] : 0.0));
-      }
-    }
-    if constexpr (BLOCK) {
-      if (a.has_z()) {   // -Z q~ of this layer: M_h^-1 along I, J (planes) and K (cells)
-        hpass<P, NT>(sq, zs, tab.Mhinv, CY, ZS1, P, ZS2, TX, P, 1);
-        __syncthreads();
-        hpass<P, NT>(zs, zs, tab.Mhinv, CX, 1, P, ZS2, TY, P * ZS1, ZS1);
-        __syncthreads();
-        hpass<P, NT>(zs, zs, tab.Mhinv, CX, 1, CY, ZS1, 1, 0, ZS2);
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < O::JC; ++j) {
-          const int col = tid + j * NT;
-          if (col < O::NCOL) {
-            const int X = col % CX, Y = col / CX;
-            const double z = sco[4 * ((TY + 1) * (TX + 1) + (Y / P + 1) * (TX + 1) + X / P + 1) + 3];
-            const double* s = zs + X + ZS1 * Y;
-#pragma unroll
-            for (int c = 0; c < P; ++c) acc[j * P + c] -= z * s[c * ZS2];
-          }
-        }
-      }
-      // y_q of this layer straight from the accumulators
-      double* yq = a.y + a.nrt;
-#pragma unroll
-      for (int j = 0; j < O::JC; ++j) {
-        const int col = tid + j * NT;
-        if (col < O::NCOL) {
-          const int X = col % CX, Y = col / CX;
-          if (X < hiX && Y < hiY) {
-            double* yc = yq + gel(X / P, Y / P, ez) * P3 + (X % P) + P * (Y % P);
-#pragma unroll
-            for (int c = 0; c < P; ++c) __stcs(yc + P * P * c, acc[j * P + c]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  cp_async_wait_all();
-}
-
-template <int P, int TX, int TY, int NT, bool BLOCK>
-cudaError_t launch_m(const hdiv_ctx* h, const double* x, double* y, const int* skip,
-                     cudaStream_t s) {
-  using M = MG<P, TX, TY>;
-  AffArgs a;
-  a.x = x; a.y = y; a.coef = h->d_coef;
-  for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
-  a.nrt = h->nrt;
-  a.ntile[0] = (int)((h->NL[0] + TX - 1) / TX);
-  a.ntile[1] = (int)((h->NL[1] + TY - 1) / TY);
-  // z chunk: 32 layers (r01 sweep), shortened when that leaves fewer than ~4 CTAs per SM
-  const long long cols = (long long)a.ntile[0] * a.ntile[1];
-  int zc = 32;
-  while (zc > 4 && cols * ((h->NL[2] + zc - 1) / zc) < 148LL * 4) zc /= 2;
-  const char* e = getenv("HDIV_ZCHUNK");
-  if (e) zc = atoi(e);
-  if (zc > h->NL[2]) zc = (int)h->NL[2];
-  a.ntile[2] = (int)((h->NL[2] + zc - 1) / zc);
-  a.flags = h->has_z ? 1 : 0;   // the marching kernel: no eliminated sides, no z-chunking
-  a.skip = skip;
-  const size_t smem = M::smem_doubles(BLOCK) * sizeof(double);
-  auto kern = affine_march_kernel<P, TX, TY, NT, BLOCK>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-    if (err != cudaSuccess) return err;
-    attr_done = true;
-  }
-  const long long nblk = cols * a.ntile[2];
-  count_op();
-  kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff, zc);
-  return cudaGetLastError();
-}
-
-// Tile shapes per order; variant 0 is the default, HDIV_AFFINE_TILE=<k> selects another (tuning).
-// halo-tile shape per order (r01 sweeps, profiles/): HDIV_AFFINE_TILE overrides
-static int tile_variant(int p) {
-  const char* e = getenv("HDIV_AFFINE_TILE");
-  if (e) return atoi(e);
-  // r01 sweeps with the generated layouts (profiles/r01_variant_sweep_v*.txt): single-buffered
-  // tiles (more CTAs per SM) win at p = 3..6, double-buffered at p = 1, 2; at p = 5, 6 the x
-  // component is written back through shared memory (coalesced copy-out), at p = 3 a
-  // 160-thread CTA owns one cell column per thread
-  // p = 5: a 3x2x2 tile (less halo, modelled 0.706 -> 0.644 wavefronts/DOF), 160 threads:
-  // 2.245 -> 2.160 ms at N = 96 (4x3x2 at p = 4 and 5x4x2 at p = 3 were slower)
-  // p = 6: 3x2x2, 224 threads: 2.556 -> 2.494 ms at N = 80
-  return (p == 3) ? 7 : (p == 4) ? 4 : (p == 5 || p == 6) ? 12 : 0;
-}
-
-// The z-marching kernel is correct at every order but no longer the fastest anywhere (same
-// sweep); HDIV_MARCH_TILE >= 0 selects a marching variant, -1 (default) the halo tiles.
-static int march_variant(int p) {
-  const char* e = getenv("HDIV_MARCH_TILE");
-  if (e) return atoi(e);
-  (void)p;
-  return -1;
+// one production tile per order (r01 sweeps, profiles/r01_variant_sweep_v*.txt): TXxTYxTZ
+// elements, NT threads, DB = double-buffered component boxes (p <= 2; single-buffered tiles
+// give more CTAs per SM at p >= 3), MINB = __launch_bounds__ min blocks, XD = x planes stored
+// straight from the line pass (else written back and copied out coalesced, p = 5, 6).
+// Eliminated essential sides use an instantiation of their own (ESS).
+template <bool BLOCK, int P, int TX, int TY, int TZ, int NT, bool DB, int MINB, bool XD>
+cudaError_t launch_tile(const hdiv_ctx* h, const double* x, double* y, const int* k,
+                        cudaStream_t s) {
+  if (h->ess) return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, true>(h, x, y, k, s);
+  return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, false>(h, x, y, k, s);
 }
 
 template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
                      cudaStream_t s) {
-  const int mv = march_variant(h->p);
-  const bool ranged = g_range.tz_out != nullptr || g_range.tz1 >= 0 || g_range.tz0 != 0;
-  if (mv >= 0 && !h->ess && !ranged) {
-    switch (h->p) {
-      case 1: return launch_m<1, 8, 8, 128, BLOCK>(h, x, y, k, s);
-      case 2:
-        if (mv == 1) return launch_m<2, 8, 8, 128, BLOCK>(h, x, y, k, s);
-        return launch_m<2, 8, 4, 128, BLOCK>(h, x, y, k, s);
-      case 3:
-        if (mv == 1) return launch_m<3, 4, 4, 128, BLOCK>(h, x, y, k, s);
-        return launch_m<3, 8, 4, 128, BLOCK>(h, x, y, k, s);
-      case 4:
-        if (mv == 1) return launch_m<4, 4, 4, 128, BLOCK>(h, x, y, k, s);
-        return launch_m<4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      case 5:
-        if (mv == 1) return launch_m<5, 2, 2, 128, BLOCK>(h, x, y, k, s);
-        return launch_m<5, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      case 6:
-        if (mv == 1) return launch_m<6, 2, 2, 128, BLOCK>(h, x, y, k, s);
-        return launch_m<6, 4, 2, 128, BLOCK>(h, x, y, k, s);
-    }
-    return cudaErrorInvalidValue;
-  }
-  // halo-tile variants: 0..3 double-buffered shapes, 4/5 single-buffered (more CTAs per SM),
-  // 6/7 other CTA sizes, 8/9 register caps (__launch_bounds__ min blocks), 10 x copy-out
-  if (h->ess) {   // eliminated essential sides: one instantiation per order (default tiles)
-    switch (h->p) {
-      case 1: return launch_t<1, 8, 8, 4, 128, BLOCK, true, 0, kXDirect, true>(h, x, y, k, s);
-      case 2: return launch_t<2, 8, 4, 4, 128, BLOCK, true, 0, kXDirect, true>(h, x, y, k, s);
-      case 3: return launch_t<3, 4, 4, 2, 160, BLOCK, false, 0, kXDirect, true>(h, x, y, k, s);
-      case 4: return launch_t<4, 4, 2, 2, 128, BLOCK, false, 0, kXDirect, true>(h, x, y, k, s);
-      case 5: return launch_t<5, 3, 2, 2, 160, BLOCK, false, 0, false, true>(h, x, y, k, s);
-      case 6: return launch_t<6, 3, 2, 2, 224, BLOCK, false, 2, false, true>(h, x, y, k, s);
-    }
-    return cudaErrorInvalidValue;
-  }
-  const int v = tile_variant(h->p);
   switch (h->p) {
-    case 1: return launch_t<1, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
-    case 2:
-      if (v == 1) return launch_t<2, 8, 8, 4, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<2, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
-      if (v == 4) return launch_t<2, 8, 4, 4, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 6) return launch_t<2, 8, 8, 4, 256, BLOCK>(h, x, y, k, s);
-      return launch_t<2, 8, 4, 4, 128, BLOCK>(h, x, y, k, s);
-    case 3:
-      if (v == 1) return launch_t<3, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<3, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 4) return launch_t<3, 8, 4, 2, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 6) return launch_t<3, 8, 4, 2, 288, BLOCK, false>(h, x, y, k, s);
-      if (v == 7) return launch_t<3, 4, 4, 2, 160, BLOCK, false>(h, x, y, k, s);
-      if (v == 8) return launch_t<3, 8, 4, 2, 128, BLOCK, false, 6>(h, x, y, k, s);
-      if (v == 10) return launch_t<3, 4, 4, 2, 160, BLOCK, false, 0, false>(h, x, y, k, s);
-      return launch_t<3, 8, 4, 2, 128, BLOCK>(h, x, y, k, s);
-    case 4:
-      if (v == 1) return launch_t<4, 4, 4, 4, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<4, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 3) return launch_t<4, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 4) return launch_t<4, 4, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 5) return launch_t<4, 4, 4, 2, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 6) return launch_t<4, 4, 4, 2, 256, BLOCK, false>(h, x, y, k, s);
-      if (v == 7) return launch_t<4, 2, 2, 2, 64, BLOCK, false>(h, x, y, k, s);
-      if (v == 8) return launch_t<4, 4, 2, 2, 128, BLOCK, false, 8>(h, x, y, k, s);
-      if (v == 9) return launch_t<4, 4, 2, 2, 128, BLOCK, false, 7>(h, x, y, k, s);
-      if (v == 10) return launch_t<4, 4, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
-      return launch_t<4, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
-    case 5:
-      if (v == 1) return launch_t<5, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<5, 4, 4, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 4) return launch_t<5, 2, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 5) return launch_t<5, 4, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 6) return launch_t<5, 4, 2, 2, 224, BLOCK, false>(h, x, y, k, s);
-      if (v == 7) return launch_t<5, 2, 2, 1, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 8) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 6>(h, x, y, k, s);
-      if (v == 9) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 5>(h, x, y, k, s);
-      if (v == 10) return launch_t<5, 2, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
-      if (v == 11) return launch_t<5, 3, 2, 2, 128, BLOCK, false, 0, false>(h, x, y, k, s);
-      if (v == 12) return launch_t<5, 3, 2, 2, 160, BLOCK, false, 0, false>(h, x, y, k, s);
-      return launch_t<5, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
-    case 6:
-      if (v == 1) return launch_t<6, 4, 2, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 2) return launch_t<6, 2, 2, 2, 128, BLOCK>(h, x, y, k, s);
-      if (v == 4) return launch_t<6, 2, 2, 1, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 5) return launch_t<6, 2, 2, 2, 128, BLOCK, false>(h, x, y, k, s);
-      if (v == 6) return launch_t<6, 2, 2, 2, 160, BLOCK, false>(h, x, y, k, s);
-      if (v == 7) return launch_t<6, 4, 2, 2, 288, BLOCK, false>(h, x, y, k, s);
-      if (v == 8) return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3>(h, x, y, k, s);
-      if (v == 10) return launch_t<6, 2, 2, 2, 160, BLOCK, false, 3, false>(h, x, y, k, s);
-      if (v == 12) return launch_t<6, 3, 2, 2, 224, BLOCK, false, 2, false>(h, x, y, k, s);
-      if (v == 9) return launch_t<6, 2, 2, 2, 128, BLOCK, false, 4>(h, x, y, k, s);
-      return launch_t<6, 2, 2, 1, 128, BLOCK>(h, x, y, k, s);
+    case 1: return launch_tile<BLOCK, 1, 8, 8, 4, 128, true, 0, kXDirect>(h, x, y, k, s);
+    case 2: return launch_tile<BLOCK, 2, 8, 4, 4, 128, true, 0, kXDirect>(h, x, y, k, s);
+    case 3: return launch_tile<BLOCK, 3, 4, 4, 2, 160, false, 0, kXDirect>(h, x, y, k, s);
+    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, 0, kXDirect>(h, x, y, k, s);
+    case 5: return launch_tile<BLOCK, 5, 3, 2, 2, 160, false, 0, false>(h, x, y, k, s);
+    case 6: return launch_tile<BLOCK, 6, 3, 2, 2, 224, false, 2, false>(h, x, y, k, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -78,19 +78,13 @@ def _problem(name, N, p):
     return pr
 
 
-# box-kernel variants: z-marching with forced chunk boundaries, and the halo-tile kernel
-VARIANTS = [("c2", (5, 3, 7), 4, {"HDIV_ZCHUNK": "2"}), ("c2", (3, 5, 5), 3, {"HDIV_ZCHUNK": "1"}),
-            ("c2", (5, 4, 6), 2, {"HDIV_ZCHUNK": "4"}), ("c2", (3, 3, 5), 5, {"HDIV_ZCHUNK": "2"}),
-            ("c2", (3, 3, 4), 6, {"HDIV_ZCHUNK": "3"}), ("c2", (9, 5, 5), 1, {"HDIV_ZCHUNK": "2"}),
-            ("c5", (5, 5, 6), 3, {"HDIV_ZCHUNK": "2"}),
-            ("c2", (5, 3, 3), 4, {"HDIV_MARCH_TILE": "-1"}), ("c2", (5, 3, 3), 4, {"HDIV_MARCH_TILE": "1"}),
-            ("c2", (3, 5, 3), 6, {"HDIV_MARCH_TILE": "1", "HDIV_ZCHUNK": "2"}),
-            # generated layouts with packed lane maps, other CTA sizes, register caps, x copy-out
-            ("c2", (9, 5, 3), 3, {"HDIV_AFFINE_TILE": "7"}), ("c2", (9, 5, 3), 3, {"HDIV_AFFINE_TILE": "6"}),
-            ("c2", (5, 3, 3), 4, {"HDIV_AFFINE_TILE": "9"}), ("c2", (5, 5, 3), 4, {"HDIV_AFFINE_TILE": "10"}),
-            ("c2", (5, 3, 3), 5, {"HDIV_AFFINE_TILE": "10"}), ("c5", (5, 5, 3), 5, {"HDIV_AFFINE_TILE": "6"}),
-            ("c2", (3, 3, 3), 6, {"HDIV_AFFINE_TILE": "10"}), ("c2", (3, 3, 5), 6, {"HDIV_AFFINE_TILE": "8"}),
-            ("c2", (5, 3, 3), 6, {"HDIV_AFFINE_TILE": "7"}), ("c2", (9, 9, 5), 2, {"HDIV_AFFINE_TILE": "6"})]
+# box kernel (one production tile per order): ragged tiles on every axis, single-element meshes,
+# graded two-material meshes
+VARIANTS = [("c2", (5, 3, 7), 4, {}), ("c2", (4, 6, 4), 3, {}), ("c2", (6, 4, 6), 5, {}),
+            ("c2", (5, 4, 6), 2, {}), ("c2", (3, 3, 4), 6, {}), ("c2", (9, 5, 5), 1, {}),
+            ("c2", (10, 10, 6), 1, {}), ("c2", (9, 9, 5), 2, {}), ("c5", (5, 5, 6), 3, {}),
+            ("c5", (6, 6, 4), 5, {}), ("c5", (5, 5, 3), 6, {}), ("c2", (1, 1, 1), 4, {}),
+            ("c2", (1, 2, 1), 5, {}), ("c2", (2, 1, 1), 6, {})]
 
 
 @pytest.mark.parametrize("name,N,p,env", VARIANTS)
