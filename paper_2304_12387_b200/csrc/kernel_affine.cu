@@ -172,27 +172,47 @@ __device__ __forceinline__ void rows(GT* gbase, long long ext0, long long ext01,
   }
 }
 
-// Element-local contraction with a P x P matrix along one axis, dst <- M src (may alias).
-// Element k of line (i0, i1, blk) lives at off + i0*s0 + i1*s1 + blk*sb + k*se; lanes run
-// over i0 first.
-template <int P, int NT>
-__device__ __forceinline__ void hpass(const double* src, double* dst, const double (*M)[MAXP],
-                                      int n0, int s0, int n1, int s1, int nb, int sb, int se) {
-  const int total = n0 * n1 * nb;
-#pragma unroll 2
-  for (int it = threadIdx.x; it < total; it += NT) {
-    const int i0 = it % n0, r = it / n0, i1 = r % n1, blk = r / n1;
-    const int o = i0 * s0 + i1 * s1 + blk * sb;
-    double v[P];
+// X- and Y-lines of (M_h^-1)^{(x)2} on the q~ tile in one register-blocked pass: a thread owns
+// the P x P (X, Y) block of one element column at one cell layer Z (lanes over Z first; the
+// element columns of consecutive item groups in the order of the layout's zmap), reads it from
+// src once, contracts along X then Y (the order of two separate line passes: same arithmetic)
+// and writes it to dst once
+template <int P, int TX, int TY, int TZ, int NT>
+__device__ __forceinline__ void z_xy_block(const double* src, double* dst, const double (*Mi)[MAXP]) {
+  using G = Geo<P, TX, TY, TZ>;
+  constexpr int LI = find_tile_layout(P, TX, TY, TZ);
+  constexpr int ZMAP = LI >= 0 ? kTileLayouts[LI].zmap : 0;
+  constexpr int CZ = G::CZ;
+  constexpr int NIT = CZ * TX * TY;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < NIT; it += NT) {
+    const int zc = it % CZ, b = it / CZ;
+    const int by = b / TX, r = b % TX;
+    const int bx = (ZMAP == 1 && TX % 2 == 0) ? (r / 2) + (r % 2) * (TX / 2) : r;
+    const int o = bx * P + G::Q1 * (by * P) + G::Q2 * zc;
+    double w[P][P];
 #pragma unroll
-    for (int k = 0; k < P; ++k) v[k] = src[o + k * se];
+    for (int k2 = 0; k2 < P; ++k2) {
+      double v[P];
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-      double t = 0.0;
+      for (int k1 = 0; k1 < P; ++k1) v[k1] = src[o + k1 + G::Q1 * k2];
 #pragma unroll
-      for (int j = 0; j < P; ++j) t = fma(M[i][j], v[j], t);
-      dst[o + i * se] = t;
+      for (int i = 0; i < P; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) t = fma(Mi[i][j], v[j], t);
+        w[k2][i] = t;
+      }
     }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1)
+#pragma unroll
+      for (int k2 = 0; k2 < P; ++k2) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) t = fma(Mi[k2][j], w[j][k1], t);
+        dst[o + k1 + G::Q1 * k2] = t;
+      }
   }
 }
 
@@ -552,9 +572,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     if (a.has_z()) {
       // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in B (subcell-major like sq):
       // X-lines (lanes over Y, odd stride Q1; sq -> B), then Y- and Z-lines (lanes over X)
-      hpass<P, NT>(sq, bufB, tab.Mhinv, G::CY, G::Q1, G::CZ, G::Q2, TX, P, 1);
-      __syncthreads();
-      hpass<P, NT>(bufB, bufB, tab.Mhinv, G::CX, 1, G::CZ, G::Q2, TY, P * G::Q1, G::Q1);
+      z_xy_block<P, TX, TY, TZ, NT>(sq, bufB, tab.Mhinv);
       __syncthreads();
       // Z-lines in registers: every thread owns whole z-columns of cells
 #pragma unroll

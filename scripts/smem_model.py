@@ -48,8 +48,9 @@ def run(NT, items, naccess, addr, acc=None, distinct_k=True):
 
 
 class Layout:
-    def __init__(self, P, T, S=None, Q=None, padL=None, padA=None):
+    def __init__(self, P, T, S=None, Q=None, padL=None, padA=None, zmap=0):
         self.P, self.T = P, T
+        self.zmap = zmap
         CX, CY, CZ = (t * P for t in T)
         self.C = (CX, CY, CZ)
         self.E = []
@@ -157,6 +158,16 @@ def comp_cost(L, AX, NT=128):
     return out
 
 
+def zblock(b, TX, zmap):
+    """element column (bx, by) of item group b in the Z xy-block pass: zmap 0 = bx fastest;
+    1 = bx split in halves interleaved (0, TX/2, 1, TX/2+1, ...: consecutive item groups are
+    TX/2 element columns apart), for even TX"""
+    by, r = b // TX, b % TX
+    if zmap == 1 and TX % 2 == 0:
+        return (r // 2) + (r % 2) * (TX // 2), by
+    return r, by
+
+
 def q_cost(L, NT=128):
     P, T = L.P, L.T
     CX, CY, CZ = L.C
@@ -171,9 +182,15 @@ def q_cost(L, NT=128):
             i1, blk = r % n1, r // n1
             return i0 * s0 + i1 * s1 + blk * sb
         return f
-    out["Z x-lines"] = run(NT, CY * CZ * T[0], 2 * P, hp(CY, Q1, CZ, Q2, T[0], P), distinct_k=False)
-    out["Z y-lines"] = run(NT, CX * CZ * T[1], 2 * P, hp(CX, 1, CZ, Q2, T[1], P * Q1),
-                           distinct_k=False)
+    # the X- and Y-lines of (M_h^-1)^{(x)2} as ONE register-blocked pass: a thread owns the
+    # P x P (X, Y) block of one element column at one cell layer Z (lanes over Z first) and
+    # reads / writes it once
+    def z2(it, k):
+        zc, b = it % CZ, it // CZ
+        bx, by = zblock(b, T[0], L.zmap)
+        kk = k % (P * P)
+        return bx * P + Q1 * by * P + Q2 * zc + (kk % P) + Q1 * (kk // P)
+    out["Z xy-block"] = run(NT, CZ * T[0] * T[1], 2 * P * P, z2, distinct_k=False)
     out["Z z-lines"] = run(NT, CX * CY, CZ, lambda col, k: col % CX + Q1 * (col // CX),
                            distinct_k=False)
     return out
@@ -199,16 +216,19 @@ def search(P, T, slack=16, smem_growth=1.10):
     CX, CY, CZ = base.C
     # q~ strides
     bestq = None
-    for q1 in range(CX, CX + slack):
-        for q2 in range(q1 * CY, q1 * CY + slack):
-            L = Layout(P, T, Q=(q1, q2))
-            if q2 * CZ > su0 * smem_growth:
-                continue
-            c = sum(q_cost(L).values())
-            for AX in range(3):
-                c += comp_cost(L, AX)["Ml q"]
-            if bestq is None or c < bestq[0]:
-                bestq = (c, (q1, q2))
+    # the q~ tile is extra shared memory (not overlaid on the component boxes): keep it within
+    # a few words of the odd-padded minimum so CTAs per SM do not drop
+    for q1 in range(CX, odd(CX) + 3):
+        for q2 in range(q1 * CY, q1 * odd(CY) + slack):
+            for zm in (0, 1):
+                L = Layout(P, T, Q=(q1, q2), zmap=zm)
+                if q2 * CZ > su0 * smem_growth:
+                    continue
+                c = sum(q_cost(L).values())
+                for AX in range(3):
+                    c += comp_cost(L, AX)["Ml q"]
+                if bestq is None or c < bestq[0]:
+                    bestq = (c, (q1, q2), zm)
     S, padL, padA = [], [], []
     for AX in range(3):
         E = base.E[AX]
@@ -221,13 +241,14 @@ def search(P, T, slack=16, smem_growth=1.10):
                     for pa in (True, False):
                         Sx = list(base.S)
                         Sx[AX] = (s1, s2)
-                        L = Layout(P, T, S=Sx, Q=bestq[1], padL=[pl] * 3, padA=[pa] * 3)
+                        L = Layout(P, T, S=Sx, Q=bestq[1], padL=[pl] * 3, padA=[pa] * 3,
+                                   zmap=bestq[2])
                         cc = comp_cost(L, AX)
                         c = sum(v for k, v in cc.items() if k != "Ml q") + cc["Ml q"]
                         if bc is None or c < bc[0]:
                             bc = (c, (s1, s2), pl, pa)
         S.append(bc[1]); padL.append(bc[2]); padA.append(bc[3])
-    return Layout(P, T, S=S, Q=bestq[1], padL=padL, padA=padA)
+    return Layout(P, T, S=S, Q=bestq[1], padL=padL, padA=padA, zmap=bestq[2])
 
 
 def report(L, title):
