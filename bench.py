@@ -222,33 +222,90 @@ def time_applies(op, x, y, steps, warmup, dist, torch):
     return ms
 
 
-def cpu_baseline(pr, budget_s: float = 15.0):
-    """Time the oracle (as it stands) on a bounded sample of the workload's elements."""
+def _oracle_sample_worker(job):
+    """One host process of the parallel oracle sample (BLAS pinned to one thread)."""
+    cfg, p, elems, budget_s = job
+    from threadpoolctl import threadpool_limits
     import numpy as np
     from oracle import sample
-    from synth import random_vector
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count() or 1
+    pr = make_problem(cfg, p)
+    n = pr.n_rt() + pr.n_l2()
+    x = np.zeros(n)   # only the sampled elements' entries matter for the timing
+    done = 0
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < budget_s and done < len(elems):
+            sample.element_apply(pr, x, elems[done:done + 8])
+            done += 8
+        dt = time.perf_counter() - t0
+    return done, dt
+
+
+def cpu_baseline(pr, budget_s: float = 15.0, cfg: str = "c4", parallel: bool = True):
+    """The oracle (as it stands) on a bounded sample of the workload's elements: element matrices
+    by direct quadrature + multiply, scaled to whole-apply DOFs.  Honest core accounting: one
+    process with BLAS pinned to 1 thread (cores = 1), and the same element loop split over all
+    host cores (one process per core, each with 1 BLAS thread) -> cores = #processes."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import sample
     n = pr.n_rt() + pr.n_l2()
     E = pr.E
-    x = random_vector(n, 9) if n < 2e8 else None
-    if x is None:   # only the sampled elements' entries are touched; use a cheap stand-in
-        x = np.zeros(n)
+    x = np.zeros(n)
     rng = np.random.default_rng(0)
     elems = rng.integers(0, E, 100000)
+    one_budget = budget_s / 2 if parallel else budget_s
     t0 = time.perf_counter()
     done = 0
-    while time.perf_counter() - t0 < budget_s and done < len(elems):
-        sample.element_apply(pr, x, elems[done:done + 8])
-        done += 8
+    with threadpool_limits(1):
+        while time.perf_counter() - t0 < one_budget and done < len(elems):
+            sample.element_apply(pr, x, elems[done:done + 8])
+            done += 8
     dt = time.perf_counter() - t0
-    dofs = n * done / E
-    return {"value": dofs / dt / 1e9, "unit": "GDOF/s", "cores": int(cores), "kind": "oracle",
-            "sample": f"{done} of {E} elements of {pr.name} p={pr.p} (element matrices by "
-                      f"direct quadrature + multiply), {dt:.1f} s, scaled to whole-apply DOFs"}
+    v1 = n * done / E / dt / 1e9
+    out = {"value": v1, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
+           "sample": f"{done} of {E} elements of {pr.name} p={pr.p} (element matrices by direct "
+                     f"quadrature + multiply), {dt:.1f} s on 1 thread, scaled to whole-apply DOFs",
+           "single_thread_value": v1}
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    ncpu = min(ncpu, 32)
+    if parallel and ncpu > 1:
+        import multiprocessing as mp
+        jobs = [(cfg, pr.p, rng.integers(0, E, 20000), budget_s / 2) for _ in range(ncpu)]
+        t1 = time.perf_counter()
+        with mp.get_context("spawn").Pool(ncpu) as pool:
+            res = pool.map(_oracle_sample_worker, jobs)
+        wall = time.perf_counter() - t1
+        tot = sum(r[0] for r in res)
+        busy = max(r[1] for r in res)
+        vp = n * tot / E / busy / 1e9
+        out.update({"value": vp, "cores": ncpu,
+                    "sample": f"{tot} of {E} elements of {pr.name} p={pr.p} over {ncpu} processes "
+                              f"x 1 BLAS thread ({busy:.1f} s each, {wall:.1f} s wall incl. "
+                              f"spawn); 1 thread alone: {v1:.3g} GDOF/s; element matrices by "
+                              f"direct quadrature + multiply, scaled to whole-apply DOFs"})
+    return out
+
+
+def oracle_minres(name: str):
+    """The oracle's MINRES (reading A8/A10: Chebyshev-Jacobi S^-1) on a full config, one
+    thread: setup (dense element matrices, assembly, S~) and time-to-solve, rtol 1e-12."""
+    from threadpoolctl import threadpool_limits
+    from oracle import operators, solvers
+    from synth import make_config, random_vector
+    pr = make_config(name)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        A = operators.Assembled(pr)
+        P = solvers.BlockDiagPrecond(A)
+        t1 = time.perf_counter()
+        n = A.n_rt + A.n_l2
+        b = A.apply_block(random_vector(n, 2 if name == "c2" else 1))
+        t2 = time.perf_counter()
+        _, it, conv, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=5000)
+        t3 = time.perf_counter()
+    return {"iters": it, "converged": bool(conv), "setup_s": t1 - t0, "time_to_solve_s": t3 - t2,
+            "cores": 1, "dofs": n}
 
 
 def run_reference(args, ws, rank):
@@ -261,8 +318,9 @@ def run_reference(args, ws, rank):
     if args.ref_seconds is not None:
         per_step_budget = args.ref_seconds
     for _ in range(args.warmup):
-        cpu_baseline(pr, budget_s=min(1.0, per_step_budget))
-    vals = [cpu_baseline(pr, budget_s=per_step_budget) for _ in range(args.steps)]
+        cpu_baseline(pr, budget_s=min(1.0, per_step_budget), cfg=args.config, parallel=False)
+    vals = [cpu_baseline(pr, budget_s=per_step_budget, cfg=args.config)
+            for _ in range(args.steps)]
     v = sorted(x["value"] for x in vals)[len(vals) // 2]
     cb = dict(vals[0])
     cb["value"] = v
@@ -450,6 +508,20 @@ def main():
             op2.close()
             del xs, b
             torch.cuda.empty_cache()
+        # config 1 (2D 4x4, p = 2, Darcy) on the GPU, and the oracle's MINRES on configs 1 and 2
+        # in full, timed beside it on one host thread
+        pr1 = make_config("c1")
+        op1 = from_problem(pr1)
+        xs1 = torch.from_numpy(random_vector(op1.sizes.n, 1)).cuda()
+        b1 = op1.apply_block(xs1)
+        op1.minres(b1, rtol=1e-12, maxit=5000)
+        _, rep1 = op1.minres(b1, rtol=1e-12, maxit=5000)
+        mres["c1_iters"] = rep1.iters
+        mres["c1_time_to_solve_s"] = rep1.t_solve_ms / 1e3
+        op1.close()
+        if not args.no_cpu:
+            for nm in ("c1", "c2"):
+                mres["oracle_" + nm] = oracle_minres(nm)
         mres["preconditioner"] = "diag(tau M~) + Chebyshev-Jacobi(S~), degree 4"
         mres["amg_preconditioner"] = ("diag(tau M~) + one smoothed-aggregation V-cycle on S~ "
                                       "(3^3 aggregates, 2+2 l1-Jacobi sweeps, Galerkin)")

@@ -121,7 +121,7 @@ def element_apply(prob, x, elements):
     n_rt = prob.n_rt()
     u, q = x[:n_rt], x[n_rt:]
     v2f, sig = space.volume_to_face(dim, p)
-    y = np.zeros_like(x)
+    y = np.zeros(x.shape)   # calloc: untouched pages stay unmapped (no full-size memset)
     for e in elements:
         Me, Ze = element_blocks(prob, int(e))
         g = space.rt_local_to_global(dim, N, p, int(e))
