@@ -628,28 +628,43 @@ def main():
         from synth import make_config
         from paper_2304_12387_b200 import from_problem
         pr3 = make_config("c3")
-        op3 = from_problem(pr3)
-        x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
-        y3 = torch.empty_like(x3)
-        ms3 = time_applies(op3, x3, y3, 20, 5, None, torch) / 20
         P3_, Q3_ = pr3.p, pr3.p + 2
         fma = 0
         for c in range(3):   # forward interpolation of component c + its transpose
             E3 = [P3_ + 1 if a == c else P3_ for a in range(3)]
             fma += E3[1] * E3[2] * E3[0] * Q3_ + Q3_ * E3[2] * E3[1] * Q3_ + Q3_ * Q3_ * E3[2] * Q3_
-        flops_el = 2 * 2 * fma + 60 * Q3_ ** 3 + 6 * P3_ ** 3 + 2 * 3 * P3_ ** 2 * (P3_ + 1)
         fp64_peak = 34.116   # measured, profiles/r01_fp64_peak.txt
-        tf = flops_el * pr3.E / (ms3 * 1e-3) / 1e12
+        c3 = {}
+        # tri_geometry 2: the paper's partial assembly (G_q = w_q mw / det J J^T J stored at the
+        # Q^3 points, 48 B each: P:684); 1: J recomputed from the vertices every apply
+        for geo, key in ((2, "stored_geometry"), (1, "on_the_fly_jacobian")):
+            op3 = from_problem(pr3, tri_geometry=geo)
+            x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
+            y3 = torch.empty_like(x3)
+            ms3 = time_applies(op3, x3, y3, 20, 5, None, torch) / 20
+            pw = 18 if geo == 2 else 60   # pointwise flops per point: 3x3 G u | J, det, J^T J u
+            flops_el = 2 * 2 * fma + pw * Q3_ ** 3 + 6 * P3_ ** 3 + 2 * 3 * P3_ ** 2 * (P3_ + 1)
+            tf = flops_el * pr3.E / (ms3 * 1e-3) / 1e12
+            alg = 16 * op3.sizes.n + (48 * Q3_ ** 3 if geo == 2 else 0) * pr3.E
+            c3[key] = {"ms": ms3, "dofs": op3.sizes.n, "GDOF_s": op3.sizes.n / ms3 / 1e6,
+                       "alu": {"achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                               "frac": tf / fp64_peak, "flops_per_element": flops_el},
+                       "hbm": {"alg_bytes_per_launch": alg, "achieved": alg / (ms3 * 1e-3) / 1e9,
+                               "frac": alg / (ms3 * 1e-3) / 1e9 / peak}}
+            op3.close()
+            del x3, y3
+            torch.cuda.empty_cache()
+        best = min(c3, key=lambda k: c3[k]["ms"])
+        b = c3[best]
         result["config3_apply"] = {
             "workload": WORKLOADS["c3"] + " (block apply; gamma = 0: no W^-1)",
-            "dofs": op3.sizes.n, "ms": ms3, "GDOF_s": op3.sizes.n / ms3 / 1e6,
-            "roofline": {"bound": "alu", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": tf / fp64_peak, "flops_per_element": flops_el,
+            "variant": best, "dofs": b["dofs"], "ms": b["ms"],
+            "GDOF_s": b["GDOF_s"],
+            "roofline": {"bound": "alu", "achieved": b["alu"]["achieved"], "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": b["alu"]["frac"],
+                         "flops_per_element": b["alu"]["flops_per_element"],
                          "peak_source": "measured FP64 FMA microbenchmark (scripts/fp64_peak.cu)"},
-            "hbm_frac": 16 * op3.sizes.n / (ms3 * 1e-3) / 1e9 / peak}
-        op3.close()
-        del x3, y3
-        torch.cuda.empty_cache()
+            "hbm_frac": b["hbm"]["frac"], "variants": c3}
         # the same mesh with a nonzero (2,2) block (grad-div, alpha/beta = 10^U(-2,2)): Z by the
         # precomputed explicit element inverses fused into the batched kernel;
         # HBM roofline with the inverses' 8 p^3 B per L2 DOF counted as algorithmic bytes

@@ -105,6 +105,13 @@ typedef struct {
    * coarsest solve pins its last unknown — for the singular pure-Neumann Darcy problem
    * (all sides essential, gamma = 0). */
   int project_mean;
+  /* Trilinear (non-affine) 3D elements, mass / gamma = 0 applies: where the Piola factors
+   * G_q = w_q mw_e / det J_q  J_q^T J_q come from.  0 = auto (stored when they fit: 48 Q^3 B
+   * per element, <= 1/4 of the free memory), 1 = recomputed from the vertices every apply,
+   * 2 = stored at setup (the paper's partial assembly: geometric factors precomputed at the
+   * quadrature points; HDIV_ERR_CUDA if they do not fit).  The block apply
+   * with the explicit W^-1 inverses fused (HBM-bound) always recomputes J. */
+  int tri_geometry;
 } hdiv_options;
 
 enum { HDIV_SCHUR_CHEBYSHEV = 0, HDIV_SCHUR_AMG = 1 };

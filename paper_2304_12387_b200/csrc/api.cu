@@ -132,6 +132,8 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_minv);
   cudaFree(h->d_zcoef);
   cudaFree(h->d_winv);
+  cudaFree(h->d_geo);
+  cudaFree(h->d_rv);
   cudaFree(h->d_gvert);
   amg_free(h);
   gmres_free(h);
@@ -182,6 +184,11 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->opts.amg_max_coarse = (opts && opts->amg_max_coarse > 0) ? opts->amg_max_coarse : 512;
   h->opts.essential_sides = opts ? opts->essential_sides : 0;
   h->opts.project_mean = opts ? (opts->project_mean != 0) : 0;
+  h->opts.tri_geometry = opts ? opts->tri_geometry : 0;
+  if (h->opts.tri_geometry < 0 || h->opts.tri_geometry > 2) {
+    delete h;
+    return fail(HDIV_ERR_SHAPE, "options.tri_geometry must be 0, 1 or 2");
+  }
   if (h->opts.essential_sides < 0 || h->opts.essential_sides >= (1 << (2 * dim))) {
     delete h;
     return fail(HDIV_ERR_SHAPE, "essential_sides: bits 0..2 dim - 1 only");
@@ -449,6 +456,26 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     if (want && bytes <= ((size_t)16 << 30) && bytes <= fr / 4) {
       SETUP_TRY(cudaMalloc(&h->d_winv, bytes));
       SETUP_TRY(build_winv(h, s));
+    }
+  }
+  // stored Piola factors at the quadrature points (partial assembly) for the
+  // trilinear mass / gamma = 0 applies: 48 Q^3 B per element (config 3, p = 4: 2.7 GB)
+  if (dim == 3 && h->geom == GEOM_TRILINEAR && h->kernel == 1 && !gvert && h->opts.tri_geometry != 1) {
+    const size_t bytes = sizeof(double) * 6 * (size_t)h->Q * h->Q * h->Q * (size_t)E;
+    size_t fr = 0, tot = 0;
+    SETUP_TRY(cudaMemGetInfo(&fr, &tot));
+    if (h->opts.tri_geometry == 2 || bytes <= fr / 4) {
+      SETUP_TRY(cudaMalloc(&h->d_geo, bytes));
+      SETUP_TRY(build_tri_geo(h, s));
+    }
+  }
+  // box kernel: rendezvous scratch for the tile-boundary planes (kernel_affine.cu)
+  if (h->kernel == 2) {
+    const char* ev = getenv("HDIV_BOX_RV");
+    if (!(ev && atoi(ev) == 0)) {
+      const size_t b = affine_rv_scratch_bytes(h);
+      SETUP_TRY(cudaMalloc(&h->d_rv, b));
+      SETUP_TRY(cudaMemsetAsync(h->d_rv, 0, b, s));
     }
   }
   SETUP_TRY(launch_mass_diag(h, h->d_mdiag, s));

@@ -46,6 +46,7 @@ struct TriArgs {
   const int* skip;
   const double* winv;   // explicit W^e inverses fused into tri_multi_kernel's y_q store (or nullptr)
   const double* zc;     // {., s_e, ., .} per element (with winv)
+  const double* geo;    // stored quadrature-point factors [E][6][Q^3] (tri_multi_kernel<SG>)
 };
 
 // padded layout of a (D0, D1, D2) array of the order-PP kernel: the strides with the fewest
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
 // passes of RT component c for all EPC elements, so a stage's lines fill the lanes (one element
 // leaves 37 % of them idle at p = 4: 16-24 lines per component and stage) — same arithmetic,
 // same order per output as tri_kernel<P, 96, MODE>.
-template <int P, int EPC, bool BLOCK>
+template <int P, int EPC, bool BLOCK, bool SG = false>
 __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
                                                        const __grid_constant__ Tab1D tab,
                                                        long long E) {
@@ -590,9 +591,10 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
   constexpr int R2 = (3 * T::SA > 3 * T::SV) ? 3 * T::SA : 3 * T::SV;
   constexpr int ES = R1 + R2;   // per-element stride of the stage arrays
   __shared__ double sreg[EPC * ES];
-  __shared__ double sX[EPC][24];
-  __shared__ double sE[EPC][3][4][3];
-  __shared__ double sJ[EPC][3][Q * Q][3];
+  constexpr int EJ = SG ? 1 : EPC;   // Jacobian scratch (on-the-fly variant only)
+  __shared__ double sX[EJ][24];
+  __shared__ double sE[EJ][3][4][3];
+  __shared__ double sJ[EJ][3][Q * Q][3];
   __shared__ double sq[BLOCK ? EPC * T::SL : 1], sy[BLOCK ? EPC * P3 : 1];
   __shared__ double smw[EPC];
   __shared__ int sEc[EPC][4];   // ex, ey, ez, valid
@@ -611,9 +613,16 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
     sEc[tid][3] = ok ? 1 : 0;
     smw[tid] = ok ? a.coef[4 * e] : 0.0;
   }
+  if constexpr (SG) {   // stored factors: pull the CTA's G block toward L2 while the passes run
+    constexpr int NLINE = (EPC * 6 * NQ * 8 + 127) / 128;
+    const char* gb = (const char*)(a.geo + e0 * 6 * NQ);
+    const long long lim = (E - e0) * 6 * NQ * 8;
+    for (int i = tid; i < NLINE; i += NT)
+      if ((long long)i * 128 < lim) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gb + i * 128));
+  }
   __syncthreads();
   // every input lands by cp.async (all loads in flight at once; masked / absent -> 0)
-  for (int i = tid; i < EPC * 24; i += NT) {
+  for (int i = tid; i < (SG ? 0 : EPC * 24); i += NT) {
     const int el = i / 24, v = (i % 24) / 3, d = i % 3;
     const bool ok = sEc[el][3];
     const long long g = ((long long)(sEc[el][2] + (v >> 2)) * (NLy + 1) + (sEc[el][1] + ((v >> 1) & 1))) *
@@ -655,7 +664,7 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
-  for (int i = tid; i < EPC * 36; i += NT) {
+  for (int i = tid; i < (SG ? 0 : EPC * 36); i += NT) {
     const int el = i / 36, j = i % 36;
     const int c = j / 12, k = (j / 3) % 4, d = j % 3;
     const int s1 = k & 1, t1 = k >> 1;
@@ -666,8 +675,8 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
     lo[o1] = hi[o1] = t1;
     sE[el][c][k][d] = sX[el][(hi[0] + 2 * hi[1] + 4 * hi[2]) * 3 + d] - sX[el][(lo[0] + 2 * lo[1] + 4 * lo[2]) * 3 + d];
   }
-  __syncthreads();
-  for (int i = tid; i < EPC * 3 * Q * Q; i += NT) {
+  if constexpr (!SG) __syncthreads();
+  for (int i = tid; i < (SG ? 0 : EPC * 3 * Q * Q); i += NT) {
     const int el = i / (3 * Q * Q), j = i % (3 * Q * Q);
     const int c = j / (Q * Q), pr = j % (Q * Q);
     const double s = tab.xq[pr % Q], t = tab.xq[pr / Q];
@@ -699,8 +708,23 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
   lines_c<NT, 1, Q, Q, P, 2, Q, TB_H, true, typename T::B1, typename T::V, EPC, ES>(sB(1), sV(1), tab);
   lines_c<NT, 2, Q, Q, P + 1, 2, Q, TB_L, true, typename T::B2, typename T::V, EPC, ES>(sB(2), sV(2), tab);
   __syncthreads();
-  // ---- pointwise G_q = w_q mw / det J  J^T J ----
-  for (int i = tid; i < EPC * NQ; i += NT) {
+  // ---- pointwise G_q = w_q mw / det J  J^T J (stored: read from the setup table) ----
+  if constexpr (SG) {
+    for (int i = tid; i < EPC * NQ; i += NT) {
+      const int el = i / NQ, qi = i - (i / NQ) * NQ;
+      if (!sEc[el][3]) continue;
+      const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
+      const double* g = a.geo + (e0 + el) * 6 * NQ + qi;
+      const double g00 = __ldcs(g), g11 = __ldcs(g + NQ), g22 = __ldcs(g + 2 * NQ);
+      const double g01 = __ldcs(g + 3 * NQ), g02 = __ldcs(g + 4 * NQ), g12 = __ldcs(g + 5 * NQ);
+      const int o = el * ES + qx + T::V::S1 * qy + T::V::S2 * qz;
+      const double u0 = sV(0)[o], u1 = sV(1)[o], u2 = sV(2)[o];
+      sV(0)[o] = g00 * u0 + g01 * u1 + g02 * u2;
+      sV(1)[o] = g01 * u0 + g11 * u1 + g12 * u2;
+      sV(2)[o] = g02 * u0 + g12 * u1 + g22 * u2;
+    }
+  }
+  for (int i = tid; i < (SG ? 0 : EPC * NQ); i += NT) {
     const int el = i / NQ, qi = i - (i / NQ) * NQ;
     const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
     const double* c0 = sJ[el][0][qy + Q * qz];
@@ -935,6 +959,7 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.skip = skip;
   a.winv = nullptr;
   a.zc = h->d_zcoef;
+  a.geo = nullptr;
   if constexpr (MODE == 2 && P <= 2) {
     if (!h->d_gvert) {
       count_op();
@@ -949,6 +974,20 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
       if (MODE == 1 && noz && fused && h->d_winv) {   // Z by the stored inverses, in the epilogue
         a.winv = h->d_winv;
         *fused = true;
+      }
+      // stored quadrature-point factors (partial assembly) — not with the fused
+      // explicit W^-1 epilogue: that path is HBM-bound (streaming the inverses), and the 48 Q^3
+      // B per element of G cost more than the Jacobian they save (r02: p = 4 1.97 -> 2.35 ms)
+      if (h->d_geo && !a.winv) {
+        a.geo = h->d_geo;
+        count_op();
+        if (P <= 3 && epc >= 2) {
+          tri_multi_kernel<P, (P <= 3 ? 2 : 1), MODE == 1, true>
+              <<<(unsigned)((h->E + (P <= 3 ? 1 : 0)) / (P <= 3 ? 2 : 1)), 96, 0, s>>>(a, h->tab, h->E);
+        } else {
+          tri_multi_kernel<P, 1, MODE == 1, true><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab, h->E);
+        }
+        return cudaGetLastError();
       }
       if constexpr (P <= 3) {
         if (epc >= 4) {
@@ -1186,7 +1225,76 @@ cudaError_t winv_apply(const hdiv_ctx* h, const double* q, double* y, const int*
   }
   return cudaErrorInvalidValue;
 }
+// Stored quadrature-point factors (the paper's partial assembly: geometric factors precomputed
+// at the quadrature points): G_q = w_q mw_e / det J_q  J_q^T J_q (symmetric, 6
+// entries {00, 11, 22, 01, 02, 12}), layout [E][6][Q^3] (q fastest: the pointwise stage reads
+// each entry coalesced).  One thread per (element, point); J from the 8 vertices (trilinear map).
+template <int P>
+__global__ void __launch_bounds__(256) geo_build_kernel(const double* __restrict__ vert, long long NLx,
+                                                        long long NLy, const __grid_constant__ Tab1D tab,
+                                                        const double* __restrict__ coef, long long E,
+                                                        double* __restrict__ geo) {
+  constexpr int Q = P + 2, NQ = Q * Q * Q;
+  const long long t = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (t >= E * NQ) return;
+  const long long e = t / NQ;
+  const int qi = (int)(t - e * NQ);
+  const int qx = qi % Q, qy = (qi / Q) % Q, qz = qi / (Q * Q);
+  const long long ex = e % NLx, ey = (e / NLx) % NLy, ez = e / (NLx * NLy);
+  double X[8][3];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const long long g = ((ez + (v >> 2)) * (NLy + 1) + (ey + ((v >> 1) & 1))) * (NLx + 1) + (ex + (v & 1));
+#pragma unroll
+    for (int d = 0; d < 3; ++d) X[v][d] = vert[g * 3 + d];
+  }
+  const double xh = tab.xq[qx], yh = tab.xq[qy], zh = tab.xq[qz];
+  double c[3][3];   // c[k][d] = dT_d / dx_hat_k
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    c[0][d] = (1 - yh) * (1 - zh) * (X[1][d] - X[0][d]) + yh * (1 - zh) * (X[3][d] - X[2][d]) +
+              (1 - yh) * zh * (X[5][d] - X[4][d]) + yh * zh * (X[7][d] - X[6][d]);
+    c[1][d] = (1 - xh) * (1 - zh) * (X[2][d] - X[0][d]) + xh * (1 - zh) * (X[3][d] - X[1][d]) +
+              (1 - xh) * zh * (X[6][d] - X[4][d]) + xh * zh * (X[7][d] - X[5][d]);
+    c[2][d] = (1 - xh) * (1 - yh) * (X[4][d] - X[0][d]) + xh * (1 - yh) * (X[5][d] - X[1][d]) +
+              (1 - xh) * yh * (X[6][d] - X[2][d]) + xh * yh * (X[7][d] - X[3][d]);
+  }
+  const double det = c[0][0] * (c[1][1] * c[2][2] - c[1][2] * c[2][1]) -
+                     c[1][0] * (c[0][1] * c[2][2] - c[0][2] * c[2][1]) +
+                     c[2][0] * (c[0][1] * c[1][2] - c[0][2] * c[1][1]);
+  const double sc = tab.wq[qx] * tab.wq[qy] * tab.wq[qz] * coef[4 * e] / det;
+  auto dot = [&](int i, int j) { return c[i][0] * c[j][0] + c[i][1] * c[j][1] + c[i][2] * c[j][2]; };
+  double* g = geo + e * 6 * NQ + qi;
+  g[0] = sc * dot(0, 0);
+  g[NQ] = sc * dot(1, 1);
+  g[2 * NQ] = sc * dot(2, 2);
+  g[3 * NQ] = sc * dot(0, 1);
+  g[4 * NQ] = sc * dot(0, 2);
+  g[5 * NQ] = sc * dot(1, 2);
+}
+
+template <int P>
+cudaError_t geo_build_p(hdiv_ctx* h, cudaStream_t s) {
+  constexpr int Q = P + 2;
+  const long long n = h->E * Q * Q * Q;
+  geo_build_kernel<P><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h->d_vert, h->NL[0], h->NL[1], h->tab,
+                                                                  h->d_coef, h->E, h->d_geo);
+  return cudaGetLastError();
+}
 }  // namespace
+
+// stored quadrature-point factors for the mass / gamma = 0 applies (d_coef[4e] = mass weight)
+cudaError_t build_tri_geo(hdiv_ctx* h, cudaStream_t s) {
+  switch (h->p) {
+    case 1: return geo_build_p<1>(h, s);
+    case 2: return geo_build_p<2>(h, s);
+    case 3: return geo_build_p<3>(h, s);
+    case 4: return geo_build_p<4>(h, s);
+    case 5: return geo_build_p<5>(h, s);
+    case 6: return geo_build_p<6>(h, s);
+  }
+  return cudaErrorInvalidValue;
+}
 
 // the explicit element inverses of W (p <= 4), built at setup when they fit the memory budget
 cudaError_t build_winv(hdiv_ctx* h, cudaStream_t s) {

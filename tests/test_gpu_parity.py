@@ -462,7 +462,7 @@ def test_trilinear_multi_element_ctas(monkeypatch, epc, N, p, ess):
     pr = _problem("c3", N, p)
     pr.essential = ess
     A = operators.Assembled(pr, with_schur=False)
-    op = _gpu(pr)
+    op = _gpu(pr, tri_geometry=1)   # Jacobian from the vertices in every apply
     s = op.sizes
     x = random_vector(s.n, 41)
     y = _host(op.apply_block(_dev(x)))
@@ -504,4 +504,30 @@ def test_trilinear_winv_modes(monkeypatch, winv, name, N, p):
     xg, rep = op.minres(_dev(b), rtol=1e-12, maxit=3000)
     assert conv_o and rep.converged and abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
     assert _rel(_host(xg), xo) < 1e-9
+    op.close()
+
+
+# ---- stored quadrature-point factors (partial assembly): tri_geometry=2 stores
+#      G_q = w_q mw / det J_q J_q^T J_q at setup; mass, gamma = 0 and explicit-W^-1 block applies
+@pytest.mark.parametrize("name,N,p,ess", [("c3", (3, 3, 1), 3, 0), ("c3", (5, 3, 1), 2, 2 | 16),
+                                          ("c3", (3, 2, 1), 6, 4), ("c3", (7, 1, 1), 1, 1 | 2),
+                                          ("c3", (5, 2, 1), 4, 1 | 32), ("c3", (3, 1, 3), 5, 0),
+                                          ("c3", (7, 1, 1), 4, 63), ("c3", (1, 1, 1), 3, 0),
+                                          ("c3", (3, 2, 3), 4, 0), ("c3gd", (3, 2, 2), 4, 0),
+                                          ("c3gd", (2, 3, 2), 3, 0), ("c3gd", (3, 2, 2), 2, 0)])
+def test_trilinear_stored_geometry(name, N, p, ess):
+    from oracle import operators
+    pr = _problem(name, N, p)
+    pr.essential = ess
+    A = operators.Assembled(pr, with_schur=False)
+    op = _gpu(pr, tri_geometry=2)
+    s = op.sizes
+    x = random_vector(s.n, 47)
+    y = _host(op.apply_block(_dev(x)))
+    yo = A.apply_block(x)
+    assert _rel(y[:s.n_rt], yo[:s.n_rt]) < TOL and _rel(y[s.n_rt:], yo[s.n_rt:]) < TOL
+    u = x[:s.n_rt]
+    assert _rel(_host(op.apply_mass(_dev(u))), A.M @ u) < TOL
+    y2 = _host(op.apply_block(_dev(x)))
+    assert np.array_equal(y, y2)
     op.close()
