@@ -133,7 +133,6 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_zcoef);
   cudaFree(h->d_winv);
   cudaFree(h->d_geo);
-  cudaFree(h->d_rv);
   cudaFree(h->d_gvert);
   amg_free(h);
   gmres_free(h);
@@ -467,15 +466,6 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     if (h->opts.tri_geometry == 2 || bytes <= fr / 4) {
       SETUP_TRY(cudaMalloc(&h->d_geo, bytes));
       SETUP_TRY(build_tri_geo(h, s));
-    }
-  }
-  // box kernel: rendezvous scratch for the tile-boundary planes (kernel_affine.cu)
-  if (h->kernel == 2) {
-    const char* ev = getenv("HDIV_BOX_RV");
-    if (!(ev && atoi(ev) == 0)) {
-      const size_t b = affine_rv_scratch_bytes(h);
-      SETUP_TRY(cudaMalloc(&h->d_rv, b));
-      SETUP_TRY(cudaMemsetAsync(h->d_rv, 0, b, s));
     }
   }
   SETUP_TRY(launch_mass_diag(h, h->d_mdiag, s));

@@ -75,7 +75,6 @@ struct hdiv_ctx {
   double* d_c2 = nullptr;         // per element alpha (grad-div) | gamma (Darcy)
   double* d_zcoef = nullptr;      // 3D: per element {mass weight, s_e = 1/alpha | gamma, 0, 0}
   double* d_winv = nullptr;       // [E][p^3][p^3] explicit W^e inverses (nullptr: local CG)
-  double* d_rv = nullptr;         // box kernel rendezvous scratch (slots + zeroed counters)
   double* d_geo = nullptr;        // [E][6][Q^3] stored G_q = w_q mw / det J J^T J (nullptr: on the fly)
   double* d_gvert = nullptr;      // NEXT-3 general gamma: per local vertex (nullptr: per element)
   double* d_sdinv = nullptr;      // 1 / diag(S~)
@@ -125,7 +124,6 @@ cudaError_t launch_affine_apply_range(const hdiv_ctx* h, const double* x, double
                                       const int* skip = nullptr);
 cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                 const int* skip, cudaStream_t s);
-size_t affine_rv_scratch_bytes(const hdiv_ctx* h);
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                  const int* skip, cudaStream_t s);
 cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s);

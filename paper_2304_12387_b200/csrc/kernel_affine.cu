@@ -60,14 +60,12 @@ constexpr bool kXDirect = HDIV_X_DIRECT;
 // smem box of component AX: extent (T_AX+1)P+1 along AX (position 0 <-> global plane
 // (e0_AX - 1) P), T P along the others.  Strides: the generated per-tile layout
 // (affine_layouts.h, fewest modelled bank-conflict wavefronts), else extents 0 and 1 padded odd.
-template <int P, int TX, int TY, int TZ, int AX, bool RV = false>
+template <int P, int TX, int TY, int TZ, int AX>
 struct CG {
-  static constexpr int LI = find_tile_layout(P, TX, TY, TZ, RV);
-  // RV (rendezvous kernel): no - side halo, position 0 = the tile's first own plane
-  static constexpr int H = RV ? 0 : 1;
-  static constexpr int E0 = (AX == 0) ? (TX + H) * P + 1 : TX * P;
-  static constexpr int E1 = (AX == 1) ? (TY + H) * P + 1 : TY * P;
-  static constexpr int E2 = (AX == 2) ? (TZ + H) * P + 1 : TZ * P;
+  static constexpr int LI = find_tile_layout(P, TX, TY, TZ);
+  static constexpr int E0 = (AX == 0) ? (TX + 1) * P + 1 : TX * P;
+  static constexpr int E1 = (AX == 1) ? (TY + 1) * P + 1 : TY * P;
+  static constexpr int E2 = (AX == 2) ? (TZ + 1) * P + 1 : TZ * P;
   static constexpr int S1 = LI >= 0 ? kTileLayouts[LI].S[AX][0] : odd_up(E0);
   static constexpr int S2 = LI >= 0 ? kTileLayouts[LI].S[AX][1] : S1 * odd_up(E1);
   static_assert(S1 >= E0 && S2 >= S1 * E1, "component layout overlaps");
@@ -87,26 +85,22 @@ struct CG {
   static constexpr int TA2 = (A2 == 1) ? TY : TZ;
 };
 
-template <int P, int TX, int TY, int TZ, bool RV = false>
+template <int P, int TX, int TY, int TZ>
 struct Geo {
   static constexpr int P3 = P * P * P;
   static constexpr int NE = TX * TY * TZ;
   static constexpr int NCELL = NE * P3;
   // cell tile (subcell-major, odd-padded): cell (X,Y,Z) at X + Q1 Y + Q2 Z
   static constexpr int CX = TX * P, CY = TY * P, CZ = TZ * P;
-  static constexpr int LI = find_tile_layout(P, TX, TY, TZ, RV);
+  static constexpr int LI = find_tile_layout(P, TX, TY, TZ);
   static constexpr int Q1 = LI >= 0 ? kTileLayouts[LI].Q[0] : odd_up(CX);
   static constexpr int Q2 = LI >= 0 ? kTileLayouts[LI].Q[1] : Q1 * odd_up(CY);
   static_assert(Q1 >= CX && Q2 >= Q1 * CY, "q tile layout overlaps");
   static constexpr int SQSIZE = Q2 * CZ;
-  static constexpr int SU = cmax(cmax(CG<P, TX, TY, TZ, 0, RV>::SIZE, CG<P, TX, TY, TZ, 1, RV>::SIZE),
-                                 cmax(CG<P, TX, TY, TZ, 2, RV>::SIZE, SQSIZE));
-  // halo q~ planes (halo-tile kernel only)
-  static constexpr int HQ0 = RV ? 0 : CY * CZ, HQ1 = RV ? 0 : CX * CZ, HQ2 = RV ? 0 : CX * CY;
-  // coefficient slots: the tile (RV) or the tile and its - halo
-  static constexpr int NCO = RV ? NE : (TX + 1) * (TY + 1) * (TZ + 1);
-  // rendezvous planes of component AX (lines over the two other axes)
-  static constexpr int PL0 = CY * CZ, PL1 = CX * CZ, PL2 = CX * CY;
+  static constexpr int SU = cmax(cmax(CG<P, TX, TY, TZ, 0>::SIZE, CG<P, TX, TY, TZ, 1>::SIZE),
+                                 cmax(CG<P, TX, TY, TZ, 2>::SIZE, SQSIZE));
+  static constexpr int HQ0 = CY * CZ, HQ1 = CX * CZ, HQ2 = CX * CY;
+  static constexpr int NCO = (TX + 1) * (TY + 1) * (TZ + 1);
   static constexpr size_t smem_doubles(bool block, bool db = true) {   // db: double buffer
     return (db ? 2 : 1) * (size_t)SU + (block ? (size_t)SQSIZE + HQ0 + HQ1 + HQ2 : 0) + 4 * NCO;
   }
@@ -127,10 +121,6 @@ struct AffArgs {
   // bits 8.. = first z tile of this launch (z-chunked host pipeline)
   int flags;
   const int* skip;     // MINRES done flag (nullptr: never skip)
-  // rendezvous kernel: per component AX, slots A/B [ntiles][PL_AX] (the - / + tile's part of
-  // the plane shared with the neighbour along AX, indexed by the + tile), then int counters
-  // [3][ntiles] (0 between applies)
-  double* rv;
   __device__ __forceinline__ int has_z() const { return flags & 1; }
   __device__ __forceinline__ int ess() const { return (flags >> 1) & 63; }
   __device__ __forceinline__ int tz0() const { return flags >> 8; }
@@ -145,7 +135,6 @@ struct TileRange {
 static thread_local TileRange g_range;
 
 struct TileInfo {
-  long long t;  // tile index (x fastest over all tiles of the local grid)
   int e0[3];    // first element of the tile
   int m[3];     // valid elements per axis (<= T)
   int h[3];     // - side halo element present
@@ -188,10 +177,10 @@ __device__ __forceinline__ void rows(GT* gbase, long long ext0, long long ext01,
 // element columns of consecutive item groups in the order of the layout's zmap), reads it from
 // src once, contracts along X then Y (the order of two separate line passes: same arithmetic)
 // and writes it to dst once
-template <int P, int TX, int TY, int TZ, int NT, bool RV>
+template <int P, int TX, int TY, int TZ, int NT>
 __device__ __forceinline__ void z_xy_block(const double* src, double* dst, const double (*Mi)[MAXP]) {
-  using G = Geo<P, TX, TY, TZ, RV>;
-  constexpr int LI = find_tile_layout(P, TX, TY, TZ, RV);
+  using G = Geo<P, TX, TY, TZ>;
+  constexpr int LI = find_tile_layout(P, TX, TY, TZ);
   constexpr int ZMAP = LI >= 0 ? kTileLayouts[LI].zmap : 0;
   constexpr int CZ = G::CZ;
   constexpr int NIT = CZ * TX * TY;
@@ -239,7 +228,7 @@ struct Own {
 };
 
 // global tile origin of component AX (position 0 of its smem box) and its face-grid extents
-template <int P, int AX, bool RV = false>
+template <int P, int AX>
 struct CompAddr {
   long long ext0, ext01, gtile;
   __device__ __forceinline__ CompAddr(const AffArgs& a, const TileInfo& ti) {
@@ -248,18 +237,18 @@ struct CompAddr {
     ext01 = ext0 * ext1;
     long long gorg[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) gorg[d] = (long long)(ti.e0[d] - (d == AX && !RV ? 1 : 0)) * P;
+    for (int d = 0; d < 3; ++d) gorg[d] = (long long)(ti.e0[d] - (d == AX ? 1 : 0)) * P;
     gtile = a.off[AX] + gorg[0] + ext0 * (gorg[1] + ext1 * gorg[2]);
   }
 };
 
 // issue the cp.async loads of component AX's tile (+ - halo) into `su` and commit a group
-template <int P, int TX, int TY, int TZ, int NT, int AX, bool RV = false>
+template <int P, int TX, int TY, int TZ, int NT, int AX>
 __device__ __forceinline__ void load_component(const AffArgs& a, const TileInfo& ti, double* su) {
-  using C = CG<P, TX, TY, TZ, AX, RV>;
-  const CompAddr<P, AX, RV> ca(a, ti);
-  const int lo_a = (RV || ti.h[AX]) ? 0 : P;          // first loaded position along AX
-  const int hi_a = (ti.m[AX] + (RV ? 0 : 1)) * P;     // last valid position along AX
+  using C = CG<P, TX, TY, TZ, AX>;
+  const CompAddr<P, AX> ca(a, ti);
+  const int lo_a = ti.h[AX] ? 0 : P;                  // first loaded position along AX
+  const int hi_a = (ti.m[AX] + 1) * P;                // last valid position along AX
   const int hi0 = ti.m[0] * P, hi1 = ti.m[1] * P, hi2 = ti.m[2] * P;
   auto okd = [&](int d, int pos) {
     if (d == AX) return pos >= lo_a && pos <= hi_a;
@@ -273,21 +262,16 @@ __device__ __forceinline__ void load_component(const AffArgs& a, const TileInfo&
 }
 
 // -------- one component phase (AX), data already in `su` ------------------------------------
-// RV = the rendezvous kernel: the box holds only the tile's own planes 0..T P along AX; the plane
-// shared with the - neighbour tile (position 0) and with the + neighbour (position T P) get one
-// contribution from each side, exchanged through the rv slots (see rendezvous() below) instead
-// of recomputing the neighbour's part from a halo.
 template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK, bool XD = kXDirect,
-          bool ESS = false, bool RV = false>
+          bool ESS = false>
 __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
                                           const TabAffine& tab, double* su, const double* sq,
                                           const double* hq, const double* sco, double* acc) {
-  using C = CG<P, TX, TY, TZ, AX, RV>;
-  using G = Geo<P, TX, TY, TZ, RV>;
+  using C = CG<P, TX, TY, TZ, AX>;
+  using G = Geo<P, TX, TY, TZ>;
   using O = Own<P, TX, TY, TZ, NT>;
-  constexpr int OFF = RV ? 0 : P;   // box position of the tile's first own plane
   const int tid = threadIdx.x;
-  const CompAddr<P, AX, RV> ca(a, ti);
+  const CompAddr<P, AX> ca(a, ti);
   const long long ext0 = ca.ext0, ext01 = ca.ext01, gtile = ca.gtile;
   const int hi0 = ti.m[0] * P, hi1 = ti.m[1] * P, hi2 = ti.m[2] * P;
   constexpr int EL1 = C::TA1 * P, EL2 = C::TA2 * P;
@@ -300,8 +284,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   if (ESS && (ess_lo || ess_hi)) {   // block-uniform
     for (int it = tid; it < EL1 * EL2; it += NT) {
       double* line = su + (it % EL1) * C::SA1 + (it / EL1) * C::SA2;
-      if (ess_lo) line[OFF * C::SA] = 0.0;
-      if (ess_hi) line[(ti.m[AX] * P + OFF) * C::SA] = 0.0;
+      if (ess_lo) line[P * C::SA] = 0.0;
+      if (ess_hi) line[(ti.m[AX] + 1) * P * C::SA] = 0.0;
     }
     __syncthreads();
   }
@@ -313,7 +297,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
       const int col = tid + j * NT;
       if (col < O::NCOL) {
         int pos[3] = {col % G::CX, col / G::CX, 0};
-        pos[AX] += OFF;
+        pos[AX] += P;
         const double* s = su + pos[0] + C::S1 * pos[1] + C::S2 * pos[2];
         if constexpr (AX == 2) {   // walk up the column: each z face read once
           double lo = s[0];
@@ -333,12 +317,12 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     __syncthreads();
   }
 
-  // ---- halo element (halo-tile kernel): only its contribution to the shared plane is needed,
-  //      and by linearity c_h sum_j M_l[P][j] (M_h (x) M_h) u_j = c_h (M_h (x) M_h) sum_j
-  //      M_l[P][j] u_j, so the raw halo planes are combined first into position P-1 ----
+  // ---- halo element: only its contribution to the shared plane is needed, and by
+  //      linearity c_h sum_j M_l[P][j] (M_h (x) M_h) u_j = c_h (M_h (x) M_h) sum_j M_l[P][j] u_j,
+  //      so the raw halo planes are combined first into position P-1 (one plane to transform)
   constexpr int EL1P = C::PADL ? (EL1 + 15) / 16 * 16 : EL1;   // half-warp aligned lane rows
-  const int m_a = ti.m[AX], h_a = RV ? 0 : ti.h[AX];
-  if (!RV && h_a) {
+  const int m_a = ti.m[AX], h_a = ti.h[AX];
+  if (h_a) {
 #pragma unroll 1
     for (int it = tid; it < EL1P * EL2; it += NT) {
       const int l1 = it % EL1P, l2 = it / EL1P;
@@ -353,15 +337,14 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   }
 
   // ---- M_h (x) M_h over the two histopolation axes: one P x P block per thread, positions
-  //      P0 .. EA-1; lanes run along AX (odd stride), the position range padded to a multiple
-  //      of 16 so a half-warp never straddles two blocks ----
-  constexpr int P0 = RV ? 0 : P - 1;
-  constexpr int EAH = C::EA - P0;
+  //      P-1 (combined halo) .. (T+1)P; lanes run along AX (odd stride), the position range
+  //      padded to a multiple of 16 so a half-warp never straddles two blocks ----
+  constexpr int EAH = C::EA - (P - 1);
   constexpr int EAP = C::PADA ? (EAH + 15) / 16 * 16 : EAH;
   constexpr int NH = EAP * C::TA1 * C::TA2;
 #pragma unroll 2
   for (int it = tid; it < NH; it += NT) {
-    const int pa = it % EAP + P0, b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
+    const int pa = it % EAP + (P - 1), b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
     if (pa >= C::EA) continue;
     double* base = su + pa * C::SA + b1 * P * C::SA1 + b2 * P * C::SA2;
     // row by row: only one input row and the P x P intermediate are live (register pressure)
@@ -403,21 +386,12 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
   const long long gsa = (AX == 0) ? 1 : (AX == 1) ? ext0 : ext01;
   const int hiA1 = (C::A1 == 0) ? hi0 : hi1, hiA2 = (C::A2 == 1) ? hi1 : hi2;
   double* yt = a.y + gtile;
-  // rendezvous (RV): the tile's first plane is shared with the - neighbour tile unless the tile
-  // starts the (local) domain; its last plane with the + neighbour unless it ends it
-  const bool hasm = RV && ti.e0[AX] > 0, hasp = RV && !ti.last[AX];
-  constexpr int NLT = RV ? (NL + NT - 1) / NT : 1;   // lines per thread
-  double Bv[NLT], Av[NLT];                           // this tile's part of the first / last plane
-#pragma unroll
-  for (int j = 0; j < NLT; ++j) Bv[j] = Av[j] = 0.0;
-#pragma unroll RV ? NLT : 1
-  for (int jt = 0; jt < (RV ? NLT : (NL + NT - 1) / NT); ++jt) {
-    const int it = tid + jt * NT;
-    if (it >= NL) continue;
+#pragma unroll 1
+  for (int it = tid; it < NL; it += NT) {
     const int l1 = it % EL1P, l2 = it / EL1P;
     if (l1 >= EL1) continue;
     const bool line_ok = l1 < hiA1 && l2 < hiA2;
-    if ((RV || AX != 0 || XD) && !line_ok) continue;
+    if ((AX != 0 || XD) && !line_ok) continue;
     double* line = su + l1 * C::SA1 + l2 * C::SA2;
     double* gl = yt + (l1 * gs1 + l2 * gs2);
     int ec[3];
@@ -425,10 +399,8 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     ec[C::A2] = l2 / P;
     ec[AX] = 0;
     const double* cbase =
-        RV ? sco + 4 * ((ec[2] * TY + ec[1]) * TX + ec[0]) + AX
-           : sco + 4 * (((ec[2] + 1) * (TY + 1) + (ec[1] + 1)) * (TX + 1) + (ec[0] + 1)) + AX;
-    constexpr int CSTEP = RV ? 4 * ((AX == 0) ? 1 : (AX == 1) ? TX : TX * TY)
-                             : 4 * ((AX == 0) ? 1 : (AX == 1) ? (TX + 1) : (TX + 1) * (TY + 1));
+        sco + 4 * (((ec[2] + 1) * (TY + 1) + (ec[1] + 1)) * (TX + 1) + (ec[0] + 1)) + AX;
+    constexpr int CSTEP = 4 * ((AX == 0) ? 1 : (AX == 1) ? (TX + 1) : (TX + 1) * (TY + 1));
     const double* ql = sq + l1 * QA1 + l2 * QA2;
     double carry = 0.0, qprev = 0.0;
     if (h_a) {   // transformed combined halo plane (position P-1)
@@ -438,7 +410,7 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
 #pragma unroll
     for (int et = 0; et < C::TA; ++et) {
       if (et < m_a) {
-        double* eb = line + (et * P + OFF) * C::SA;
+        double* eb = line + (et + 1) * P * C::SA;
         double v[P + 1];
 #pragma unroll
         for (int i = 0; i <= P; ++i) v[i] = eb[i * C::SA];
@@ -455,10 +427,9 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
             qprev = qc;
           }
           if (ESS && i == 0 && et == 0 && ess_lo)   // identity row of the eliminated plane
-            o = a.x[gtile + (l1 * gs1 + l2 * gs2) + OFF * gsa];
-          if (RV && i == 0 && et == 0 && hasm) Bv[jt] = o;   // completed by the rendezvous
-          else if (AX == 0 && !XD) eb[i * C::SA] = o;
-          else __stcs(gl + (et * P + i + OFF) * gsa, o);
+            o = a.x[gtile + (l1 * gs1 + l2 * gs2) + P * gsa];
+          if (AX == 0 && !XD) eb[i * C::SA] = o;
+          else __stcs(gl + ((et + 1) * P + i) * gsa, o);
         }
         double s = 0.0;
 #pragma unroll
@@ -466,79 +437,21 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
         carry = c * s;
       }
     }
-    const double oA = carry + (BLOCK ? qprev : 0.0);
     if (ti.last[AX]) {
-      const double o = (ESS && ess_hi) ? a.x[gtile + (l1 * gs1 + l2 * gs2) + (m_a * P + OFF) * gsa] : oA;
-      if (AX == 0 && !XD) line[(m_a * P + OFF) * C::SA] = o;
-      else __stcs(gl + (m_a * P + OFF) * gsa, o);
-    } else if (RV) {
-      Av[jt] = oA;
-    }
-  }
-  if constexpr (RV) {
-    // ---- rendezvous on the two shared planes: each side posts its part (A from the - tile,
-    //      B from the + tile) to the slots of the boundary (indexed by the + tile), fences, and
-    //      bumps the boundary's counter; the second arriver stores A + B (the same sum in the
-    //      same order whichever side finishes last: bitwise reproducible) and resets the
-    //      counter to 0 for the next apply.  No waiting, so any launch / scheduling order of
-    //      the tiles is fine (z-chunked host pipeline, slab boundary layers first). ----
-    if (hasm || hasp) {   // block-uniform
-      constexpr int PL = EL1 * EL2;
-      const long long ntot = (long long)a.ntile[0] * a.ntile[1] * a.ntile[2];
-      long long sbase = 0;   // start of this component's slots
-#pragma unroll
-      for (int c = 0; c < AX; ++c) sbase += 2 * ntot * (c == 0 ? G::PL0 : c == 1 ? G::PL1 : G::PL2);
-      double* slotA = a.rv + sbase;               // [ntiles][PL]: - tile's part
-      double* slotB = slotA + ntot * PL;          // [ntiles][PL]: + tile's part
-      int* cnt = (int*)(a.rv + 2 * ntot * (G::PL0 + G::PL1 + G::PL2)) + AX * ntot;
-      const long long tstride = (AX == 0) ? 1 : (AX == 1) ? a.ntile[0] : (long long)a.ntile[0] * a.ntile[1];
-      const long long tme = ti.t;
-      const long long tpl = tme + tstride;
-#pragma unroll
-      for (int jt = 0; jt < NLT; ++jt) {
-        const int it = tid + jt * NT;
-        const int l1 = it % EL1P, l2 = it / EL1P;
-        if (it < NL && l1 < EL1 && l1 < hiA1 && l2 < hiA2) {
-          if (hasm) __stcg(slotB + tme * PL + l1 + EL1 * l2, Bv[jt]);
-          if (hasp) __stcg(slotA + tpl * PL + l1 + EL1 * l2, Av[jt]);
-        }
-      }
-      __threadfence();
-      __syncthreads();
-      __shared__ int s_second;
-      if (tid == 0) {
-        int f = 0;
-        if (hasm && atomicAdd(cnt + tme, 1) == 1) { f |= 1; cnt[tme] = 0; }
-        if (hasp && atomicAdd(cnt + tpl, 1) == 1) { f |= 2; cnt[tpl] = 0; }
-        __threadfence();
-        s_second = f;
-      }
-      __syncthreads();
-      const int f = s_second;
-      if (f) {
-#pragma unroll
-        for (int jt = 0; jt < NLT; ++jt) {
-          const int it = tid + jt * NT;
-          const int l1 = it % EL1P, l2 = it / EL1P;
-          if (it < NL && l1 < EL1 && l1 < hiA1 && l2 < hiA2) {
-            double* gl = yt + (l1 * gs1 + l2 * gs2);
-            if (f & 1) __stcs(gl, __ldcg(slotA + tme * PL + l1 + EL1 * l2) + Bv[jt]);
-            if (f & 2) __stcs(gl + m_a * P * gsa, Av[jt] + __ldcg(slotB + tpl * PL + l1 + EL1 * l2));
-          }
-        }
-      }
+      const double o = (ESS && ess_hi) ? a.x[gtile + (l1 * gs1 + l2 * gs2) + (m_a + 1) * P * gsa]
+                              : carry + (BLOCK ? qprev : 0.0);
+      if (AX == 0 && !XD) line[(m_a + 1) * P * C::SA] = o;
+      else __stcs(gl + (m_a + 1) * P * gsa, o);
     }
   }
   __syncthreads();
 
   if constexpr (AX == 0 && !XD) {
-    // ---- copy-out of the owned x planes (coalesced, streaming); RV: the shared planes are
-    //      stored by the rendezvous ----
+    // ---- copy-out of the owned x planes (coalesced, streaming) ----
     constexpr int NO0 = TX * P + 1;
-    const int own_lo = (RV && hasm) ? 1 : 0;
-    const int own_hi = m_a * P + ((ti.last[0] && !(RV && hasp)) ? 1 : 0);   // exclusive, relative to OFF
+    const int own_hi = m_a * P + (ti.last[0] ? 1 : 0);   // exclusive, relative to position P
     rows<NT, NO0, C::E1, C::E2, C::S1, C::S2>(
-        yt + OFF, ext0, ext01, su + OFF, [&](int i) { return i >= own_lo && i < own_hi; },
+        yt + P, ext0, ext01, su + P, [&](int i) { return i < own_hi; },
         [&](int i) { return i < hi1; }, [&](int i) { return i < hi2; },
         [&](double* g, const double* s) { __stcs(g, *s); });
     __syncthreads();
@@ -546,10 +459,10 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
 }
 
 template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB, int MINB, bool XD,
-          bool ESS = false, bool RV = false>
+          bool ESS = false>
 __global__ void __launch_bounds__(NT, MINB)
 affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
-  using G = Geo<P, TX, TY, TZ, RV>;
+  using G = Geo<P, TX, TY, TZ>;
   using O = Own<P, TX, TY, TZ, NT>;
   constexpr int P3 = G::P3;
   if (a.skip && *a.skip) return;
@@ -570,7 +483,6 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     t /= a.ntile[0];
     const int ty = t % a.ntile[1];
     const int tz = t / a.ntile[1] + a.tz0();
-    ti.t = tx + (long long)a.ntile[0] * (ty + (long long)a.ntile[1] * tz);
     const int T3[3] = {TX, TY, TZ};
     const int tt[3] = {tx, ty, tz};
 #pragma unroll
@@ -590,13 +502,12 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     return ((long long)(ti.e0[2] + ez) * NLy + (ti.e0[1] + ey)) * NLx + (ti.e0[0] + ex);
   };
 
-  // ---- group 0: coefficients of the tile (and its - halo), q~ tile, halo q~ ----
+  // ---- group 0: coefficients of the tile and its - halo, q~ tile, halo q~ ----
   for (int l = tid; l < 4 * G::NCO; l += NT) {   // lanes over (slot, k): contiguous runs
     const int i = l >> 2, k = l & 3;
-    constexpr int H = RV ? 0 : 1;
-    const int ix = i % (TX + H), iy = (i / (TX + H)) % (TY + H), iz = i / ((TX + H) * (TY + H));
-    const int ex = ti.e0[0] - H + ix, ey = ti.e0[1] - H + iy, ez = ti.e0[2] - H + iz;
-    if (ex >= 0 && ey >= 0 && ez >= 0 && ix < ti.m[0] + H && iy < ti.m[1] + H && iz < ti.m[2] + H)
+    const int ix = i % (TX + 1), iy = (i / (TX + 1)) % (TY + 1), iz = i / ((TX + 1) * (TY + 1));
+    const int ex = ti.e0[0] - 1 + ix, ey = ti.e0[1] - 1 + iy, ez = ti.e0[2] - 1 + iz;
+    if (ex >= 0 && ey >= 0 && ez >= 0 && ix <= ti.m[0] && iy <= ti.m[1] && iz <= ti.m[2])
       cp_async8(sco + l, a.coef + 4 * (((long long)ez * NLy + ey) * NLx + ex) + k);
   }
   if constexpr (BLOCK) {
@@ -618,7 +529,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
       }
     }
     // halo q~ of the - neighbour's adjacent cell layer (for D^T at the owned - planes)
-    if (!RV && ti.h[0])
+    if (ti.h[0])
       for (int i = tid; i < G::HQ0; i += NT) {
         const int J = i % G::CY, K = i / G::CY;
         if (J < ti.m[1] * P && K < ti.m[2] * P) {
@@ -627,7 +538,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
           cp_async8(hq0 + i, q + ge * P3 + (P - 1) + P * ((J % P) + P * (K % P)));
         }
       }
-    if (!RV && ti.h[1])
+    if (ti.h[1])
       for (int i = tid; i < G::HQ1; i += NT) {
         const int I = i % G::CX, K = i / G::CX;
         if (I < ti.m[0] * P && K < ti.m[2] * P) {
@@ -636,7 +547,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
           cp_async8(hq1 + i, q + ge * P3 + (I % P) + P * ((P - 1) + P * (K % P)));
         }
       }
-    if (!RV && ti.h[2])
+    if (ti.h[2])
       for (int i = tid; i < G::HQ2; i += NT) {
         const int I = i % G::CX, J = i / G::CX;
         if (I < ti.m[0] * P && J < ti.m[1] * P) {
@@ -648,7 +559,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   }
   cp_async_commit();
   // ---- group 1 (DB): x component -> A, overlapping the Z passes (scratch B) ----
-  if constexpr (DB) load_component<P, TX, TY, TZ, NT, 0, RV>(a, ti, bufA);
+  if constexpr (DB) load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
 
   double acc[O::NACC];
 #pragma unroll
@@ -661,7 +572,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     if (a.has_z()) {
       // -Z q~ = -z_e (Mh^-1)^{(x)3} q~_e in B (subcell-major like sq):
       // X-lines (lanes over Y, odd stride Q1; sq -> B), then Y- and Z-lines (lanes over X)
-      z_xy_block<P, TX, TY, TZ, NT, RV>(sq, bufB, tab.Mhinv);
+      z_xy_block<P, TX, TY, TZ, NT>(sq, bufB, tab.Mhinv);
       __syncthreads();
       // Z-lines in registers: every thread owns whole z-columns of cells
 #pragma unroll
@@ -669,16 +580,14 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
         const int col = tid + j * NT;
         if (col < O::NCOL) {
           const int X = col % G::CX, Y = col / G::CX;
-          const double* sz = RV ? sco + 4 * ((Y / P) * TX + (X / P)) + 3
-                                : sco + 4 * (((Y / P) + 1) * (TX + 1) + (X / P) + 1) + 3;
-          constexpr int ZSTEP = RV ? 4 * TX * TY : 4 * (TX + 1) * (TY + 1);
+          const double* sz = sco + 4 * (((Y / P) + 1) * (TX + 1) + (X / P) + 1) + 3;
           const double* s = bufB + X + G::Q1 * Y;
 #pragma unroll
           for (int zb = 0; zb < TZ; ++zb) {
             double v[P];
 #pragma unroll
             for (int k = 0; k < P; ++k) v[k] = s[(zb * P + k) * G::Q2];
-            const double ze = sz[ZSTEP * (zb + (RV ? 0 : 1))];
+            const double ze = sz[4 * (TX + 1) * (TY + 1) * (zb + 1)];
 #pragma unroll
             for (int i = 0; i < P; ++i) {
               double t = 0.0;
@@ -694,31 +603,31 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   }
   if constexpr (DB) {
     // ---- group 2: y component -> B ; compute x from A ----
-    load_component<P, TX, TY, TZ, NT, 1, RV>(a, ti, bufB);
+    load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS, RV>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq0, sco, acc);
     // ---- group 3: z component -> A ; compute y from B ----
-    load_component<P, TX, TY, TZ, NT, 2, RV>(a, ti, bufA);
+    load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS, RV>(a, ti, tab, bufB, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS>(a, ti, tab, bufB, sq, hq1, sco, acc);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS, RV>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq2, sco, acc);
   } else {
-    load_component<P, TX, TY, TZ, NT, 0, RV>(a, ti, bufA);
+    load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS, RV>(a, ti, tab, bufA, sq, hq0, sco, acc);
-    load_component<P, TX, TY, TZ, NT, 1, RV>(a, ti, bufA);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS, RV>(a, ti, tab, bufA, sq, hq1, sco, acc);
-    load_component<P, TX, TY, TZ, NT, 2, RV>(a, ti, bufA);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq1, sco, acc);
+    load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS, RV>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq2, sco, acc);
   }
 
   if constexpr (BLOCK) {
@@ -742,10 +651,10 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
 }
 
 template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true, int MINB = 0, bool XD = kXDirect,
-          bool ESS = false, bool RV = false>
+          bool ESS = false>
 cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* skip,
                      cudaStream_t s) {
-  using G = Geo<P, TX, TY, TZ, RV>;
+  using G = Geo<P, TX, TY, TZ>;
   AffArgs a;
   a.x = x; a.y = y; a.coef = h->d_coef;
   for (int d = 0; d < 3; ++d) { a.NL[d] = h->NL[d]; a.n[d] = h->n[d]; a.off[d] = h->off[d]; }
@@ -755,8 +664,6 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.ntile[2] = (int)((h->NL[2] + TZ - 1) / TZ);
   a.flags = (h->has_z ? 1 : 0) | (h->ess << 1);
   a.skip = skip;
-  a.rv = h->d_rv;
-  if (RV && !h->d_rv) return cudaErrorInvalidValue;   // scratch not allocated
   if (g_range.tz_out) {   // query: the variant's tile depth along z
     *g_range.tz_out = TZ;
     return cudaSuccess;
@@ -766,7 +673,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.flags |= tz0 << 8;
   if (tz1 <= tz0) return cudaSuccess;
   const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
-  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, ESS, RV>;
+  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, ESS>;
   static bool attr_done = false;   // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -788,21 +695,8 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
 template <bool BLOCK, int P, int TX, int TY, int TZ, int NT, bool DB, int MINB, bool XD>
 cudaError_t launch_tile(const hdiv_ctx* h, const double* x, double* y, const int* k,
                         cudaStream_t s) {
-  if (h->d_rv) {
-    if (h->ess) return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, true, true>(h, x, y, k, s);
-    return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, false, true>(h, x, y, k, s);
-  }
   if (h->ess) return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, true>(h, x, y, k, s);
   return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, false>(h, x, y, k, s);
-}
-
-// rendezvous scratch of one tile shape: slots A/B of the three components + counters
-template <int P, int TX, int TY, int TZ>
-size_t rv_bytes(const hdiv_ctx* h) {
-  using G = Geo<P, TX, TY, TZ, true>;
-  const size_t nt = (size_t)((h->NL[0] + TX - 1) / TX) * ((h->NL[1] + TY - 1) / TY) *
-                    ((h->NL[2] + TZ - 1) / TZ);
-  return sizeof(double) * 2 * nt * (G::PL0 + G::PL1 + G::PL2) + sizeof(int) * 3 * nt;
 }
 
 template <bool BLOCK>
@@ -820,20 +714,6 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
 }
 
 }  // namespace
-
-// bytes of the rendezvous scratch of h's tile shape (zeroed once at setup: the counters must
-// start at 0; every apply leaves them at 0)
-size_t affine_rv_scratch_bytes(const hdiv_ctx* h) {
-  switch (h->p) {
-    case 1: return rv_bytes<1, 8, 8, 4>(h);
-    case 2: return rv_bytes<2, 8, 4, 4>(h);
-    case 3: return rv_bytes<3, 4, 4, 2>(h);
-    case 4: return rv_bytes<4, 4, 2, 2>(h);
-    case 5: return rv_bytes<5, 3, 2, 2>(h);
-    case 6: return rv_bytes<6, 3, 2, 2>(h);
-  }
-  return 0;
-}
 
 cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                 const int* skip, cudaStream_t s) {

@@ -48,18 +48,15 @@ def run(NT, items, naccess, addr, acc=None, distinct_k=True):
 
 
 class Layout:
-    def __init__(self, P, T, S=None, Q=None, padL=None, padA=None, zmap=0, rv=False):
+    def __init__(self, P, T, S=None, Q=None, padL=None, padA=None, zmap=0):
         self.P, self.T = P, T
         self.zmap = zmap
-        # rv: the rendezvous kernel (no - side halo: the box starts at the tile's first own
-        # plane, E_AX = T_AX P + 1; no halo-combine pass; coefficients of own elements only)
-        self.rv = rv
         CX, CY, CZ = (t * P for t in T)
         self.C = (CX, CY, CZ)
         self.E = []
         for AX in range(3):
             E = [T[d] * P for d in range(3)]
-            E[AX] = T[AX] * P + 1 if rv else (T[AX] + 1) * P + 1
+            E[AX] = (T[AX] + 1) * P + 1
             self.E.append(E)
         self.S = S or [(odd(E[0]), odd(E[0]) * odd(E[1])) for E in self.E]
         self.Q = Q or (odd(CX), odd(CX) * odd(CY))
@@ -103,7 +100,7 @@ def comp_cost(L, AX, NT=128):
     def du(col, k):
         X, Y = col % CX, col // CX
         pos = [X, Y, 0]
-        pos[AX] += 0 if L.rv else P
+        pos[AX] += P
         base = pos[0] + S1 * pos[1] + S2 * pos[2]
         if AX == 2:
             return base + k * S2
@@ -121,14 +118,12 @@ def comp_cost(L, AX, NT=128):
         if l1 is None:
             return None
         return l1 * SA1 + l2 * SA2 + (k if k <= P else P - 1) * SA
-    if not L.rv:
-        out["halo"] = run(NT, EL1P * EL2, P + 2, halo, distinct_k=False)
-    P0 = 0 if L.rv else P - 1   # first M_h (x) M_h position
-    EAH = EA - P0
+    out["halo"] = run(NT, EL1P * EL2, P + 2, halo, distinct_k=False)
+    EAH = EA - (P - 1)
     EAP = (EAH + 15) // 16 * 16 if L.padA[AX] else EAH
 
     def mh(it, k):
-        pa = it % EAP + P0
+        pa = it % EAP + (P - 1)
         b1 = (it // EAP) % TA1
         b2 = it // (EAP * TA1)
         if pa >= EA:
@@ -158,10 +153,8 @@ def comp_cost(L, AX, NT=128):
             return None
         ec = [0, 0, 0]
         ec[A1], ec[A2] = l1 // P, l2 // P
-        if L.rv:
-            return 4 * ((ec[2] * T[1] + ec[1]) * T[0] + ec[0])
         return 4 * (((ec[2] + 1) * (T[1] + 1) + (ec[1] + 1)) * (T[0] + 1) + (ec[0] + 1))
-    out["Ml coef"] = run(NT, EL1P * EL2, TA if L.rv else TA + 1, mlc, distinct_k=False)
+    out["Ml coef"] = run(NT, EL1P * EL2, TA + 1, mlc, distinct_k=False)
     return out
 
 
@@ -216,8 +209,8 @@ def ndof(P, T):
     return 4 * P ** 3 * T[0] * T[1] * T[2]
 
 
-def search(P, T, slack=16, smem_growth=1.10, rv=False):
-    base = Layout(P, T, rv=rv)
+def search(P, T, slack=16, smem_growth=1.10):
+    base = Layout(P, T)
     su0 = base.smem()
     best = None
     CX, CY, CZ = base.C
@@ -228,7 +221,7 @@ def search(P, T, slack=16, smem_growth=1.10, rv=False):
     for q1 in range(CX, odd(CX) + 3):
         for q2 in range(q1 * CY, q1 * odd(CY) + slack):
             for zm in (0, 1):
-                L = Layout(P, T, Q=(q1, q2), zmap=zm, rv=rv)
+                L = Layout(P, T, Q=(q1, q2), zmap=zm)
                 if q2 * CZ > su0 * smem_growth:
                     continue
                 c = sum(q_cost(L).values())
@@ -249,13 +242,13 @@ def search(P, T, slack=16, smem_growth=1.10, rv=False):
                         Sx = list(base.S)
                         Sx[AX] = (s1, s2)
                         L = Layout(P, T, S=Sx, Q=bestq[1], padL=[pl] * 3, padA=[pa] * 3,
-                                   zmap=bestq[2], rv=rv)
+                                   zmap=bestq[2])
                         cc = comp_cost(L, AX)
                         c = sum(v for k, v in cc.items() if k != "Ml q") + cc["Ml q"]
                         if bc is None or c < bc[0]:
                             bc = (c, (s1, s2), pl, pa)
         S.append(bc[1]); padL.append(bc[2]); padA.append(bc[3])
-    return Layout(P, T, S=S, Q=bestq[1], padL=padL, padA=padA, zmap=bestq[2], rv=rv)
+    return Layout(P, T, S=S, Q=bestq[1], padL=padL, padA=padA, zmap=bestq[2])
 
 
 def report(L, title):
