@@ -35,7 +35,7 @@ def _stale(src: str) -> bool:
     t = os.path.getmtime(o)
     deps = [os.path.join(CSRC, src), os.path.join(CSRC, "internal.h"),
             os.path.join(ROOT, "include", "hdiv.h"), os.path.join(CSRC, "affine_layouts.h"),
-            os.path.join(CSRC, "tri_layouts.h")]
+            os.path.join(CSRC, "tri_layouts.h"), os.path.join(CSRC, "cell_stencil.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 

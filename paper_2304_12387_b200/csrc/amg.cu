@@ -24,6 +24,7 @@
 #include <cmath>
 #include <vector>
 
+#include "cell_stencil.h"
 #include "internal.h"
 
 namespace hdiv {
@@ -770,14 +771,32 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   const int nu = H->nu;
   const long long n = L.n;
   const unsigned g = nbk(n);
-  SellA sa{h->d_ecol, h->d_eval, 2 * h->dim + 1, (int)h->nl2};
   StA sta = make_sta(L);
   const bool lev0 = (l == 0);
+  // level 0 (S~ itself): the cell stencil in 3D (cell_stencil.h), the SELL copy in 2D
+  auto lev0_acc = [&](auto&& fn) {
+    if (h->d_cw) {
+      const CellGeo cg = make_cellgeo(h);
+      switch (h->p) {
+        case 1: fn(CellA<1>{cg}); break;
+        case 2: fn(CellA<2>{cg}); break;
+        case 3: fn(CellA<3>{cg}); break;
+        case 4: fn(CellA<4>{cg}); break;
+        case 5: fn(CellA<5>{cg}); break;
+        default: fn(CellA<6>{cg}); break;
+      }
+    } else {
+      fn(SellA{h->d_ecol, h->d_eval, 2 * h->dim + 1, (int)h->nl2});
+    }
+  };
   // buffers: pre-smoothing ping-pong in xa/xb, final post-smoothing output in x
   double* cur = L.xa;
   double* nxt = L.xb;
   auto jac = [&](const double* xin, double* xout) {
-    if (lev0) jacobi_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, b, xin, xout, L.dl1inv, done);
+    if (lev0)
+      lev0_acc([&](auto acc) {
+        jacobi_kernel<decltype(acc)><<<g, ANT, 0, s>>>(acc, n, b, xin, xout, L.dl1inv, done);
+      });
     else jacobi_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, xin, xout, L.dl1inv, done);
   };
   if (nu >= 1) {
@@ -788,8 +807,10 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   }
   // r = b - A x ; s = r - omega A D^-1 r ; b_c = aggregate sums of s
   if (lev0) {
-    resid_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, b, cur, L.r, L.dinv, nxt, done);
-    smooth_r_kernel<SellA><<<g, ANT, 0, s>>>(sa, n, L.r, nxt, L.omega, L.sv, done);
+    lev0_acc([&](auto acc) {
+      resid_kernel<decltype(acc)><<<g, ANT, 0, s>>>(acc, n, b, cur, L.r, L.dinv, nxt, done);
+      smooth_r_kernel<decltype(acc)><<<g, ANT, 0, s>>>(acc, n, L.r, nxt, L.omega, L.sv, done);
+    });
     aggsum0_kernel<<<nbk(C.n), ANT, 0, s>>>(make_op0(h), C.d[0], C.d[1], C.n, L.sv, C.b, done);
   } else {
     resid_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, cur, L.r, L.dinv, nxt, done);
@@ -804,7 +825,10 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   const double* ecv = C.e;
   // prolongate: cur + P e_c -> nxt
   if (lev0)
-    prolong_kernel<SellA, Agg0><<<g, ANT, 0, s>>>(sa, Agg0{H->agg0}, n, cur, ecv, L.dinv, L.omega, nxt, done);
+    lev0_acc([&](auto acc) {
+      prolong_kernel<decltype(acc), Agg0><<<g, ANT, 0, s>>>(acc, Agg0{H->agg0}, n, cur, ecv, L.dinv,
+                                                             L.omega, nxt, done);
+    });
   else
     prolong_st_kernel<<<g, ANT, 0, s>>>(sta, C.d[0], C.d[1], n, cur, ecv, L.dinv, L.omega, nxt,
                                         done);
@@ -817,7 +841,10 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   for (int k = 0; k < nu; ++k) {
     double* out = (k == nu - 1) ? x : nxt;
     if (k == nu - 1 && part && lev0)
-      jacobi_dot_kernel<SellA><<<nbpart, ANT, 0, s>>>(sa, n, b, cur, out, L.dl1inv, part, done);
+      lev0_acc([&](auto acc) {
+        jacobi_dot_kernel<decltype(acc)><<<nbpart, ANT, 0, s>>>(acc, n, b, cur, out, L.dl1inv, part,
+                                                                 done);
+      });
     else
       jac(cur, out);
     if (k < nu - 1) std::swap(cur, nxt);

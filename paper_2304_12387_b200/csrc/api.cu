@@ -129,7 +129,7 @@ void hdiv_destroy(hdiv_handle h) {
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
   cudaFree(h->d_ecol);
-  cudaFree(h->d_minv);
+  cudaFree(h->d_cw);
   cudaFree(h->d_zcoef);
   cudaFree(h->d_winv);
   cudaFree(h->d_geo);
@@ -479,10 +479,8 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     if (cs != HDIV_OK) { hdiv_destroy(h); return cs; }
   }
   {
-    // SpMV inside S^-1: the SELL-32 copy of S~ (default, fastest measured: profiles/) or the
-    // matrix-free face stencil (HDIV_CHEB_STENCIL=1)
-    const char* ev = getenv("HDIV_CHEB_STENCIL");
-    h->cheb_sell = !(ev && atoi(ev) != 0);
+    // S~ inside S^-1: the cell stencil (3D, kernel_sparse.cu / cell_stencil.h) or a SELL-32
+    // copy (2D); the CSR itself serves the ABI exports and hdiv_apply_schur
     hdiv_status ss = build_schur(h, s);
     if (ss != HDIV_OK) { hdiv_destroy(h); return ss; }
     if (nranks > 1) {

@@ -81,10 +81,10 @@ struct hdiv_ctx {
   int64_t* d_srow = nullptr;      // S~ CSR (local rows; ghost columns >= nl2 for multi-GPU)
   int32_t* d_scol = nullptr;
   double* d_sval = nullptr;
-  int32_t* d_ecol = nullptr;      // S~ as SELL-32, fixed width 2d+1 (padding: col=row, val=0),
-  double* d_eval = nullptr;       //   used by the Chebyshev SpMV unless HDIV_CHEB_STENCIL=1
-  double* d_minv = nullptr;       // 1 / M~ per RT face: face weights of the S~ stencil (if used)
-  bool cheb_sell = false;         // Chebyshev SpMV through SELL (true) or the face stencil
+  int32_t* d_ecol = nullptr;      // 2D: S~ as SELL-32, fixed width 2d+1 (padding: col=row,
+  double* d_eval = nullptr;       //   val=0) for the SpMVs inside S^-1
+  double* d_cw = nullptr;         // 3D: [4][n_l2] diag(S~), +x/+y/+z face weights, + one plane
+                                  //   (the cell stencil inside S^-1, cell_stencil.h)
   int64_t snnz = 0;
   double* d_scratch = nullptr;    // reduction partials etc.
   double* d_xbuf = nullptr;       // host-API staging (lazily allocated)

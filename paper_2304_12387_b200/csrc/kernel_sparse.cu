@@ -183,6 +183,34 @@ __global__ void schur_fill_kernel(Grid g, const double* __restrict__ mdiag,
   sdinv[i] = 1.0 / d;
 }
 
+// Cell-major face weights of S~ for the matrix-free Chebyshev stencil (3D): cw[0] = S~_ii (the
+// same sum in the same face order as schur_fill_kernel), cw[1..3] = w_k = 1/M~_kk of the cell's
+// +x / +y / +z face when a neighbour (or a ghost) lies across it, else 0; cw[4] (one plane,
+// indexed X + n_x Y) = the -z interface face of a slab whose lower neighbour is a ghost.  The
+// -x / -y / -z weights of a cell are its neighbours' + weights, so every array is read
+// coalesced in the L2 (element-major) numbering.
+__global__ void cellw_kernel(Grid g, const double* __restrict__ mdiag,
+                             const double* __restrict__ ctil, double* __restrict__ cw,
+                             long long nl2) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= nl2) return;
+  long long X, Y, Z, face[6], nb[6];
+  g.cell_of_l2(i, &X, &Y, &Z);
+  faces_of(g, X, Y, Z, face, nb);
+  double d = ctil[i], w[6];
+  for (int k = 0; k < 6; ++k) {
+    w[k] = 0.0;
+    if (nb[k] < 0 && ((g.ess >> k) & 1)) continue;   // eliminated: not in F(i)
+    w[k] = 1.0 / mdiag[face[k]];
+    d += w[k];
+  }
+  cw[i] = d;
+  cw[nl2 + i] = nb[1] >= 0 ? w[1] : 0.0;
+  cw[2 * nl2 + i] = nb[3] >= 0 ? w[3] : 0.0;
+  cw[3 * nl2 + i] = nb[5] >= 0 ? w[5] : 0.0;
+  if (Z == 0 && g.ghost_lo >= 0) cw[4 * nl2 + X + g.n[0] * Y] = w[4];
+}
+
 // CSR -> SELL-32 with fixed width W: entry (row, k) at (row/32)*32*W + k*32 + row%32
 __global__ void sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ c,
                             const double* __restrict__ v, int32_t* ec, double* ev, long long n,
@@ -390,14 +418,15 @@ hdiv_status build_schur(hdiv_ctx* h, cudaStream_t s) {
   schur_fill_kernel<<<nblocks(n, 256), 256, 0, s>>>(g, h->d_mdiag, h->d_ctil, h->d_srow,
                                                     h->d_scol, h->d_sval, h->d_sdinv, n);
   HDIV_CUDA_TRY(cudaGetLastError());
-  if (!h->cheb_sell) {   // face weights 1/M~ of the matrix-free S~ stencil used inside S^-1
-    HDIV_CUDA_TRY(cudaMalloc(&h->d_minv, sizeof(double) * (h->nrt > 0 ? h->nrt : 1)));
-    recip_kernel<<<nblocks(h->nrt, 256), 256, 0, s>>>(h->d_mdiag, h->d_minv, h->nrt);
+  if (h->dim == 3) {   // S~ inside S^-1 (Chebyshev, AMG level 0): the cell stencil's weights
+    const long long lplane = h->n[0] * h->n[1];
+    HDIV_CUDA_TRY(cudaMalloc(&h->d_cw, sizeof(double) * (4 * n + lplane)));
+    HDIV_CUDA_TRY(cudaMemsetAsync(h->d_cw, 0, sizeof(double) * (4 * n + lplane), s));
+    cellw_kernel<<<nblocks(n, 256), 256, 0, s>>>(g, h->d_mdiag, h->d_ctil, h->d_cw, n);
     HDIV_CUDA_TRY(cudaGetLastError());
-    if (h->ess) HDIV_CUDA_TRY(launch_ess_fixup(h, nullptr, h->d_minv, 0.0, nullptr, s));
     return HDIV_OK;
   }
-  // sliced-ELL copy used by the SpMV inside S^-1 (coalesced slot loads)
+  // 2D: sliced-ELL copy used by the SpMV inside S^-1 (coalesced slot loads)
   const int W = 2 * h->dim + 1;
   const long long ns = (n + 31) / 32;
   HDIV_CUDA_TRY(cudaMalloc(&h->d_ecol, sizeof(int32_t) * ns * 32 * W));

@@ -981,9 +981,9 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
       if (h->d_geo && !a.winv) {
         a.geo = h->d_geo;
         count_op();
-        if (P <= 3 && epc >= 2) {
-          tri_multi_kernel<P, (P <= 3 ? 2 : 1), MODE == 1, true>
-              <<<(unsigned)((h->E + (P <= 3 ? 1 : 0)) / (P <= 3 ? 2 : 1)), 96, 0, s>>>(a, h->tab, h->E);
+        if (P <= 4 && epc >= 2) {   // (two elements fit the 48 KB of static shared memory)
+          tri_multi_kernel<P, (P <= 4 ? 2 : 1), MODE == 1, true>
+              <<<(unsigned)((h->E + (P <= 4 ? 1 : 0)) / (P <= 4 ? 2 : 1)), 96, 0, s>>>(a, h->tab, h->E);
         } else {
           tri_multi_kernel<P, 1, MODE == 1, true><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab, h->E);
         }

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <vector>
 
+#include "cell_stencil.h"
 #include "internal.h"
 
 namespace hdiv {
@@ -133,8 +134,7 @@ vupd_kernel(const double* __restrict__ Az, const double* __restrict__ v,
   }
 }
 
-// Chebyshev semi-iteration (reading A10).  first: y = d = Dinv r / theta.
-// step: r_new = r - S~ d ; d_new = c1 d + c2 Dinv r_new ; y += d_new.  `last` adds <y, v>.
+// Chebyshev semi-iteration (reading A10), first term: y_0 = D^-1 v / theta.  `last` adds <y, v>.
 __global__ void __launch_bounds__(RED_NT)
 cheb_first_kernel(const double* __restrict__ rin, const double* __restrict__ dinv, double itheta,
                   double* __restrict__ d, double* __restrict__ y, long long n, int last,
@@ -154,15 +154,17 @@ cheb_first_kernel(const double* __restrict__ rin, const double* __restrict__ din
   }
 }
 
-// S~ d with S~ in SELL-32 of width W (padding slots: col = row, val = 0)
+// Chebyshev step as a three-term recurrence on the iterate (the same polynomial as the r/d form
+// of reading A10: d_i = y_i - y_{i-1}, r_i = v - S~ y_{i-1}):
+//   y_i = y_{i-1} + c1 (y_{i-1} - y_{i-2}) + c2 D^-1 (v - S~ y_{i-1})        (y_{-1} = 0)
+// S~ through the SELL-32 copy; per row: the slots, y_{i-1} (gathered), y_{i-2}, v, D^-1 -> y_i
+// (124 B instead of the r/d form's 140: no residual / direction vectors are written).
 template <int W>
 __global__ void __launch_bounds__(RED_NT)
-cheb_step_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ eval,
-                 const double* rin, double* rout,
-                 const double* __restrict__ d, double* __restrict__ dn,
-                 const double* __restrict__ dinv, double* __restrict__ y, double c1, double c2,
-                 long long n, int last, const double* __restrict__ vin, double* part,
-                 const int* __restrict__ done) {
+cheb3_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+             const double* __restrict__ v, const double* ym1, const double* ym2,
+             const double* __restrict__ dinv, double* yout, double c1, double c2, long long n,
+             int last, double* part, const int* __restrict__ done) {
   if (done && *done) return;
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
@@ -170,14 +172,12 @@ cheb_step_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ ev
     const long long base = (i >> 5) * (32 * W) + (i & 31);
     double sd = 0.0;
 #pragma unroll
-    for (int k = 0; k < W; ++k) sd = fma(eval[base + 32 * k], d[ecol[base + 32 * k]], sd);
-    double r = rin[i] - sd;
-    rout[i] = r;
-    double dd = c1 * d[i] + c2 * dinv[i] * r;
-    dn[i] = dd;
-    double yy = y[i] + dd;
-    y[i] = yy;
-    if (last) s = fma(yy, vin[i], s);
+    for (int k = 0; k < W; ++k) sd = fma(eval[base + 32 * k], ym1[ecol[base + 32 * k]], sd);
+    const double y = ym1[i];
+    const double dprev = ym2 ? y - ym2[i] : y;
+    const double yn = y + (c1 * dprev + c2 * dinv[i] * (v[i] - sd));
+    yout[i] = yn;
+    if (last) s = fma(yn, v[i], s);
   }
   if (last && part) {
     s = block_sum(s);
@@ -185,97 +185,27 @@ cheb_step_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ ev
   }
 }
 
-// The same Chebyshev step with S~ applied matrix-free from its definition (P:463-473 entry
-// formula): S~_ii = C~_ii + sum_{k in F(i)} w_k, S~_ij = -w_k across interior face k, with the
-// face weights w_k = 1/M~_kk.  Reads per row: C~_i, the 2d face weights (each shared by two
-// rows), the neighbours' d (cache hits) instead of 2d+1 (col, val) pairs.  The diagonal is summed
-// in the same face order as the CSR rows (-x,+x,-y,+y,-z,+z), so diag and 1/diag match it.
-// One thread per element row of P cells along x: the index arithmetic is amortised over the
-// row, the row's x faces are P+1 contiguous weights and its y/z faces P contiguous ones.
-struct StencilGeo {
-  long long n[3], off[3], nl2, ghost_lo, ghost_hi;   // ghost_*: first ghost row or -1
-  int NL[3];
-  unsigned long long mx, my;                         // ceil(2^64 / NL0), ceil(2^64 / NL1)
-};
-
-__device__ __forceinline__ unsigned fdiv(unsigned v, unsigned long long m) {
-  return m ? (unsigned)__umul64hi((unsigned long long)v, m) : v;   // m = 0 <-> divisor 1
-}
-
-template <int DIM, int P>
-__global__ void __launch_bounds__(RED_NT, 6)
-cheb_stencil_kernel(StencilGeo g, const double* __restrict__ minv, const double* __restrict__ ctil,
-                    const double* rin, double* rout, const double* __restrict__ d,
-                    double* __restrict__ dn, double* __restrict__ y, double c1, double c2,
-                    int last, const double* __restrict__ vin, double* part,
-                    const int* __restrict__ done) {
+// The same step with S~ y from the cell-major weights (3D, one thread per cell, lanes over
+// consecutive cells: every stream coalesced, the six neighbours shifted copies of the same
+// rows): per cell diag, three + weights, y_{i-1}, y_{i-2}, v, y_i = 64 B, vs SELL's 124.
+#ifndef HDIV_CHEB3C_MINB
+#define HDIV_CHEB3C_MINB 8
+#endif
+template <int P>
+__global__ void __launch_bounds__(RED_NT, HDIV_CHEB3C_MINB)
+cheb3c_kernel(CellGeo g, const double* __restrict__ v, const double* __restrict__ ym1,
+              const double* ym2, double* yout, double c1, double c2, int last, double* part,
+              const int* __restrict__ done) {
   if (done && *done) return;
-  constexpr int PD = (DIM == 3) ? P * P * P : P * P;
-  const long long n0 = g.n[0], n1 = g.n[1];
-  const long long rowx = (long long)g.NL[0] * PD;      // one element row along y
-  const long long lay = rowx * g.NL[1];                // one element layer along z
   double s = 0.0;
-  // one thread per cell, lanes over consecutive cells (coalesced vectors); all divisions are
-  // by compile-time constants or by multiply-high
-  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < g.nl2;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < g.n;
        i += (long long)gridDim.x * RED_NT) {
-    const unsigned e = (unsigned)(i / PD);
-    const int il = (int)(i - (long long)e * PD);
-    const int a = il % P, b = (il / P) % P, c = (DIM == 3) ? il / (P * P) : 0;
-    const unsigned t = fdiv(e, g.mx);
-    const int ex = (int)(e - t * (unsigned)g.NL[0]);
-    int ey, ez;
-    if constexpr (DIM == 3) {
-      const unsigned u = fdiv(t, g.my);
-      ey = (int)(t - u * (unsigned)g.NL[1]);
-      ez = (int)u;
-    } else {
-      ey = (int)t;
-      ez = 0;
-    }
-    const long long X = (long long)ex * P + a, Y = (long long)ey * P + b, Z = (long long)ez * P + c;
-    const long long fx = g.off[0] + X + (n0 + 1) * (DIM == 3 ? Y + n1 * Z : Y);
-    const long long fy = g.off[1] + X + n0 * (DIM == 3 ? Y + (n1 + 1) * Z : Y);
-    const double w0 = minv[fx], w1 = minv[fx + 1], w2 = minv[fy], w3 = minv[fy + n0];
-    double w4 = 0.0, w5 = 0.0;
-    if constexpr (DIM == 3) {
-      const long long fz = g.off[2] + X + n0 * (Y + n1 * Z);
-      w4 = minv[fz];
-      w5 = minv[fz + n0 * n1];
-    }
-    double diag = ctil[i];
-    diag += w0;
-    diag += w1;
-    diag += w2;
-    diag += w3;
-    if constexpr (DIM == 3) {
-      diag += w4;
-      diag += w5;
-    }
-    const double di = d[i];
-    double sd = diag * di;
-    if (X > 0) sd -= w0 * d[a > 0 ? i - 1 : i - PD + (P - 1)];
-    if (X + 1 < n0) sd -= w1 * d[a < P - 1 ? i + 1 : i + PD - (P - 1)];
-    if constexpr (DIM == 3) {
-      if (Y > 0) sd -= w2 * d[b > 0 ? i - P : i - rowx + P * (P - 1)];
-      if (Y + 1 < n1) sd -= w3 * d[b < P - 1 ? i + P : i + rowx - P * (P - 1)];
-      if (Z > 0) sd -= w4 * d[c > 0 ? i - P * P : i - lay + P * P * (P - 1)];
-      else if (g.ghost_lo >= 0) sd -= w4 * d[g.ghost_lo + X + n0 * Y];
-      if (Z + 1 < g.n[2]) sd -= w5 * d[c < P - 1 ? i + P * P : i + lay - P * P * (P - 1)];
-      else if (g.ghost_hi >= 0) sd -= w5 * d[g.ghost_hi + X + n0 * Y];
-    } else {
-      if (Y > 0) sd -= w2 * d[b > 0 ? i - P : i - rowx + P * (P - 1)];
-      else if (g.ghost_lo >= 0) sd -= w2 * d[g.ghost_lo + X];
-      if (Y + 1 < n1) sd -= w3 * d[b < P - 1 ? i + P : i + rowx - P * (P - 1)];
-      else if (g.ghost_hi >= 0) sd -= w3 * d[g.ghost_hi + X];
-    }
-    const double r = rin[i] - sd;
-    rout[i] = r;
-    const double dd = c1 * di + c2 * (1.0 / diag) * r;
-    dn[i] = dd;
-    const double yy = y[i] + dd;
-    y[i] = yy;
-    if (last) s = fma(yy, vin[i], s);
+    const double sy = cell_apply<P, true>(g, i, [&](long long j) { return ym1[j]; });
+    const double y = ym1[i];
+    const double dprev = ym2 ? y - ym2[i] : y;
+    const double yn = y + (c1 * dprev + c2 * ((v[i] - sy) / g.cw[i]));
+    yout[i] = yn;
+    if (last) s = fma(yn, v[i], s);
   }
   if (last && part) {
     s = block_sum(s);
@@ -493,40 +423,21 @@ void minres_free(hdiv_ctx* h) {
   h->mw = nullptr;
 }
 
-template <int DIM, int P>
-static cudaError_t stencil_p(const hdiv_ctx* h, const StencilGeo& g, const double* rin,
-                             double* rout, const double* d, double* dn, double* y, double c1,
-                             double c2, int last, const double* vin, double* part, const int* done,
-                             cudaStream_t s) {
-  cheb_stencil_kernel<DIM, P><<<h->mw->nb, RED_NT, 0, s>>>(g, h->d_minv, h->d_ctil, rin, rout, d,
-                                                            dn, y, c1, c2, last, vin, part, done);
+static cudaError_t launch_cheb3c(const hdiv_ctx* h, const double* v, const double* ym1,
+                                 const double* ym2, double* yo, double c1, double c2, int last,
+                                 double* part, const int* done, cudaStream_t s) {
+  const CellGeo g = make_cellgeo(h);
+  const unsigned nbk = h->mw->nb;   // the reduction grid (the consumers sum nb partials)
+  switch (h->p) {
+    case 1: cheb3c_kernel<1><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    case 2: cheb3c_kernel<2><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    case 3: cheb3c_kernel<3><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    case 4: cheb3c_kernel<4><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    case 5: cheb3c_kernel<5><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    case 6: cheb3c_kernel<6><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
-}
-
-static cudaError_t launch_cheb_stencil(const hdiv_ctx* h, const double* rin, double* rout,
-                                       const double* d, double* dn, double* y, double c1,
-                                       double c2, int last, const double* vin, double* part,
-                                       const int* done, cudaStream_t s) {
-  StencilGeo g;
-  for (int a = 0; a < 3; ++a) { g.n[a] = h->n[a]; g.off[a] = h->off[a]; g.NL[a] = (int)h->NL[a]; }
-  g.nl2 = h->nl2;
-  const long long lplane = (h->dim == 3) ? h->n[0] * h->n[1] : h->n[0];
-  g.ghost_lo = (h->rank > 0) ? h->nl2 : -1;
-  g.ghost_hi = (h->rank < h->nranks - 1) ? h->nl2 + lplane : -1;
-  // exact 32-bit division by multiply-high: q = umulhi64(v, ceil(2^64 / D)) for v, D < 2^32
-  auto magic = [](unsigned long long D) {
-    return D <= 1 ? 0ull : (~0ull) / D + 1ull;
-  };
-  g.mx = magic((unsigned long long)h->NL[0]);
-  g.my = magic((unsigned long long)h->NL[1]);
-#define HDIV_STENCIL_CASE(DD, PP) \
-  if (h->dim == DD && h->p == PP) return stencil_p<DD, PP>(h, g, rin, rout, d, dn, y, c1, c2, last, vin, part, done, s);
-  HDIV_STENCIL_CASE(3, 1) HDIV_STENCIL_CASE(3, 2) HDIV_STENCIL_CASE(3, 3)
-  HDIV_STENCIL_CASE(3, 4) HDIV_STENCIL_CASE(3, 5) HDIV_STENCIL_CASE(3, 6)
-  HDIV_STENCIL_CASE(2, 1) HDIV_STENCIL_CASE(2, 2) HDIV_STENCIL_CASE(2, 3)
-  HDIV_STENCIL_CASE(2, 4) HDIV_STENCIL_CASE(2, 5) HDIV_STENCIL_CASE(2, 6)
-#undef HDIV_STENCIL_CASE
-  return cudaErrorInvalidValue;
 }
 
 static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
@@ -552,32 +463,28 @@ static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, doub
   }
   const long long n = h->nl2;
   const int k = h->opts.cheb_degree;
-  cheb_first_kernel<<<h->mw->nb, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0], y, n,
-                                                  k == 1, part, done);
+  // three-term recurrence on the iterate: y_i in d[i & 1] (ghost space for slabs), the last
+  // one straight into y; S~ y_{i-1} by the cell stencil (3D) or the SELL copy (2D)
+  cheb_first_kernel<<<h->mw->nb, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0],
+                                                  k == 1 ? y : mw->d[0], n, k == 1, part, done);
   HDIV_CUDA_TRY(cudaGetLastError());
-  const double* rin = vq;
   for (int i = 1; i < k; ++i) {
-    double* dprev = mw->d[(i - 1) & 1];
+    double* ym1 = mw->d[(i - 1) & 1];
     if (h->nranks > 1) {
-      hdiv_status st = comm_l2_ghosts(h, dprev, s);
+      hdiv_status st = comm_l2_ghosts(h, ym1, s);
       if (st != HDIV_OK) return st;
     }
-    if (!h->cheb_sell) {
-      cudaError_t e = launch_cheb_stencil(h, rin, mw->r, dprev, mw->d[i & 1], y, mw->c1[i - 1],
-                                          mw->c2[i - 1], i == k - 1, vq, part, done, s);
-      HDIV_CUDA_TRY(e);
-    } else if (h->dim == 3)
-      cheb_step_kernel<7><<<h->mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
-                                                        mw->d[i & 1], h->d_sdinv, y,
-                                                        mw->c1[i - 1], mw->c2[i - 1], n,
-                                                        i == k - 1, vq, part, done);
-    else
-      cheb_step_kernel<5><<<h->mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, mw->r, dprev,
-                                                        mw->d[i & 1], h->d_sdinv, y,
-                                                        mw->c1[i - 1], mw->c2[i - 1], n,
-                                                        i == k - 1, vq, part, done);
-    HDIV_CUDA_TRY(cudaGetLastError());
-    rin = mw->r;
+    double* yo = (i == k - 1) ? y : mw->d[i & 1];
+    const double* ym2 = (i == 1) ? nullptr : mw->d[i & 1];
+    if (h->d_cw) {
+      HDIV_CUDA_TRY(launch_cheb3c(h, vq, ym1, ym2, yo, mw->c1[i - 1], mw->c2[i - 1], i == k - 1,
+                                  part, done, s));
+    } else {
+      cheb3_kernel<5><<<h->mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, vq, ym1, ym2, h->d_sdinv,
+                                                    yo, mw->c1[i - 1], mw->c2[i - 1], n, i == k - 1,
+                                                    part, done);
+      HDIV_CUDA_TRY(cudaGetLastError());
+    }
   }
   return HDIV_OK;
 }

@@ -144,17 +144,17 @@ def test_uniform_flow_on_the_gpu():
     op.close()
 
 
-def test_masked_chebyshev_stencil_path(monkeypatch):
-    """The matrix-free face-stencil SpMV inside S^-1 (HDIV_CHEB_STENCIL=1) drops the eliminated
-    faces too (1/M~ weights zeroed there)."""
+@pytest.mark.parametrize("ess", [1 | 2 | 16, 63, 4 | 32])
+def test_masked_chebyshev_cell_stencil(ess):
+    """The matrix-free cell stencil inside S^-1 (3D) drops the eliminated faces too (their
+    weights are 0 in the cell-major arrays and they are not in diag(S~))."""
     from oracle import operators, solvers
     from paper_2304_12387_b200 import from_problem
-    pr = _problem("c2", (4, 3, 3), 3, 1 | 2 | 16)
+    pr = _problem("c2", (4, 3, 3), 3, ess)
     A = operators.Assembled(pr)
     P = solvers.BlockDiagPrecond(A)
     v = random_vector(A.n_rt + A.n_l2, 13)
     zo = P.apply(v)
-    monkeypatch.setenv("HDIV_CHEB_STENCIL", "1")
     op = from_problem(pr)
     z = _host(op.apply_precond(_dev(v)))
     op.close()
