@@ -203,7 +203,10 @@ def test_config2_minres_full():
 # full BASELINE sizes + the bench's p sweep sizes (bench.py `sweep`: N = 160/128/128/96/80 for
 # p = 2..6), each in the launch configuration bench.py times
 FULL_CASES = [("c4", 4, None), ("c3", 4, None), ("c3gv", 4, None),
-              ("c4", 2, 160), ("c4", 3, 128), ("c4", 5, 96), ("c4", 6, 80)]
+              ("c4", 2, 160), ("c4", 3, 128), ("c4", 5, 96), ("c4", 6, 80),
+              # config 5b's size (128^3, p = 6): 1.81e9 DOFs, S~ with 3.2e9 nonzeros (> 2^31: the
+              # int64 row pointers of the setup's scan and every 64-bit index of the apply)
+              ("c4", 6, 128)]
 
 
 @pytest.mark.parametrize("name,p,Nn", FULL_CASES)
