@@ -124,6 +124,10 @@ cudaError_t launch_affine_apply_range(const hdiv_ctx* h, const double* x, double
                                       const int* skip = nullptr);
 cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                 const int* skip, cudaStream_t s);
+// box-kernel block apply with the fused MINRES partial <y, x> (one partial per tile)
+cudaError_t launch_affine_apply_dot(const hdiv_ctx* h, const double* x, double* y, const int* skip,
+                                    double* dpart, cudaStream_t s);
+long long affine_num_tiles(const hdiv_ctx* h);
 cudaError_t launch_general_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                  const int* skip, cudaStream_t s);
 cudaError_t launch_l2_diag(const hdiv_ctx* h, double* w1, cudaStream_t s);

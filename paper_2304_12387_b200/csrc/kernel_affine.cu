@@ -263,10 +263,11 @@ __device__ __forceinline__ void load_component(const AffArgs& a, const TileInfo&
 
 // -------- one component phase (AX), data already in `su` ------------------------------------
 template <int P, int TX, int TY, int TZ, int NT, int AX, bool BLOCK, bool XD = kXDirect,
-          bool ESS = false>
+          bool ESS = false, bool DOT = false>
 __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
                                           const TabAffine& tab, double* su, const double* sq,
-                                          const double* hq, const double* sco, double* acc) {
+                                          const double* hq, const double* sco, double* acc,
+                                          double& dsum) {
   using C = CG<P, TX, TY, TZ, AX>;
   using G = Geo<P, TX, TY, TZ>;
   using O = Own<P, TX, TY, TZ, NT>;
@@ -429,7 +430,10 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
           if (ESS && i == 0 && et == 0 && ess_lo)   // identity row of the eliminated plane
             o = a.x[gtile + (l1 * gs1 + l2 * gs2) + P * gsa];
           if (AX == 0 && !XD) eb[i * C::SA] = o;
-          else __stcs(gl + ((et + 1) * P + i) * gsa, o);
+          else {
+            __stcs(gl + ((et + 1) * P + i) * gsa, o);
+            if constexpr (DOT) dsum = fma(o, __ldg(a.x + (gl - a.y) + ((et + 1) * P + i) * gsa), dsum);
+          }
         }
         double s = 0.0;
 #pragma unroll
@@ -441,7 +445,10 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
       const double o = (ESS && ess_hi) ? a.x[gtile + (l1 * gs1 + l2 * gs2) + (m_a + 1) * P * gsa]
                               : carry + (BLOCK ? qprev : 0.0);
       if (AX == 0 && !XD) line[(m_a + 1) * P * C::SA] = o;
-      else __stcs(gl + (m_a + 1) * P * gsa, o);
+      else {
+        __stcs(gl + (m_a + 1) * P * gsa, o);
+        if constexpr (DOT) dsum = fma(o, __ldg(a.x + (gl - a.y) + (m_a + 1) * P * gsa), dsum);
+      }
     }
   }
   __syncthreads();
@@ -453,15 +460,20 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     rows<NT, NO0, C::E1, C::E2, C::S1, C::S2>(
         yt + P, ext0, ext01, su + P, [&](int i) { return i < own_hi; },
         [&](int i) { return i < hi1; }, [&](int i) { return i < hi2; },
-        [&](double* g, const double* s) { __stcs(g, *s); });
+        [&](double* g, const double* s) {
+          __stcs(g, *s);
+          if constexpr (DOT) dsum = fma(*s, __ldg(a.x + (g - a.y)), dsum);
+        });
     __syncthreads();
   }
 }
 
+// DOT: the MINRES partial <y, x> of this tile's owned outputs -> dpart[blockIdx.x] (the separate
+// dot pass over both vectors is saved; x is re-read where each output is stored: L1/L2 hits)
 template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB, int MINB, bool XD,
-          bool ESS = false>
+          bool ESS = false, bool DOT = false>
 __global__ void __launch_bounds__(NT, MINB)
-affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
+affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab, double* __restrict__ dpart) {
   using G = Geo<P, TX, TY, TZ>;
   using O = Own<P, TX, TY, TZ, NT>;
   constexpr int P3 = G::P3;
@@ -564,6 +576,7 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
   double acc[O::NACC];
 #pragma unroll
   for (int k = 0; k < O::NACC; ++k) acc[k] = 0.0;
+  double dsum = 0.0;
 
   if constexpr (DB) cp_async_wait_group<1>();
   else cp_async_wait_group<0>();
@@ -606,28 +619,28 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
     load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufB);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS, DOT>(a, ti, tab, bufA, sq, hq0, sco, acc, dsum);
     // ---- group 3: z component -> A ; compute y from B ----
     load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<1>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS>(a, ti, tab, bufB, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS, DOT>(a, ti, tab, bufB, sq, hq1, sco, acc, dsum);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS, DOT>(a, ti, tab, bufA, sq, hq2, sco, acc, dsum);
   } else {
     load_component<P, TX, TY, TZ, NT, 0>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq0, sco, acc);
+    component<P, TX, TY, TZ, NT, 0, BLOCK, XD, ESS, DOT>(a, ti, tab, bufA, sq, hq0, sco, acc, dsum);
     load_component<P, TX, TY, TZ, NT, 1>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq1, sco, acc);
+    component<P, TX, TY, TZ, NT, 1, BLOCK, XD, ESS, DOT>(a, ti, tab, bufA, sq, hq1, sco, acc, dsum);
     load_component<P, TX, TY, TZ, NT, 2>(a, ti, bufA);
     cp_async_wait_group<0>();
     __syncthreads();
-    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS>(a, ti, tab, bufA, sq, hq2, sco, acc);
+    component<P, TX, TY, TZ, NT, 2, BLOCK, XD, ESS, DOT>(a, ti, tab, bufA, sq, hq2, sco, acc, dsum);
   }
 
   if constexpr (BLOCK) {
@@ -642,18 +655,33 @@ affine_apply_kernel(const AffArgs a, const __grid_constant__ TabAffine tab) {
           double* yc = yq + gelem(X / P, Y / P, 0) * P3 + (X % P) + P * (Y % P);
 #pragma unroll
           for (int z = 0; z < G::CZ; ++z)
-            if (z < ti.m[2] * P)
-              __stcs(yc + (long long)(z / P) * NLx * NLy * P3 + P * P * (z % P), acc[j * G::CZ + z]);
+            if (z < ti.m[2] * P) {
+              const long long off = (long long)(z / P) * NLx * NLy * P3 + P * P * (z % P);
+              __stcs(yc + off, acc[j * G::CZ + z]);
+              if constexpr (DOT) dsum = fma(acc[j * G::CZ + z], __ldg(a.x + (yc - a.y) + off), dsum);
+            }
         }
       }
+    }
+  }
+  if constexpr (DOT) {   // fixed-order block sum -> this tile's partial
+    __shared__ double red[NT / 32];
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, o);
+    if ((tid & 31) == 0) red[tid >> 5] = dsum;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) t += red[w];
+      dpart[blockIdx.x] = t;
     }
   }
 }
 
 template <int P, int TX, int TY, int TZ, int NT, bool BLOCK, bool DB = true, int MINB = 0, bool XD = kXDirect,
-          bool ESS = false>
+          bool ESS = false, bool DOT = false>
 cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* skip,
-                     cudaStream_t s) {
+                     cudaStream_t s, double* dpart = nullptr) {
   using G = Geo<P, TX, TY, TZ>;
   AffArgs a;
   a.x = x; a.y = y; a.coef = h->d_coef;
@@ -673,7 +701,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   a.flags |= tz0 << 8;
   if (tz1 <= tz0) return cudaSuccess;
   const size_t smem = G::smem_doubles(BLOCK, DB) * sizeof(double);
-  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, ESS>;
+  auto kern = affine_apply_kernel<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, ESS, DOT>;
   static bool attr_done = false;   // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -683,7 +711,7 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
   }
   const long long nblk = (long long)a.ntile[0] * a.ntile[1] * (tz1 - tz0);
   count_op();
-  kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff);
+  kern<<<(unsigned)nblk, NT, smem, s>>>(a, h->taff, dpart);
   return cudaGetLastError();
 }
 
@@ -694,26 +722,56 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
 // Eliminated essential sides use an instantiation of their own (ESS).
 template <bool BLOCK, int P, int TX, int TY, int TZ, int NT, bool DB, int MINB, bool XD>
 cudaError_t launch_tile(const hdiv_ctx* h, const double* x, double* y, const int* k,
-                        cudaStream_t s) {
+                        cudaStream_t s, double* dpart) {
+  if (dpart) {   // block apply with the fused MINRES partial <y, x> (whole grid, one launch)
+    if constexpr (BLOCK) {
+      if (h->ess) return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, true, true>(h, x, y, k, s, dpart);
+      return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, false, true>(h, x, y, k, s, dpart);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (h->ess) return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, true>(h, x, y, k, s);
   return launch_t<P, TX, TY, TZ, NT, BLOCK, DB, MINB, XD, false>(h, x, y, k, s);
 }
 
+// tiles of h's production tile shape (the DOT partials: one per tile)
+template <int TX, int TY, int TZ>
+long long ntiles_of(const hdiv_ctx* h) {
+  return ((h->NL[0] + TX - 1) / TX) * ((h->NL[1] + TY - 1) / TY) * ((h->NL[2] + TZ - 1) / TZ);
+}
+
 template <bool BLOCK>
 cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k,
-                     cudaStream_t s) {
+                     cudaStream_t s, double* dpart = nullptr) {
   switch (h->p) {
-    case 1: return launch_tile<BLOCK, 1, 8, 8, 4, 128, true, 0, kXDirect>(h, x, y, k, s);
-    case 2: return launch_tile<BLOCK, 2, 8, 4, 4, 128, true, 0, kXDirect>(h, x, y, k, s);
-    case 3: return launch_tile<BLOCK, 3, 4, 4, 2, 160, false, 0, kXDirect>(h, x, y, k, s);
-    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, 0, kXDirect>(h, x, y, k, s);
-    case 5: return launch_tile<BLOCK, 5, 3, 2, 2, 160, false, 0, false>(h, x, y, k, s);
-    case 6: return launch_tile<BLOCK, 6, 3, 2, 2, 224, false, 2, false>(h, x, y, k, s);
+    case 1: return launch_tile<BLOCK, 1, 8, 8, 4, 128, true, 0, kXDirect>(h, x, y, k, s, dpart);
+    case 2: return launch_tile<BLOCK, 2, 8, 4, 4, 128, true, 0, kXDirect>(h, x, y, k, s, dpart);
+    case 3: return launch_tile<BLOCK, 3, 4, 4, 2, 160, false, 0, kXDirect>(h, x, y, k, s, dpart);
+    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, 0, kXDirect>(h, x, y, k, s, dpart);
+    case 5: return launch_tile<BLOCK, 5, 3, 2, 2, 160, false, 0, false>(h, x, y, k, s, dpart);
+    case 6: return launch_tile<BLOCK, 6, 3, 2, 2, 224, false, 2, false>(h, x, y, k, s, dpart);
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
+
+// the block apply with the fused partial <y, x>: one partial per tile into dpart (the caller
+// sums affine_num_tiles(h) of them); single launch over all tiles
+cudaError_t launch_affine_apply_dot(const hdiv_ctx* h, const double* x, double* y, const int* skip,
+                                    double* dpart, cudaStream_t s) {
+  return dispatch<true>(h, x, y, skip, s, dpart);
+}
+
+long long affine_num_tiles(const hdiv_ctx* h) {
+  switch (h->p) {
+    case 1: return ntiles_of<8, 8, 4>(h);
+    case 2: return ntiles_of<8, 4, 4>(h);
+    case 3: return ntiles_of<4, 4, 2>(h);
+    case 4: return ntiles_of<4, 2, 2>(h);
+    default: return ntiles_of<3, 2, 2>(h);
+  }
+}
 
 cudaError_t launch_affine_apply(const hdiv_ctx* h, const double* x, double* y, int mode,
                                 const int* skip, cudaStream_t s) {

@@ -352,6 +352,8 @@ struct MinresWork {
   double *v[3], *w[3], *z[2], *Az, *r, *d[2];
   double *part_a, *part_b, *part_c, *loc, *glob;
   double* mtinv = nullptr;         // 1 / (tau M~) [n_rt]
+  double* part_t = nullptr;        // box kernel, one rank: per-tile partials of <A z, z>
+  long long ntiles = 0;
   MState* st = nullptr;            // [2]: iteration j reads st[j & 1], publishes st[(j + 1) & 1]
   MState* st_host = nullptr;       // pinned
   cudaStream_t stream = nullptr;   // own non-blocking stream (graph capture needs one)
@@ -391,6 +393,10 @@ static hdiv_status ensure_work(hdiv_ctx* h) {
     mw->ex_hi = h->off[last] + lplane;
   }
   HDIV_CUDA_TRY(cudaMalloc(&mw->st, 2 * sizeof(MState)));
+  if (h->kernel == 2 && h->nranks == 1) {   // <A z, z> fused into the block apply
+    mw->ntiles = affine_num_tiles(h);
+    HDIV_CUDA_TRY(cudaMalloc(&mw->part_t, sizeof(double) * mw->ntiles));
+  }
   HDIV_CUDA_TRY(cudaMalloc(&mw->mtinv, sizeof(double) * (h->nrt > 0 ? h->nrt : 1)));
   tau_minv_kernel<<<nb(h->nrt, 256), 256>>>(h->d_mdiag, h->opts.tau, mw->mtinv, h->nrt);
   HDIV_CUDA_TRY(cudaGetLastError());
@@ -417,6 +423,7 @@ void minres_free(hdiv_ctx* h) {
   cudaFree(h->mw->buf);
   cudaFree(h->mw->st);
   cudaFree(h->mw->mtinv);
+  cudaFree(h->mw->part_t);
   cudaFreeHost(h->mw->st_host);
   if (h->mw->stream) cudaStreamDestroy(h->mw->stream);
   delete h->mw;
@@ -579,18 +586,28 @@ hdiv_status minres(hdiv_ctx* h, const double* b, double* x, double rtol, int max
     MState* stc = mw->st + (j & 1);
     MState* stn = mw->st + ((j + 1) & 1);
     const int* done = &stc->done;
-    HDIV_CUDA_TRY(apply_block_dev(h, zc, mw->Az, done, s));
-    // single rank: the consumers (vupd, scalar) sum the partials themselves — two launches
-    // fewer per iteration; multi-rank: local reduction + all-gather as before
     const bool one = (P == 1);
-    dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_c,
-                                             done);
-    HDIV_CUDA_TRY(cudaGetLastError());
     hdiv_status st = HDIV_OK;
-    if (!one && (st = reduce_scalar(h, mw->part_c, nullptr, done, s)) != HDIV_OK) return st;
+    const double* dpart = nullptr;   // vupd sums these nb partials itself (single rank)
+    if (mw->part_t) {
+      // box kernel, one rank: <A z, z> fused into the block apply (one partial per tile, summed
+      // in tile order) — the separate pass over A z and z is saved
+      HDIV_CUDA_TRY(launch_affine_apply_dot(h, zc, mw->Az, done, mw->part_t, s));
+      local_reduce_kernel<<<1, RED_NT, 0, s>>>(mw->part_t, nullptr, mw->loc, done, (int)mw->ntiles);
+      HDIV_CUDA_TRY(cudaGetLastError());
+    } else {
+      HDIV_CUDA_TRY(apply_block_dev(h, zc, mw->Az, done, s));
+      // single rank: the consumers (vupd, scalar) sum the partials themselves — two launches
+      // fewer per iteration; multi-rank: local reduction + all-gather as before
+      dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, zc, n, mw->ex_lo, mw->ex_hi, mw->part_c,
+                                               done);
+      HDIV_CUDA_TRY(cudaGetLastError());
+      if (!one && (st = reduce_scalar(h, mw->part_c, nullptr, done, s)) != HDIV_OK) return st;
+      if (one) dpart = mw->part_c;
+    }
     vupd_kernel<<<h->mw->nb, RED_NT, 0, s>>>(mw->Az, vc, vo, vn, zn, mw->mtinv, h->opts.tau,
                                               nrt, n, mw->ex_lo, mw->ex_hi, stc, mw->glob, P,
-                                              one ? mw->part_c : nullptr, mw->nb, mw->part_a);
+                                              dpart, mw->nb, mw->part_a);
     HDIV_CUDA_TRY(cudaGetLastError());
     if ((st = cheb_apply(h, vn + nrt, zn + nrt, mw->part_b, done, s)) != HDIV_OK) return st;
     if (!one && (st = reduce_scalar(h, mw->part_a, mw->part_b, done, s)) != HDIV_OK) return st;
