@@ -191,18 +191,28 @@ cheb3_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ eval,
 #ifndef HDIV_CHEB3C_MINB
 #define HDIV_CHEB3C_MINB 8
 #endif
-template <int P>
+// Y0 = 1: y_{i-1} is the first term y_0 = D^-1 v / theta, formed on the fly from v and D^-1 at
+// each stencil point (the first term is never stored: one pass over the L2 vectors fewer);
+// Y0 = 2: y_{i-2} is y_0 (the second step), likewise
+template <int P, int Y0>
 __global__ void __launch_bounds__(RED_NT, HDIV_CHEB3C_MINB)
 cheb3c_kernel(CellGeo g, const double* __restrict__ v, const double* __restrict__ ym1,
-              const double* ym2, double* yout, double c1, double c2, int last, double* part,
-              const int* __restrict__ done) {
+              const double* ym2, const double* __restrict__ dinv, double itheta, double* yout,
+              double c1, double c2, int last, double* part, const int* __restrict__ done) {
   if (done && *done) return;
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < g.n;
        i += (long long)gridDim.x * RED_NT) {
-    const double sy = cell_apply<P, true>(g, i, [&](long long j) { return ym1[j]; });
-    const double y = ym1[i];
-    const double dprev = ym2 ? y - ym2[i] : y;
+    double sy, y;
+    if constexpr (Y0 == 1) {
+      sy = cell_apply<P, false>(g, i, [&](long long j) { return dinv[j] * v[j] * itheta; });
+      y = dinv[i] * v[i] * itheta;
+    } else {
+      sy = cell_apply<P, true>(g, i, [&](long long j) { return ym1[j]; });
+      y = ym1[i];
+    }
+    const double yo = (Y0 == 2) ? dinv[i] * v[i] * itheta : (ym2 ? ym2[i] : 0.0);
+    const double dprev = (Y0 == 1) ? y : y - yo;
     const double yn = y + (c1 * dprev + c2 * ((v[i] - sy) / g.cw[i]));
     yout[i] = yn;
     if (last) s = fma(yn, v[i], s);
@@ -430,21 +440,34 @@ void minres_free(hdiv_ctx* h) {
   h->mw = nullptr;
 }
 
-static cudaError_t launch_cheb3c(const hdiv_ctx* h, const double* v, const double* ym1,
-                                 const double* ym2, double* yo, double c1, double c2, int last,
-                                 double* part, const int* done, cudaStream_t s) {
-  const CellGeo g = make_cellgeo(h);
+template <int Y0>
+static cudaError_t cheb3c_y0(const hdiv_ctx* h, const CellGeo& g, const double* v, const double* ym1,
+                             const double* ym2, double* yo, double c1, double c2, int last,
+                             double* part, const int* done, cudaStream_t s) {
   const unsigned nbk = h->mw->nb;   // the reduction grid (the consumers sum nb partials)
+  const double* di = h->d_sdinv;
+  const double it = h->mw->itheta;
   switch (h->p) {
-    case 1: cheb3c_kernel<1><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
-    case 2: cheb3c_kernel<2><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
-    case 3: cheb3c_kernel<3><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
-    case 4: cheb3c_kernel<4><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
-    case 5: cheb3c_kernel<5><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
-    case 6: cheb3c_kernel<6><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, yo, c1, c2, last, part, done); break;
+    case 1: cheb3c_kernel<1, Y0><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, di, it, yo, c1, c2, last, part, done); break;
+    case 2: cheb3c_kernel<2, Y0><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, di, it, yo, c1, c2, last, part, done); break;
+    case 3: cheb3c_kernel<3, Y0><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, di, it, yo, c1, c2, last, part, done); break;
+    case 4: cheb3c_kernel<4, Y0><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, di, it, yo, c1, c2, last, part, done); break;
+    case 5: cheb3c_kernel<5, Y0><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, di, it, yo, c1, c2, last, part, done); break;
+    case 6: cheb3c_kernel<6, Y0><<<nbk, RED_NT, 0, s>>>(g, v, ym1, ym2, di, it, yo, c1, c2, last, part, done); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+// step i of the recurrence through the cell stencil; y0: 1 = y_{i-1} is y_0 (formed on the fly),
+// 2 = y_{i-2} is y_0, 0 = both stored
+static cudaError_t launch_cheb3c(const hdiv_ctx* h, const double* v, const double* ym1,
+                                 const double* ym2, double* yo, double c1, double c2, int last,
+                                 double* part, const int* done, cudaStream_t s, int y0 = 0) {
+  const CellGeo g = make_cellgeo(h);
+  if (y0 == 1) return cheb3c_y0<1>(h, g, v, ym1, ym2, yo, c1, c2, last, part, done, s);
+  if (y0 == 2) return cheb3c_y0<2>(h, g, v, ym1, ym2, yo, c1, c2, last, part, done, s);
+  return cheb3c_y0<0>(h, g, v, ym1, ym2, yo, c1, c2, last, part, done, s);
 }
 
 static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
@@ -472,9 +495,17 @@ static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, doub
   const int k = h->opts.cheb_degree;
   // three-term recurrence on the iterate: y_i in d[i & 1] (ghost space for slabs), the last
   // one straight into y; S~ y_{i-1} by the cell stencil (3D) or the SELL copy (2D)
-  cheb_first_kernel<<<h->mw->nb, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0],
-                                                  k == 1 ? y : mw->d[0], n, k == 1, part, done);
-  HDIV_CUDA_TRY(cudaGetLastError());
+  // one rank, cell stencil, degree >= 2: y_0 = D^-1 v / theta is never stored (steps 1 and 2
+  // form it on the fly); otherwise the first term is written by its own pass
+#ifndef HDIV_Y0_FLY
+#define HDIV_Y0_FLY 1
+#endif
+  const bool y0_fly = HDIV_Y0_FLY && h->d_cw && h->nranks == 1 && k >= 2;
+  if (!y0_fly) {
+    cheb_first_kernel<<<h->mw->nb, RED_NT, 0, s>>>(vq, h->d_sdinv, mw->itheta, mw->d[0],
+                                                    k == 1 ? y : mw->d[0], n, k == 1, part, done);
+    HDIV_CUDA_TRY(cudaGetLastError());
+  }
   for (int i = 1; i < k; ++i) {
     double* ym1 = mw->d[(i - 1) & 1];
     if (h->nranks > 1) {
@@ -484,8 +515,9 @@ static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, doub
     double* yo = (i == k - 1) ? y : mw->d[i & 1];
     const double* ym2 = (i == 1) ? nullptr : mw->d[i & 1];
     if (h->d_cw) {
+      const int y0 = y0_fly ? (i == 1 ? 1 : i == 2 ? 2 : 0) : 0;
       HDIV_CUDA_TRY(launch_cheb3c(h, vq, ym1, ym2, yo, mw->c1[i - 1], mw->c2[i - 1], i == k - 1,
-                                  part, done, s));
+                                  part, done, s, y0));
     } else {
       cheb3_kernel<5><<<h->mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, vq, ym1, ym2, h->d_sdinv,
                                                     yo, mw->c1[i - 1], mw->c2[i - 1], n, i == k - 1,
