@@ -799,15 +799,9 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
       });
     else jacobi_kernel<StA><<<g, ANT, 0, s>>>(sta, n, b, xin, xout, L.dl1inv, done);
   };
-#ifndef HDIV_AMG_FUSE1
-#define HDIV_AMG_FUSE1 1
-#endif
-  if (HDIV_AMG_FUSE1 && nu >= 2) {
-    // the first sweep from x = 0 is x_1 = D^-1 b; the second takes x_1 on the fly from b
-    // (jacobi_kernel with xin = nullptr): one level pass fewer than storing x_1 first
-    jac(nullptr, cur);
-    for (int k = 2; k < nu; ++k) { jac(cur, nxt); std::swap(cur, nxt); }
-  } else if (nu >= 1) {
+  if (nu >= 1) {
+    // (forming x_1 = D^-1 b on the fly inside the second sweep instead of storing it measured
+    //  slower at config 4: 25.0 -> 25.5 ms per MINRES iteration — two loads per neighbour)
     scale_kernel<<<g, ANT, 0, s>>>(n, b, L.dl1inv, cur, done);
     for (int k = 1; k < nu; ++k) { jac(cur, nxt); std::swap(cur, nxt); }
   } else {
