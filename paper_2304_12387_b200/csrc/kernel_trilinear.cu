@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(NT) tri_kernel(const TriArgs a, const __grid_c
 // passes of RT component c for all EPC elements, so a stage's lines fill the lanes (one element
 // leaves 37 % of them idle at p = 4: 16-24 lines per component and stage) — same arithmetic,
 // same order per output as tri_kernel<P, 96, MODE>.
-template <int P, int EPC, bool BLOCK, bool SG = false>
+template <int P, int EPC, bool BLOCK, bool SG = false, bool ESS = true>
 __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
                                                        const __grid_constant__ Tab1D tab,
                                                        long long E) {
@@ -630,26 +630,34 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
     cp_async8z(&sX[el][v * 3 + d], a.vert + (ok ? g * 3 + d : 0), ok);
   }
   // gather u (eliminated essential faces act as zero inputs; absent elements as zeros)
+  // component strides (64-bit, once): face (li, lj, lk) of component c of element (ex, ey, ez)
+  // at g_c(e) + li + lj s1_c + lk s2_c
+  const long long s1x = nx + 1, s2x = (nx + 1) * ny, s1y = nx, s2y = nx * (ny + 1), s1z = nx, s2z = nx * ny;
+  auto gbase = [&](int c, int ex, int ey, int ez) -> long long {
+    const long long X = (long long)ex * P, Y = (long long)ey * P, Z = (long long)ez * P;
+    return c == 0 ? a.off[0] + X + Y * s1x + Z * s2x
+         : c == 1 ? a.off[1] + X + Y * s1y + Z * s2y : a.off[2] + X + Y * s1z + Z * s2z;
+  };
   for (int l = tid; l < EPC * NU; l += NT) {
     const int el = l / NU, r = l - (l / NU) * NU;
     const int ex = sEc[el][0], ey = sEc[el][1], ez = sEc[el][2];
     double* sr = sreg + el * ES;
     {
       const int li = r % (P + 1), lj = (r / (P + 1)) % P, lk = r / ((P + 1) * P);
-      const long long g = a.off[0] + (long long)ex * P + li + (nx + 1) * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
-      const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 0, (long long)ex * P + li, nx));
+      const long long g = gbase(0, ex, ey, ez) + li + lj * s1x + lk * s2x;
+      const bool m = !sEc[el][3] || (ESS && a.ess && face_masked(a.ess, 0, (long long)ex * P + li, nx));
       cp_async8z(sr + 0 * T::SU + li + T::U0::S1 * lj + T::U0::S2 * lk, a.x + (m ? 0 : g), !m);
     }
     {
       const int li = r % P, lj = (r / P) % (P + 1), lk = r / (P * (P + 1));
-      const long long g = a.off[1] + (long long)ex * P + li + nx * ((long long)ey * P + lj + (ny + 1) * ((long long)ez * P + lk));
-      const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 1, (long long)ey * P + lj, ny));
+      const long long g = gbase(1, ex, ey, ez) + li + lj * s1y + lk * s2y;
+      const bool m = !sEc[el][3] || (ESS && a.ess && face_masked(a.ess, 1, (long long)ey * P + lj, ny));
       cp_async8z(sr + 1 * T::SU + li + T::U1::S1 * lj + T::U1::S2 * lk, a.x + (m ? 0 : g), !m);
     }
     {
       const int li = r % P, lj = (r / P) % P, lk = r / (P * P);
-      const long long g = a.off[2] + (long long)ex * P + li + nx * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
-      const bool m = !sEc[el][3] || (a.ess && face_masked(a.ess, 2, (long long)ez * P + lk, a.n[2]));
+      const long long g = gbase(2, ex, ey, ez) + li + lj * s1z + lk * s2z;
+      const bool m = !sEc[el][3] || (ESS && a.ess && face_masked(a.ess, 2, (long long)ez * P + lk, a.n[2]));
       cp_async8z(sr + 2 * T::SU + li + T::U2::S1 * lj + T::U2::S2 * lk, a.x + (m ? 0 : g), !m);
     }
   }
@@ -759,7 +767,7 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
   // ---- D^T q~ and scatter (boundary faces by atomics onto the zeroed y, eliminated faces skipped) ----
   auto put = [&](double* g, double v, int ic, int c, long long gi) {
     if (ic == 0 || ic == P) {
-      if (!(a.ess && face_masked(a.ess, c, gi, a.n[c]))) atomicAdd(g, v);
+      if (!(ESS && a.ess && face_masked(a.ess, c, gi, a.n[c]))) atomicAdd(g, v);
     } else {
       *g = v;
     }
@@ -778,8 +786,7 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
         if (li > 0) v += sqe[cell - 1];
         if (li < P) v -= sqe[cell];
       }
-      const long long g = a.off[0] + (long long)ex * P + li + (nx + 1) * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
-      put(a.y + g, v, li, 0, (long long)ex * P + li);
+      put(a.y + gbase(0, ex, ey, ez) + li + lj * s1x + lk * s2x, v, li, 0, (long long)ex * P + li);
     }
     {
       const int li = r % P, lj = (r / P) % (P + 1), lk = r / (P * (P + 1));
@@ -789,8 +796,7 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
         if (lj > 0) v += sqe[cell - T::L2::S1];
         if (lj < P) v -= sqe[cell];
       }
-      const long long g = a.off[1] + (long long)ex * P + li + nx * ((long long)ey * P + lj + (ny + 1) * ((long long)ez * P + lk));
-      put(a.y + g, v, lj, 1, (long long)ey * P + lj);
+      put(a.y + gbase(1, ex, ey, ez) + li + lj * s1y + lk * s2y, v, lj, 1, (long long)ey * P + lj);
     }
     {
       const int li = r % P, lj = (r / P) % P, lk = r / (P * P);
@@ -800,8 +806,7 @@ __global__ void __launch_bounds__(96) tri_multi_kernel(const TriArgs a,
         if (lk > 0) v += sqe[cell - T::L2::S2];
         if (lk < P) v -= sqe[cell];
       }
-      const long long g = a.off[2] + (long long)ex * P + li + nx * ((long long)ey * P + lj + ny * ((long long)ez * P + lk));
-      put(a.y + g, v, lk, 2, (long long)ez * P + lk);
+      put(a.y + gbase(2, ex, ey, ez) + li + lj * s1z + lk * s2z, v, lk, 2, (long long)ez * P + lk);
     }
   }
   if constexpr (BLOCK) {
@@ -982,10 +987,13 @@ cudaError_t launch_p(const hdiv_ctx* h, const double* x, double* y, const int* s
         a.geo = h->d_geo;
         count_op();
         if (P <= 4 && epc >= 2) {   // (two elements fit the 48 KB of static shared memory)
-          tri_multi_kernel<P, (P <= 4 ? 2 : 1), MODE == 1, true>
-              <<<(unsigned)((h->E + (P <= 4 ? 1 : 0)) / (P <= 4 ? 2 : 1)), 96, 0, s>>>(a, h->tab, h->E);
+          auto k2 = h->ess ? tri_multi_kernel<P, (P <= 4 ? 2 : 1), MODE == 1, true, true>
+                           : tri_multi_kernel<P, (P <= 4 ? 2 : 1), MODE == 1, true, false>;
+          k2<<<(unsigned)((h->E + (P <= 4 ? 1 : 0)) / (P <= 4 ? 2 : 1)), 96, 0, s>>>(a, h->tab, h->E);
         } else {
-          tri_multi_kernel<P, 1, MODE == 1, true><<<(unsigned)h->E, 96, 0, s>>>(a, h->tab, h->E);
+          auto k1 = h->ess ? tri_multi_kernel<P, 1, MODE == 1, true, true>
+                           : tri_multi_kernel<P, 1, MODE == 1, true, false>;
+          k1<<<(unsigned)h->E, 96, 0, s>>>(a, h->tab, h->E);
         }
         return cudaGetLastError();
       }
