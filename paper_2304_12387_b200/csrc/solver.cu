@@ -40,7 +40,8 @@ constexpr int RED_NT = 256;
 struct MState {
   double gamma, gamma_old, eta, gamma1, s, s_old, c, c_old, delta;
   double wz, wa3, wa2, xc, rtol, rel;
-  int done, iters, maxit, breakdown, conv, pad;
+  double xcp;   // deferred x-update coefficient of w_{j-1} (odd iterations defer, see wstep)
+  int done, iters, maxit, breakdown, conv, pend;
 };
 
 __device__ __forceinline__ double block_sum(double v) {
@@ -302,17 +303,34 @@ wstep_kernel(const double* __restrict__ glob, int P, const MState* __restrict__ 
   if (threadIdx.x == 0) sm = scalar_step(*S, pa ? red : rank_sum(glob, P));
   __syncthreads();
   const MState m = sm;
+  // x += c_j eta_j w_j is applied two iterations at a time: an odd iteration only records its
+  // coefficient (x is neither read nor written), the next one adds xcp w_{j-1} + xc w_j — w_{j-1}
+  // is the `w` this pass reads anyway — so x streams through HBM every other iteration; a
+  // finishing iteration (done = 2) always flushes
+  const bool defer = (m.iters & 1) && m.done != 2;
   if (!m.breakdown) {
     const double wz = m.wz, wa3 = m.wa3, wa2 = m.wa2, xc = m.xc;
-    for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
-         i += (long long)gridDim.x * RED_NT) {
-      const double wn = wz * z[i] - wa3 * w_old[i] - wa2 * w[i];
-      w_new[i] = wn;
-      x[i] = fma(xc, wn, x[i]);
+    if (defer) {
+      for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+           i += (long long)gridDim.x * RED_NT)
+        w_new[i] = wz * z[i] - wa3 * w_old[i] - wa2 * w[i];
+    } else {
+      const double xcp = m.pend ? m.xcp : 0.0;
+      for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+           i += (long long)gridDim.x * RED_NT) {
+        const double wi = w[i];
+        const double wn = wz * z[i] - wa3 * w_old[i] - wa2 * wi;
+        w_new[i] = wn;
+        x[i] = fma(xc, wn, fma(xcp, wi, x[i]));
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     MState o = m;
+    if (!o.breakdown) {
+      o.pend = defer ? 1 : 0;
+      o.xcp = defer ? m.xc : 0.0;
+    }
     if (o.done == 2) o.done = 1;
     *Snext = o;
   }
