@@ -146,7 +146,7 @@ def winv_bench(torch):
                                  ", ".join(f"p{p} {t} s" for p, t in _PAPER_WINV_S.items())}
     def run(pr):
         t0 = time.perf_counter()
-        op = from_problem(pr)
+        op = from_problem(pr, schur="chebyshev")   # (the (2,2) block alone: no S^-1 needed)
         torch.cuda.synchronize()
         setup = time.perf_counter() - t0
         q = torch.from_numpy(random_vector(op.sizes.n_l2, 5)).cuda()
@@ -188,12 +188,12 @@ def build_operator(pr, ws, rank, dist, nccl_id=None):
     from paper_2304_12387_b200 import HdivOperator
     if ws == 1:
         from paper_2304_12387_b200 import from_problem
-        return from_problem(pr)
+        return from_problem(pr, schur="chebyshev")   # (apply timing: no AMG hierarchy needed)
     from paper_2304_12387_b200.slabs import slab_bounds, slab_inputs
     z0, z1 = slab_bounds(pr.N[pr.dim - 1], ws, rank)
     V, a, b, g, e = slab_inputs(pr, z0, z1)
     return HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b, gamma=g, eps=e,
-                        essential=pr.essential, project_mean=pr.project_mean,
+                        essential=pr.essential, project_mean=pr.project_mean, schur="chebyshev",
                         slab=(z0, z1), nccl_id=nccl_id, rank=rank, nranks=ws)
 
 
@@ -638,7 +638,7 @@ def main():
         # tri_geometry 2: the paper's partial assembly (G_q = w_q mw / det J J^T J stored at the
         # Q^3 points, 48 B each: P:684); 1: J recomputed from the vertices every apply
         for geo, key in ((2, "stored_geometry"), (1, "on_the_fly_jacobian")):
-            op3 = from_problem(pr3, tri_geometry=geo)
+            op3 = from_problem(pr3, tri_geometry=geo, schur="chebyshev")
             x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
             y3 = torch.empty_like(x3)
             ms3 = time_applies(op3, x3, y3, 20, 5, None, torch) / 20
@@ -674,7 +674,7 @@ def main():
             pr3.kind = "grad_div"
             pr3.alpha = 10.0 ** random_vector(pr3.E, 33, -2.0, 2.0)
             pr3.beta = 10.0 ** random_vector(pr3.E, 34, -2.0, 2.0)
-            op3 = from_problem(pr3)
+            op3 = from_problem(pr3, schur="chebyshev")
             x3 = torch.rand(op3.sizes.n, dtype=torch.float64, device="cuda")
             y3 = torch.empty_like(x3)
             ms3 = time_applies(op3, x3, y3, 20, 5, None, torch) / 20

@@ -86,9 +86,10 @@ typedef struct {
   int cheb_degree;     /* S^-1 = Chebyshev-Jacobi polynomial degree on S~; <= 0 => 4 (A10)   */
   double cheb_ratio;   /* interval [2/ratio, 2]; <= 0 => 30                                  */
   int kernel;          /* 0 auto, 1 force the general quadrature kernel, 2 force affine tile */
-  int schur_solver;    /* S^-1: HDIV_SCHUR_CHEBYSHEV (0, reading A10) or HDIV_SCHUR_AMG (1):  */
+  int schur_solver;    /* S^-1: HDIV_SCHUR_CHEBYSHEV (0, reading A10), HDIV_SCHUR_AMG (1):    */
                        /* one smoothed-aggregation V-cycle (reading A9b); with     */
-                       /* slabs the block-Jacobi of per-slab V-cycles (reading A9c)          */
+                       /* slabs the block-Jacobi of per-slab V-cycles (reading A9c), or      */
+                       /* HDIV_SCHUR_AUTO (2: AMG at >= 10^6 global L2 rows, else Chebyshev) */
   int amg_sweeps;      /* l1-Jacobi sweeps before and after the coarse correction; <= 0 => 2 */
   int amg_max_coarse;  /* dense solve once a level has <= this many rows; <= 0 => 512        */
   /* NEXT-3 (reading A21).  essential_sides: bitmask of domain sides whose RT
@@ -114,7 +115,9 @@ typedef struct {
   int tri_geometry;
 } hdiv_options;
 
-enum { HDIV_SCHUR_CHEBYSHEV = 0, HDIV_SCHUR_AMG = 1 };
+/* HDIV_SCHUR_AUTO: the AMG V-cycle when the global L2 space has >= 10^6 rows (the Chebyshev
+ * polynomial is not h-robust), else Chebyshev; the choice is made once at setup. */
+enum { HDIV_SCHUR_CHEBYSHEV = 0, HDIV_SCHUR_AMG = 1, HDIV_SCHUR_AUTO = 2 };
 
 typedef struct {
   int iters;           /* first j with |eta_j| <= rtol * gamma_1 (reading A8)         */

@@ -45,7 +45,7 @@ class Options(C.Structure):
                 ("project_mean", C.c_int), ("tri_geometry", C.c_int)]
 
 
-SCHUR_SOLVERS = {"chebyshev": 0, "amg": 1}
+SCHUR_SOLVERS = {"chebyshev": 0, "amg": 1, "auto": 2}
 
 
 class Report(C.Structure):
@@ -174,7 +174,7 @@ class HdivOperator:
 
     def __init__(self, dim, N, p, kind, vertices=None, alpha=None, beta=None, gamma=None,
                  eps=None, gamma_vertex=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
-                 schur="chebyshev", amg_sweeps=2, amg_max_coarse=512, essential=0,
+                 schur="auto", amg_sweeps=2, amg_max_coarse=512, essential=0,
                  project_mean=False, tri_geometry=0, slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
         import torch
         self.lib = load_library()

@@ -349,13 +349,18 @@ struct StA {
   }
 };
 
+// level-0 sweeps: 8 resident 256-thread CTAs per SM (the reduction / sweep grid is 148 x 8: one
+// wave; at 36-48 registers only 5-7 fit and the last CTAs ran as a second, mostly empty wave)
+#ifndef AMG_MINB
+#define AMG_MINB 8
+#endif
 #define AMG_LOOP(n) \
   for (long long i = blockIdx.x * (long long)ANT + threadIdx.x; i < (n); i += (long long)gridDim.x * ANT)
 
 // the last level-0 post-smoothing sweep with the MINRES partial <x_out, b> (b = the V-cycle's
 // right-hand side = v_q): saves the separate dot pass; part has gridDim.x entries
 template <class Acc>
-__global__ void __launch_bounds__(ANT) jacobi_dot_kernel(Acc A, long long n,
+__global__ void __launch_bounds__(ANT, AMG_MINB) jacobi_dot_kernel(Acc A, long long n,
                                                          const double* __restrict__ b,
                                                          const double* __restrict__ xin,
                                                          double* __restrict__ xout,
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(ANT) jacobi_dot_kernel(Acc A, long long n,
 
 // x_out = x_in + Dl1^-1 (b - A x_in); x_in = nullptr means x_in = Dl1^-1 b (first sweep from 0)
 template <class Acc>
-__global__ void __launch_bounds__(ANT) jacobi_kernel(Acc A, long long n, const double* __restrict__ b,
+__global__ void __launch_bounds__(ANT, AMG_MINB) jacobi_kernel(Acc A, long long n, const double* __restrict__ b,
                                                      const double* __restrict__ xin,
                                                      double* __restrict__ xout,
                                                      const double* __restrict__ dl1inv,
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(ANT) scale_kernel(long long n, const double* _
 // s = r - omega A D^-1 r with r = b - A x  (computed in two passes: r then s)
 // r = b - A x and t = D^-1 r (so the next pass gathers one vector, not two)
 template <class Acc>
-__global__ void __launch_bounds__(ANT) resid_kernel(Acc A, long long n, const double* __restrict__ b,
+__global__ void __launch_bounds__(ANT, AMG_MINB) resid_kernel(Acc A, long long n, const double* __restrict__ b,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ r,
                                                     const double* __restrict__ dinv,
@@ -431,7 +436,7 @@ __global__ void __launch_bounds__(ANT) resid_kernel(Acc A, long long n, const do
 
 // s = r - omega A t, t = D^-1 r
 template <class Acc>
-__global__ void __launch_bounds__(ANT) smooth_r_kernel(Acc A, long long n,
+__global__ void __launch_bounds__(ANT, AMG_MINB) smooth_r_kernel(Acc A, long long n,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ t, double omega,
                                                        double* __restrict__ s,
@@ -498,7 +503,7 @@ __global__ void __launch_bounds__(ANT) aggsumS_kernel(long long d0, long long d1
 
 // x_out = x + e_f - omega D^-1 A e_f,  e_f(j) = e_c[agg(j)]
 template <class Acc, class Agg>
-__global__ void __launch_bounds__(ANT) prolong_kernel(Acc A, Agg agg, long long n,
+__global__ void __launch_bounds__(ANT, AMG_MINB) prolong_kernel(Acc A, Agg agg, long long n,
                                                       const double* __restrict__ x,
                                                       const double* __restrict__ ec,
                                                       const double* __restrict__ dinv, double omega,

@@ -192,9 +192,10 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     delete h;
     return fail(HDIV_ERR_SHAPE, "essential_sides: bits 0..2 dim - 1 only");
   }
-  if (h->opts.schur_solver != HDIV_SCHUR_CHEBYSHEV && h->opts.schur_solver != HDIV_SCHUR_AMG) {
+  if (h->opts.schur_solver != HDIV_SCHUR_CHEBYSHEV && h->opts.schur_solver != HDIV_SCHUR_AMG &&
+      h->opts.schur_solver != HDIV_SCHUR_AUTO) {
     delete h;
-    return fail(HDIV_ERR_SHAPE, "schur_solver must be HDIV_SCHUR_CHEBYSHEV or HDIV_SCHUR_AMG");
+    return fail(HDIV_ERR_SHAPE, "schur_solver must be HDIV_SCHUR_CHEBYSHEV, _AMG or _AUTO");
   }
   for (int d = 0; d < 3; ++d) { h->N[d] = N[d]; h->NL[d] = N[d]; }
   h->ez0 = mesh->ez_begin; h->ez1 = mesh->ez_end;
@@ -219,6 +220,11 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     int64_t ng[3] = {N[0] * p, N[1] * p, dim == 3 ? N[2] * p : 1};
     h->nrt_g = rt_count(ng);
     h->nl2_g = N[0] * N[1] * N[2] * pd;
+    // auto S^-1: the fixed Chebyshev polynomial is not h-robust (config 3: 1903 MINRES iterations
+    // vs 695 with the AMG V-cycle; config 4 does not converge in 600) but is the cheaper one on
+    // small grids (config 2: 120 its / 4.2 ms vs 105 / 5.6 ms)
+    if (h->opts.schur_solver == HDIV_SCHUR_AUTO)
+      h->opts.schur_solver = (h->nl2_g >= kAutoAmgRows) ? HDIV_SCHUR_AMG : HDIV_SCHUR_CHEBYSHEV;
   }
   if (dim == 2) {
     h->off[0] = 0; h->off[1] = (h->n[0] + 1) * h->n[1]; h->off[2] = h->nrt;

@@ -14,6 +14,7 @@
 namespace hdiv {
 
 constexpr int MAXP = HDIV_MAX_ORDER;
+constexpr long long kAutoAmgRows = 1000000;   // HDIV_SCHUR_AUTO: AMG from this many L2 rows
 constexpr int MAXQ = MAXP + 2;
 
 // 1D tables on [0,1].  Passed to kernels by value (__grid_constant__).

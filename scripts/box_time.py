@@ -8,7 +8,7 @@ from paper_2304_12387_b200 import from_problem
 for p in [int(a) for a in (sys.argv[1:] or ["4", "2", "3", "5", "6"])]:
     N = {1: 192, 2: 160, 3: 128, 4: 128, 5: 96, 6: 80}[p]
     pr = make_config("c4", N=(N,) * 3, p=p)
-    op = from_problem(pr)
+    op = from_problem(pr, schur="chebyshev")
     n = op.sizes.n
     x = torch.rand(n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)

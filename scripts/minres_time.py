@@ -7,7 +7,7 @@ from paper_2304_12387_b200 import from_problem
 
 for name, p, N in [("c4", 4, None), ("c3", 4, None), ("c2", 3, None)]:
     pr = make_config(name, p=p, N=N)
-    op = from_problem(pr)
+    op = from_problem(pr, schur="chebyshev")
     b = torch.rand(op.sizes.n, dtype=torch.float64, device="cuda")
     op.minres(b, rtol=1e-12, maxit=12)
     x, rep = op.minres(b, rtol=1e-12, maxit=60)

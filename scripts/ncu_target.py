@@ -11,7 +11,7 @@ p = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 kern = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 pr = make_config(cfg, p=p)
-op = from_problem(pr, kernel=kern)
+op = from_problem(pr, kernel=kern, schur="chebyshev")
 x = torch.rand(op.sizes.n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
 for _ in range(n):

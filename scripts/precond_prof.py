@@ -5,7 +5,7 @@ import torch
 from synth import make_config
 from paper_2304_12387_b200 import from_problem
 pr = make_config(sys.argv[1] if len(sys.argv) > 1 else "c4", p=4)
-op = from_problem(pr)
+op = from_problem(pr, schur="chebyshev")
 b = torch.rand(op.sizes.n, dtype=torch.float64, device="cuda")
 z = torch.empty_like(b)
 for _ in range(3):

@@ -536,3 +536,20 @@ def test_trilinear_stored_geometry(name, N, p, ess):
     y2 = _host(op.apply_block(_dev(x)))
     assert np.array_equal(y, y2)
     op.close()
+
+
+def test_schur_auto_choice():
+    """HDIV_SCHUR_AUTO (the binding's default): Chebyshev below 10^6 global L2 rows, the AMG
+    V-cycle from there on (the polynomial is not h-robust); explicit choices are kept."""
+    def levels(op):
+        try:
+            return op.amg_levels()
+        except Exception:   # HDIV_ERR_UNSUPPORTED: the handle has no AMG hierarchy
+            return 0
+    small = make_config("c2", N=(4, 4, 4), p=3)            # 1728 L2 rows
+    big = make_config("c2", N=(40, 40, 40), p=3)           # 1.73e6 L2 rows
+    for pr, kw, amg in [(small, {}, False), (big, {}, True), (big, {"schur": "chebyshev"}, False),
+                        (small, {"schur": "amg"}, True)]:
+        op = _gpu(pr, **kw)
+        assert (levels(op) >= 1) == amg, (pr.N, kw)
+        op.close()
