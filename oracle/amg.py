@@ -130,10 +130,22 @@ class AMGSchur:
     (slab-local aggregation of the block's own subcell grid; couplings between slabs dropped).
     In the element-contiguous L2 numbering every slab is one contiguous index range."""
 
-    def __init__(self, asm, nu=2, max_coarse=512, pin=False, slabs=None):
+    def __init__(self, asm, nu=2, max_coarse=512, pin=False, slabs=None, cheb_degree=1,
+                 cheb_ratio=20.0):
         coords = l2_cell_coords(asm.dim, asm.N, asm.p)
         dims = [int(asm.N[a]) * asm.p for a in range(asm.dim)]
         self.nu = nu
+        self.S = asm.S.tocsr()
+        # cheb_degree >= 2 (reading A9d): S^-1 = the Chebyshev polynomial of degree cheb_degree
+        # in B S~ (B = the V-cycle below, SPD with spectrum in (0, 1] for the symmetric l1-Jacobi
+        # V-cycle) on [b / ratio, b], b = 1.1 — the Chebyshev-Jacobi recurrence of reading A10
+        # with B in place of D^-1; degree 1 is the plain V-cycle
+        self.cheb_degree = int(cheb_degree)
+        if self.cheb_degree >= 2:
+            b_ = 1.1
+            a_ = b_ / float(cheb_ratio)
+            self.theta, self.delta = 0.5 * (b_ + a_), 0.5 * (b_ - a_)
+            self.sigma = self.theta / self.delta
         last = asm.dim - 1
         per_layer = int(np.prod(asm.N[:last])) * asm.p ** asm.dim
         if not slabs:
@@ -150,8 +162,25 @@ class AMGSchur:
             self.blocks.append((a, b, lv))
         self.levels = self.blocks[0][2] if len(self.blocks) == 1 else None
 
-    def __call__(self, r):
+    def vcycles(self, r):
         out = np.empty_like(r)
         for a, b, lv in self.blocks:
             out[a:b] = vcycle(lv, r[a:b], self.nu)
         return out
+
+    def __call__(self, r):
+        if self.cheb_degree < 2:
+            return self.vcycles(r)
+        # r/d form, step by step: d_0 = B r / theta, y = d_0; r_i = r_{i-1} - S~ d_{i-1},
+        # d_i = c1 d_{i-1} + c2 B r_i, y += d_i
+        rho = 1.0 / self.sigma
+        d = self.vcycles(r) / self.theta
+        y = d.copy()
+        res = r.copy()
+        for _ in range(1, self.cheb_degree):
+            res = res - self.S @ d
+            rn = 1.0 / (2.0 * self.sigma - rho)
+            d = (rn * rho) * d + (2.0 * rn / self.delta) * self.vcycles(res)
+            y = y + d
+            rho = rn
+        return y

@@ -151,3 +151,40 @@ def test_block_jacobi_amg_of_slabs():
     Bm = np.column_stack([deep(e) for e in np.eye(n)])
     assert np.abs(Bm - Bm.T).max() < 1e-12 * np.abs(Bm).max()
     assert np.linalg.eigvalsh(0.5 * (Bm + Bm.T)).min() > 0
+
+
+@pytest.mark.parametrize("k,ratio", [(2, 20.0), (3, 20.0), (4, 30.0)])
+def test_chebyshev_accelerated_vcycle(k, ratio):
+    """Reading A9d: S^-1 = the degree-k Chebyshev polynomial in B S~ on [1.1 / ratio, 1.1].
+    With a one-level hierarchy (B = S~^-1 exactly, B S~ = I) the r/d recurrence must reduce to
+    the closed form (1 - T_k(s1) / T_k(s0)) S~^-1, s0 = (b + a) / (b - a), s1 = (b + a - 2) / (b - a)
+    (the residual polynomial at the eigenvalue 1); with a deep hierarchy it is SPD and the
+    preconditioned Schur operator is better conditioned than with one V-cycle."""
+    import scipy.sparse.linalg as spla
+    from numpy.polynomial import chebyshev as cheb
+    from oracle import amg as amgmod, operators
+    from synth import make_config, random_vector
+    A = operators.Assembled(make_config("c2", N=(3, 3, 3), p=2))
+    v = random_vector(A.n_l2, 5)
+    exact = amgmod.AMGSchur(A, max_coarse=10 ** 6, cheb_degree=k, cheb_ratio=ratio)
+    b, a = 1.1, 1.1 / ratio
+    s0, s1 = (b + a) / (b - a), (b + a - 2.0) / (b - a)
+    Tk = lambda t: cheb.chebval(t, [0] * k + [1])
+    ref = (1.0 - Tk(s1) / Tk(s0)) * spla.spsolve(A.S.tocsc(), v)
+    assert np.abs(exact(v) - ref).max() < 1e-11 * np.abs(ref).max()
+    # heterogeneous coefficients (config 3's jittered mesh, contrast 10^4): one V-cycle leaves
+    # cond(B S~) ~ 4 here, the polynomial brings it down
+    A = operators.Assembled(make_config("c3", N=(4, 4, 4), p=2))
+    deep = amgmod.AMGSchur(A, max_coarse=8, cheb_degree=k, cheb_ratio=ratio)
+    one = amgmod.AMGSchur(A, max_coarse=8)
+    n = A.n_l2
+    Bm = np.column_stack([deep(e) for e in np.eye(n)])
+    assert np.abs(Bm - Bm.T).max() < 1e-12 * np.abs(Bm).max()
+    assert np.linalg.eigvalsh(0.5 * (Bm + Bm.T)).min() > 0
+    S = A.S.toarray()
+    B1 = np.column_stack([one(e) for e in np.eye(n)])
+    def cond(Bx):   # spectrum of B S~ (similar to the SPD S^1/2 B S^1/2)
+        lam = np.sort(np.linalg.eigvals(Bx @ S).real)
+        assert lam[0] > 0
+        return lam[-1] / lam[0]
+    assert cond(Bm) < cond(B1), (cond(Bm), cond(B1))
