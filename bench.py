@@ -618,8 +618,39 @@ def main():
             "u_err": ((xo[:nrt] - xs[:nrt]).abs().max() / xs[:nrt].abs().max()).item(),
             "q_err_mod_const": ((dq - dq.mean()).abs().max() / xs[nrt:].abs().max()).item()}
         ops.close()
+        del xo, dq
+        torch.cuda.empty_cache()
+        # reading A9d: S^-1 = degree-3 Chebyshev polynomial in (V-cycle) S~ — fewer MINRES
+        # iterations for three V-cycles and two S~ applies per S^-1
+        ops = from_problem(prs, schur="amg", amg_cheb_degree=3)
+        ops.minres(bs, rtol=1e-12, maxit=6)
+        xo, rs = ops.minres(bs, rtol=1e-12, maxit=5000)
+        dq = xo[nrt:] - xs[nrt:]
+        result["spe10_like"]["amg_chebyshev3"] = {
+            "iters": rs.iters, "converged": bool(rs.converged),
+            "time_to_solve_s": rs.t_solve_ms / 1e3,
+            "u_err": ((xo[:nrt] - xs[:nrt]).abs().max() / xs[:nrt].abs().max()).item(),
+            "q_err_mod_const": ((dq - dq.mean()).abs().max() / xs[nrt:].abs().max()).item()}
+        ops.close()
         del xs, bs, xo, dq
         torch.cuda.empty_cache()
+        # config 3 itself (Darcy, gamma = 0 but natural conditions: S~ nonsingular), b = A x*
+        prc3 = make_config("c3")
+        c3m = {"workload": WORKLOADS["c3"] + ", MINRES b = A x* (x* = U(-1,1)), x0 = 0, rtol 1e-12"}
+        for k in (1, 3):
+            opm = from_problem(prc3, schur="amg", amg_cheb_degree=k)
+            xs = torch.rand(opm.sizes.n, dtype=torch.float64, device="cuda") * 2 - 1
+            bs = opm.apply_block(xs)
+            opm.minres(bs, rtol=1e-12, maxit=6)
+            xo, rs = opm.minres(bs, rtol=1e-12, maxit=5000)
+            c3m["amg" if k == 1 else "amg_chebyshev3"] = {
+                "iters": rs.iters, "converged": bool(rs.converged),
+                "time_to_solve_s": rs.t_solve_ms / 1e3,
+                "solution_err": ((xo - xs).abs().max() / xs.abs().max()).item()}
+            opm.close()
+            del xs, bs, xo
+            torch.cuda.empty_cache()
+        result["config3_minres"] = c3m
 
     # Config 3's own apply (trilinear hexes: quadrature kernel, FP64-ALU-class):
     # GDOF/s and the fraction of the measured FP64 FMA peak (profiles/r01_fp64_peak.txt) for the

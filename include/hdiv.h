@@ -113,6 +113,14 @@ typedef struct {
    * quadrature points; HDIV_ERR_CUDA if they do not fit).  The block apply
    * with the explicit W^-1 inverses fused (HBM-bound) always recomputes J. */
   int tri_geometry;
+  /* schur_solver == HDIV_SCHUR_AMG (reading A9d): S^-1 = the degree-amg_cheb_degree Chebyshev
+   * polynomial in B S~ (B = the V-cycle above) on [b / amg_cheb_ratio, b], b = 1.1 (one rank)
+   * or 2.2 (slabs: block-Jacobi over a chain, spectrum <= 2) — the r/d
+   * recurrence of reading A10 with B in place of D^-1, amg_cheb_degree V-cycles and
+   * amg_cheb_degree - 1 S~ applies per S^-1.  <= 1 => 1 (the plain V-cycle);
+   * amg_cheb_ratio <= 0 => 20. */
+  int amg_cheb_degree;
+  double amg_cheb_ratio;
 } hdiv_options;
 
 /* HDIV_SCHUR_AUTO: the AMG V-cycle when the global L2 space has >= 10^6 rows (the Chebyshev

@@ -66,7 +66,8 @@ def build_hierarchy(S, coords, dims, agg=3, max_coarse=512, max_levels=25, coars
     """Levels l = 0..L with A_0 = S; coords: the grid coordinates of the rows of S.
     coarse_solve=False skips the coarsest inverse (tests on singular operators).
     pin=True (singular S~ of the pure-Neumann problem, NEXT-3, reading A21): the coarsest
-    solve inverts A_L with its last row and column replaced by the identity's."""
+    solve fixes the last unknown at 0 and drops its equation (A_L without its last row and
+    column inverted; the last entry of the correction is 0)."""
     levels = [Level(S, dims, coords)]
     while True:
         lv = levels[-1]
@@ -101,7 +102,11 @@ def build_hierarchy(S, coords, dims, agg=3, max_coarse=512, max_levels=25, coars
             Ad[-1, :] = 0.0
             Ad[:, -1] = 0.0
             Ad[-1, -1] = 1.0
-        levels[-1].Ainv = np.linalg.inv(Ad)
+        Ainv = np.linalg.inv(Ad)
+        if pin:   # the last unknown fixed at 0 and its (redundant) equation dropped:
+            Ainv[-1, :] = 0.0   # e = [A_red^-1 b_red; 0] — B stays positive semidefinite with
+            Ainv[:, -1] = 0.0   # B S~ = I on the mean-zero space for an exact solve
+        levels[-1].Ainv = Ainv
     return levels
 
 
@@ -139,17 +144,20 @@ class AMGSchur:
         # cheb_degree >= 2 (reading A9d): S^-1 = the Chebyshev polynomial of degree cheb_degree
         # in B S~ (B = the V-cycle below, SPD with spectrum in (0, 1] for the symmetric l1-Jacobi
         # V-cycle) on [b / ratio, b], b = 1.1 — the Chebyshev-Jacobi recurrence of reading A10
-        # with B in place of D^-1; degree 1 is the plain V-cycle
+        # with B in place of D^-1; degree 1 is the plain V-cycle.  With slabs (reading A9c) B is
+        # block-Jacobi over a chain of slabs: two colours (even / odd slabs), each colour's
+        # blocks decoupled, so the spectrum of B S~ is bounded by 2 (the additive-Schwarz
+        # colouring bound, one per colour) and b = 2.2
         self.cheb_degree = int(cheb_degree)
-        if self.cheb_degree >= 2:
-            b_ = 1.1
-            a_ = b_ / float(cheb_ratio)
-            self.theta, self.delta = 0.5 * (b_ + a_), 0.5 * (b_ - a_)
-            self.sigma = self.theta / self.delta
         last = asm.dim - 1
         per_layer = int(np.prod(asm.N[:last])) * asm.p ** asm.dim
         if not slabs:
             slabs = [(0, int(asm.N[last]))]
+        if self.cheb_degree >= 2:
+            b_ = 1.1 if len(slabs) == 1 else 2.2
+            a_ = b_ / float(cheb_ratio)
+            self.theta, self.delta = 0.5 * (b_ + a_), 0.5 * (b_ - a_)
+            self.sigma = self.theta / self.delta
         self.blocks = []
         S = asm.S.tocsr()
         for z0, z1 in slabs:
@@ -158,7 +166,11 @@ class AMGSchur:
             c[:, last] -= z0 * asm.p
             d = list(dims)
             d[last] = (z1 - z0) * asm.p
-            lv = build_hierarchy(S[a:b, a:b], c, tuple(d), max_coarse=max_coarse, pin=pin)
+            # the pin only where the block is singular: a slab's diagonal block keeps the
+            # interface couplings on its diagonal (S~_ii sums all face weights), so with two or
+            # more slabs every block is nonsingular and is inverted as it is (reading A9c)
+            lv = build_hierarchy(S[a:b, a:b], c, tuple(d), max_coarse=max_coarse,
+                                 pin=pin and len(slabs) == 1)
             self.blocks.append((a, b, lv))
         self.levels = self.blocks[0][2] if len(self.blocks) == 1 else None
 

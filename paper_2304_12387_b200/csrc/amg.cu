@@ -744,8 +744,11 @@ hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
       }
     }
   }
-  if (h->opts.project_mean) {   // singular pure-Neumann S~ (NEXT-3, reading A21): pin the
-    for (long long i = 0; i < nc; ++i) {   // last unknown (identity row and column)
+  // singular pure-Neumann S~ (NEXT-3, reading A21): pin the last unknown (identity row and
+  // column) — one rank only: a slab's block keeps its interface weights on the diagonal and is
+  // nonsingular (reading A9c)
+  if (h->opts.project_mean && h->nranks == 1) {
+    for (long long i = 0; i < nc; ++i) {
       Ad[(nc - 1) * nc + i] = 0.0;
       Ad[i * nc + (nc - 1)] = 0.0;
     }
@@ -754,6 +757,12 @@ hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
   if (!invert_dense(Ad, nc)) {
     set_error("AMG: singular coarsest operator");
     return HDIV_ERR_BREAKDOWN;
+  }
+  if (h->opts.project_mean && h->nranks == 1) {   // the pinned unknown is 0 and its (redundant)
+    for (long long i = 0; i < nc; ++i) {           // equation is dropped: B stays semidefinite
+      Ad[(nc - 1) * nc + i] = 0.0;
+      Ad[i * nc + (nc - 1)] = 0.0;
+    }
   }
   H->nc = nc;
   HDIV_CUDA_TRY(cudaMalloc(&H->cinv, sizeof(double) * nc * nc));

@@ -184,6 +184,8 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->opts.essential_sides = opts ? opts->essential_sides : 0;
   h->opts.project_mean = opts ? (opts->project_mean != 0) : 0;
   h->opts.tri_geometry = opts ? opts->tri_geometry : 0;
+  h->opts.amg_cheb_degree = (opts && opts->amg_cheb_degree > 1) ? opts->amg_cheb_degree : 1;
+  h->opts.amg_cheb_ratio = (opts && opts->amg_cheb_ratio > 0) ? opts->amg_cheb_ratio : 20.0;
   if (h->opts.tri_geometry < 0 || h->opts.tri_geometry > 2) {
     delete h;
     return fail(HDIV_ERR_SHAPE, "options.tri_geometry must be 0, 1 or 2");

@@ -224,6 +224,71 @@ cheb3c_kernel(CellGeo g, const double* __restrict__ v, const double* __restrict_
   }
 }
 
+// Reading A9d: Chebyshev polynomial in B S~ (B = one AMG V-cycle) in the r/d form of the
+// oracle (oracle/amg.py AMGSchur.__call__): d_0 = B r / theta, y = d_0; for i >= 1:
+// r_i = r_{i-1} - S~ d_{i-1}, d_i = c1 d_{i-1} + c2 B r_i, y += d_i.
+// pcheb_first: d = t / theta, y = d (t = B r_0); `last` (degree 1 never gets here) unused.
+__global__ void __launch_bounds__(RED_NT)
+pcheb_first_kernel(const double* __restrict__ t, double itheta, double* __restrict__ d,
+                   double* __restrict__ y, long long n, const int* __restrict__ done) {
+  if (done && *done) return;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    const double di = t[i] * itheta;
+    d[i] = di;
+    y[i] = di;
+  }
+}
+
+// r_out = r_in - S~ d through the cell stencil (3D; d in ghost space for slabs)
+template <int P>
+__global__ void __launch_bounds__(RED_NT, HDIV_CHEB3C_MINB)
+pcheb_res_cell_kernel(CellGeo g, const double* __restrict__ rin, const double* __restrict__ d,
+                      double* __restrict__ rout, const int* __restrict__ done) {
+  if (done && *done) return;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < g.n;
+       i += (long long)gridDim.x * RED_NT)
+    rout[i] = rin[i] - cell_apply<P, true>(g, i, [&](long long j) { return d[j]; });
+}
+
+// the same through the SELL-32 copy (2D; ghost columns >= n read from d's ghost space)
+template <int W>
+__global__ void __launch_bounds__(RED_NT)
+pcheb_res_sell_kernel(const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                      const double* __restrict__ rin, const double* __restrict__ d,
+                      double* __restrict__ rout, long long n, const int* __restrict__ done) {
+  if (done && *done) return;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    const long long base = (i >> 5) * (32 * W) + (i & 31);
+    double sd = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) sd = fma(eval[base + 32 * k], d[ecol[base + 32 * k]], sd);
+    rout[i] = rin[i] - sd;
+  }
+}
+
+// d = c1 d + c2 t, y += d; `last` adds the partial <y, v>
+__global__ void __launch_bounds__(RED_NT)
+pcheb_upd_kernel(const double* __restrict__ t, double* __restrict__ d, double* __restrict__ y,
+                 const double* __restrict__ v, double c1, double c2, long long n, int last,
+                 double* part, const int* __restrict__ done) {
+  if (done && *done) return;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * RED_NT) {
+    const double dn = c1 * d[i] + c2 * t[i];
+    d[i] = dn;
+    const double yn = y[i] + dn;
+    y[i] = yn;
+    if (last) s = fma(yn, v[i], s);
+  }
+  if (last && part) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
 // 1 / (tau M~) once per handle (the (1,1) preconditioner block as a multiply, not a division)
 __global__ void tau_minv_kernel(const double* __restrict__ mdiag, double tau, double* __restrict__ r,
                                 long long n) {
@@ -491,10 +556,59 @@ static cudaError_t launch_cheb3c(const hdiv_ctx* h, const double* v, const doubl
 static hdiv_status reduce_scalar(hdiv_ctx* h, const double* pa, const double* pb, const int* done,
                                  cudaStream_t s);
 
+// Reading A9d: y = the degree-k Chebyshev polynomial in B S~ applied to vq (B = one V-cycle);
+// d in mw->d[0] (ghost space for slabs), r in mw->d[1], t = B r in mw->r
+static hdiv_status amg_cheb_apply(hdiv_ctx* h, const double* vq, double* y, double* part,
+                                  const int* done, cudaStream_t s) {
+  MinresWork* mw = h->mw;
+  const long long n = h->nl2;
+  const int k = h->opts.amg_cheb_degree;
+  // spectrum of B S~: (0, 1] for one V-cycle, (0, 2] for the block-Jacobi over a chain of
+  // slabs (two colours, oracle/amg.py) -> b = 1.1 / 2.2
+  const double b = (h->nranks > 1) ? 2.2 : 1.1, a = b / h->opts.amg_cheb_ratio;
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
+  double* d = mw->d[0];
+  double* r = mw->d[1];
+  double* t = mw->r;
+  hdiv_status st = amg_vcycle(h, vq, t, done, s);
+  if (st != HDIV_OK) return st;
+  pcheb_first_kernel<<<mw->nb, RED_NT, 0, s>>>(t, 1.0 / theta, d, y, n, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  double rho = 1.0 / sigma;
+  for (int i = 1; i < k; ++i) {
+    if (h->nranks > 1 && (st = comm_l2_ghosts(h, d, s)) != HDIV_OK) return st;
+    const double* rin = (i == 1) ? vq : r;
+    if (h->d_cw) {
+      const CellGeo g = make_cellgeo(h);
+      switch (h->p) {
+        case 1: pcheb_res_cell_kernel<1><<<mw->nb, RED_NT, 0, s>>>(g, rin, d, r, done); break;
+        case 2: pcheb_res_cell_kernel<2><<<mw->nb, RED_NT, 0, s>>>(g, rin, d, r, done); break;
+        case 3: pcheb_res_cell_kernel<3><<<mw->nb, RED_NT, 0, s>>>(g, rin, d, r, done); break;
+        case 4: pcheb_res_cell_kernel<4><<<mw->nb, RED_NT, 0, s>>>(g, rin, d, r, done); break;
+        case 5: pcheb_res_cell_kernel<5><<<mw->nb, RED_NT, 0, s>>>(g, rin, d, r, done); break;
+        case 6: pcheb_res_cell_kernel<6><<<mw->nb, RED_NT, 0, s>>>(g, rin, d, r, done); break;
+        default: return HDIV_ERR_UNSUPPORTED;
+      }
+    } else {
+      pcheb_res_sell_kernel<5><<<mw->nb, RED_NT, 0, s>>>(h->d_ecol, h->d_eval, rin, d, r, n, done);
+    }
+    HDIV_CUDA_TRY(cudaGetLastError());
+    if ((st = amg_vcycle(h, r, t, done, s)) != HDIV_OK) return st;
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    pcheb_upd_kernel<<<mw->nb, RED_NT, 0, s>>>(t, d, y, vq, rn * rho, 2.0 * rn / delta, n,
+                                               i == k - 1, part, done);
+    HDIV_CUDA_TRY(cudaGetLastError());
+    rho = rn;
+  }
+  return HDIV_OK;
+}
+
 // Chebyshev-Jacobi S^-1 applied to vq -> y (uses mw->r, mw->d); partial <y, vq> if part
 static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, double* part,
                                   const int* done, cudaStream_t s) {
   MinresWork* mw = h->mw;
+  if (h->opts.schur_solver == HDIV_SCHUR_AMG && h->opts.amg_cheb_degree >= 2)
+    return amg_cheb_apply(h, vq, y, part, done, s);
   if (h->opts.schur_solver == HDIV_SCHUR_AMG) {   // NEXT-1: one V-cycle
     if (part) {   // the partial <y, vq> fused into the last level-0 smoothing sweep
       hdiv_status st = amg_vcycle(h, vq, y, done, s, part, h->mw->nb);

@@ -333,6 +333,38 @@ def test_amg_precond_and_minres_parity(name, N, p, mc):
     assert _rel(_host(x), xo) < 1e-9
 
 
+@pytest.mark.parametrize("name,N,p,mc,k,ratio", [("c2", (5, 4, 3), 3, 16, 3, 20.0),
+                                                 ("c1", (6, 5), 2, 8, 2, 20.0),
+                                                 ("c3", (4, 3, 3), 2, 20, 3, 20.0),
+                                                 ("c3", (3, 3, 4), 3, 20, 2, 10.0),
+                                                 ("c3s", (3, 4, 3), 2, 20, 3, 20.0),
+                                                 ("c5", (5, 5, 3), 2, 30, 4, 40.0)])
+def test_amg_chebyshev_precond_and_minres_parity(name, N, p, mc, k, ratio):
+    """Reading A9d: S^-1 = the degree-k Chebyshev polynomial in B S~ (B = one V-cycle) — the
+    preconditioner output and the MINRES iteration count (+-1) against the oracle's r/d form."""
+    from oracle import operators, solvers
+    pr = _problem(name, N, p)
+    A = operators.Assembled(pr)
+    P = solvers.BlockDiagPrecond(A, schur="amg", amg_nu=2, amg_max_coarse=mc, amg_cheb_degree=k,
+                                 amg_cheb_ratio=ratio)
+    op = _gpu(pr, schur="amg", amg_max_coarse=mc, amg_cheb_degree=k, amg_cheb_ratio=ratio)
+    n = A.n_rt + A.n_l2
+    v = random_vector(n, 23)
+    z = _host(op.apply_precond(_dev(v)))
+    zo = P.apply(v)
+    assert _rel(z[:A.n_rt], zo[:A.n_rt]) < TOL
+    assert _rel(z[A.n_rt:], zo[A.n_rt:]) < 1e-11
+    b = A.apply_block(random_vector(n, 1))
+    if getattr(pr, "project_mean", False):
+        b[A.n_rt:] -= b[A.n_rt:].mean()
+    xo, it_o, conv_o, _ = solvers.minres(A.apply_block, P.apply, b, rtol=1e-12, maxit=2000)
+    x, rep = op.minres(_dev(b), rtol=1e-12, maxit=2000)
+    assert conv_o and rep.converged
+    assert abs(rep.iters - it_o) <= 1, (rep.iters, it_o)
+    if not getattr(pr, "project_mean", False):
+        assert _rel(_host(x), xo) < 1e-9
+
+
 @pytest.mark.parametrize("name,N,p", [("c3gd", (3, 2, 2), 2), ("c3gd", (2, 2, 3), 5), ("c3g", (2, 3, 2), 4),
                                       ("c2", (3, 2, 2), 3), ("c5", (5, 5, 3), 1), ("c1", None, None),
                                       ("c1", (5, 3), 4)])

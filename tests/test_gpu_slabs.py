@@ -142,11 +142,14 @@ def test_slab_minres(name, N, p, P, ess, project):
         assert np.abs(dq - c).max() < 1e-9 * np.abs(x1[n_rt:]).max()
 
 
-@pytest.mark.parametrize("name,N,p,P,ess,project", [("c2", (4, 3, 7), 3, 2, 0, False),
-                                                    ("c3", (3, 3, 6), 2, 3, 0, False),
-                                                    ("c5", (5, 5, 6), 2, 2, 0, False),
-                                                    ("c3", (3, 3, 4), 2, 2, 63, True)])
-def test_slab_minres_amg(name, N, p, P, ess, project):
+@pytest.mark.parametrize("name,N,p,P,ess,project,k", [("c2", (4, 3, 7), 3, 2, 0, False, 1),
+                                                      ("c3", (3, 3, 6), 2, 3, 0, False, 1),
+                                                      ("c5", (5, 5, 6), 2, 2, 0, False, 1),
+                                                      ("c3", (3, 3, 4), 2, 2, 63, True, 1),
+                                                      ("c3", (3, 3, 6), 2, 3, 0, False, 3),
+                                                      ("c1", (5, 8), 2, 2, 0, False, 2),
+                                                      ("c3", (3, 3, 4), 2, 2, 63, True, 2)])
+def test_slab_minres_amg(name, N, p, P, ess, project, k):
     """Multi-rank S^-1 = block-Jacobi of per-slab AMG V-cycles (reading A9c): each rank's
     preconditioner output and the MINRES iteration counts (+-1) against the oracle's
     block-Jacobi AMG on the same slabs."""
@@ -159,7 +162,8 @@ def test_slab_minres_amg(name, N, p, P, ess, project):
     A = operators.Assembled(pr)
     last = pr.dim - 1
     bounds = [sl.slab_bounds(pr.N[last], P, r) for r in range(P)]
-    Po = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds)
+    Po = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds,
+                                  amg_cheb_degree=k)
     n_rt = A.n_rt
     v = random_vector(A.n_rt + A.n_l2, 8)
     if project:
@@ -176,8 +180,8 @@ def test_slab_minres_amg(name, N, p, P, ess, project):
         xl, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
         return zl, xl.cpu().numpy(), rep.iters, rep.converged, rt, l2
 
-    res = _run_slabs(pr, P, fn, key=3000 + hash((name, N, p, P, ess)) % 1000,
-                     schur="amg", amg_max_coarse=16)
+    res = _run_slabs(pr, P, fn, key=3000 + hash((name, N, p, P, ess, k)) % 1000,
+                     schur="amg", amg_max_coarse=16, amg_cheb_degree=k)
     assert conv_o
     its = {r[2] for r in res}
     assert len(its) == 1 and all(r[3] for r in res), its
@@ -235,3 +239,35 @@ def test_slab_gmres(name, N, p, P, schur):
         nrl = len(rt)
         assert _rel(xl[:nrl], x1[:n_rt][rt]) < 1e-8
         assert _rel(xl[nrl:], x1[n_rt:][l2]) < 1e-7
+
+
+@pytest.mark.gpu
+def test_slab_amg_chebyshev_iterations_flat_in_P():
+    """Reading A9d on slabs: with the polynomial (b = 2.2) over the block-Jacobi V-cycles the
+    MINRES iteration count barely grows with the rank count, where the plain block-Jacobi
+    V-cycle's does (10^4-contrast config-3 mesh, loopback ranks on one GPU)."""
+    import torch
+    from paper_2304_12387_b200 import from_problem
+    pr = _problem("c3", (4, 4, 8), 2)
+    its = {}
+    for k in (1, 3):
+        op = from_problem(pr, schur="amg", amg_max_coarse=16, amg_cheb_degree=k)
+        n = op.sizes.n
+        xs = torch.from_numpy(random_vector(n, 3)).cuda()
+        b = op.apply_block(xs).cpu().numpy()
+        _, rep = op.minres(torch.from_numpy(b).cuda(), rtol=1e-12, maxit=3000)
+        op.close()
+        assert rep.converged
+        its[(k, 1)] = rep.iters
+        for P in (2, 4):
+            def fn(r, op, rt, l2):
+                nrt_g = len(b) - pr.E * pr.p ** 3
+                bl = np.concatenate([b[:nrt_g][rt], b[nrt_g:][l2]])
+                _, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
+                return rep.iters, rep.converged
+            res = _run_slabs(pr, P, fn, key=4000 + 10 * k + P, schur="amg", amg_max_coarse=16,
+                             amg_cheb_degree=k)
+            assert all(r[1] for r in res)
+            its[(k, P)] = res[0][0]
+    assert its[(3, 4)] <= 1.15 * its[(3, 1)] + 4, its
+    assert its[(3, 4)] < its[(1, 4)], its

@@ -188,3 +188,55 @@ def test_chebyshev_accelerated_vcycle(k, ratio):
         assert lam[0] > 0
         return lam[-1] / lam[0]
     assert cond(Bm) < cond(B1), (cond(Bm), cond(B1))
+
+
+def test_slab_block_jacobi_spectrum_bound():
+    """Reading A9d with slabs (A9c): the block-Jacobi B over a chain of slabs has spectrum of
+    B S~ in (0, 2] — checked with exact slab solves (one-level hierarchies, B = blockdiag
+    S~[slab, slab]^-1) and with V-cycles on a 10^4-contrast mesh; it exceeds 1.1 (so the
+    single-block interval would not cover it), which is why the slab polynomial takes b = 2.2."""
+    from oracle import amg as amgmod, operators
+    from synth import make_config
+    A = operators.Assembled(make_config("c3", N=(3, 3, 6), p=2))
+    S = A.S.toarray()
+    n = A.n_l2
+    for mc, bounds in [(10 ** 6, [(0, 2), (2, 4), (4, 6)]), (8, [(0, 3), (3, 6)]),
+                       (8, [(0, 1), (1, 2), (2, 4), (4, 6)])]:
+        B = amgmod.AMGSchur(A, max_coarse=mc, slabs=bounds)
+        Bm = np.column_stack([B(e) for e in np.eye(n)])
+        lam = np.sort(np.linalg.eigvals(Bm @ S).real)
+        assert lam[0] > 0 and lam[-1] <= 2.0 + 1e-10, (mc, bounds, lam[0], lam[-1])
+        if mc > n:
+            assert lam[-1] > 1.1
+
+
+def test_pinned_coarse_solve_spectrum():
+    """Reading A21 (pure-Neumann S~, constants in its nullspace): the pinned coarsest solve fixes
+    the last unknown at 0 and drops its equation, so with an exact one-level hierarchy
+    B S~ x = x - x_last 1 — eigenvalues exactly {0, 1} — and with a deep hierarchy the spectrum
+    of B S~ stays in [0, 1] (the interval the A9d polynomial assumes).  The identity-row pin
+    alone (without dropping the equation) overshoots 1."""
+    from oracle import amg as amgmod, operators
+    from synth import make_config
+    pr = make_config("c3", N=(3, 3, 4), p=2)
+    pr.essential, pr.project_mean, pr.gamma = 63, True, np.zeros(pr.E)
+    A = operators.Assembled(pr)
+    S = A.S.toarray()
+    n = A.n_l2
+    assert np.abs(S @ np.ones(n)).max() < 1e-10 * np.abs(S).max()   # singular: constants
+    for mc in (10 ** 6, 16):
+        B = amgmod.AMGSchur(A, max_coarse=mc, pin=True)
+        Bm = np.column_stack([B(e) for e in np.eye(n)])
+        lam = np.sort(np.linalg.eigvals(Bm @ S).real)
+        assert lam[0] > -1e-12 and lam[-1] < 1.0 + 1e-10, (mc, lam[0], lam[-1])
+        if mc > n:
+            x = np.arange(n, dtype=float) % 7
+            assert np.abs(Bm @ (S @ x) - (x - x[-1])).max() < 1e-10 * np.abs(x).max()
+    lv = amgmod.build_hierarchy(A.S.tocsr(), amgmod.l2_cell_coords(3, pr.N, 2), (6, 6, 8),
+                                max_coarse=10 ** 6, coarse_solve=False)
+    Ad = lv[-1].A.toarray()
+    Ad[-1, :] = 0.0
+    Ad[:, -1] = 0.0
+    Ad[-1, -1] = 1.0
+    lam = np.linalg.eigvals(np.linalg.inv(Ad) @ S).real
+    assert lam.max() > 1.01
