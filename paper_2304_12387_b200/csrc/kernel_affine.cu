@@ -56,20 +56,6 @@ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 #define HDIV_X_DIRECT 1
 #endif
 constexpr bool kXDirect = HDIV_X_DIRECT;
-// M_h (x) M_h as two in-place passes (rows, then columns) from this order up (register relief)
-#ifndef HDIV_MH2_MINP
-#define HDIV_MH2_MINP 7
-#endif
-constexpr int kMh2MinP = HDIV_MH2_MINP;
-#ifndef HDIV_P4_MINB
-#define HDIV_P4_MINB 0
-#endif
-#ifndef HDIV_P5_MINB
-#define HDIV_P5_MINB 0
-#endif
-#ifndef HDIV_P6_MINB
-#define HDIV_P6_MINB 2
-#endif
 
 // smem box of component AX: extent (T_AX+1)P+1 along AX (position 0 <-> global plane
 // (e0_AX - 1) P), T P along the others.  Strides: the generated per-tile layout
@@ -362,38 +348,6 @@ __device__ __forceinline__ void component(const AffArgs& a, const TileInfo& ti,
     const int pa = it % EAP + (P - 1), b1 = (it / EAP) % C::TA1, b2 = it / (EAP * C::TA1);
     if (pa >= C::EA) continue;
     double* base = su + pa * C::SA + b1 * P * C::SA1 + b2 * P * C::SA2;
-    if constexpr (P >= kMh2MinP) {
-      // two in-place passes by the same thread (rows along A1, then columns along A2; the same
-      // arithmetic): P live values instead of the P x P block, one more smem read + write each
-#pragma unroll
-      for (int k2 = 0; k2 < P; ++k2) {
-        double v[P];
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) v[k1] = base[k1 * C::SA1 + k2 * C::SA2];
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) {
-          double t = 0.0;
-#pragma unroll
-          for (int j = 0; j < P; ++j) t = fma(tab.Mh[k1][j], v[j], t);
-          base[k1 * C::SA1 + k2 * C::SA2] = t;
-        }
-      }
-      asm volatile("" ::: "memory");   // keep the round trip through smem (no forwarding)
-#pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) {
-        double v[P];
-#pragma unroll
-        for (int k2 = 0; k2 < P; ++k2) v[k2] = base[k1 * C::SA1 + k2 * C::SA2];
-#pragma unroll
-        for (int k2 = 0; k2 < P; ++k2) {
-          double t = 0.0;
-#pragma unroll
-          for (int j = 0; j < P; ++j) t = fma(tab.Mh[k2][j], v[j], t);
-          base[k1 * C::SA1 + k2 * C::SA2] = t;
-        }
-      }
-      continue;
-    }
     // row by row: only one input row and the P x P intermediate are live (register pressure)
     double w[P][P];
 #pragma unroll
@@ -793,9 +747,9 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
     case 1: return launch_tile<BLOCK, 1, 8, 8, 4, 128, true, 0, kXDirect>(h, x, y, k, s, dpart);
     case 2: return launch_tile<BLOCK, 2, 8, 4, 4, 128, true, 0, kXDirect>(h, x, y, k, s, dpart);
     case 3: return launch_tile<BLOCK, 3, 4, 4, 2, 160, false, 0, kXDirect>(h, x, y, k, s, dpart);
-    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, HDIV_P4_MINB, kXDirect>(h, x, y, k, s, dpart);
-    case 5: return launch_tile<BLOCK, 5, 3, 2, 2, 160, false, HDIV_P5_MINB, false>(h, x, y, k, s, dpart);
-    case 6: return launch_tile<BLOCK, 6, 3, 2, 2, 224, false, HDIV_P6_MINB, false>(h, x, y, k, s, dpart);
+    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, 0, kXDirect>(h, x, y, k, s, dpart);
+    case 5: return launch_tile<BLOCK, 5, 3, 2, 2, 160, false, 0, false>(h, x, y, k, s, dpart);
+    case 6: return launch_tile<BLOCK, 6, 3, 2, 2, 224, false, 2, false>(h, x, y, k, s, dpart);
   }
   return cudaErrorInvalidValue;
 }
