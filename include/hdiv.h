@@ -117,7 +117,8 @@ typedef struct {
    * polynomial in B S~ (B = the V-cycle above) on [b / amg_cheb_ratio, b], b = 1.1 (one rank)
    * or 2.2 (slabs: block-Jacobi over a chain, spectrum <= 2) — the r/d
    * recurrence of reading A10 with B in place of D^-1, amg_cheb_degree V-cycles and
-   * amg_cheb_degree - 1 S~ applies per S^-1.  <= 1 => 1 (the plain V-cycle);
+   * amg_cheb_degree - 1 S~ applies per S^-1.  1 = the plain V-cycle; <= 0 = auto:
+   * 3 when the element mass weights (beta | 1/eps) span more than 10^2 or with slabs, else 1;
    * amg_cheb_ratio <= 0 => 20. */
   int amg_cheb_degree;
   double amg_cheb_ratio;

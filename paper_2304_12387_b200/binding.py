@@ -176,7 +176,7 @@ class HdivOperator:
     def __init__(self, dim, N, p, kind, vertices=None, alpha=None, beta=None, gamma=None,
                  eps=None, gamma_vertex=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
                  schur="auto", amg_sweeps=2, amg_max_coarse=512, essential=0,
-                 project_mean=False, tri_geometry=0, amg_cheb_degree=1, amg_cheb_ratio=20.0,
+                 project_mean=False, tri_geometry=0, amg_cheb_degree=0, amg_cheb_ratio=20.0,
                  slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
         import torch
         self.lib = load_library()

@@ -19,6 +19,7 @@ def _rel(a, b):
 
 def _gpu(prob, **kw):
     from paper_2304_12387_b200 import from_problem
+    kw.setdefault("amg_cheb_degree", 1)   # the oracle's BlockDiagPrecond default (plain V-cycle)
     return from_problem(prob, **kw)
 
 
@@ -584,4 +585,25 @@ def test_schur_auto_choice():
                         (small, {"schur": "amg"}, True)]:
         op = _gpu(pr, **kw)
         assert (levels(op) >= 1) == amg, (pr.N, kw)
+        op.close()
+
+
+@pytest.mark.gpu
+def test_amg_auto_polynomial_degree():
+    """options.amg_cheb_degree = 0 (the binding default): the degree-3 polynomial (reading A9d)
+    when the element mass weights span more than 10^2 (config 3's eps = 10^U(-2,2)), the plain
+    V-cycle on constant coefficients — checked through the preconditioner output against the
+    oracle at both degrees."""
+    from oracle import operators, solvers
+    from paper_2304_12387_b200 import from_problem
+    for name, N, p, k in [("c3", (4, 3, 3), 2, 3), ("c4", (4, 3, 3), 2, 1)]:
+        pr = make_config(name, N=N, p=p)
+        A = operators.Assembled(pr)
+        op = from_problem(pr, schur="amg", amg_max_coarse=20)
+        v = random_vector(A.n_rt + A.n_l2, 23)
+        z = _host(op.apply_precond(_dev(v)))[A.n_rt:]
+        for kk in (1, 3):
+            P = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=20, amg_cheb_degree=kk)
+            err = _rel(z, P.apply(v)[A.n_rt:])
+            assert (err < 1e-11) == (kk == k), (name, kk, err)
         op.close()

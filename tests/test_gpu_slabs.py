@@ -38,7 +38,7 @@ def _run_slabs(pr, P, fn, key, **kw):
                 op = HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b,
                                   gamma=g, eps=e, essential=pr.essential,
                                   project_mean=pr.project_mean, slab=(z0, z1), nccl_id=uid,
-                                  rank=r, nranks=P, **kw)
+                                  rank=r, nranks=P, **{"amg_cheb_degree": 1, **kw})
                 rt = slabs.local_to_global_rt(pr.dim, pr.N, pr.p, z0, z1)
                 l2 = slabs.local_to_global_l2(pr.dim, pr.N, pr.p, z0, z1)
                 out[r] = fn(r, op, rt, l2)
@@ -207,7 +207,7 @@ def test_slab_gmres(name, N, p, P, schur):
     from paper_2304_12387_b200 import from_problem, slabs as sl
     pr = _problem(name, N, p)
     kw = {"schur": schur, "amg_max_coarse": 16}
-    ref = from_problem(pr, **kw)
+    ref = from_problem(pr, amg_cheb_degree=1, **kw)
     n_rt = ref.sizes.n_rt
     xs = random_vector(ref.sizes.n, 3)
     b = ref.apply_block(torch.from_numpy(xs).cuda())
