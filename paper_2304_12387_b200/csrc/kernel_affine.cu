@@ -717,7 +717,9 @@ cudaError_t launch_t(const hdiv_ctx* h, const double* x, double* y, const int* s
 
 // one production tile per order (r01 sweeps, profiles/r01_variant_sweep_v*.txt): TXxTYxTZ
 // elements, NT threads, DB = double-buffered component boxes (p <= 2; single-buffered tiles
-// give more CTAs per SM at p >= 3), MINB = __launch_bounds__ min blocks, XD = x planes stored
+// give more CTAs per SM at p >= 3), MINB = __launch_bounds__ min blocks (p = 4: 7 -> 72 registers,
+// 7 CTAs per SM, the shared-memory limit; 2.30 -> 2.26 ms, profiles/r02_box_experiments_late.txt),
+// XD = x planes stored
 // straight from the line pass (else written back and copied out coalesced, p = 5, 6).
 // Eliminated essential sides use an instantiation of their own (ESS).
 template <bool BLOCK, int P, int TX, int TY, int TZ, int NT, bool DB, int MINB, bool XD>
@@ -747,7 +749,7 @@ cudaError_t dispatch(const hdiv_ctx* h, const double* x, double* y, const int* k
     case 1: return launch_tile<BLOCK, 1, 8, 8, 4, 128, true, 0, kXDirect>(h, x, y, k, s, dpart);
     case 2: return launch_tile<BLOCK, 2, 8, 4, 4, 128, true, 0, kXDirect>(h, x, y, k, s, dpart);
     case 3: return launch_tile<BLOCK, 3, 4, 4, 2, 160, false, 0, kXDirect>(h, x, y, k, s, dpart);
-    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, 0, kXDirect>(h, x, y, k, s, dpart);
+    case 4: return launch_tile<BLOCK, 4, 4, 2, 2, 128, false, 7, kXDirect>(h, x, y, k, s, dpart);
     case 5: return launch_tile<BLOCK, 5, 3, 2, 2, 160, false, 0, false>(h, x, y, k, s, dpart);
     case 6: return launch_tile<BLOCK, 6, 3, 2, 2, 224, false, 2, false>(h, x, y, k, s, dpart);
   }
