@@ -165,11 +165,13 @@ class BlockTriPrecond:
     polynomial, so GMRES converges in at most two iterations."""
 
     def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, schur="chebyshev", exact_blocks=False,
-                 amg_nu=2, amg_max_coarse=512):
+                 amg_nu=2, amg_max_coarse=512, amg_cheb_degree=1, amg_cheb_ratio=20.0):
         self.asm, self.tau = asm, tau
         self.diag = BlockDiagPrecond(asm, tau=tau, degree=degree, ratio=ratio, schur=schur,
                                      exact_blocks=exact_blocks, amg_nu=amg_nu,
-                                     amg_max_coarse=amg_max_coarse, project_mean=False)
+                                     amg_max_coarse=amg_max_coarse, project_mean=False,
+                                     amg_cheb_degree=amg_cheb_degree,
+                                     amg_cheb_ratio=amg_cheb_ratio)
         self.exact_blocks = exact_blocks
         self.n_rt = asm.n_rt
 

@@ -76,7 +76,7 @@ def test_masked_applies(name, N, p, ess):
     op.close()
 
 
-@pytest.mark.parametrize("schur", ["chebyshev", "amg"])
+@pytest.mark.parametrize("schur", ["chebyshev", "amg", "amg3"])
 @pytest.mark.parametrize("name,N,p", [("c3", (3, 3, 2), 2), ("c2", (4, 3, 3), 3), ("c1", (5, 4), 2)])
 def test_pure_neumann_minres_parity(name, N, p, schur):
     """All sides essential, Darcy gamma = 0 (the SPE10 shape): singular S~,
@@ -93,8 +93,10 @@ def test_pure_neumann_minres_parity(name, N, p, schur):
     n = A.n_rt + A.n_l2
     xs = random_vector(n, 4)
     b = A.apply_block(xs)
-    P = solvers.BlockDiagPrecond(A, schur=schur, amg_max_coarse=16)
-    op = from_problem(pr, schur=schur, amg_max_coarse=16, amg_cheb_degree=1)
+    k = 3 if schur == "amg3" else 1   # amg3: the A9d polynomial over the pinned V-cycle
+    schur = "amg" if k == 3 else schur
+    P = solvers.BlockDiagPrecond(A, schur=schur, amg_max_coarse=16, amg_cheb_degree=k)
+    op = from_problem(pr, schur=schur, amg_max_coarse=16, amg_cheb_degree=k)
     v = random_vector(n, 8)
     v[A.n_rt:] -= v[A.n_rt:].mean()
     z, zo = _host(op.apply_precond(_dev(v))), P.apply(v)

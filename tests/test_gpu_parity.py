@@ -382,15 +382,17 @@ def test_apply_z_parity(name, N, p):
 
 
 # ---- NEXT-4: block-triangular preconditioner + GMRES ----
-@pytest.mark.parametrize("name,N,p,schur", [("c1", None, None, "chebyshev"), ("c2", (3, 2, 2), 3, "chebyshev"),
-                                            ("c3", (2, 2, 2), 2, "amg"), ("c5", (5, 5, 3), 1, "amg")])
-def test_gmres_triangular_parity(name, N, p, schur):
+@pytest.mark.parametrize("name,N,p,schur,k", [("c1", None, None, "chebyshev", 1),
+                                              ("c2", (3, 2, 2), 3, "chebyshev", 1),
+                                              ("c3", (2, 2, 2), 2, "amg", 1), ("c5", (5, 5, 3), 1, "amg", 1),
+                                              ("c3", (3, 2, 3), 2, "amg", 3)])
+def test_gmres_triangular_parity(name, N, p, schur, k):
     from oracle import operators, solvers
     pr = _problem(name, N, p)
     A = operators.Assembled(pr)
     mc = 16
-    B = solvers.BlockTriPrecond(A, schur=schur, amg_max_coarse=mc)
-    op = _gpu(pr, schur=schur, amg_max_coarse=mc)
+    B = solvers.BlockTriPrecond(A, schur=schur, amg_max_coarse=mc, amg_cheb_degree=k)
+    op = _gpu(pr, schur=schur, amg_max_coarse=mc, amg_cheb_degree=k)
     n = A.n_rt + A.n_l2
     v = random_vector(n, 41)
     z = _host(op.apply_precond_tri(_dev(v)))
