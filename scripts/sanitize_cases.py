@@ -31,6 +31,10 @@ if which in ("all", "c12"):
     run(make_config("c1"), schur="amg")
     run(make_config("c2"))
     run(make_config("c2"), schur="amg")
+if which in ("all", "a9d"):   # reading A9d: Chebyshev polynomial in (V-cycle) S~, 3D and 2D
+    run(make_config("c3", N=(4, 4, 3), p=2), schur="amg", amg_cheb_degree=3, amg_max_coarse=16)
+    run(make_config("c3s", N=(3, 4, 3), p=2), schur="amg", amg_cheb_degree=2, amg_max_coarse=16)
+    run(make_config("c1", N=(6, 5)), schur="amg", amg_cheb_degree=3, amg_max_coarse=8)
 if which in ("all", "box"):
     for p, N in [(1, (9, 5, 5)), (2, (9, 5, 5)), (3, (5, 5, 3)), (4, (5, 3, 3)), (5, (4, 3, 3)),
                  (6, (4, 3, 2))]:
