@@ -445,9 +445,36 @@ def main():
         e2e = {"value": n_glob * args.e2e_steps / te / 1e9, "unit": "GDOF/s",
                "h2d_bytes_per_step": 8 * s.n, "d2h_bytes_per_step": 8 * s.n,
                "note": "hdiv_apply_block_host: pinned host x -> device, apply, device -> pinned "
-                       "host y every step; box meshes pipeline ~16 z-chunks (H2D of chunk c+1 "
+                       "host y every step; box meshes pipeline ~32 z-chunks (H2D of chunk c+1 "
                        "and D2H of chunk c-1 overlap the fused apply of chunk c, three streams)"}
-        del xh, yh
+        # the PCIe ceiling of that number: the same bytes copied both ways at once (torch
+        # copies on two streams, no apply) -> the e2e value a zero-cost apply would reach
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        ycp = torch.empty_like(x)
+
+        def both():
+            cur = torch.cuda.current_stream()
+            s1.wait_stream(cur)
+            s2.wait_stream(cur)
+            with torch.cuda.stream(s1):
+                ycp.copy_(xh, non_blocking=True)
+            with torch.cuda.stream(s2):
+                yh.copy_(x, non_blocking=True)
+            cur.wait_stream(s1)
+            cur.wait_stream(s2)
+        both()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(2):
+            both()
+        c1.record()
+        torch.cuda.synchronize()
+        tc = c0.elapsed_time(c1) / 2 / 1e3
+        e2e["pcie_ceiling"] = {"value": n_glob / tc / 1e9, "unit": "GDOF/s",
+                               "copy_gbs_per_direction": 8 * s.n / tc / 1e9,
+                               "frac": e2e["value"] / (n_glob / tc / 1e9)}
+        del xh, yh, ycp
 
     result = {"metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws,
               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
