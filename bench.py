@@ -758,7 +758,7 @@ def main():
     if not args.no_minres and ws == 1:
         result["winv"] = winv_bench(torch)
 
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu:   # (the oracle baseline: N = 1 only)
         result["cpu_baseline"] = cpu_baseline(pr)
     if rank == 0:
         print(json.dumps(result), flush=True)
