@@ -303,7 +303,7 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->has_z = (kind == HDIV_GRAD_DIV) || any_gamma;
   // A9d auto degree: the polynomial where one V-cycle of the geometric aggregation degrades —
   // element-wise contrast of the mass weight above 10^2 (config 3: 890 -> 330 MINRES iterations,
-  // 3.6 -> 2.7 s) or slabs (block-Jacobi across ranks: flat iteration counts in P); else the plain
+  // 3.6 -> 2.7 s) or slabs (block-Jacobi across ranks: config-3 mesh 24^3 p=4 at 8 slabs 637 -> 316 its); else the plain
   // V-cycle (config 4: 155 its / 3.7 s, the polynomial no faster)
   if (h->opts.amg_cheb_degree <= 0) {
     double lo = mw.empty() ? 1.0 : mw[0], hi = lo;

@@ -244,8 +244,9 @@ def test_slab_gmres(name, N, p, P, schur):
 @pytest.mark.gpu
 def test_slab_amg_chebyshev_iterations_flat_in_P():
     """Reading A9d on slabs: with the polynomial (b = 2.2) over the block-Jacobi V-cycles the
-    MINRES iteration count barely grows with the rank count, where the plain block-Jacobi
-    V-cycle's does (10^4-contrast config-3 mesh, loopback ranks on one GPU)."""
+    MINRES iteration count stays below the plain block-Jacobi V-cycle's, and on this small
+    10^4-contrast config-3 mesh barely grows with the rank count (loopback ranks on one GPU; at
+    24^3 p = 4 it does grow, 191 -> 316 from 1 to 8 slabs: profiles/r02_slab_iterations.txt)."""
     import torch
     from paper_2304_12387_b200 import from_problem
     pr = _problem("c3", (4, 4, 8), 2)
