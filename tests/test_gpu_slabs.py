@@ -196,7 +196,8 @@ def test_slab_minres_amg(name, N, p, P, ess, project, k):
 @pytest.mark.parametrize("name,N,p,P,schur", [("c2", (4, 3, 6), 3, 2, "chebyshev"),
                                               ("c2", (4, 3, 12), 3, 2, "amg"),
                                               ("c3", (3, 3, 6), 2, 3, "chebyshev"),
-                                              ("c5", (5, 5, 6), 2, 2, "amg")])
+                                              ("c5", (5, 5, 6), 2, 2, "amg"),
+                                              ("c3", (3, 3, 6), 2, 3, "amg3")])
 def test_slab_gmres(name, N, p, P, schur):
     """NEXT-4 on slabs: block-triangular preconditioner (D^T reverse-added) + GMRES with
     all-gathered projections — every rank takes the same decisions; iteration counts +-1 and
@@ -206,8 +207,10 @@ def test_slab_gmres(name, N, p, P, schur):
     from oracle import operators, solvers
     from paper_2304_12387_b200 import from_problem, slabs as sl
     pr = _problem(name, N, p)
-    kw = {"schur": schur, "amg_max_coarse": 16}
-    ref = from_problem(pr, amg_cheb_degree=1, **kw)
+    k = 3 if schur == "amg3" else 1   # amg3: the A9d polynomial over the block-Jacobi V-cycles
+    schur = "amg" if k == 3 else schur
+    kw = {"schur": schur, "amg_max_coarse": 16, "amg_cheb_degree": k}
+    ref = from_problem(pr, **kw)
     n_rt = ref.sizes.n_rt
     xs = random_vector(ref.sizes.n, 3)
     b = ref.apply_block(torch.from_numpy(xs).cuda())
@@ -222,7 +225,7 @@ def test_slab_gmres(name, N, p, P, schur):
         bounds = [sl.slab_bounds(pr.N[last], P, r) for r in range(P)]
         B = solvers.BlockTriPrecond(A, schur="amg", amg_max_coarse=16)
         B.diag = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds,
-                                          project_mean=False)
+                                          project_mean=False, amg_cheb_degree=k)
         x1, it1, conv, _ = solvers.gmres(A.apply_block, B.apply, b, rtol=1e-10, restart=20)
         assert conv
 
