@@ -136,7 +136,7 @@ class AMGSchur:
     In the element-contiguous L2 numbering every slab is one contiguous index range."""
 
     def __init__(self, asm, nu=2, max_coarse=512, pin=False, slabs=None, cheb_degree=1,
-                 cheb_ratio=20.0):
+                 cheb_ratio=20.0, global_coarse=False):
         coords = l2_cell_coords(asm.dim, asm.N, asm.p)
         dims = [int(asm.N[a]) * asm.p for a in range(asm.dim)]
         self.nu = nu
@@ -173,12 +173,56 @@ class AMGSchur:
                                  pin=pin and len(slabs) == 1)
             self.blocks.append((a, b, lv))
         self.levels = self.blocks[0][2] if len(self.blocks) == 1 else None
+        # reading A9e (slabs only): a global coarse space couples the slabs — the indicator
+        # vectors of the aggregates of a fixed coarse grid of the GLOBAL subcell grid (ceil(n_a /
+        # C) subcells per aggregate along axis a, C = 8 in 3D, 16 in 2D), R the aggregate-sum
+        # restriction, A0 = R S~ R^T (the exact Galerkin operator, dense), B0 = R^T A0^-1 R, and
+        # the block-Jacobi V-cycles B_bj enter the balancing (hybrid two-level) form
+        #   B = B0 + (I - B0 S~) B_bj (I - S~ B0),
+        # symmetric, with B S~ = I on range(R^T) and the spectrum of B S~ still in (0, 2]
+        # (b = 2.2 for the A9d polynomial).  The singular pure-Neumann S~ (pin) makes A0 singular
+        # with the constants as its nullspace: its last unknown is fixed at 0 (as A21).
+        self.global_coarse = bool(global_coarse) and len(slabs) > 1
+        if self.global_coarse:
+            C = 8 if asm.dim == 3 else 16
+            g = [max(1, -(-d // C)) for d in dims]
+            cd = [-(-d // gg) for d, gg in zip(dims, g)]
+            agg = coords[:, 0] // g[0]
+            stride = 1
+            for a in range(1, asm.dim):
+                stride *= cd[a - 1]
+                agg = agg + stride * (coords[:, a] // g[a])
+            n0 = int(np.prod(cd))
+            self.R = sp.csr_matrix((np.ones(len(agg)), (agg, np.arange(len(agg)))),
+                                   shape=(n0, len(agg)))
+            A0 = (self.R @ S @ self.R.T).toarray()
+            if pin:
+                A0[-1, :] = 0.0
+                A0[:, -1] = 0.0
+                A0[-1, -1] = 1.0
+            A0inv = np.linalg.inv(A0)
+            if pin:
+                A0inv[-1, :] = 0.0
+                A0inv[:, -1] = 0.0
+            self.A0inv = A0inv
 
-    def vcycles(self, r):
+    def B0(self, r):
+        return self.R.T @ (self.A0inv @ (self.R @ r))
+
+    def block_vcycles(self, r):
         out = np.empty_like(r)
         for a, b, lv in self.blocks:
             out[a:b] = vcycle(lv, r[a:b], self.nu)
         return out
+
+    def vcycles(self, r):
+        """B r: the (block-Jacobi) V-cycles, with the balancing global coarse correction when
+        global_coarse (A9e), step by step: e0 = B0 r, w = B_bj (r - S~ e0), B r = e0 + w - B0 S~ w."""
+        if not self.global_coarse:
+            return self.block_vcycles(r)
+        e0 = self.B0(r)
+        w = self.block_vcycles(r - self.S @ e0)
+        return e0 + w - self.B0(self.S @ w)
 
     def __call__(self, r):
         if self.cheb_degree < 2:

@@ -40,7 +40,7 @@ class BlockDiagPrecond:
     def __init__(self, asm, tau=1.0, degree=4, ratio=30.0, exact_schur=False, exact_blocks=False,
                  schur="chebyshev", amg_nu=2, amg_max_coarse=512, project_mean=None,
                  amg_cheb_degree=1, amg_cheb_ratio=20.0,
-                 amg_slabs=None):
+                 amg_slabs=None, amg_global_coarse=False):
         self.asm, self.tau, self.degree, self.ratio = asm, tau, degree, ratio
         # NEXT-3: with pure-Neumann (all-essential flux) Darcy and gamma = 0 the
         # Schur complement is singular with the constants as nullspace, so every application of
@@ -54,7 +54,7 @@ class BlockDiagPrecond:
             from .amg import AMGSchur
             self.amg = AMGSchur(asm, nu=amg_nu, max_coarse=amg_max_coarse, pin=project_mean,
                                 cheb_degree=amg_cheb_degree, cheb_ratio=amg_cheb_ratio,
-                                slabs=amg_slabs)
+                                slabs=amg_slabs, global_coarse=amg_global_coarse)
         self.n_rt = asm.n_rt
         self.exact_schur = exact_schur
         self.exact_blocks = exact_blocks

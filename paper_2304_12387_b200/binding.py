@@ -43,7 +43,8 @@ class Options(C.Structure):
                 ("kernel", C.c_int), ("schur_solver", C.c_int), ("amg_sweeps", C.c_int),
                 ("amg_max_coarse", C.c_int), ("essential_sides", C.c_int),
                 ("project_mean", C.c_int), ("tri_geometry", C.c_int),
-                ("amg_cheb_degree", C.c_int), ("amg_cheb_ratio", C.c_double)]
+                ("amg_cheb_degree", C.c_int), ("amg_cheb_ratio", C.c_double),
+                ("amg_global_coarse", C.c_int)]
 
 
 SCHUR_SOLVERS = {"chebyshev": 0, "amg": 1, "auto": 2}
@@ -177,6 +178,7 @@ class HdivOperator:
                  eps=None, gamma_vertex=None, tau=1.0, cheb_degree=4, cheb_ratio=30.0, kernel=0,
                  schur="auto", amg_sweeps=2, amg_max_coarse=512, essential=0,
                  project_mean=False, tri_geometry=0, amg_cheb_degree=0, amg_cheb_ratio=20.0,
+                 amg_global_coarse=0,
                  slab=None, nccl_id: Optional[bytes] = None, rank=0, nranks=1, stream=None):
         import torch
         self.lib = load_library()
@@ -200,7 +202,7 @@ class HdivOperator:
         co = Coeffs(_dptr(a_), _dptr(b_), _dptr(g_), _dptr(e_), 1.0, 1.0, 0.0, 1.0, _dptr(gv_))
         op = Options(tau, cheb_degree, cheb_ratio, kernel, SCHUR_SOLVERS[schur], amg_sweeps,
                      amg_max_coarse, int(essential), int(bool(project_mean)), int(tri_geometry),
-                     int(amg_cheb_degree), float(amg_cheb_ratio))
+                     int(amg_cheb_degree), float(amg_cheb_ratio), int(amg_global_coarse))
         h = C.c_void_p()
         idbuf = None
         if nccl_id is not None:

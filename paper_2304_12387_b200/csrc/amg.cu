@@ -41,7 +41,24 @@ struct AmgLevel {
   double *b = nullptr, *e = nullptr;   // levels >= 1: restricted rhs, coarse correction
 };
 
+// reading A9e: the balancing global coarse correction across slabs (3D)
+struct GlobalCoarse {
+  long long n0 = 0;          // global aggregates
+  int g[3] = {1, 1, 1};      // aggregate extents (global subcells)
+  int cd[3] = {1, 1, 1};     // aggregate grid
+  long long z0c = 0;         // the slab's first global subcell layer
+  double* a0inv = nullptr;   // [n0][n0] (A0 = R S~ R^T, pinned for the pure-Neumann S~)
+  double* part = nullptr;    // [n0] this rank's aggregate sums
+  double* glob = nullptr;    // [P][n0] all ranks' sums
+  double* c = nullptr;       // [n0] summed in rank order
+  double* e0 = nullptr;      // [n0]
+  double* e1 = nullptr;      // [n0]
+  double* rp = nullptr;      // [n_l2] r - S~ R^T e0
+  double* w = nullptr;       // [n_l2 + 2 plane] the block-Jacobi V-cycles (ghost space)
+};
+
 struct AmgHier {
+  GlobalCoarse* gc = nullptr;
   std::vector<AmgLevel> L;
   int32_t* agg0 = nullptr;      // level-0 row -> level-1 aggregate
   double* cinv = nullptr;       // dense inverse of the coarsest operator [nc][nc]
@@ -628,12 +645,19 @@ void amg_free(hdiv_ctx* h) {
     cudaFree(L.st); cudaFree(L.dinv); cudaFree(L.dl1inv);
     cudaFree(L.xa); cudaFree(L.xb); cudaFree(L.r); cudaFree(L.sv); cudaFree(L.b); cudaFree(L.e);
   }
+  if (GlobalCoarse* G = h->amg->gc) {
+    cudaFree(G->a0inv); cudaFree(G->part); cudaFree(G->glob); cudaFree(G->c); cudaFree(G->e0);
+    cudaFree(G->e1); cudaFree(G->rp); cudaFree(G->w);
+    delete G;
+  }
   cudaFree(h->amg->agg0);
   cudaFree(h->amg->cinv);
   cudaFree(h->amg->red);
   delete h->amg;
   h->amg = nullptr;
 }
+
+static hdiv_status gc_setup(hdiv_ctx* h, cudaStream_t s);
 
 hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
   auto* H = new AmgHier();
@@ -768,6 +792,7 @@ hdiv_status amg_setup(hdiv_ctx* h, cudaStream_t s) {
   HDIV_CUDA_TRY(cudaMalloc(&H->cinv, sizeof(double) * nc * nc));
   HDIV_CUDA_TRY(cudaMemcpyAsync(H->cinv, Ad.data(), sizeof(double) * nc * nc, cudaMemcpyHostToDevice, s));
   HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h->opts.amg_global_coarse && h->nranks > 1 && h->dim == 3) return gc_setup(h, s);   // A9e
   return HDIV_OK;
 }
 
@@ -869,13 +894,279 @@ static hdiv_status vcycle(hdiv_ctx* h, size_t l, const double* b, double* x, con
   return HDIV_OK;
 }
 
+// ---- reading A9e: B = B0 + (I - B0 S~) B_bj (I - S~ B0), B0 = R^T A0^-1 R ----
+hdiv_status comm_l2_ghosts(hdiv_ctx* h, double* x, cudaStream_t s);
+hdiv_status comm_allgather(hdiv_ctx* h, const double* loc, double* glob, int k, cudaStream_t s);
+
+namespace {
+
+struct GcGeo {
+  CellGeo g;
+  int p;
+  int gx, gy, gz, cdx, cdy;
+  long long nzg, z0c;
+  // aggregate of a local cell (element-major index) or of a ghost cell (index >= n)
+  __device__ __forceinline__ long long agg(long long j) const {
+    long long X, Y, Zg;
+    if (j < g.n) {
+      const long long pd = (long long)p * p * p;
+      const long long e = j / pd, il = j - e * pd;
+      const long long ex = e % g.NL[0], ey = (e / g.NL[0]) % g.NL[1], ez = e / ((long long)g.NL[0] * g.NL[1]);
+      X = ex * p + il % p;
+      Y = ey * p + (il / p) % p;
+      Zg = z0c + ez * p + il / (p * p);
+    } else {
+      const long long plane = g.nx * g.ny;
+      const long long q = j - g.n;
+      const bool lo = q < plane;
+      const long long idx = lo ? q : q - plane;
+      X = idx % g.nx;
+      Y = idx / g.nx;
+      Zg = lo ? z0c - 1 : z0c + g.nz;
+    }
+    return X / gx + cdx * (Y / gy + (long long)cdy * (Zg / gz));
+  }
+};
+
+template <class F>
+__device__ __forceinline__ double gc_block_sum(double v, F) {
+  __shared__ double red[ANT / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < ANT / 32; ++w) t += red[w];
+  return t;
+}
+
+// part[I] = sum over this slab's cells of aggregate I of v (MODE 0) or of (S~ v) (MODE 1, v in
+// ghost space); one CTA per aggregate, fixed-order sums
+template <int P, int MODE>
+__global__ void __launch_bounds__(ANT) gc_restrict_kernel(GcGeo G, const double* __restrict__ v,
+                                                          double* __restrict__ part,
+                                                          const int* __restrict__ done) {
+  if (done && *done) return;
+  const long long I = blockIdx.x;
+  const int Ix = (int)(I % G.cdx), Iy = (int)((I / G.cdx) % G.cdy), Iz = (int)(I / ((long long)G.cdx * G.cdy));
+  const long long x0 = (long long)Ix * G.gx, x1 = min(x0 + G.gx, G.g.nx);
+  const long long y0 = (long long)Iy * G.gy, y1 = min(y0 + G.gy, G.g.ny);
+  const long long zg0 = max((long long)Iz * G.gz, G.z0c), zg1 = min((long long)(Iz + 1) * G.gz, G.z0c + G.g.nz);
+  double acc = 0.0;
+  if (zg1 > zg0 && x1 > x0 && y1 > y0) {
+    const long long bx = x1 - x0, by = y1 - y0, cnt = bx * by * (zg1 - zg0);
+    constexpr int PD = P * P * P;
+    for (long long t = threadIdx.x; t < cnt; t += ANT) {
+      const long long X = x0 + t % bx, Y = y0 + (t / bx) % by, Z = zg0 - G.z0c + t / (bx * by);
+      const long long e = (X / P) + G.g.NL[0] * ((Y / P) + (long long)G.g.NL[1] * (Z / P));
+      const long long i = e * PD + (X % P) + P * ((Y % P) + P * (Z % P));
+      if constexpr (MODE == 0) acc += v[i];
+      else acc += cell_apply<P, true>(G.g, i, [&](long long j) { return v[j]; });
+    }
+  }
+  const double tot = gc_block_sum(acc, 0);
+  if (threadIdx.x == 0) part[I] = tot;
+}
+
+__global__ void gc_sum_kernel(const double* __restrict__ glob, int P, long long n0,
+                              double* __restrict__ c, const int* __restrict__ done) {
+  if (done && *done) return;
+  const long long I = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (I >= n0) return;
+  double t = 0.0;
+  for (int r = 0; r < P; ++r) t += glob[r * n0 + I];
+  c[I] = t;
+}
+
+// rp = b - S~ R^T e0 (the coarse correction's residual; ghosts: the neighbours' aggregates)
+template <int P>
+__global__ void __launch_bounds__(ANT) gc_resid_kernel(GcGeo G, const double* __restrict__ b,
+                                                       const double* __restrict__ e0,
+                                                       double* __restrict__ rp,
+                                                       const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(G.g.n) rp[i] = b[i] - cell_apply<P, true>(G.g, i, [&](long long j) { return e0[G.agg(j)]; });
+}
+
+// x = R^T e0 + w - R^T e1
+__global__ void __launch_bounds__(ANT) gc_final_kernel(GcGeo G, const double* __restrict__ e0,
+                                                       const double* __restrict__ w,
+                                                       const double* __restrict__ e1,
+                                                       double* __restrict__ x,
+                                                       const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(G.g.n) {
+    const long long I = G.agg(i);
+    x[i] = (e0[I] + w[i]) - e1[I];
+  }
+}
+
+GcGeo make_gcgeo(const hdiv_ctx* h) {
+  const GlobalCoarse* C = h->amg->gc;
+  GcGeo G;
+  G.g = make_cellgeo(h);
+  G.p = h->p;
+  G.gx = C->g[0]; G.gy = C->g[1]; G.gz = C->g[2];
+  G.cdx = C->cd[0]; G.cdy = C->cd[1];
+  G.nzg = h->N[2] * h->p;
+  G.z0c = C->z0c;
+  return G;
+}
+
+}  // namespace
+
+static hdiv_status gc_setup(hdiv_ctx* h, cudaStream_t s) {
+  auto* C = new GlobalCoarse();
+  h->amg->gc = C;
+  const int p = h->p;
+  const long long ng[3] = {h->N[0] * p, h->N[1] * p, h->N[2] * p};
+  long long n0 = 1;
+  for (int a = 0; a < 3; ++a) {
+    C->g[a] = (int)std::max(1LL, (ng[a] + 7) / 8);
+    C->cd[a] = (int)((ng[a] + C->g[a] - 1) / C->g[a]);
+    n0 *= C->cd[a];
+  }
+  C->n0 = n0;
+  C->z0c = h->ez0 * p;
+  const long long n = h->nl2, plane = h->n[0] * h->n[1];
+  HDIV_CUDA_TRY(cudaMalloc(&C->a0inv, sizeof(double) * n0 * n0));
+  HDIV_CUDA_TRY(cudaMalloc(&C->part, sizeof(double) * n0));
+  HDIV_CUDA_TRY(cudaMalloc(&C->glob, sizeof(double) * n0 * h->nranks));
+  HDIV_CUDA_TRY(cudaMalloc(&C->c, sizeof(double) * n0));
+  HDIV_CUDA_TRY(cudaMalloc(&C->e0, sizeof(double) * n0));
+  HDIV_CUDA_TRY(cudaMalloc(&C->e1, sizeof(double) * n0));
+  HDIV_CUDA_TRY(cudaMalloc(&C->rp, sizeof(double) * n));
+  HDIV_CUDA_TRY(cudaMalloc(&C->w, sizeof(double) * (n + 2 * plane)));
+  HDIV_CUDA_TRY(cudaMemsetAsync(C->w, 0, sizeof(double) * (n + 2 * plane), s));
+  // A0 = R S~ R^T: this rank's rows of S~ (the CSR, ghost columns for the slab neighbours),
+  // summed per aggregate pair on the host in row order, all-gathered and summed in rank order
+  std::vector<int64_t> rp(n + 1);
+  HDIV_CUDA_TRY(cudaMemcpyAsync(rp.data(), h->d_srow, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t nnz = rp[n];
+  std::vector<int32_t> col(nnz);
+  std::vector<double> val(nnz);
+  HDIV_CUDA_TRY(cudaMemcpyAsync(col.data(), h->d_scol, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, s));
+  HDIV_CUDA_TRY(cudaMemcpyAsync(val.data(), h->d_sval, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  const long long pd = (long long)p * p * p;
+  auto agg_of = [&](long long j) -> long long {
+    long long X, Y, Zg;
+    if (j < n) {
+      const long long e = j / pd, il = j - e * pd;
+      const long long ex = e % h->NL[0], ey = (e / h->NL[0]) % h->NL[1], ez = e / (h->NL[0] * h->NL[1]);
+      X = ex * p + il % p;
+      Y = ey * p + (il / p) % p;
+      Zg = C->z0c + ez * p + il / (p * p);
+    } else {
+      const long long q = j - n;
+      const bool lo = q < plane;
+      const long long idx = lo ? q : q - plane;
+      X = idx % h->n[0];
+      Y = idx / h->n[0];
+      Zg = lo ? C->z0c - 1 : C->z0c + h->n[2];
+    }
+    return X / C->g[0] + C->cd[0] * (Y / C->g[1] + (long long)C->cd[1] * (Zg / C->g[2]));
+  };
+  std::vector<double> A0(n0 * n0, 0.0);
+  for (long long i = 0; i < n; ++i) {
+    const long long I = agg_of(i);
+    for (int64_t t = rp[i]; t < rp[i + 1]; ++t) A0[I * n0 + agg_of(col[t])] += val[t];
+  }
+  double* dA0 = nullptr;
+  double* dG = nullptr;
+  HDIV_CUDA_TRY(cudaMalloc(&dA0, sizeof(double) * n0 * n0));
+  HDIV_CUDA_TRY(cudaMalloc(&dG, sizeof(double) * n0 * n0 * h->nranks));
+  HDIV_CUDA_TRY(cudaMemcpyAsync(dA0, A0.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice, s));
+  hdiv_status st = comm_allgather(h, dA0, dG, (int)(n0 * n0), s);
+  if (st != HDIV_OK) { cudaFree(dA0); cudaFree(dG); return st; }
+  std::vector<double> all(n0 * n0 * h->nranks);
+  HDIV_CUDA_TRY(cudaMemcpyAsync(all.data(), dG, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(dA0);
+  cudaFree(dG);
+  for (long long k = 0; k < n0 * n0; ++k) {
+    double t = 0.0;
+    for (int r = 0; r < h->nranks; ++r) t += all[r * n0 * n0 + k];
+    A0[k] = t;
+  }
+  const bool pin = h->opts.project_mean != 0;   // A0 singular: constants (A21)
+  if (pin) {
+    for (long long i = 0; i < n0; ++i) { A0[(n0 - 1) * n0 + i] = 0.0; A0[i * n0 + (n0 - 1)] = 0.0; }
+    A0[(n0 - 1) * n0 + (n0 - 1)] = 1.0;
+  }
+  if (!invert_dense(A0, n0)) {
+    set_error("AMG: singular global coarse operator");
+    return HDIV_ERR_BREAKDOWN;
+  }
+  if (pin)
+    for (long long i = 0; i < n0; ++i) { A0[(n0 - 1) * n0 + i] = 0.0; A0[i * n0 + (n0 - 1)] = 0.0; }
+  HDIV_CUDA_TRY(cudaMemcpyAsync(C->a0inv, A0.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice, s));
+  HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  return HDIV_OK;
+}
+
+template <int MODE>
+static hdiv_status gc_restrict(hdiv_ctx* h, const GcGeo& G, const double* v, double* e,
+                               const int* done, cudaStream_t s) {
+  GlobalCoarse* C = h->amg->gc;
+  const unsigned nb = (unsigned)C->n0;
+  switch (h->p) {
+    case 1: gc_restrict_kernel<1, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+    case 2: gc_restrict_kernel<2, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+    case 3: gc_restrict_kernel<3, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+    case 4: gc_restrict_kernel<4, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+    case 5: gc_restrict_kernel<5, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+    default: gc_restrict_kernel<6, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+  }
+  HDIV_CUDA_TRY(cudaGetLastError());
+  hdiv_status st = comm_allgather(h, C->part, C->glob, (int)C->n0, s);
+  if (st != HDIV_OK) return st;
+  gc_sum_kernel<<<(unsigned)((C->n0 + 255) / 256), 256, 0, s>>>(C->glob, h->nranks, C->n0, C->c, done);
+  coarse_kernel<<<(unsigned)((C->n0 + ANT / 32 - 1) / (ANT / 32)), ANT, 0, s>>>(C->a0inv, C->n0, C->c,
+                                                                                e, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  return HDIV_OK;
+}
+
+// x = B b with the A9e balancing form when the global coarse space is set up, else the
+// (block-Jacobi) V-cycles
+hdiv_status amg_apply(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s) {
+  if (!h->amg) {
+    set_error("AMG hierarchy missing");
+    return HDIV_ERR_UNSUPPORTED;
+  }
+  GlobalCoarse* C = h->amg->gc;
+  if (!C) return vcycle(h, 0, b, x, done, s);
+  const GcGeo G = make_gcgeo(h);
+  hdiv_status st = gc_restrict<0>(h, G, b, C->e0, done, s);   // e0 = A0^-1 R b
+  if (st != HDIV_OK) return st;
+  const unsigned g = nbk(h->nl2);
+  switch (h->p) {
+    case 1: gc_resid_kernel<1><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
+    case 2: gc_resid_kernel<2><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
+    case 3: gc_resid_kernel<3><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
+    case 4: gc_resid_kernel<4><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
+    case 5: gc_resid_kernel<5><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
+    default: gc_resid_kernel<6><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
+  }
+  HDIV_CUDA_TRY(cudaGetLastError());
+  if ((st = vcycle(h, 0, C->rp, C->w, done, s)) != HDIV_OK) return st;   // w = B_bj rp
+  if ((st = comm_l2_ghosts(h, C->w, s)) != HDIV_OK) return st;
+  if ((st = gc_restrict<1>(h, G, C->w, C->e1, done, s)) != HDIV_OK) return st;   // e1 = A0^-1 R S~ w
+  gc_final_kernel<<<g, ANT, 0, s>>>(G, C->e0, C->w, C->e1, x, done);
+  HDIV_CUDA_TRY(cudaGetLastError());
+  return HDIV_OK;
+}
+
 hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s,
                        double* part, int nbpart) {
   if (!h->amg) {
     set_error("AMG hierarchy missing");
     return HDIV_ERR_UNSUPPORTED;
   }
-  if (part && (h->amg->nu < 1 || h->amg->L.size() < 2)) return HDIV_ERR_UNSUPPORTED;
+  if (part && (h->amg->nu < 1 || h->amg->L.size() < 2 || h->amg->gc)) return HDIV_ERR_UNSUPPORTED;
+  if (h->amg->gc) return amg_apply(h, b, x, done, s);
   return vcycle(h, 0, b, x, done, s, part, nbpart);
 }
 

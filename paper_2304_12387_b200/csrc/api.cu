@@ -186,6 +186,10 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
   h->opts.tri_geometry = opts ? opts->tri_geometry : 0;
   h->opts.amg_cheb_degree = opts ? opts->amg_cheb_degree : 0;   // 0: auto (after the coefficients)
   h->opts.amg_cheb_ratio = (opts && opts->amg_cheb_ratio > 0) ? opts->amg_cheb_ratio : 20.0;
+  {
+    const int gc = opts ? opts->amg_global_coarse : 0;
+    h->opts.amg_global_coarse = (dim == 3 && nranks > 1 && gc != 2) ? 1 : 0;   // A9e
+  }
   if (h->opts.tri_geometry < 0 || h->opts.tri_geometry > 2) {
     delete h;
     return fail(HDIV_ERR_SHAPE, "options.tri_geometry must be 0, 1 or 2");

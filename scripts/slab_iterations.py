@@ -1,5 +1,5 @@
 """MINRES iteration count vs the number of z-slab ranks (reading A9c block-Jacobi AMG, with and
-without the A9d polynomial), on ONE GPU through the loopback communicator (iteration counts
+without the A9d polynomial, with and without the A9e global coarse space), on ONE GPU through the loopback communicator (iteration counts
 only — no timing: loopback ranks share one device and meet at host barriers).
     python scripts/slab_iterations.py [N] [p]"""
 import sys
@@ -20,13 +20,13 @@ n_rt = op.sizes.n_rt
 op.close()
 
 
-def run(P, k):
+def run(P, k, gc):
     if P == 1:
         o = from_problem(pr, schur="amg", amg_cheb_degree=k)
         _, rep = o.minres(torch.from_numpy(b).cuda(), rtol=1e-12, maxit=5000)
         o.close()
         return rep.iters, rep.converged
-    uid = loopback_id(7000 + 10 * P + k)
+    uid = loopback_id(7000 + 100 * gc + 10 * P + k)
     out, errs = [None] * P, []
 
     def work(r):
@@ -36,7 +36,8 @@ def run(P, k):
                 z0, z1 = slabs.slab_bounds(N, P, r)
                 V, a, bb, g, e = slabs.slab_inputs(pr, z0, z1)
                 o = HdivOperator(3, pr.N, p, pr.kind, vertices=V, alpha=a, beta=bb, gamma=g, eps=e,
-                                 schur="amg", amg_cheb_degree=k, slab=(z0, z1), nccl_id=uid,
+                                 schur="amg", amg_cheb_degree=k, amg_global_coarse=1 if gc else 2,
+                                 slab=(z0, z1), nccl_id=uid,
                                  rank=r, nranks=P)
                 rt = slabs.local_to_global_rt(3, pr.N, p, z0, z1)
                 l2 = slabs.local_to_global_l2(3, pr.N, p, z0, z1)
@@ -58,7 +59,11 @@ def run(P, k):
 
 
 print(f"config 3 mesh {N}^3, p = {p}, {len(b)} DOFs, b = A x*, rtol 1e-12", flush=True)
-for k in (1, 3):
-    for P in (1, 2, 4, 8):
-        its, conv = run(P, k)
-        print(f"  A9d degree {k}, {P} slab ranks: {its} iterations (converged {bool(conv)})", flush=True)
+for gc in (0, 1):
+    for k in (1, 3):
+        for P in (1, 2, 4, 8):
+            if gc and P == 1:
+                continue
+            its, conv = run(P, k, gc)
+            print(f"  A9d degree {k}, A9e global coarse {gc}, {P} slab ranks: {its} iterations "
+                  f"(converged {bool(conv)})", flush=True)

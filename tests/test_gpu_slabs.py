@@ -38,7 +38,7 @@ def _run_slabs(pr, P, fn, key, **kw):
                 op = HdivOperator(pr.dim, pr.N, pr.p, pr.kind, vertices=V, alpha=a, beta=b,
                                   gamma=g, eps=e, essential=pr.essential,
                                   project_mean=pr.project_mean, slab=(z0, z1), nccl_id=uid,
-                                  rank=r, nranks=P, **{"amg_cheb_degree": 1, **kw})
+                                  rank=r, nranks=P, **{"amg_cheb_degree": 1, "amg_global_coarse": 2, **kw})
                 rt = slabs.local_to_global_rt(pr.dim, pr.N, pr.p, z0, z1)
                 l2 = slabs.local_to_global_l2(pr.dim, pr.N, pr.p, z0, z1)
                 out[r] = fn(r, op, rt, l2)
@@ -142,17 +142,23 @@ def test_slab_minres(name, N, p, P, ess, project):
         assert np.abs(dq - c).max() < 1e-9 * np.abs(x1[n_rt:]).max()
 
 
-@pytest.mark.parametrize("name,N,p,P,ess,project,k", [("c2", (4, 3, 7), 3, 2, 0, False, 1),
-                                                      ("c3", (3, 3, 6), 2, 3, 0, False, 1),
-                                                      ("c5", (5, 5, 6), 2, 2, 0, False, 1),
-                                                      ("c3", (3, 3, 4), 2, 2, 63, True, 1),
-                                                      ("c3", (3, 3, 6), 2, 3, 0, False, 3),
-                                                      ("c1", (5, 8), 2, 2, 0, False, 2),
-                                                      ("c3", (3, 3, 4), 2, 2, 63, True, 2)])
-def test_slab_minres_amg(name, N, p, P, ess, project, k):
-    """Multi-rank S^-1 = block-Jacobi of per-slab AMG V-cycles (reading A9c): each rank's
-    preconditioner output and the MINRES iteration counts (+-1) against the oracle's
-    block-Jacobi AMG on the same slabs."""
+@pytest.mark.parametrize("name,N,p,P,ess,project,k,gc", [("c2", (4, 3, 7), 3, 2, 0, False, 1, False),
+                                                         ("c3", (3, 3, 6), 2, 3, 0, False, 1, False),
+                                                         ("c5", (5, 5, 6), 2, 2, 0, False, 1, False),
+                                                         ("c3", (3, 3, 4), 2, 2, 63, True, 1, False),
+                                                         ("c3", (3, 3, 6), 2, 3, 0, False, 3, False),
+                                                         ("c1", (5, 8), 2, 2, 0, False, 2, False),
+                                                         ("c3", (3, 3, 4), 2, 2, 63, True, 2, False),
+                                                         ("c3", (3, 3, 6), 2, 3, 0, False, 1, True),
+                                                         ("c3", (4, 3, 8), 2, 4, 0, False, 3, True),
+                                                         ("c2", (4, 3, 7), 3, 2, 0, False, 3, True),
+                                                         ("c3", (3, 3, 4), 2, 2, 63, True, 3, True),
+                                                         ("c5", (5, 5, 6), 2, 3, 0, False, 1, True)])
+def test_slab_minres_amg(name, N, p, P, ess, project, k, gc):
+    """Multi-rank S^-1 = block-Jacobi of per-slab AMG V-cycles (reading A9c) — plain, inside the
+    A9d polynomial (k > 1), and in the A9e balancing form with the global coarse space (gc):
+    each rank's preconditioner output and the MINRES iteration counts (+-1) against the
+    oracle's on the same slabs."""
     import torch
     from oracle import operators, solvers
     from paper_2304_12387_b200 import slabs as sl
@@ -163,7 +169,7 @@ def test_slab_minres_amg(name, N, p, P, ess, project, k):
     last = pr.dim - 1
     bounds = [sl.slab_bounds(pr.N[last], P, r) for r in range(P)]
     Po = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds,
-                                  amg_cheb_degree=k)
+                                  amg_cheb_degree=k, amg_global_coarse=gc)
     n_rt = A.n_rt
     v = random_vector(A.n_rt + A.n_l2, 8)
     if project:
@@ -180,8 +186,9 @@ def test_slab_minres_amg(name, N, p, P, ess, project, k):
         xl, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
         return zl, xl.cpu().numpy(), rep.iters, rep.converged, rt, l2
 
-    res = _run_slabs(pr, P, fn, key=3000 + hash((name, N, p, P, ess, k)) % 1000,
-                     schur="amg", amg_max_coarse=16, amg_cheb_degree=k)
+    res = _run_slabs(pr, P, fn, key=3000 + hash((name, N, p, P, ess, k, gc)) % 1000,
+                     schur="amg", amg_max_coarse=16, amg_cheb_degree=k,
+                     amg_global_coarse=1 if gc else 2)
     assert conv_o
     its = {r[2] for r in res}
     assert len(its) == 1 and all(r[3] for r in res), its
@@ -245,33 +252,39 @@ def test_slab_gmres(name, N, p, P, schur):
 
 
 @pytest.mark.gpu
-def test_slab_amg_chebyshev_iterations_flat_in_P():
-    """Reading A9d on slabs: with the polynomial (b = 2.2) over the block-Jacobi V-cycles the
-    MINRES iteration count stays below the plain block-Jacobi V-cycle's, and on this small
-    10^4-contrast config-3 mesh barely grows with the rank count (loopback ranks on one GPU; at
-    24^3 p = 4 it does grow, 191 -> 316 from 1 to 8 slabs: profiles/r02_slab_iterations.txt)."""
+def test_slab_amg_iterations_vs_P():
+    """Iteration counts vs the slab count (loopback ranks on one GPU, 10^4-contrast config-3
+    mesh): the A9d polynomial (b = 2.2 with slabs) stays below the plain block-Jacobi V-cycle's
+    count, and with the A9e global coarse space (the default for 3D slabs) the count no longer
+    grows from 2 to 8 slabs — at 24^3 p = 4 (profiles/r02_slab_iterations.txt): 251 / 251 / 256
+    at P = 2 / 4 / 8 against 265 / 287 / 316 block-Jacobi."""
     import torch
     from paper_2304_12387_b200 import from_problem
     pr = _problem("c3", (4, 4, 8), 2)
     its = {}
+    op = from_problem(pr, schur="amg", amg_max_coarse=16, amg_cheb_degree=1)
+    b = op.apply_block(torch.from_numpy(random_vector(op.sizes.n, 3)).cuda()).cpu().numpy()
+    op.close()
     for k in (1, 3):
         op = from_problem(pr, schur="amg", amg_max_coarse=16, amg_cheb_degree=k)
-        n = op.sizes.n
-        xs = torch.from_numpy(random_vector(n, 3)).cuda()
-        b = op.apply_block(xs).cpu().numpy()
         _, rep = op.minres(torch.from_numpy(b).cuda(), rtol=1e-12, maxit=3000)
         op.close()
         assert rep.converged
-        its[(k, 1)] = rep.iters
-        for P in (2, 4):
-            def fn(r, op, rt, l2):
-                nrt_g = len(b) - pr.E * pr.p ** 3
-                bl = np.concatenate([b[:nrt_g][rt], b[nrt_g:][l2]])
-                _, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
-                return rep.iters, rep.converged
-            res = _run_slabs(pr, P, fn, key=4000 + 10 * k + P, schur="amg", amg_max_coarse=16,
-                             amg_cheb_degree=k)
-            assert all(r[1] for r in res)
-            its[(k, P)] = res[0][0]
-    assert its[(3, 4)] <= 1.15 * its[(3, 1)] + 4, its
-    assert its[(3, 4)] < its[(1, 4)], its
+        its[(k, 1, 0)] = rep.iters
+        for gc in (0, 1):
+            for P in (2, 4, 8):
+                def fn(r, op, rt, l2):
+                    nrt_g = len(b) - pr.E * pr.p ** 3
+                    bl = np.concatenate([b[:nrt_g][rt], b[nrt_g:][l2]])
+                    _, rep = op.minres(torch.from_numpy(bl).cuda(), rtol=1e-12, maxit=3000)
+                    return rep.iters, rep.converged
+                res = _run_slabs(pr, P, fn, key=4000 + 100 * gc + 10 * k + P, schur="amg",
+                                 amg_max_coarse=16, amg_cheb_degree=k,
+                                 amg_global_coarse=1 if gc else 2)
+                assert all(r[1] for r in res)
+                its[(k, P, gc)] = res[0][0]
+    for P in (2, 4, 8):
+        assert its[(3, P, 0)] < its[(1, P, 0)], its
+        assert its[(3, P, 1)] <= its[(3, P, 0)], its
+    assert its[(3, 8, 1)] <= 1.1 * its[(3, 2, 1)] + 3, its
+    assert its[(1, 8, 1)] <= 1.1 * its[(1, 2, 1)] + 3, its

@@ -240,3 +240,45 @@ def test_pinned_coarse_solve_spectrum():
     Ad[-1, -1] = 1.0
     lam = np.linalg.eigvals(np.linalg.inv(Ad) @ S).real
     assert lam.max() > 1.01
+
+
+@pytest.mark.parametrize("name,N,p,bounds,pin", [
+    ("c3", (3, 3, 6), 2, [(0, 2), (2, 4), (4, 6)], False),
+    ("c2", (4, 3, 5), 2, [(0, 3), (3, 5)], False),
+    ("c1", (6, 7), 2, [(0, 3), (3, 7)], False),
+    ("c3", (3, 3, 4), 2, [(0, 2), (2, 4)], True)])
+def test_global_coarse_balancing(name, N, p, bounds, pin):
+    """Reading A9e: B = B0 + (I - B0 S~) B_bj (I - S~ B0), B0 = R^T A0^-1 R, A0 = R S~ R^T.
+    Pins: (i) A0 equals the brute-force Galerkin sums sum_{i in I, j in J} S~_ij; (ii) B S~ is
+    the identity on range(R^T) (a wrong A0 or R breaks it; with pin: modulo the constants);
+    (iii) B is symmetric positive semidefinite (definite without pin) and the spectrum of B S~ lies
+    in [0, 2] (the interval the A9d polynomial takes, b = 2.2)."""
+    from oracle import amg as amgmod, operators
+    from synth import make_config
+    pr = make_config(name, N=N, p=p)
+    if pin:
+        pr.essential, pr.project_mean, pr.gamma = 63, True, np.zeros(pr.E)
+    A = operators.Assembled(pr)
+    S = A.S.toarray()
+    n = A.n_l2
+    B = amgmod.AMGSchur(A, max_coarse=8, slabs=bounds, global_coarse=True, pin=pin)
+    R = B.R.toarray()
+    agg = R.argmax(axis=0)
+    A0 = np.zeros((R.shape[0], R.shape[0]))
+    for i in range(n):
+        for j in np.nonzero(S[i])[0]:
+            A0[agg[i], agg[j]] += S[i, j]
+    ref = (B.R @ A.S @ B.R.T).toarray()
+    assert np.abs(A0 - ref).max() < 1e-12 * np.abs(ref).max()
+    Bm = np.column_stack([B.vcycles(e) for e in np.eye(n)])
+    assert np.abs(Bm - Bm.T).max() < 1e-11 * np.abs(Bm).max()
+    RT = R.T
+    E = Bm @ S @ RT
+    if pin:   # the constants are in the nullspace: compare after removing the mean
+        E = E - E.mean(axis=0, keepdims=True)
+        RT = RT - RT.mean(axis=0, keepdims=True)
+    assert np.abs(E - RT).max() < 1e-10, np.abs(E - RT).max()
+    lam = np.sort(np.linalg.eigvals(Bm @ S).real)
+    assert lam[0] > -1e-10 and lam[-1] < 2.0 + 1e-9, (lam[0], lam[-1])
+    if not pin:
+        assert np.linalg.eigvalsh(0.5 * (Bm + Bm.T)).min() > 0
