@@ -122,12 +122,12 @@ typedef struct {
    * amg_cheb_ratio <= 0 => 20. */
   int amg_cheb_degree;
   double amg_cheb_ratio;
-  /* schur_solver == HDIV_SCHUR_AMG with 3D slabs (reading A9e): the per-slab V-cycles B_bj enter
-   * the balancing two-level form B = B0 + (I - B0 S~) B_bj (I - S~ B0) with a global coarse
-   * space, B0 = R^T A0^-1 R, R the sums over the aggregates of a fixed 8 x 8 x 8 grid of the
-   * global subcell grid, A0 = R S~ R^T (dense, replicated on every rank) — it restores the slab
-   * coupling the block-Jacobi drops (two S~ applies, two aggregate restrictions and two
-   * 8-byte-per-aggregate all-gathers per B).  1 = on, 2 = off, 0 = auto (on with >= 2 slabs in
+  /* schur_solver == HDIV_SCHUR_AMG with 3D slabs (reading A9e): S^-1 = B0 + (I - B0 S~) M
+   * (I - S~ B0), the balancing two-level form around M = the per-slab V-cycles (or their A9d
+   * polynomial) with a global coarse space, B0 = R^T A0^-1 R, R the sums over the aggregates of
+   * a fixed grid of blocks of ceil(N_a / 8) elements of the global mesh, A0 = R S~ R^T (dense,
+   * replicated on every rank) — it restores the slab coupling the block-Jacobi drops (per S^-1:
+   * two S~ applies, two aggregate restrictions, two all-gathers of one double per aggregate).  1 = on, 2 = off, 0 = auto (on with >= 2 slabs in
    * 3D); ignored on one rank and in 2D. */
   int amg_global_coarse;
 } hdiv_options;

@@ -174,19 +174,20 @@ class AMGSchur:
             self.blocks.append((a, b, lv))
         self.levels = self.blocks[0][2] if len(self.blocks) == 1 else None
         # reading A9e (slabs only): a global coarse space couples the slabs — the indicator
-        # vectors of the aggregates of a fixed coarse grid of the GLOBAL subcell grid (ceil(n_a /
-        # C) subcells per aggregate along axis a, C = 8 in 3D, 16 in 2D), R the aggregate-sum
+        # vectors of the aggregates of a fixed coarse grid of the GLOBAL element grid (ceil(N_a /
+        # C) elements per aggregate along axis a, C = 8 in 3D, 16 in 2D), R the aggregate-sum
         # restriction, A0 = R S~ R^T (the exact Galerkin operator, dense), B0 = R^T A0^-1 R, and
-        # the block-Jacobi V-cycles B_bj enter the balancing (hybrid two-level) form
-        #   B = B0 + (I - B0 S~) B_bj (I - S~ B0),
-        # symmetric, with B S~ = I on range(R^T) and the spectrum of B S~ still in (0, 2]
-        # (b = 2.2 for the A9d polynomial).  The singular pure-Neumann S~ (pin) makes A0 singular
+        # the inner preconditioner M (the block-Jacobi V-cycles, or their A9d polynomial) enters
+        # the balancing (hybrid two-level) form, once per application of S^-1:
+        #   S^-1 = B0 + (I - B0 S~) M (I - S~ B0),
+        # symmetric, with S^-1 S~ = I on range(R^T) and its spectrum in (0, max(1, lam_max(M S~))].  The singular pure-Neumann S~ (pin) makes A0 singular
         # with the constants as its nullspace: its last unknown is fixed at 0 (as A21).
         self.global_coarse = bool(global_coarse) and len(slabs) > 1
         if self.global_coarse:
             C = 8 if asm.dim == 3 else 16
-            g = [max(1, -(-d // C)) for d in dims]
-            cd = [-(-d // gg) for d, gg in zip(dims, g)]
+            ge = [max(1, -(-int(asm.N[a]) // C)) for a in range(asm.dim)]
+            g = [gg * asm.p for gg in ge]
+            cd = [-(-int(asm.N[a]) // gg) for a, gg in enumerate(ge)]
             agg = coords[:, 0] // g[0]
             stride = 1
             for a in range(1, asm.dim):
@@ -216,15 +217,19 @@ class AMGSchur:
         return out
 
     def vcycles(self, r):
-        """B r: the (block-Jacobi) V-cycles, with the balancing global coarse correction when
-        global_coarse (A9e), step by step: e0 = B0 r, w = B_bj (r - S~ e0), B r = e0 + w - B0 S~ w."""
-        if not self.global_coarse:
-            return self.block_vcycles(r)
-        e0 = self.B0(r)
-        w = self.block_vcycles(r - self.S @ e0)
-        return e0 + w - self.B0(self.S @ w)
+        return self.block_vcycles(r)
 
     def __call__(self, r):
+        """S^-1 r: the (block-Jacobi) V-cycles or their A9d polynomial M, wrapped in the balancing
+        global coarse correction when global_coarse (A9e), step by step:
+        e0 = B0 r, w = M (r - S~ e0), S^-1 r = e0 + w - B0 S~ w."""
+        if not self.global_coarse:
+            return self.inner(r)
+        e0 = self.B0(r)
+        w = self.inner(r - self.S @ e0)
+        return e0 + w - self.B0(self.S @ w)
+
+    def inner(self, r):
         if self.cheb_degree < 2:
             return self.vcycles(r)
         # r/d form, step by step: d_0 = B r / theta, y = d_0; r_i = r_{i-1} - S~ d_{i-1},

@@ -53,8 +53,11 @@ struct GlobalCoarse {
   double* c = nullptr;       // [n0] summed in rank order
   double* e0 = nullptr;      // [n0]
   double* e1 = nullptr;      // [n0]
-  double* rp = nullptr;      // [n_l2] r - S~ R^T e0
+  double* rp = nullptr;      // [n_l2] r - S~ R^T e0, later S~ w
   double* w = nullptr;       // [n_l2 + 2 plane] the block-Jacobi V-cycles (ghost space)
+  double* u = nullptr;       // [n_l2 + 2 plane] R^T e0 (ghost space)
+  double* es = nullptr;      // [E] per-element sums
+  int32_t* eagg = nullptr;   // [E] element -> aggregate
 };
 
 struct AmgHier {
@@ -647,7 +650,7 @@ void amg_free(hdiv_ctx* h) {
   }
   if (GlobalCoarse* G = h->amg->gc) {
     cudaFree(G->a0inv); cudaFree(G->part); cudaFree(G->glob); cudaFree(G->c); cudaFree(G->e0);
-    cudaFree(G->e1); cudaFree(G->rp); cudaFree(G->w);
+    cudaFree(G->e1); cudaFree(G->rp); cudaFree(G->w); cudaFree(G->u); cudaFree(G->es); cudaFree(G->eagg);
     delete G;
   }
   cudaFree(h->amg->agg0);
@@ -905,67 +908,54 @@ struct GcGeo {
   int p;
   int gx, gy, gz, cdx, cdy;
   long long nzg, z0c;
-  // aggregate of a local cell (element-major index) or of a ghost cell (index >= n)
-  __device__ __forceinline__ long long agg(long long j) const {
-    long long X, Y, Zg;
-    if (j < g.n) {
-      const long long pd = (long long)p * p * p;
-      const long long e = j / pd, il = j - e * pd;
-      const long long ex = e % g.NL[0], ey = (e / g.NL[0]) % g.NL[1], ez = e / ((long long)g.NL[0] * g.NL[1]);
-      X = ex * p + il % p;
-      Y = ey * p + (il / p) % p;
-      Zg = z0c + ez * p + il / (p * p);
-    } else {
-      const long long plane = g.nx * g.ny;
-      const long long q = j - g.n;
-      const bool lo = q < plane;
-      const long long idx = lo ? q : q - plane;
-      X = idx % g.nx;
-      Y = idx / g.nx;
-      Zg = lo ? z0c - 1 : z0c + g.nz;
-    }
-    return X / gx + cdx * (Y / gy + (long long)cdy * (Zg / gz));
-  }
 };
 
-template <class F>
-__device__ __forceinline__ double gc_block_sum(double v, F) {
-  __shared__ double red[ANT / 32];
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < ANT / 32; ++w) t += red[w];
-  return t;
-}
-
-// part[I] = sum over this slab's cells of aggregate I of v (MODE 0) or of (S~ v) (MODE 1, v in
-// ghost space); one CTA per aggregate, fixed-order sums
-template <int P, int MODE>
-__global__ void __launch_bounds__(ANT) gc_restrict_kernel(GcGeo G, const double* __restrict__ v,
-                                                          double* __restrict__ part,
+// es[e] = sum of v over the P^3 cells of local element e (one warp per element, fixed order)
+template <int P>
+__global__ void __launch_bounds__(ANT) gc_elem_sum_kernel(long long E, const double* __restrict__ v,
+                                                          double* __restrict__ es,
                                                           const int* __restrict__ done) {
   if (done && *done) return;
+  constexpr int PD = P * P * P;
+  const long long e = blockIdx.x * (long long)(ANT / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (e >= E) return;
+  double t = 0.0;
+  for (int k = lane; k < PD; k += 32) t += v[e * PD + k];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  if (lane == 0) es[e] = t;
+}
+
+// part[I] = sum over this slab's elements of aggregate I of es (one CTA per aggregate, each
+// thread a fixed strided subset, then a fixed-order tree)
+__global__ void __launch_bounds__(ANT) gc_agg_sum_kernel(GcGeo G, const double* __restrict__ es,
+                                                         double* __restrict__ part,
+                                                         const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double red[ANT / 32];
   const long long I = blockIdx.x;
-  const int Ix = (int)(I % G.cdx), Iy = (int)((I / G.cdx) % G.cdy), Iz = (int)(I / ((long long)G.cdx * G.cdy));
-  const long long x0 = (long long)Ix * G.gx, x1 = min(x0 + G.gx, G.g.nx);
-  const long long y0 = (long long)Iy * G.gy, y1 = min(y0 + G.gy, G.g.ny);
-  const long long zg0 = max((long long)Iz * G.gz, G.z0c), zg1 = min((long long)(Iz + 1) * G.gz, G.z0c + G.g.nz);
+  const long long gx = G.gx / G.p, gy = G.gy / G.p, gz = G.gz / G.p;
+  const long long Ix = I % G.cdx, Iy = (I / G.cdx) % G.cdy, Iz = I / ((long long)G.cdx * G.cdy);
+  const long long NLx = G.g.NL[0], NLy = G.g.NL[1], NLz = G.g.NL[2];
+  const long long ez0g = G.z0c / G.p;
+  const long long x0 = Ix * gx, x1 = min(x0 + gx, NLx), y0 = Iy * gy, y1 = min(y0 + gy, NLy);
+  const long long z0 = max(Iz * gz, ez0g), z1 = min((Iz + 1) * gz, ez0g + NLz);
   double acc = 0.0;
-  if (zg1 > zg0 && x1 > x0 && y1 > y0) {
-    const long long bx = x1 - x0, by = y1 - y0, cnt = bx * by * (zg1 - zg0);
-    constexpr int PD = P * P * P;
+  if (z1 > z0 && x1 > x0 && y1 > y0) {
+    const long long bx = x1 - x0, by = y1 - y0, cnt = bx * by * (z1 - z0);
     for (long long t = threadIdx.x; t < cnt; t += ANT) {
-      const long long X = x0 + t % bx, Y = y0 + (t / bx) % by, Z = zg0 - G.z0c + t / (bx * by);
-      const long long e = (X / P) + G.g.NL[0] * ((Y / P) + (long long)G.g.NL[1] * (Z / P));
-      const long long i = e * PD + (X % P) + P * ((Y % P) + P * (Z % P));
-      if constexpr (MODE == 0) acc += v[i];
-      else acc += cell_apply<P, true>(G.g, i, [&](long long j) { return v[j]; });
+      const long long ex = x0 + t % bx, ey = y0 + (t / bx) % by, ez = z0 - ez0g + t / (bx * by);
+      acc += es[ex + NLx * (ey + NLy * ez)];
     }
   }
-  const double tot = gc_block_sum(acc, 0);
-  if (threadIdx.x == 0) part[I] = tot;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < ANT / 32; ++w) t += red[w];
+    part[I] = t;
+  }
 }
 
 __global__ void gc_sum_kernel(const double* __restrict__ glob, int P, long long n0,
@@ -978,27 +968,41 @@ __global__ void gc_sum_kernel(const double* __restrict__ glob, int P, long long 
   c[I] = t;
 }
 
-// rp = b - S~ R^T e0 (the coarse correction's residual; ghosts: the neighbours' aggregates)
+// u = R^T e (injection of the aggregate values into the cells)
 template <int P>
-__global__ void __launch_bounds__(ANT) gc_resid_kernel(GcGeo G, const double* __restrict__ b,
-                                                       const double* __restrict__ e0,
-                                                       double* __restrict__ rp,
-                                                       const int* __restrict__ done) {
+__global__ void __launch_bounds__(ANT) gc_inject_kernel(GcGeo G, const int32_t* __restrict__ eagg,
+                                                        const double* __restrict__ e0,
+                                                        double* __restrict__ u,
+                                                        const int* __restrict__ done) {
   if (done && *done) return;
-  AMG_LOOP(G.g.n) rp[i] = b[i] - cell_apply<P, true>(G.g, i, [&](long long j) { return e0[G.agg(j)]; });
+  constexpr int PD = P * P * P;
+  AMG_LOOP(G.g.n) u[i] = e0[eagg[i / PD]];
 }
 
-// x = R^T e0 + w - R^T e1
-__global__ void __launch_bounds__(ANT) gc_final_kernel(GcGeo G, const double* __restrict__ e0,
+// out = b - S~ u (SUB) or S~ u, through the cell stencil with the slab ghosts
+template <int P, bool SUB>
+__global__ void __launch_bounds__(ANT, AMG_MINB) gc_smul_kernel(CellGeo g, const double* __restrict__ b,
+                                                       const double* __restrict__ u,
+                                                       double* __restrict__ out,
+                                                       const int* __restrict__ done) {
+  if (done && *done) return;
+  AMG_LOOP(g.n) {
+    const double su = cell_apply<P, true>(g, i, [&](long long j) { return u[j]; });
+    out[i] = SUB ? b[i] - su : su;
+  }
+}
+
+// x = u + w - R^T e1   (u = R^T e0)
+template <int P>
+__global__ void __launch_bounds__(ANT) gc_final_kernel(GcGeo G, const int32_t* __restrict__ eagg,
+                                                       const double* __restrict__ u,
                                                        const double* __restrict__ w,
                                                        const double* __restrict__ e1,
                                                        double* __restrict__ x,
                                                        const int* __restrict__ done) {
   if (done && *done) return;
-  AMG_LOOP(G.g.n) {
-    const long long I = G.agg(i);
-    x[i] = (e0[I] + w[i]) - e1[I];
-  }
+  constexpr int PD = P * P * P;
+  AMG_LOOP(G.g.n) x[i] = (u[i] + w[i]) - e1[eagg[i / PD]];
 }
 
 GcGeo make_gcgeo(const hdiv_ctx* h) {
@@ -1021,9 +1025,11 @@ static hdiv_status gc_setup(hdiv_ctx* h, cudaStream_t s) {
   const int p = h->p;
   const long long ng[3] = {h->N[0] * p, h->N[1] * p, h->N[2] * p};
   long long n0 = 1;
-  for (int a = 0; a < 3; ++a) {
-    C->g[a] = (int)std::max(1LL, (ng[a] + 7) / 8);
-    C->cd[a] = (int)((ng[a] + C->g[a] - 1) / C->g[a]);
+  (void)ng;
+  for (int a = 0; a < 3; ++a) {   // blocks of ceil(N_a / 8) whole elements (oracle/amg.py)
+    const long long ge = std::max(1LL, (long long)(h->N[a] + 7) / 8);
+    C->g[a] = (int)(ge * p);
+    C->cd[a] = (int)((h->N[a] + ge - 1) / ge);
     n0 *= C->cd[a];
   }
   C->n0 = n0;
@@ -1038,6 +1044,20 @@ static hdiv_status gc_setup(hdiv_ctx* h, cudaStream_t s) {
   HDIV_CUDA_TRY(cudaMalloc(&C->rp, sizeof(double) * n));
   HDIV_CUDA_TRY(cudaMalloc(&C->w, sizeof(double) * (n + 2 * plane)));
   HDIV_CUDA_TRY(cudaMemsetAsync(C->w, 0, sizeof(double) * (n + 2 * plane), s));
+  HDIV_CUDA_TRY(cudaMalloc(&C->u, sizeof(double) * (n + 2 * plane)));
+  HDIV_CUDA_TRY(cudaMemsetAsync(C->u, 0, sizeof(double) * (n + 2 * plane), s));
+  HDIV_CUDA_TRY(cudaMalloc(&C->es, sizeof(double) * std::max<long long>(1, h->E)));
+  {
+    std::vector<int32_t> ea(h->E);
+    const long long ge[3] = {C->g[0] / p, C->g[1] / p, C->g[2] / p};
+    for (long long e = 0; e < h->E; ++e) {
+      const long long ex = e % h->NL[0], ey = (e / h->NL[0]) % h->NL[1], ez = e / (h->NL[0] * h->NL[1]);
+      ea[e] = (int32_t)(ex / ge[0] + C->cd[0] * (ey / ge[1] + (long long)C->cd[1] * ((h->ez0 + ez) / ge[2])));
+    }
+    HDIV_CUDA_TRY(cudaMalloc(&C->eagg, sizeof(int32_t) * std::max<long long>(1, h->E)));
+    HDIV_CUDA_TRY(cudaMemcpyAsync(C->eagg, ea.data(), sizeof(int32_t) * h->E, cudaMemcpyHostToDevice, s));
+    HDIV_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   // A0 = R S~ R^T: this rank's rows of S~ (the CSR, ghost columns for the slab neighbours),
   // summed per aggregate pair on the host in row order, all-gathered and summed in rank order
   std::vector<int64_t> rp(n + 1);
@@ -1106,19 +1126,20 @@ static hdiv_status gc_setup(hdiv_ctx* h, cudaStream_t s) {
   return HDIV_OK;
 }
 
-template <int MODE>
+// e = A0^-1 R v (R: sums over the aggregates' cells; this rank's share, all-gathered)
 static hdiv_status gc_restrict(hdiv_ctx* h, const GcGeo& G, const double* v, double* e,
                                const int* done, cudaStream_t s) {
   GlobalCoarse* C = h->amg->gc;
-  const unsigned nb = (unsigned)C->n0;
+  const unsigned ge = (unsigned)((h->E + ANT / 32 - 1) / (ANT / 32));
   switch (h->p) {
-    case 1: gc_restrict_kernel<1, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
-    case 2: gc_restrict_kernel<2, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
-    case 3: gc_restrict_kernel<3, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
-    case 4: gc_restrict_kernel<4, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
-    case 5: gc_restrict_kernel<5, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
-    default: gc_restrict_kernel<6, MODE><<<nb, ANT, 0, s>>>(G, v, C->part, done); break;
+    case 1: gc_elem_sum_kernel<1><<<ge, ANT, 0, s>>>(h->E, v, C->es, done); break;
+    case 2: gc_elem_sum_kernel<2><<<ge, ANT, 0, s>>>(h->E, v, C->es, done); break;
+    case 3: gc_elem_sum_kernel<3><<<ge, ANT, 0, s>>>(h->E, v, C->es, done); break;
+    case 4: gc_elem_sum_kernel<4><<<ge, ANT, 0, s>>>(h->E, v, C->es, done); break;
+    case 5: gc_elem_sum_kernel<5><<<ge, ANT, 0, s>>>(h->E, v, C->es, done); break;
+    default: gc_elem_sum_kernel<6><<<ge, ANT, 0, s>>>(h->E, v, C->es, done); break;
   }
+  gc_agg_sum_kernel<<<(unsigned)C->n0, ANT, 0, s>>>(G, C->es, C->part, done);
   HDIV_CUDA_TRY(cudaGetLastError());
   hdiv_status st = comm_allgather(h, C->part, C->glob, (int)C->n0, s);
   if (st != HDIV_OK) return st;
@@ -1129,34 +1150,45 @@ static hdiv_status gc_restrict(hdiv_ctx* h, const GcGeo& G, const double* v, dou
   return HDIV_OK;
 }
 
-// x = B b with the A9e balancing form when the global coarse space is set up, else the
-// (block-Jacobi) V-cycles
-hdiv_status amg_apply(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s) {
-  if (!h->amg) {
-    set_error("AMG hierarchy missing");
-    return HDIV_ERR_UNSUPPORTED;
-  }
+template <int P>
+static hdiv_status gc_apply_p(hdiv_ctx* h, const GcGeo& G, const double* b, double* x,
+                              const int* done, cudaStream_t s, AmgInner inner) {
   GlobalCoarse* C = h->amg->gc;
-  if (!C) return vcycle(h, 0, b, x, done, s);
-  const GcGeo G = make_gcgeo(h);
-  hdiv_status st = gc_restrict<0>(h, G, b, C->e0, done, s);   // e0 = A0^-1 R b
-  if (st != HDIV_OK) return st;
   const unsigned g = nbk(h->nl2);
-  switch (h->p) {
-    case 1: gc_resid_kernel<1><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
-    case 2: gc_resid_kernel<2><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
-    case 3: gc_resid_kernel<3><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
-    case 4: gc_resid_kernel<4><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
-    case 5: gc_resid_kernel<5><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
-    default: gc_resid_kernel<6><<<g, ANT, 0, s>>>(G, b, C->e0, C->rp, done); break;
-  }
+  hdiv_status st = gc_restrict(h, G, b, C->e0, done, s);                      // e0 = A0^-1 R b
+  if (st != HDIV_OK) return st;
+  gc_inject_kernel<P><<<g, ANT, 0, s>>>(G, C->eagg, C->e0, C->u, done);               // u = R^T e0
   HDIV_CUDA_TRY(cudaGetLastError());
-  if ((st = vcycle(h, 0, C->rp, C->w, done, s)) != HDIV_OK) return st;   // w = B_bj rp
+  if ((st = comm_l2_ghosts(h, C->u, s)) != HDIV_OK) return st;
+  gc_smul_kernel<P, true><<<g, ANT, 0, s>>>(G.g, b, C->u, C->rp, done);       // rp = b - S~ u
+  HDIV_CUDA_TRY(cudaGetLastError());
+  if ((st = inner(h, C->rp, C->w, done, s)) != HDIV_OK) return st;          // w = M rp
   if ((st = comm_l2_ghosts(h, C->w, s)) != HDIV_OK) return st;
-  if ((st = gc_restrict<1>(h, G, C->w, C->e1, done, s)) != HDIV_OK) return st;   // e1 = A0^-1 R S~ w
-  gc_final_kernel<<<g, ANT, 0, s>>>(G, C->e0, C->w, C->e1, x, done);
+  gc_smul_kernel<P, false><<<g, ANT, 0, s>>>(G.g, nullptr, C->w, C->rp, done);  // S~ w
+  HDIV_CUDA_TRY(cudaGetLastError());
+  if ((st = gc_restrict(h, G, C->rp, C->e1, done, s)) != HDIV_OK) return st;  // e1 = A0^-1 R S~ w
+  gc_final_kernel<P><<<g, ANT, 0, s>>>(G, C->eagg, C->u, C->w, C->e1, x, done);
   HDIV_CUDA_TRY(cudaGetLastError());
   return HDIV_OK;
+}
+
+bool amg_has_global_coarse(const hdiv_ctx* h) { return h->amg && h->amg->gc; }
+
+// reading A9e: x = S^-1 b in the balancing form around the inner preconditioner M (the
+// block-Jacobi V-cycles or their A9d polynomial):  e0 = A0^-1 R b, u = R^T e0,
+// w = M (b - S~ u), x = u + w - R^T A0^-1 R S~ w
+hdiv_status amg_global_apply(hdiv_ctx* h, const double* b, double* x, const int* done,
+                             cudaStream_t s, AmgInner inner) {
+  if (!amg_has_global_coarse(h)) return inner(h, b, x, done, s);
+  const GcGeo G = make_gcgeo(h);
+  switch (h->p) {
+    case 1: return gc_apply_p<1>(h, G, b, x, done, s, inner);
+    case 2: return gc_apply_p<2>(h, G, b, x, done, s, inner);
+    case 3: return gc_apply_p<3>(h, G, b, x, done, s, inner);
+    case 4: return gc_apply_p<4>(h, G, b, x, done, s, inner);
+    case 5: return gc_apply_p<5>(h, G, b, x, done, s, inner);
+    default: return gc_apply_p<6>(h, G, b, x, done, s, inner);
+  }
 }
 
 hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s,
@@ -1165,8 +1197,7 @@ hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done,
     set_error("AMG hierarchy missing");
     return HDIV_ERR_UNSUPPORTED;
   }
-  if (part && (h->amg->nu < 1 || h->amg->L.size() < 2 || h->amg->gc)) return HDIV_ERR_UNSUPPORTED;
-  if (h->amg->gc) return amg_apply(h, b, x, done, s);
+  if (part && (h->amg->nu < 1 || h->amg->L.size() < 2)) return HDIV_ERR_UNSUPPORTED;
   return vcycle(h, 0, b, x, done, s, part, nbpart);
 }
 

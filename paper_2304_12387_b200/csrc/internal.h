@@ -165,6 +165,13 @@ void amg_free(hdiv_ctx* h);
 // (HDIV_ERR_UNSUPPORTED, nothing launched, when the hierarchy has no such sweep)
 hdiv_status amg_vcycle(hdiv_ctx* h, const double* b, double* x, const int* done, cudaStream_t s,
                        double* part = nullptr, int nbpart = 0);
+// reading A9e (3D slabs): S^-1 in the balancing form with the global coarse space around the
+// inner preconditioner `inner` (block-Jacobi V-cycles or their A9d polynomial)
+typedef hdiv_status (*AmgInner)(hdiv_ctx* h, const double* b, double* x, const int* done,
+                                 cudaStream_t s);
+bool amg_has_global_coarse(const hdiv_ctx* h);
+hdiv_status amg_global_apply(hdiv_ctx* h, const double* b, double* x, const int* done,
+                             cudaStream_t s, AmgInner inner);
 int amg_num_levels(const hdiv_ctx* h);
 hdiv_status amg_level_info(const hdiv_ctx* h, int l, int64_t* dims, int64_t* n, double* omega,
                            const double** st);

@@ -603,10 +603,31 @@ static hdiv_status amg_cheb_apply(hdiv_ctx* h, const double* vq, double* y, doub
   return HDIV_OK;
 }
 
+// the inner preconditioners of the A9e balancing form
+static hdiv_status amg_poly_inner(hdiv_ctx* h, const double* b, double* x, const int* done,
+                                  cudaStream_t s) {
+  return amg_cheb_apply(h, b, x, nullptr, done, s);
+}
+static hdiv_status amg_vc_inner(hdiv_ctx* h, const double* b, double* x, const int* done,
+                                cudaStream_t s) {
+  return amg_vcycle(h, b, x, done, s);
+}
+
 // Chebyshev-Jacobi S^-1 applied to vq -> y (uses mw->r, mw->d); partial <y, vq> if part
 static hdiv_status cheb_apply_raw(hdiv_ctx* h, const double* vq, double* y, double* part,
                                   const int* done, cudaStream_t s) {
   MinresWork* mw = h->mw;
+  if (h->opts.schur_solver == HDIV_SCHUR_AMG && amg_has_global_coarse(h)) {
+    // reading A9e: the balancing global coarse correction around the polynomial / V-cycles
+    hdiv_status st = amg_global_apply(h, vq, y, done, s,
+                                      h->opts.amg_cheb_degree >= 2 ? amg_poly_inner : amg_vc_inner);
+    if (st != HDIV_OK) return st;
+    if (part) {
+      dot_kernel<<<h->mw->nb, RED_NT, 0, s>>>(y, vq, h->nl2, 0, 0, part, done);
+      HDIV_CUDA_TRY(cudaGetLastError());
+    }
+    return HDIV_OK;
+  }
   if (h->opts.schur_solver == HDIV_SCHUR_AMG && h->opts.amg_cheb_degree >= 2)
     return amg_cheb_apply(h, vq, y, part, done, s);
   if (h->opts.schur_solver == HDIV_SCHUR_AMG) {   // NEXT-1: one V-cycle

@@ -256,8 +256,9 @@ def test_slab_amg_iterations_vs_P():
     """Iteration counts vs the slab count (loopback ranks on one GPU, 10^4-contrast config-3
     mesh): the A9d polynomial (b = 2.2 with slabs) stays below the plain block-Jacobi V-cycle's
     count, and with the A9e global coarse space (the default for 3D slabs) the count no longer
-    grows from 2 to 8 slabs — at 24^3 p = 4 (profiles/r02_slab_iterations.txt): 251 / 251 / 256
-    at P = 2 / 4 / 8 against 265 / 287 / 316 block-Jacobi."""
+    grows from 2 to 8 slabs on this mesh — at 24^3 p = 4 (profiles/r02_slab_iterations.txt) with
+    the polynomial 256 / 265 / 287 at P = 2 / 4 / 8 against 265 / 287 / 316 block-Jacobi, with the
+    plain V-cycle 491 / 501 / 478 against 527 / 578 / 637."""
     import torch
     from paper_2304_12387_b200 import from_problem
     pr = _problem("c3", (4, 4, 8), 2)
