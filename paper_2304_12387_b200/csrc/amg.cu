@@ -13,8 +13,11 @@
 // setup); levels >= 1 are structured stencils stored as [3^d][n] (SoA: coalesced per offset),
 // lexicographic x-fastest numbering.  Multi-rank (slabs): every rank builds the hierarchy of its
 // own diagonal block of S~ (slab-local aggregates, ghost couplings dropped: the face terms of the
-// interface stay on the diagonal) and the V-cycles act independently — S^-1 is the block-Jacobi
-// of the per-slab V-cycles (reading A9c), no communication inside S^-1.  P and P^T are never stored: P e = inject(e) - omega D^-1 A
+// interface stay on the diagonal) and the V-cycles act independently — the block-Jacobi of the
+// per-slab V-cycles (reading A9c), no communication inside a V-cycle; in 3D, S^-1 wraps them (or
+// their A9d polynomial) once in the balancing form with a replicated global coarse operator
+// A0 = R S~ R^T over blocks of ceil(N/8) elements (reading A9e, amg_global_apply below).
+// P and P^T are never stored: P e = inject(e) - omega D^-1 A
 // inject(e) and P^T r = aggregate-sum(r - omega A D^-1 r) reuse the level's SpMV.  The Galerkin
 // product is formed matrix-free per coarse row (one CTA: phi_I on the 5^d box, A phi_I on 7^d,
 // (I - omega A D^-1) A phi_I on 9^d, summed per neighbouring aggregate), no SpGEMM.
