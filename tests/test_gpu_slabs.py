@@ -204,7 +204,9 @@ def test_slab_minres_amg(name, N, p, P, ess, project, k, gc):
                                               ("c2", (4, 3, 12), 3, 2, "amg"),
                                               ("c3", (3, 3, 6), 2, 3, "chebyshev"),
                                               ("c5", (5, 5, 6), 2, 2, "amg"),
-                                              ("c3", (3, 3, 6), 2, 3, "amg3")])
+                                              ("c3", (3, 3, 6), 2, 3, "amg3"),
+                                              ("c3", (4, 3, 8), 2, 4, "amg3gc"),
+                                              ("c2", (4, 3, 7), 3, 2, "amggc")])
 def test_slab_gmres(name, N, p, P, schur):
     """NEXT-4 on slabs: block-triangular preconditioner (D^T reverse-added) + GMRES with
     all-gathered projections — every rank takes the same decisions; iteration counts +-1 and
@@ -214,9 +216,12 @@ def test_slab_gmres(name, N, p, P, schur):
     from oracle import operators, solvers
     from paper_2304_12387_b200 import from_problem, slabs as sl
     pr = _problem(name, N, p)
-    k = 3 if schur == "amg3" else 1   # amg3: the A9d polynomial over the block-Jacobi V-cycles
-    schur = "amg" if k == 3 else schur
-    kw = {"schur": schur, "amg_max_coarse": 16, "amg_cheb_degree": k}
+    # amg3: the A9d polynomial over the block-Jacobi V-cycles; ...gc: the A9e global coarse space
+    k = 3 if schur.startswith("amg3") else 1
+    gc = schur.endswith("gc")
+    schur = "amg" if schur.startswith("amg") else schur
+    kw = {"schur": schur, "amg_max_coarse": 16, "amg_cheb_degree": k,
+          "amg_global_coarse": 1 if gc else 2}
     ref = from_problem(pr, **kw)
     n_rt = ref.sizes.n_rt
     xs = random_vector(ref.sizes.n, 3)
@@ -232,7 +237,8 @@ def test_slab_gmres(name, N, p, P, schur):
         bounds = [sl.slab_bounds(pr.N[last], P, r) for r in range(P)]
         B = solvers.BlockTriPrecond(A, schur="amg", amg_max_coarse=16)
         B.diag = solvers.BlockDiagPrecond(A, schur="amg", amg_max_coarse=16, amg_slabs=bounds,
-                                          project_mean=False, amg_cheb_degree=k)
+                                          project_mean=False, amg_cheb_degree=k,
+                                          amg_global_coarse=gc)
         x1, it1, conv, _ = solvers.gmres(A.apply_block, B.apply, b, rtol=1e-10, restart=20)
         assert conv
 
@@ -241,7 +247,7 @@ def test_slab_gmres(name, N, p, P, schur):
         xl, rep = op.gmres(torch.from_numpy(bl).cuda(), rtol=1e-10, restart=20, maxit=2000)
         return xl.cpu().numpy(), rep.iters, rep.converged, rt, l2
 
-    res = _run_slabs(pr, P, fn, key=4000 + hash((name, N, p, P, schur)) % 1000, **kw)
+    res = _run_slabs(pr, P, fn, key=4000 + hash((name, N, p, P, schur, k, gc)) % 1000, **kw)
     its = {r[1] for r in res}
     assert len(its) == 1 and all(r[2] for r in res), its
     assert abs(res[0][1] - it1) <= 1, (res[0][1], it1)
