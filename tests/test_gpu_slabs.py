@@ -153,7 +153,9 @@ def test_slab_minres(name, N, p, P, ess, project):
                                                          ("c3", (4, 3, 8), 2, 4, 0, False, 3, True),
                                                          ("c2", (4, 3, 7), 3, 2, 0, False, 3, True),
                                                          ("c3", (3, 3, 4), 2, 2, 63, True, 3, True),
-                                                         ("c5", (5, 5, 6), 2, 3, 0, False, 1, True)])
+                                                         ("c5", (5, 5, 6), 2, 3, 0, False, 1, True),
+                                                         ("c3", (3, 3, 6), 2, 3, 3 | 16, False, 3, True),
+                                                         ("c2", (3, 4, 6), 4, 2, 32, False, 2, True)])
 def test_slab_minres_amg(name, N, p, P, ess, project, k, gc):
     """Multi-rank S^-1 = block-Jacobi of per-slab AMG V-cycles (reading A9c) — plain, inside the
     A9d polynomial (k > 1), and in the A9e balancing form with the global coarse space (gc):
