@@ -118,7 +118,8 @@ typedef struct {
    * or 2.2 (slabs: block-Jacobi over a chain, spectrum <= 2) — the r/d
    * recurrence of reading A10 with B in place of D^-1, amg_cheb_degree V-cycles and
    * amg_cheb_degree - 1 S~ applies per S^-1.  1 = the plain V-cycle; <= 0 = auto:
-   * 3 when the element mass weights (beta | 1/eps) span more than 10^2 or with slabs, else 1;
+   * one rank: 3 when the element mass weights (beta | 1/eps) span more than 10^2, else 1;
+   * slabs: 1 with the A9e global coarse space (amg_global_coarse), else 3;
    * amg_cheb_ratio <= 0 => 20. */
   int amg_cheb_degree;
   double amg_cheb_ratio;

@@ -305,14 +305,17 @@ hdiv_status hdiv_setup(const hdiv_mesh_desc* mesh, int p, const hdiv_coeffs* co,
     }
   }
   h->has_z = (kind == HDIV_GRAD_DIV) || any_gamma;
-  // A9d auto degree: the polynomial where one V-cycle of the geometric aggregation degrades —
-  // element-wise contrast of the mass weight above 10^2 (config 3: 890 -> 330 MINRES iterations,
-  // 3.6 -> 2.7 s) or slabs (block-Jacobi across ranks: config-3 mesh 24^3 p=4 at 8 slabs 637 -> 316 its); else the plain
-  // V-cycle (config 4: 155 its / 3.7 s, the polynomial no faster)
+  // A9d auto degree.  One rank: the polynomial where one V-cycle of the geometric aggregation
+  // degrades — element-wise contrast of the mass weight above 10^2 (config 3: 890 -> 330 MINRES
+  // iterations, 3.6 -> 2.7 s); else the plain V-cycle (config 4: 155 its / 3.7 s, the polynomial
+  // no faster).  Slabs: with the A9e global coarse space the plain V-cycle (config-3 mesh 32^3
+  // p=4, 2..16 slabs: 544..553 its, flat, at half the cost per iteration of the polynomial's
+  // 285..348); without it (2D, or switched off) the polynomial (block-Jacobi: 737 -> 356 at 8)
   if (h->opts.amg_cheb_degree <= 0) {
     double lo = mw.empty() ? 1.0 : mw[0], hi = lo;
     for (double v : mw) { lo = std::min(lo, v); hi = std::max(hi, v); }
-    h->opts.amg_cheb_degree = (nranks > 1 || hi > 100.0 * lo) ? 3 : 1;
+    if (nranks > 1) h->opts.amg_cheb_degree = h->opts.amg_global_coarse ? 1 : 3;
+    else h->opts.amg_cheb_degree = (hi > 100.0 * lo) ? 3 : 1;
   }
 
   // ---- geometry classification per element (host) ----

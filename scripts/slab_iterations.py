@@ -1,7 +1,7 @@
 """MINRES iteration count vs the number of z-slab ranks (reading A9c block-Jacobi AMG, with and
 without the A9d polynomial, with and without the A9e global coarse space), on ONE GPU through the loopback communicator (iteration counts
 only — no timing: loopback ranks share one device and meet at host barriers).
-    python scripts/slab_iterations.py [N] [p]"""
+    python scripts/slab_iterations.py [N] [p] [P list, e.g. 1,2,4,8,16]"""
 import sys
 import threading
 sys.path.insert(0, ".")
@@ -13,6 +13,7 @@ from paper_2304_12387_b200.binding import loopback_id
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 p = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+PS = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4, 8]
 pr = make_config("c3", N=(N, N, N), p=p)
 op = from_problem(pr, schur="amg", amg_cheb_degree=1)
 b = op.apply_block(torch.from_numpy(random_vector(op.sizes.n, 3)).cuda()).cpu().numpy()
@@ -61,7 +62,7 @@ def run(P, k, gc):
 print(f"config 3 mesh {N}^3, p = {p}, {len(b)} DOFs, b = A x*, rtol 1e-12", flush=True)
 for gc in (0, 1):
     for k in (1, 3):
-        for P in (1, 2, 4, 8):
+        for P in PS:
             if gc and P == 1:
                 continue
             its, conv = run(P, k, gc)
